@@ -1,0 +1,108 @@
+/*
+ * apax_b200.h -- C ABI of the B200-native APAX codec (libapax_b200.so).
+ *
+ * Plain pointers and sizes only (no torch types).  All buffer arguments are
+ * DEVICE pointers (cudaMalloc / torch CUDA tensors) unless marked host; every
+ * call enqueues on `stream` (a cudaStream_t, NULL = legacy default stream)
+ * and returns without synchronising.  Host return values are synchronous
+ * argument/launch errors; data-dependent errors (corrupt stream, non-finite
+ * input, ...) land in the 4-word device `status` buffer, read after the
+ * caller synchronises:
+ *     status[0]  first non-finite sample index (UINT64_MAX if none)
+ *     status[1]  (block_index << 8) | apax_status of the first failing block
+ *                (UINT64_MAX if none; lowest block wins, like the serial walk)
+ *     status[2]  encode: total container bytes written
+ *     status[3]  reserved
+ * Status codes: include/apax_status.h (1:1 with the reference exceptions).
+ *
+ * Reference interfaces replaced (paths relative to the reference package):
+ *   apax_encode           <- encode_stream       pkg/src/apax/codec.py:258-285
+ *                            (+ encode_block     pkg/src/apax/codec.py:192-255)
+ *   apax_decode           <- decode_stream       pkg/src/apax/codec.py:308-329
+ *   apax_find_blocks      <- the block walk in   pkg/src/apax/codec.py:317-323
+ *   apax_max_encoded_bytes: output sizing (no reference counterpart; the
+ *                            reference returns fresh `bytes`)
+ *   apax_parse_file_header <- parse_file_header  pkg/src/apax/codec.py:288-305
+ *                            (host pointer, host-side)
+ */
+#ifndef APAX_B200_H
+#define APAX_B200_H
+
+#include <stdint.h>
+
+#include "apax_status.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* wire codes (reference dtypes.py:24-28, 55-58) */
+enum { APAX_I8 = 0, APAX_I16 = 1, APAX_I32 = 2, APAX_F32 = 3, APAX_F64 = 4 };
+enum { APAX_LOSSLESS = 0, APAX_FIXED_RATE = 1, APAX_FIXED_QUALITY = 2 };
+enum { APAX_POLICY_COLD = 0, APAX_POLICY_WARM_SELF = 1 };
+
+/* Library version string. */
+const char* apax_version(void);
+
+/* Human-readable text for a status code. */
+const char* apax_status_string(int code);
+
+/* Worst-case container size for n samples (28-byte file header included). */
+int64_t apax_max_encoded_bytes(int64_t n, int dtype, int block_size);
+
+/* Device workspace needed by apax_encode for these arguments. */
+int64_t apax_encode_workspace_bytes(int64_t n, int dtype, int mode, int block_size,
+                                    int64_t segment_blocks);
+
+/* Encode n samples of `dtype` at x (device) into a container at out (device).
+ *   segment_blocks <= 0 : whole-stream semantics, byte-identical to the
+ *                         reference encode_stream (LOSSLESS is still block
+ *                         parallel; FIXED_RATE / FIXED_QUALITY run as one
+ *                         serial chain).
+ *   segment_blocks  > 0 : container of independent segments of that many
+ *                         blocks, each a fresh CodecState with restart flag
+ *                         (decodable by the unmodified reference decoder).
+ *   policy              : APAX_POLICY_COLD (= reference encode_stream per
+ *                         segment) or APAX_POLICY_WARM_SELF (FIXED_RATE:
+ *                         attenuator preset from the segment's first block).
+ *   out_cap must be >= apax_max_encoded_bytes(n, dtype, block_size).
+ *   block_offsets (nullable, n_blocks + 1 int64): byte offset of every block
+ *   header, then the container length (side-band index for apax_decode).
+ *   trace (nullable, 10 doubles per block): att_db, a, code, fbe, selector,
+ *   cost0..2, block bytes, restart.
+ *   status: 4 uint64 (device).  ws/ws_bytes: device workspace. */
+int apax_encode(const void* x, int64_t n, int dtype, int mode, double target, int block_size,
+                int64_t segment_blocks, int policy, uint8_t* out, int64_t out_cap,
+                int64_t* block_offsets, uint64_t* status, double* trace, void* ws,
+                int64_t ws_bytes, void* stream);
+
+/* Device workspace needed by apax_decode (with offsets == NULL it includes
+ * room for the block walk's offset table). */
+int64_t apax_decode_workspace_bytes(int64_t n, int dtype, int block_size);
+
+/* Decode a container body.  blob (device) holds the full container of
+ * `nbytes` bytes (file header included; the caller parsed the header with
+ * apax_parse_file_header for n / dtype / block_size).  block_offsets
+ * (device, nullable): n_blocks + 1 offsets from apax_encode or
+ * apax_find_blocks; NULL runs the block walk first.  y (device) receives n
+ * samples of dtype. */
+int apax_decode(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, int block_size,
+                const int64_t* block_offsets, void* y, uint64_t* status, void* ws,
+                int64_t ws_bytes, void* stream);
+
+/* The reference's serial boundary walk on the device: offsets (device,
+ * n_blocks + 1) receives every block header offset and the end offset;
+ * errors go to status[1]. */
+int apax_find_blocks(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, int block_size,
+                     int64_t* offsets, uint64_t* status, void* stream);
+
+/* Host-side parse of the 28-byte file header (host pointer).  Returns an
+ * apax_status code; *detail carries the offending value for messages. */
+int apax_parse_file_header(const uint8_t* host_blob, int64_t len, int* dtype, int* mode,
+                           int* block_size, int64_t* count, double* target, int64_t* detail);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

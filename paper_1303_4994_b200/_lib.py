@@ -1,0 +1,60 @@
+"""Loader for the in-tree C-ABI extension libapax_b200.so (include/apax_b200.h).
+
+There is no CPU fallback: every codec entry point calls `lib()`, which raises
+ExtensionMissing when the .so is absent or fails to load, and DeviceMissing
+when no CUDA device is present.
+"""
+from __future__ import annotations
+
+import ctypes
+import pathlib
+
+_HERE = pathlib.Path(__file__).resolve().parent
+LIB_PATH = _HERE / "libapax_b200.so"
+
+
+class ExtensionMissing(ImportError):
+    """libapax_b200.so is not built (run __graft_entry__.build())."""
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise ExtensionMissing(f"{LIB_PATH} not found: build it with `python -c "
+                               f"'import __graft_entry__ as g; g.build()'`")
+    try:
+        L = ctypes.CDLL(str(LIB_PATH))
+    except OSError as exc:  # pragma: no cover
+        raise ExtensionMissing(f"cannot load {LIB_PATH}: {exc}") from exc
+    P, I64, I32, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
+    L.apax_version.restype = ctypes.c_char_p
+    L.apax_status_string.argtypes = [I32]
+    L.apax_status_string.restype = ctypes.c_char_p
+    L.apax_max_encoded_bytes.argtypes = [I64, I32, I32]
+    L.apax_max_encoded_bytes.restype = I64
+    L.apax_encode_workspace_bytes.argtypes = [I64, I32, I32, I32, I64]
+    L.apax_encode_workspace_bytes.restype = I64
+    L.apax_encode.argtypes = [P, I64, I32, I32, D, I32, I64, I32, P, I64, P, P, P, P, I64, P]
+    L.apax_encode.restype = I32
+    L.apax_decode_workspace_bytes.argtypes = [I64, I32, I32]
+    L.apax_decode_workspace_bytes.restype = I64
+    L.apax_decode.argtypes = [P, I64, I64, I32, I32, P, P, P, P, I64, P]
+    L.apax_decode.restype = I32
+    L.apax_find_blocks.argtypes = [P, I64, I64, I32, I32, P, P, P]
+    L.apax_find_blocks.restype = I32
+    L.apax_parse_file_header.argtypes = [P, I64, P, P, P, P, P, P]
+    L.apax_parse_file_header.restype = I32
+    _lib = L
+    return L
+
+
+EXPORTED_SYMBOLS = (
+    "apax_version", "apax_status_string", "apax_max_encoded_bytes",
+    "apax_encode_workspace_bytes", "apax_encode", "apax_decode_workspace_bytes",
+    "apax_decode", "apax_find_blocks", "apax_parse_file_header",
+)

@@ -1,0 +1,306 @@
+"""Drop-in encode/decode API over the B200 C-ABI extension.
+
+Reference interface mirrored (pkg/src/apax/codec.py):
+  encode_stream(samples, config) -> bytes      codec.py:258-285
+  decode_stream(data) -> np.ndarray            codec.py:308-329
+  parse_file_header(data) -> (config, count)   codec.py:288-305
+plus device-resident entry points for throughput work:
+  encode_device / decode_device and the reusable Encoder / Decoder plans,
+which keep inputs and outputs in HBM (torch CUDA tensors as buffers).
+
+All arithmetic runs in libapax_b200.so kernels; this module only validates,
+allocates device buffers, launches and maps status codes onto the
+reference's exception classes.  There is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import struct
+from dataclasses import dataclass
+from typing import Optional, Tuple
+
+import numpy as np
+
+from . import _lib
+from .dtypes import Dtype, Mode, StreamConfig
+from .errors import InvalidConfig, raise_status, status_exception
+
+MAGIC = b"APAX"
+VERSION = 1
+FILE_HEADER_FMT = "<4sBBBBIQd"
+FILE_HEADER_SIZE = struct.calcsize(FILE_HEADER_FMT)
+_U64_MAX = (1 << 64) - 1
+_POLICY = {"cold": 0, "warm_self": 1}
+
+
+def _torch():
+    import torch
+    return torch
+
+
+_TORCH_DT = {}
+
+
+def torch_dtype(dt: Dtype):
+    torch = _torch()
+    if not _TORCH_DT:
+        _TORCH_DT.update({Dtype.I8: torch.int8, Dtype.I16: torch.int16, Dtype.I32: torch.int32,
+                          Dtype.F32: torch.float32, Dtype.F64: torch.float64})
+    return _TORCH_DT[dt]
+
+
+def _require_cuda():
+    torch = _torch()
+    L = _lib.lib()  # raises ExtensionMissing loudly
+    if not torch.cuda.is_available():
+        raise _lib.ExtensionMissing("no CUDA device: the B200 codec has no CPU fallback")
+    return torch, L
+
+
+def _stream_ptr(stream) -> int:
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def _check_status(status_host: np.ndarray) -> None:
+    """Raise the reference exception for a device status buffer (4 x u64)."""
+    nonfinite = int(status_host[0])
+    if nonfinite != _U64_MAX:
+        raise status_exception(9, nonfinite)
+    key = int(status_host[1])
+    if key != _U64_MAX:
+        code = key & 0xFF
+        raise status_exception(code, key >> 8)
+
+
+# ---------------------------------------------------------------------------
+# file header (codec.py:288-305)
+# ---------------------------------------------------------------------------
+def parse_file_header(data) -> Tuple[StreamConfig, int]:
+    """Parse the container file header; returns (config, element_count)."""
+    L = _lib.lib()
+    buf = np.frombuffer(bytes(memoryview(data)[:FILE_HEADER_SIZE]), np.uint8)
+    dt, mode, bs = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    count, target, detail = ctypes.c_int64(), ctypes.c_double(), ctypes.c_int64()
+    st = L.apax_parse_file_header(buf.ctypes.data_as(ctypes.c_void_p), len(data),
+                                  ctypes.byref(dt), ctypes.byref(mode), ctypes.byref(bs),
+                                  ctypes.byref(count), ctypes.byref(target), ctypes.byref(detail))
+    raise_status(st, detail.value)
+    cfg = StreamConfig(dtype=Dtype.from_wire(dt.value), block_size=bs.value,
+                       mode=Mode(mode.value), target=target.value)
+    return cfg, int(count.value) & _U64_MAX
+
+
+def max_encoded_bytes(n: int, dtype: Dtype, block_size: int) -> int:
+    return int(_lib.lib().apax_max_encoded_bytes(int(n), dtype.wire_code, int(block_size)))
+
+
+# ---------------------------------------------------------------------------
+# reusable device plans
+# ---------------------------------------------------------------------------
+@dataclass
+class EncodedStream:
+    """A container resident in HBM."""
+
+    blob: "object"            # torch.uint8 CUDA tensor (capacity >= nbytes)
+    nbytes: int
+    block_offsets: "object"   # torch.int64 CUDA tensor, n_blocks + 1
+    config: StreamConfig
+    count: int
+
+    def to_bytes(self) -> bytes:
+        return bytes(self.blob[:self.nbytes].cpu().numpy().tobytes())
+
+
+class Encoder:
+    """Preallocated encode plan for (n, config) on one CUDA device.
+
+    encode(x) enqueues one kernel launch on the current stream and returns
+    immediately; `finish()` synchronises, checks the status buffer and
+    returns the container length.
+    """
+
+    def __init__(self, n: int, config: StreamConfig, device=None, with_offsets: bool = True,
+                 trace: bool = False):
+        torch, L = _require_cuda()
+        config.validate()
+        if n < 1:
+            raise InvalidConfig("element_count must be >= 1")
+        self.n, self.config = int(n), config
+        self.device = torch.device(device or "cuda")
+        dt, bs = config.dtype.wire_code, config.block_size
+        self.seg = int(config.segment_blocks or 0)
+        self.policy = _POLICY[config.segment_policy]
+        self.cap = int(L.apax_max_encoded_bytes(self.n, dt, bs))
+        wsb = int(L.apax_encode_workspace_bytes(self.n, dt, config.mode.value, bs, self.seg))
+        if wsb < 0:
+            raise InvalidConfig("invalid encode arguments")
+        self.n_blocks = (self.n + bs - 1) // bs
+        self.out = torch.empty(self.cap + 64, dtype=torch.uint8, device=self.device)
+        self.ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device=self.device)
+        self.status = torch.empty(4, dtype=torch.int64, device=self.device)
+        self.offsets = (torch.empty(self.n_blocks + 1, dtype=torch.int64, device=self.device)
+                        if with_offsets else None)
+        self.trace = (torch.zeros(self.n_blocks, 10, dtype=torch.float64, device=self.device)
+                      if trace else None)
+        self._lib = L
+
+    def encode(self, x, stream=None) -> None:
+        torch = _torch()
+        if x.device.type != "cuda" or x.dtype != torch_dtype(self.config.dtype) or x.numel() != self.n:
+            raise InvalidConfig("input must be a CUDA tensor of the config dtype and length n")
+        if not x.is_contiguous():
+            x = x.contiguous()
+        c = self.config
+        st = self._lib.apax_encode(
+            ctypes.c_void_p(x.data_ptr()), self.n, c.dtype.wire_code, c.mode.value,
+            float(c.target), c.block_size, self.seg, self.policy,
+            ctypes.c_void_p(self.out.data_ptr()), self.cap,
+            ctypes.c_void_p(self.offsets.data_ptr()) if self.offsets is not None else None,
+            ctypes.c_void_p(self.status.data_ptr()),
+            ctypes.c_void_p(self.trace.data_ptr()) if self.trace is not None else None,
+            ctypes.c_void_p(self.ws.data_ptr()), self.ws.numel(),
+            ctypes.c_void_p(_stream_ptr(stream)))
+        raise_status(st)
+
+    def finish(self, stream=None) -> int:
+        torch = _torch()
+        (stream or torch.cuda.current_stream()).synchronize()
+        s = self.status.cpu().numpy().view(np.uint64)
+        _check_status(s)
+        return int(s[2])
+
+    def result(self) -> EncodedStream:
+        nbytes = self.finish()
+        return EncodedStream(self.out, nbytes, self.offsets, self.config, self.n)
+
+
+class Decoder:
+    """Preallocated decode plan for containers of (n, dtype, block_size)."""
+
+    def __init__(self, n: int, dtype: Dtype, block_size: int, device=None):
+        torch, L = _require_cuda()
+        self.n, self.dtype, self.bs = int(n), dtype, int(block_size)
+        self.device = torch.device(device or "cuda")
+        wsb = int(L.apax_decode_workspace_bytes(self.n, dtype.wire_code, self.bs))
+        if wsb < 0:
+            raise InvalidConfig("invalid decode arguments")
+        self.ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device=self.device)
+        self.status = torch.empty(4, dtype=torch.int64, device=self.device)
+        self.y = torch.empty(max(self.n, 1), dtype=torch_dtype(dtype), device=self.device)
+        self._lib = L
+
+    def decode(self, blob, nbytes: int, offsets=None, stream=None, out=None) -> None:
+        y = self.y if out is None else out
+        st = self._lib.apax_decode(
+            ctypes.c_void_p(blob.data_ptr()), int(nbytes), self.n, self.dtype.wire_code, self.bs,
+            ctypes.c_void_p(offsets.data_ptr()) if offsets is not None else None,
+            ctypes.c_void_p(y.data_ptr()), ctypes.c_void_p(self.status.data_ptr()),
+            ctypes.c_void_p(self.ws.data_ptr()), self.ws.numel(),
+            ctypes.c_void_p(_stream_ptr(stream)))
+        raise_status(st)
+
+    def finish(self, stream=None):
+        torch = _torch()
+        (stream or torch.cuda.current_stream()).synchronize()
+        _check_status(self.status.cpu().numpy().view(np.uint64))
+        return self.y[:self.n]
+
+
+# ---------------------------------------------------------------------------
+# one-shot device API
+# ---------------------------------------------------------------------------
+def encode_device(x, config: StreamConfig, trace: bool = False) -> EncodedStream:
+    """Encode a CUDA tensor; the container stays in HBM."""
+    enc = Encoder(int(x.numel()), config, device=x.device, trace=trace)
+    enc.encode(x.reshape(-1))
+    res = enc.result()
+    res.trace = enc.trace  # type: ignore[attr-defined]
+    return res
+
+
+def _decodable_count(count: int, nbytes: int, cfg: StreamConfig) -> int:
+    """Samples worth decoding: every block costs >= header + 2 bytes, so a
+    count beyond what `nbytes` can hold is guaranteed to fail (truncated)
+    within the first `limit + 1` blocks -- the same block the reference's
+    serial walk stops at.  Caps the output allocation for crafted headers."""
+    hs = 6 if cfg.dtype.is_float else 4
+    limit_blocks = max(nbytes - FILE_HEADER_SIZE, 0) // (hs + 2) + 1
+    return min(count, limit_blocks * cfg.block_size)
+
+
+def decode_device(blob, nbytes: Optional[int] = None, offsets=None):
+    """Decode a container held in a CUDA uint8 tensor; returns a CUDA tensor."""
+    torch = _torch()
+    nbytes = int(blob.numel() if nbytes is None else nbytes)
+    head = bytes(blob[:min(nbytes, FILE_HEADER_SIZE)].cpu().numpy().tobytes())
+    if len(head) < FILE_HEADER_SIZE:
+        raise_status(13)
+    cfg, count = parse_file_header(head)
+    if count == 0:
+        return torch.empty(0, dtype=torch_dtype(cfg.dtype), device=blob.device)
+    n = _decodable_count(count, nbytes, cfg)
+    dec = Decoder(n, cfg.dtype, cfg.block_size, device=blob.device)
+    dec.decode(blob, nbytes, offsets if n == count else None)
+    return dec.finish()
+
+
+# ---------------------------------------------------------------------------
+# drop-in host API (bytes / ndarray)
+# ---------------------------------------------------------------------------
+def _as_config_dtype(x: np.ndarray, dt: Dtype) -> np.ndarray:
+    """Exact conversion of the caller's array to the config dtype.  The
+    reference converts to int64 / float64 (codec.py:266-272) and quantizes
+    those values; the kernels read the container dtype, so only
+    value-preserving conversions are accepted."""
+    if x.dtype == dt.np_dtype:
+        return np.ascontiguousarray(x)
+    if dt.is_float:
+        if x.dtype.kind not in "fiub":
+            raise InvalidConfig(f"cannot encode {x.dtype} samples as {dt.code}")
+        y = x.astype(dt.np_dtype)
+        xf = x.astype(np.float64)
+        same = (y.astype(np.float64) == xf) | (np.isnan(xf) & np.isnan(y.astype(np.float64)))
+        if not same.all():
+            raise InvalidConfig(f"{x.dtype} samples are not exactly representable as {dt.code}")
+        return np.ascontiguousarray(y)
+    if x.dtype.kind not in "iub" and not (x.dtype.kind == "f" and np.all(np.isfinite(x))
+                                           and np.all(x == np.round(x))):
+        raise InvalidConfig(f"cannot encode {x.dtype} samples as {dt.code}")
+    info = np.iinfo(dt.np_dtype)
+    if x.size and (x.min() < info.min or x.max() > info.max):
+        raise InvalidConfig(f"samples outside the {dt.code} range")
+    return np.ascontiguousarray(x.astype(dt.np_dtype))
+
+
+def encode_stream(samples, config: StreamConfig) -> bytes:
+    """Encode a full sample stream into a standalone container (GPU)."""
+    config.validate()
+    x = np.asarray(samples)
+    if x.ndim != 1:
+        x = x.reshape(-1)
+    if x.size < 1:
+        raise InvalidConfig("element_count must be >= 1")
+    torch, _ = _require_cuda()
+    x = _as_config_dtype(x, config.dtype)
+    xd = torch.from_numpy(x).to("cuda", non_blocking=False)
+    enc = Encoder(x.size, config, with_offsets=False)
+    enc.encode(xd)
+    nbytes = enc.finish()
+    return bytes(enc.out[:nbytes].cpu().numpy().tobytes())
+
+
+def decode_stream(data) -> np.ndarray:
+    """Decode a container back into a typed sample array (GPU)."""
+    cfg, count = parse_file_header(data)
+    if count == 0:
+        return np.empty(0, dtype=cfg.dtype.np_dtype)
+    torch, _ = _require_cuda()
+    raw = np.frombuffer(bytes(data), np.uint8)
+    blob = torch.empty(raw.size + 64, dtype=torch.uint8, device="cuda")
+    blob[:raw.size].copy_(torch.from_numpy(raw.copy()))
+    dec = Decoder(_decodable_count(count, raw.size, cfg), cfg.dtype, cfg.block_size)
+    dec.decode(blob, raw.size, None)
+    y = dec.finish()
+    return y.cpu().numpy()

@@ -1,0 +1,286 @@
+// apax_capi.cu -- extern "C" boundary of libapax_b200.so (include/apax_b200.h).
+//
+// Host side: argument validation, workspace carving, glibc-evaluated host
+// constants (the clamp bound 20*log10(2^-31) of reference dtypes.py:202 and
+// 10**(T/20) of codec.py:167 are computed here with the same libm the
+// reference's CPython calls), status-buffer reset, kernel launches.
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <cuda_runtime.h>
+
+#include "../../include/apax_b200.h"
+#include "apax_device.cuh"
+
+#include "apax_kernels.cuh"
+
+using namespace apax;
+
+namespace {
+
+constexpr long long kLosslessUnit = 4;  // blocks per CTA unit, lossless whole stream
+
+struct EncPlan {
+    long long n_blocks, unit_blocks, n_units;
+    int halo;
+    int stage_bytes;
+    size_t smem;
+    int grid;
+    long long slot_bytes;
+    long long ws_lookback, ws_ticket, ws_slots, ws_total;
+};
+
+bool valid_dtype(int dt) { return dt >= 0 && dt <= 4; }
+
+int env_int(const char* name, int def) {
+    const char* v = getenv(name);
+    if (!v || !*v) return def;
+    return atoi(v);
+}
+
+int plan_encode(long long n, int dt, int mode, int bs, long long seg, EncPlan* p) {
+    if (!valid_dtype(dt) || mode < 0 || mode > 2) return APAX_ERR_ARG;
+    if (bs < 64 || bs > 16384) return APAX_ERR_CFG_BLOCK_RANGE;
+    if (bs % 4) return APAX_ERR_CFG_BLOCK_MULT;
+    if (n < 1) return APAX_ERR_EMPTY;
+    p->n_blocks = (n + bs - 1) / bs;
+    if (seg > 0) {
+        p->unit_blocks = seg < p->n_blocks ? seg : p->n_blocks;
+        p->halo = 0;
+    } else if (mode == APAX_LOSSLESS) {
+        p->unit_blocks = kLosslessUnit;
+        p->halo = 1;
+    } else {
+        p->unit_blocks = p->n_blocks;
+        p->halo = 0;
+    }
+    p->n_units = (p->n_blocks + p->unit_blocks - 1) / p->unit_blocks;
+    const long long mbb = max_block_bytes(dt, bs);
+    long long want = env_int("APAX_STAGE_BYTES", 48 * 1024);
+    long long st = want > mbb + 64 ? want : mbb + 64;
+    st = (st + 15) & ~15LL;
+    p->stage_bytes = (int)st;
+    p->smem = encode_smem_bytes(dt, bs, p->stage_bytes);
+    int resident = encode_resident_ctas(dt, p->smem);
+    p->grid = (int)(p->n_units < resident ? p->n_units : resident);
+    if (p->grid < 1) p->grid = 1;
+    p->slot_bytes = (p->n_units > 1) ? ((p->unit_blocks * mbb + 64 + 255) & ~255LL) : 0;
+    p->ws_lookback = 0;
+    p->ws_ticket = (p->n_units * 8 + 255) & ~255LL;
+    p->ws_slots = p->ws_ticket + 256;
+    p->ws_total = p->ws_slots + (long long)p->grid * p->slot_bytes;
+    return APAX_OK;
+}
+
+struct DecPlan {
+    long long n_blocks;
+    int payload_cap;
+    size_t smem;
+    int grid;
+    long long ws_carry, ws_ticket, ws_offsets, ws_total;
+};
+
+int plan_decode(long long n, int dt, int bs, DecPlan* p) {
+    if (!valid_dtype(dt)) return APAX_ERR_ARG;
+    if (bs < 64 || bs > 16384) return APAX_ERR_CFG_BLOCK_RANGE;
+    if (bs % 4) return APAX_ERR_CFG_BLOCK_MULT;
+    if (n < 0) return APAX_ERR_ARG;
+    p->n_blocks = (n + bs - 1) / bs;
+    long long cap = max_block_bytes(dt, bs) + 64;
+    p->payload_cap = (int)((cap + 15) & ~15LL);
+    p->smem = decode_smem_bytes(dt, bs, p->payload_cap);
+    int resident = decode_resident_ctas(dt, p->smem);
+    long long g = p->n_blocks < resident ? p->n_blocks : resident;
+    p->grid = (int)(g < 1 ? 1 : g);
+    p->ws_carry = 0;
+    p->ws_ticket = (p->n_blocks * 64 + 255) & ~255LL;
+    p->ws_offsets = p->ws_ticket + 256;
+    p->ws_total = p->ws_offsets + (((p->n_blocks + 1) * 8 + 255) & ~255LL);
+    return APAX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* apax_version(void) { return "apax-b200 0.1.0 (sm_100a)"; }
+
+const char* apax_status_string(int code) {
+    switch (code) {
+        case APAX_OK: return "ok";
+        case APAX_ERR_JEE_TRUNCATED: return "JEE nibble stream exhausted";
+        case APAX_ERR_JEE_RESERVED: return "reserved JEE nibble 14";
+        case APAX_ERR_JEE_RANGE: return "decoded exponent outside [0, 34]";
+        case APAX_ERR_JEE_TOO_MANY: return "JEE token stream yields too many exponents";
+        case APAX_ERR_JEE_NO_ABS: return "JEE stream must start with an absolute exponent";
+        case APAX_ERR_SELECTOR: return "reserved selector value 3";
+        case APAX_ERR_NOT_APAX: return "bad magic";
+        case APAX_ERR_VERSION: return "container version";
+        case APAX_ERR_NONFINITE: return "non-finite value at index";
+        case APAX_ERR_INTERNAL: return "sample outside 34-bit range";
+        case APAX_ERR_MANTISSA_TRUNCATED: return "mantissa section truncated";
+        case APAX_ERR_BLOCK_HDR_TRUNCATED: return "block header truncated";
+        case APAX_ERR_FILE_HDR_TRUNCATED: return "file header truncated";
+        case APAX_ERR_DTYPE_WIRE: return "unknown dtype wire code";
+        case APAX_ERR_MODE_WIRE: return "unknown mode code";
+        case APAX_ERR_CFG_BLOCK_RANGE: return "block_size outside [64, 16384]";
+        case APAX_ERR_CFG_BLOCK_MULT: return "block_size not a multiple of 4";
+        case APAX_ERR_CFG_LOSSLESS_FLOAT: return "lossless unsupported for floats";
+        case APAX_ERR_CFG_FR_TARGET: return "FixedRate target must be > 0 bits/sample";
+        case APAX_ERR_EMPTY: return "element_count must be >= 1";
+        case APAX_ERR_OVERFLOW: return "cannot convert float infinity to integer";
+        case APAX_ERR_RANGE: return "attenuation outside [2^-31, 2^33)";
+        case APAX_ERR_INTERNAL_WIDTH: return "sample exceeds its group exponent width";
+        case APAX_ERR_NONFINITE_BLOCK: return "non-finite float input";
+        case APAX_ERR_CAPACITY: return "output buffer too small";
+        case APAX_ERR_ALLOC: return "allocation failure";
+        case APAX_ERR_ARG: return "invalid argument";
+        case APAX_ERR_CUDA: return "CUDA error";
+        case APAX_ERR_WORKSPACE: return "workspace too small";
+    }
+    return "unknown status";
+}
+
+int64_t apax_max_encoded_bytes(int64_t n, int dtype, int block_size) {
+    if (!valid_dtype(dtype) || block_size < 64 || block_size % 4 || n < 0) return -1;
+    int64_t nb = (n + block_size - 1) / block_size;
+    return kFileHeader + nb * max_block_bytes(dtype, block_size);
+}
+
+int64_t apax_encode_workspace_bytes(int64_t n, int dtype, int mode, int block_size,
+                                    int64_t segment_blocks) {
+    EncPlan p;
+    if (plan_encode(n, dtype, mode, block_size, segment_blocks, &p)) return -1;
+    return p.ws_total;
+}
+
+int apax_encode(const void* x, int64_t n, int dtype, int mode, double target, int block_size,
+                int64_t segment_blocks, int policy, uint8_t* out, int64_t out_cap,
+                int64_t* block_offsets, uint64_t* status, double* trace, void* ws,
+                int64_t ws_bytes, void* stream) {
+    EncPlan p;
+    int st = plan_encode(n, dtype, mode, block_size, segment_blocks, &p);
+    if (st) return st;
+    if (mode == APAX_LOSSLESS && dtype >= APAX_F32) return APAX_ERR_CFG_LOSSLESS_FLOAT;
+    if (mode == APAX_FIXED_RATE && !(target > 0)) return APAX_ERR_CFG_FR_TARGET;
+    if (!x || !out || !status || (p.ws_total > 0 && !ws)) return APAX_ERR_ARG;
+    if (out_cap < apax_max_encoded_bytes(n, dtype, block_size)) return APAX_ERR_CAPACITY;
+    if (ws_bytes < p.ws_total) return APAX_ERR_WORKSPACE;
+    cudaStream_t s = (cudaStream_t)stream;
+    uint8_t* w = (uint8_t*)ws;
+    if (cudaMemsetAsync(status, 0xFF, 4 * sizeof(uint64_t), s) != cudaSuccess) return APAX_ERR_CUDA;
+    if (cudaMemsetAsync(w, 0, (size_t)p.ws_slots, s) != cudaSuccess) return APAX_ERR_CUDA;
+    EncParams P;
+    memset(&P, 0, sizeof(P));
+    P.x = x;
+    P.n = n;
+    P.mode = mode;
+    P.bs = block_size;
+    P.target = target;
+    P.n_blocks = p.n_blocks;
+    P.unit_blocks = p.unit_blocks;
+    P.n_units = p.n_units;
+    P.halo = p.halo;
+    P.policy = policy;
+    P.out = out;
+    P.out_cap = out_cap;
+    P.block_offsets = (long long*)block_offsets;
+    P.status = (unsigned long long*)status;
+    P.lookback = (unsigned long long*)(w + p.ws_lookback);
+    P.ticket = (unsigned int*)(w + p.ws_ticket);
+    P.slots = w + p.ws_slots;
+    P.slot_bytes = p.slot_bytes;
+    P.stage_bytes = p.stage_bytes;
+    // glibc-evaluated constants (same libm as the reference's CPython)
+    P.att_lo = 20.0 * log10(ldexp(1.0, -31));
+    P.pow10_t20 = pow(10.0, target / 20.0);
+    P.sqrt12 = sqrt(12.0);
+    P.trace = trace;
+    return launch_encode(dtype, P, p.grid, p.smem, s);
+}
+
+int64_t apax_decode_workspace_bytes(int64_t n, int dtype, int block_size) {
+    DecPlan p;
+    if (plan_decode(n, dtype, block_size, &p)) return -1;
+    return p.ws_total;
+}
+
+int apax_find_blocks(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, int block_size,
+                     int64_t* offsets, uint64_t* status, void* stream) {
+    if (!valid_dtype(dtype) || block_size < 64 || block_size > 16384 || block_size % 4 || n < 0)
+        return APAX_ERR_ARG;
+    if (!blob || !offsets || !status) return APAX_ERR_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    long long nb = (n + block_size - 1) / block_size;
+    if (cudaMemsetAsync(status, 0xFF, 4 * sizeof(uint64_t), s) != cudaSuccess) return APAX_ERR_CUDA;
+    if (cudaMemsetAsync(offsets, 0xFF, (size_t)(nb + 1) * 8, s) != cudaSuccess) return APAX_ERR_CUDA;
+    if (nb == 0) return APAX_OK;
+    return launch_walk(blob, nbytes, n, block_size, dtype, nb, (long long*)offsets,
+                       (unsigned long long*)status, s);
+}
+
+int apax_decode(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, int block_size,
+                const int64_t* block_offsets, void* y, uint64_t* status, void* ws,
+                int64_t ws_bytes, void* stream) {
+    DecPlan p;
+    int st = plan_decode(n, dtype, block_size, &p);
+    if (st) return st;
+    if (!blob || !status || (n > 0 && !y)) return APAX_ERR_ARG;
+    if (ws_bytes < p.ws_total || !ws) return APAX_ERR_WORKSPACE;
+    cudaStream_t s = (cudaStream_t)stream;
+    uint8_t* w = (uint8_t*)ws;
+    if (cudaMemsetAsync(status, 0xFF, 4 * sizeof(uint64_t), s) != cudaSuccess) return APAX_ERR_CUDA;
+    if (p.n_blocks == 0) return APAX_OK;
+    if (cudaMemsetAsync(w, 0, (size_t)p.ws_offsets, s) != cudaSuccess) return APAX_ERR_CUDA;
+    const long long* offs = (const long long*)block_offsets;
+    if (!offs) {
+        long long* wo = (long long*)(w + p.ws_offsets);
+        if (cudaMemsetAsync(wo, 0xFF, (size_t)(p.n_blocks + 1) * 8, s) != cudaSuccess) return APAX_ERR_CUDA;
+        st = launch_walk(blob, nbytes, n, block_size, dtype, p.n_blocks, wo, (unsigned long long*)status, s);
+        if (st) return st;
+        offs = wo;
+    }
+    DecParams P;
+    memset(&P, 0, sizeof(P));
+    P.blob = blob;
+    P.nbytes = nbytes;
+    P.offsets = offs;
+    P.y = y;
+    P.n = n;
+    P.bs = block_size;
+    P.n_blocks = p.n_blocks;
+    P.status = (unsigned long long*)status;
+    P.carry = (unsigned long long*)(w + p.ws_carry);
+    P.ticket = (unsigned int*)(w + p.ws_ticket);
+    P.payload_cap = p.payload_cap;
+    return launch_decode(dtype, P, p.grid, p.smem, s);
+}
+
+int apax_parse_file_header(const uint8_t* d, int64_t len, int* dt, int* mode, int* bs,
+                           int64_t* count, double* target, int64_t* detail) {
+    // reference parse_file_header (codec.py:288-305) + StreamConfig.validate
+    *detail = -1;
+    if (len < kFileHeader) return APAX_ERR_FILE_HDR_TRUNCATED;
+    if (memcmp(d, "APAX", 4) != 0) return APAX_ERR_NOT_APAX;
+    if (d[4] != 1) { *detail = d[4]; return APAX_ERR_VERSION; }
+    if (d[5] > 4) { *detail = d[5]; return APAX_ERR_DTYPE_WIRE; }
+    if (d[6] > 2) { *detail = d[6]; return APAX_ERR_MODE_WIRE; }
+    uint32_t b32;
+    uint64_t c64;
+    memcpy(&b32, d + 8, 4);
+    memcpy(&c64, d + 12, 8);
+    memcpy(target, d + 20, 8);
+    *dt = d[5];
+    *mode = d[6];
+    *bs = (int)b32;
+    *count = (int64_t)c64;
+    *detail = (int64_t)b32;
+    if (!(64 <= b32 && b32 <= 16384)) return APAX_ERR_CFG_BLOCK_RANGE;
+    if (b32 % 4) return APAX_ERR_CFG_BLOCK_MULT;
+    if (*mode == APAX_LOSSLESS && *dt >= APAX_F32) return APAX_ERR_CFG_LOSSLESS_FLOAT;
+    if (*mode == APAX_FIXED_RATE && !(*target > 0)) return APAX_ERR_CFG_FR_TARGET;
+    *detail = -1;
+    return APAX_OK;
+}
+
+}  // extern "C"

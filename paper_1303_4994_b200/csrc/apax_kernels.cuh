@@ -1,0 +1,59 @@
+// apax_kernels.cuh -- parameter blocks and launch entry points shared by
+// the kernels (apax_encode.cu, apax_decode.cu) and the C ABI (apax_capi.cu).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace apax {
+
+struct EncParams {
+    const void* x;
+    long long n;
+    int mode;              // 0 lossless, 1 fixed-rate, 2 fixed-quality
+    int bs;
+    double target;
+    long long n_blocks;
+    long long unit_blocks;
+    long long n_units;
+    int halo;              // 1: lossless whole-stream units (no restart)
+    int policy;            // 0 cold, 1 warm_self (FR only)
+    uint8_t* out;
+    long long out_cap;
+    long long* block_offsets;     // nullable, n_blocks + 1
+    unsigned long long* status;   // 4 words
+    unsigned long long* lookback; // n_units
+    unsigned int* ticket;
+    uint8_t* slots;               // gridDim.x slots of slot_bytes
+    long long slot_bytes;
+    int stage_bytes;              // staging window (bytes, multiple of 16)
+    double att_lo;                // 20*log10(2^-31), glibc (dtypes.py:202)
+    double pow10_t20;             // 10**(T/20), glibc (codec.py:167)
+    double sqrt12;                // math.sqrt(12)
+    double* trace;                // nullable, 10 doubles per block
+};
+
+struct DecParams {
+    const uint8_t* blob;
+    long long nbytes;
+    const long long* offsets;   // n_blocks + 1 (entries < 0: block not present)
+    void* y;
+    long long n;
+    int bs;
+    long long n_blocks;
+    unsigned long long* status; // 4 words
+    unsigned long long* carry;  // 8 words per block
+    unsigned int* ticket;
+    int payload_cap;            // smem bytes reserved for one block payload
+};
+
+size_t encode_smem_bytes(int dt, int bs, int stage_bytes);
+int encode_resident_ctas(int dt, size_t smem);
+int launch_encode(int dt, const EncParams& P, int grid, size_t smem, cudaStream_t st);
+size_t decode_smem_bytes(int dt, int bs, int payload_cap);
+int decode_resident_ctas(int dt, size_t smem);
+int launch_decode(int dt, const DecParams& P, int grid, size_t smem, cudaStream_t st);
+int launch_walk(const uint8_t* blob, long long nbytes, long long n, int bs, int dt, long long n_blocks,
+                long long* offsets, unsigned long long* status, cudaStream_t st);
+
+}  // namespace apax

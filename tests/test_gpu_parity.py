@@ -1,0 +1,173 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the reference's
+frozen outputs (tests/golden, generated from the live reference) and the CPU
+oracle.  Bit-exact for every byte and sample."""
+import json
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, golden_containers, load_container
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+from paper_1303_4994_b200 import (Decoder, Dtype, Encoder, Mode, StreamConfig,  # noqa: E402
+                                  decode_device, decode_stream, encode_device, encode_stream)
+from paper_1303_4994_b200 import workloads as W  # noqa: E402
+
+DT = {"i8": Dtype.I8, "i16": Dtype.I16, "i32": Dtype.I32, "f32": Dtype.F32, "f64": Dtype.F64}
+POL = {0: "cold", 1: "warm_self"}
+
+
+def _cfg(m):
+    seg = m["segment_blocks"] or None
+    return StreamConfig(DT[m["dtype"]], m["block_size"], Mode(m["mode"]),
+                        float.fromhex(m["target_hex"]), segment_blocks=seg,
+                        segment_policy=POL[m["policy"]])
+
+
+@pytest.mark.parametrize("name", golden_containers())
+def test_golden_container_encode(name):
+    c = load_container(GOLDEN / "containers" / f"{name}.npz")
+    cfg = _cfg(c["meta"])
+    x = torch.from_numpy(np.ascontiguousarray(c["x"])).cuda()
+    res = encode_device(x, cfg)
+    got = res.to_bytes()
+    if got != c["blob"]:
+        n = min(len(got), len(c["blob"]))
+        first = next((i for i in range(n) if got[i] != c["blob"][i]), n)
+        pytest.fail(f"{name}: first differing byte {first} (len {len(got)} vs {len(c['blob'])})")
+    assert np.array_equal(res.block_offsets.cpu().numpy(), c["offsets"])
+
+
+@pytest.mark.parametrize("name", golden_containers())
+def test_golden_container_decode(name):
+    c = load_container(GOLDEN / "containers" / f"{name}.npz")
+    blob = torch.from_numpy(np.frombuffer(c["blob"], np.uint8).copy()).cuda()
+    # with the device block walk
+    y = decode_device(blob, len(c["blob"])).cpu().numpy()
+    assert y.dtype == c["y"].dtype and np.array_equal(y, c["y"])
+    # with the side-band offsets
+    offs = torch.from_numpy(c["offsets"]).cuda()
+    y2 = decode_device(blob, len(c["blob"]), offs).cpu().numpy()
+    assert np.array_equal(y2, c["y"])
+
+
+def test_drop_in_bytes_api():
+    c = load_container(GOLDEN / "containers" / "cfg1_i16_fr4.npz")
+    cfg = _cfg(c["meta"])
+    assert encode_stream(c["x"], cfg) == c["blob"]
+    y = decode_stream(c["blob"])
+    assert y.dtype == np.int16 and np.array_equal(y, c["y"])
+
+
+def test_reference_entropy_golden_vectors_through_encoder():
+    # A one-block LOSSLESS stream codes D0 = the samples themselves, so its
+    # payload must equal the reference's pack_block golden payload.
+    vecs = json.loads((GOLDEN / "entropy_vectors_ref.json").read_text())
+    extra = json.loads((GOLDEN / "entropy_vectors_extra.json").read_text())["vectors"]
+    n_checked = 0
+    for vec in vecs + extra:
+        v = np.asarray(vec["samples"], np.int64)
+        if v.size > 4096 or np.abs(v).max(initial=0) >= 2 ** 31 - 1:
+            continue
+        blob = encode_stream(v.astype(np.int32), StreamConfig(Dtype.I32, 4096))
+        assert blob[28 + 4:].hex() == vec["payload_hex"]
+        assert np.array_equal(decode_stream(blob), v.astype(np.int32))
+        n_checked += 1
+    assert n_checked >= 10
+
+
+def test_decode_errors_match_reference():
+    d = json.loads((GOLDEN / "decode_errors.json").read_text())
+    for case in d["cases"]:
+        blob = bytes.fromhex(case["blob_hex"])
+        if case["exc"] is None:
+            y = decode_stream(blob)
+            assert y.tobytes().hex() == case["y_hex"] and str(y.dtype) == case["y_dtype"]
+            continue
+        with pytest.raises(Exception) as ei:
+            decode_stream(blob)
+        assert type(ei.value).__name__ == case["exc"], case["name"]
+        assert str(ei.value) == case["msg"], case["name"]
+
+
+def test_encode_errors_match_reference():
+    for case in json.loads((GOLDEN / "encode_errors.json").read_text()):
+        if case["exc"] is None:
+            continue
+        dt = DT[case["dtype"]]
+        x = np.frombuffer(bytes.fromhex(case["x_hex"]), dt.np_dtype)
+        cfg = StreamConfig(dt, case["block_size"], Mode(case["mode"]), case["target"])
+        with pytest.raises(Exception) as ei:
+            encode_stream(x, cfg)
+        assert type(ei.value).__name__ == case["exc"], case["name"]
+        assert str(ei.value) == case["msg"], case["name"]
+
+
+def _random_case(rng, dt):
+    n = int(rng.integers(1, 20000))
+    if dt is Dtype.F32:
+        x = (np.cumsum(rng.standard_normal(n)) * 10.0 ** rng.uniform(-3, 3)).astype(np.float32)
+    elif dt is Dtype.F64:
+        x = np.cumsum(rng.standard_normal(n)) * 10.0 ** rng.uniform(-30, 30)
+    else:
+        info = np.iinfo(dt.np_dtype)
+        kind = rng.integers(0, 3)
+        if kind == 0:
+            x = rng.integers(info.min, info.max + 1, n)
+        else:
+            x = np.clip(np.cumsum(rng.integers(-50, 51, n)) * (1 + (kind == 2) * 1000),
+                        info.min, info.max)
+        x = x.astype(dt.np_dtype)
+    return x
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_configs_vs_oracle(seed):
+    rng = np.random.default_rng(1000 + seed)
+    for _ in range(8):
+        dt = [Dtype.I8, Dtype.I16, Dtype.I32, Dtype.F32, Dtype.F64][rng.integers(0, 5)]
+        modes = [Mode.FIXED_RATE, Mode.FIXED_QUALITY] + ([] if dt.is_float else [Mode.LOSSLESS])
+        mode = modes[rng.integers(0, len(modes))]
+        bs = int(rng.choice([64, 100, 128, 256, 500, 1024, 2048, 4096, 6000, 8192, 16384]))
+        target = float(rng.uniform(1, 12)) if mode is Mode.FIXED_RATE else float(rng.uniform(10, 100))
+        seg = int(rng.choice([0, 0, 1, 2, 3, 8]))
+        pol = "warm_self" if (mode is Mode.FIXED_RATE and rng.integers(0, 2)) else "cold"
+        x = _random_case(rng, dt)
+        cfg = StreamConfig(dt, bs, mode, target, segment_blocks=seg or None, segment_policy=pol)
+        ref, offs, _ = O.encode(x, dt.wire_code, mode.value, target, bs, segment_blocks=seg,
+                                policy=1 if pol == "warm_self" else 0, nthreads=4)
+        res = encode_device(torch.from_numpy(x).cuda(), cfg)
+        got = res.to_bytes()
+        assert got == ref, (dt, mode, bs, target, seg, pol, x.size)
+        y = decode_device(res.blob, res.nbytes).cpu().numpy()
+        assert np.array_equal(y, O.decode(ref)), (dt, mode, bs, seg)
+
+
+def test_bench_size_cfg2_segmented_vs_oracle():
+    """Full BASELINE cfg2 size (2^26 f32, FQ at the profiler target, P=16):
+    byte-exact container and bit-exact decode against the oracle."""
+    x = W.cfg2_ar2_f32()
+    cfg = StreamConfig(Dtype.F32, 4096, Mode.FIXED_QUALITY, W.CFG2_TARGET_DB, segment_blocks=16)
+    enc = Encoder(x.size, cfg)
+    enc.encode(torch.from_numpy(x).cuda())
+    res = enc.result()
+    ref, offs, _ = O.encode(x, 3, 2, W.CFG2_TARGET_DB, 4096, segment_blocks=16, nthreads=0)
+    assert res.to_bytes() == ref
+    assert np.array_equal(res.block_offsets.cpu().numpy(), offs)
+    dec = Decoder(x.size, Dtype.F32, 4096)
+    dec.decode(res.blob, res.nbytes, res.block_offsets)
+    y = dec.finish().cpu().numpy()
+    assert np.array_equal(y, O.decode(ref, offs, nthreads=0))
+
+
+def test_bench_size_cfg1_lossless_round_trip():
+    x = W.cfg1_sines_i16()
+    res = encode_device(torch.from_numpy(x).cuda(), StreamConfig(Dtype.I16, 4096))
+    ref, offs, _ = O.encode(x, 1, 0, 0.0, 4096, nthreads=0)
+    assert res.to_bytes() == ref
+    y = decode_device(res.blob, res.nbytes, res.block_offsets).cpu().numpy()
+    assert np.array_equal(y, x)
