@@ -24,6 +24,7 @@ struct EncPlan {
     long long n_blocks, unit_blocks, n_units;
     int halo;
     int stage_bytes;
+    int x_in_smem;
     size_t smem;
     int grid;
     long long slot_bytes;
@@ -60,7 +61,17 @@ int plan_encode(long long n, int dt, int mode, int bs, long long seg, EncPlan* p
     long long st = want > mbb + 64 ? want : mbb + 64;
     st = (st + 15) & ~15LL;
     p->stage_bytes = (int)st;
-    p->smem = encode_smem_bytes(dt, bs, p->stage_bytes);
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess ||
+        optin <= 0)
+        optin = 227 * 1024;
+    p->x_in_smem = 1;
+    p->smem = encode_smem_bytes(dt, bs, p->stage_bytes, 1);
+    if (p->smem > (size_t)optin) {
+        p->x_in_smem = 0;
+        p->smem = encode_smem_bytes(dt, bs, p->stage_bytes, 0);
+    }
     int resident = encode_resident_ctas(dt, p->smem);
     p->grid = (int)(p->n_units < resident ? p->n_units : resident);
     if (p->grid < 1) p->grid = 1;
@@ -93,7 +104,7 @@ int plan_decode(long long n, int dt, int bs, DecPlan* p) {
     long long g = p->n_blocks < resident ? p->n_blocks : resident;
     p->grid = (int)(g < 1 ? 1 : g);
     p->ws_carry = 0;
-    p->ws_ticket = (p->n_blocks * 64 + 255) & ~255LL;
+    p->ws_ticket = (p->n_blocks * 128 + 255) & ~255LL;
     p->ws_offsets = p->ws_ticket + 256;
     p->ws_total = p->ws_offsets + (((p->n_blocks + 1) * 8 + 255) & ~255LL);
     return APAX_OK;
@@ -191,6 +202,7 @@ int apax_encode(const void* x, int64_t n, int dtype, int mode, double target, in
     P.slots = w + p.ws_slots;
     P.slot_bytes = p.slot_bytes;
     P.stage_bytes = p.stage_bytes;
+    P.x_in_smem = p.x_in_smem;
     // glibc-evaluated constants (same libm as the reference's CPython)
     P.att_lo = 20.0 * log10(ldexp(1.0, -31));
     P.pow10_t20 = pow(10.0, target / 20.0);

@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(kNT) decode_kernel(DecParams P) {
         const int n = (int)((P.n - start) < bs ? (P.n - start) : bs);
         const int G = (n + 3) >> 2;
         const int np = 4 * G;
-        unsigned long long* cw = P.carry + 8 * b;
+        unsigned long long* cw = P.carry + 16 * b;  // [0] flag, [1..6] map, [8..9] value
         const long long boff = P.offsets[b];
         const long long bend = P.offsets[b + 1];
 
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(kNT) decode_kernel(DecParams P) {
             if (tid == 0) {
                 if (err > 0) report_error(P.status, b, err);
                 // publish a dummy concrete history so successors never stall
-                cw[1] = 0; cw[2] = 0;
+                cw[8] = 0; cw[9] = 0;
                 __threadfence();
                 st_release(&cw[0], kFlagInc);
             }
@@ -397,16 +397,16 @@ __global__ void __launch_bounds__(kNT) decode_kernel(DecParams P) {
                 Aff acc = {1, 0, 0, 1, 0, 0};
                 long long k = b - 1;
                 for (;;) {
-                    unsigned long long fl = ld_acquire(&P.carry[8 * k]);
+                    const unsigned long long* ck = P.carry + 16 * k;
+                    unsigned long long fl = ld_acquire(&ck[0]);
                     if (fl == kFlagInc) {
-                        unsigned long long p1 = P.carry[8 * k + 1], p2 = P.carry[8 * k + 2];
+                        unsigned long long p1 = ck[8], p2 = ck[9];
                         in1 = acc.m11 * p1 + acc.m12 * p2 + acc.c1;
                         in2 = acc.m21 * p1 + acc.m22 * p2 + acc.c2;
                         break;
                     }
                     if (fl == kFlagAgg) {
-                        Aff Mk = {P.carry[8 * k + 1], P.carry[8 * k + 2], P.carry[8 * k + 3],
-                                  P.carry[8 * k + 4], P.carry[8 * k + 5], P.carry[8 * k + 6]};
+                        Aff Mk = {ck[1], ck[2], ck[3], ck[4], ck[5], ck[6]};
                         acc = aff_compose(acc, Mk);
                         k--;
                         continue;
@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(kNT) decode_kernel(DecParams P) {
             // concrete output history of this block
             unsigned long long o1 = M.m11 * in1 + M.m12 * in2 + M.c1;
             unsigned long long o2 = M.m21 * in1 + M.m22 * in2 + M.c2;
-            cw[1] = o1; cw[2] = o2;
+            cw[8] = o1; cw[9] = o2;
             __threadfence();
             st_release(&cw[0], kFlagInc);
             S->p1 = (long long)in1;

@@ -153,13 +153,18 @@ __device__ double block_pairwise(F term, int n, EncState* S, LeafList* LL) {
         const int groups = L < 32 ? L : 32;          // active 8-lane groups
         const int lpg = L / groups;                  // leaves per group (1,2,4)
         double gsum = 0.0;
-        if (grp < groups) {
+        // warp-uniform: every lane of a warp holding an active group takes
+        // part in the shuffles (inactive groups shuffle zeros among themselves)
+        if (warp * 4 < groups) {
             double ls[4];
             for (int q = 0; q < lpg; q++) {
-                int base = (grp * lpg + q) << 7;
-                double r = term(base + j);
+                double r = 0.0;
+                if (grp < groups) {
+                    int base = (grp * lpg + q) << 7;
+                    r = term(base + j);
 #pragma unroll 4
-                for (int i = 1; i < 16; i++) r += term(base + 8 * i + j);
+                    for (int i = 1; i < 16; i++) r += term(base + 8 * i + j);
+                }
                 r += __shfl_xor_sync(0xffffffffu, r, 1);
                 r += __shfl_xor_sync(0xffffffffu, r, 2);
                 r += __shfl_xor_sync(0xffffffffu, r, 4);
@@ -350,8 +355,9 @@ __global__ void __launch_bounds__(kNT) encode_kernel(EncParams P) {
     size_t off = (sizeof(EncState) + 15) & ~(size_t)15;
     LeafList* LL = (LeafList*)(smem + off);
     off += (sizeof(LeafList) + 15) & ~(size_t)15;
-    T* xb = (T*)(smem + off);
-    off += ((size_t)bs * sizeof(T) + 15) & ~(size_t)15;
+    T* const xs_smem = (T*)(smem + off);
+    if (P.x_in_smem) off += ((size_t)bs * sizeof(T) + 15) & ~(size_t)15;
+    const T* xb = xs_smem;  // current block's samples (smem copy or global)
     Q* qb = (Q*)(smem + off);
     off += ((size_t)(bs + 4) * sizeof(Q) + 15) & ~(size_t)15;
     uint8_t* es = (uint8_t*)(smem + off);       // 3 x Gfull exponents
@@ -384,16 +390,22 @@ __global__ void __launch_bounds__(kNT) encode_kernel(EncParams P) {
         //            or halo history set by the caller
         auto load_block = [&](long long b, int n) {
             const T* src = (const T*)P.x + b * (long long)bs;
+            if (!P.x_in_smem) {  // large blocks: read the samples from global / L2
+                xb = src;
+                return;
+            }
+            T* dst = xs_smem;
+            xb = dst;
             // 16-byte vector loads when aligned
             const int bytes = n * (int)sizeof(T);
             if ((((uintptr_t)src) & 15) == 0) {
                 const int nv = bytes >> 4;
                 const uint4* s4 = (const uint4*)src;
-                uint4* d4 = (uint4*)xb;
+                uint4* d4 = (uint4*)dst;
                 for (int i = tid; i < nv; i += kNT) d4[i] = __ldcs(s4 + i);
-                for (int i = (nv << 4) / (int)sizeof(T) + tid; i < n; i += kNT) xb[i] = src[i];
+                for (int i = (nv << 4) / (int)sizeof(T) + tid; i < n; i += kNT) dst[i] = src[i];
             } else {
-                for (int i = tid; i < n; i += kNT) xb[i] = src[i];
+                for (int i = tid; i < n; i += kNT) dst[i] = src[i];
             }
         };
 
@@ -979,11 +991,11 @@ __global__ void __launch_bounds__(kNT) encode_kernel(EncParams P) {
 // ---------------------------------------------------------------------------
 // host-side launch helper
 // ---------------------------------------------------------------------------
-size_t encode_smem_bytes(int dt, int bs, int stage_bytes) {
+size_t encode_smem_bytes(int dt, int bs, int stage_bytes, int x_in_smem) {
     auto al = [](size_t v) { return (v + 15) & ~(size_t)15; };
     size_t w = (size_t)dt_width(dt);
     size_t qw = dt == 4 ? 8 : 4;
-    return al(sizeof(EncState)) + al(sizeof(LeafList)) + al((size_t)bs * w) +
+    return al(sizeof(EncState)) + al(sizeof(LeafList)) + (x_in_smem ? al((size_t)bs * w) : 0) +
            al((size_t)(bs + 4) * qw) + al((size_t)3 * (bs / 4) + 16) + (size_t)stage_bytes + 16;
 }
 

@@ -27,6 +27,7 @@ struct EncParams {
     uint8_t* slots;               // gridDim.x slots of slot_bytes
     long long slot_bytes;
     int stage_bytes;              // staging window (bytes, multiple of 16)
+    int x_in_smem;                // 1: stage each block's samples in smem
     double att_lo;                // 20*log10(2^-31), glibc (dtypes.py:202)
     double pow10_t20;             // 10**(T/20), glibc (codec.py:167)
     double sqrt12;                // math.sqrt(12)
@@ -47,7 +48,7 @@ struct DecParams {
     int payload_cap;            // smem bytes reserved for one block payload
 };
 
-size_t encode_smem_bytes(int dt, int bs, int stage_bytes);
+size_t encode_smem_bytes(int dt, int bs, int stage_bytes, int x_in_smem);
 int encode_resident_ctas(int dt, size_t smem);
 int launch_encode(int dt, const EncParams& P, int grid, size_t smem, cudaStream_t st);
 size_t decode_smem_bytes(int dt, int bs, int payload_cap);
