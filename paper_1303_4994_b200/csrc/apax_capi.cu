@@ -25,6 +25,7 @@ struct EncPlan {
     int halo;
     int stage_bytes;
     int x_in_smem;
+    int v2;
     size_t smem;
     int grid;
     long long slot_bytes;
@@ -57,23 +58,36 @@ int plan_encode(long long n, int dt, int mode, int bs, long long seg, EncPlan* p
     }
     p->n_units = (p->n_blocks + p->unit_blocks - 1) / p->unit_blocks;
     const long long mbb = max_block_bytes(dt, bs);
-    long long want = env_int("APAX_STAGE_BYTES", 48 * 1024);
-    long long st = want > mbb + 64 ? want : mbb + 64;
-    st = (st + 15) & ~15LL;
-    p->stage_bytes = (int)st;
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess ||
         optin <= 0)
         optin = 227 * 1024;
-    p->x_in_smem = 1;
-    p->smem = encode_smem_bytes(dt, bs, p->stage_bytes, 1);
-    if (p->smem > (size_t)optin) {
-        p->x_in_smem = 0;
-        p->smem = encode_smem_bytes(dt, bs, p->stage_bytes, 0);
+    p->v2 = encode_v2_supported(bs) && env_int("APAX_FORCE_V1", 0) == 0;
+    if (p->v2) {
+        // v2: the window holds one block plus a <16-byte tail
+        p->stage_bytes = (int)((mbb + 64 + 15) & ~15LL);
+        p->x_in_smem = 1;
+        p->smem = encode_v2_smem_bytes(dt, mode, p->stage_bytes);
+        if (p->smem > (size_t)optin) p->v2 = 0;
     }
-    int resident = encode_resident_ctas(dt, p->smem);
-    p->grid = (int)(p->n_units < resident ? p->n_units : resident);
+    if (p->v2) {
+        int resident = encode_v2_resident_ctas(dt, p->smem);
+        p->grid = (int)(p->n_units < resident ? p->n_units : resident);
+    } else {
+        long long want = env_int("APAX_STAGE_BYTES", 48 * 1024);
+        long long st = want > mbb + 64 ? want : mbb + 64;
+        st = (st + 15) & ~15LL;
+        p->stage_bytes = (int)st;
+        p->x_in_smem = 1;
+        p->smem = encode_smem_bytes(dt, bs, p->stage_bytes, 1);
+        if (p->smem > (size_t)optin) {
+            p->x_in_smem = 0;
+            p->smem = encode_smem_bytes(dt, bs, p->stage_bytes, 0);
+        }
+        int resident = encode_resident_ctas(dt, p->smem);
+        p->grid = (int)(p->n_units < resident ? p->n_units : resident);
+    }
     if (p->grid < 1) p->grid = 1;
     p->slot_bytes = (p->n_units > 1) ? ((p->unit_blocks * mbb + 64 + 255) & ~255LL) : 0;
     p->ws_lookback = 0;
@@ -208,6 +222,7 @@ int apax_encode(const void* x, int64_t n, int dtype, int mode, double target, in
     P.pow10_t20 = pow(10.0, target / 20.0);
     P.sqrt12 = sqrt(12.0);
     P.trace = trace;
+    if (p.v2) return launch_encode_v2(dtype, P, p.grid, p.smem, s);
     return launch_encode(dtype, P, p.grid, p.smem, s);
 }
 

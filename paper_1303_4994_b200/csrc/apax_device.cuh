@@ -168,10 +168,78 @@ constexpr unsigned long long kFlagAgg = 1ULL << 62;
 constexpr unsigned long long kFlagInc = 2ULL << 62;
 constexpr unsigned long long kValMask = (1ULL << 62) - 1;
 
+// ---------------------------------------------------------------------------
+// Warp-parallel decoupled look-back over unit byte lengths (call with the
+// whole warp).  Publishes AGG(len), sums predecessors 32 at a time until the
+// nearest INC, publishes INC(prefix + len) and returns the exclusive prefix.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ long long warp_lookback(unsigned long long* lb, long long u, long long len) {
+    const int lane = threadIdx.x & 31;
+    if (u == 0) {
+        if (lane == 0) st_release(&lb[0], kFlagInc | (unsigned long long)len);
+        return 0;
+    }
+    if (lane == 0) st_release(&lb[u], kFlagAgg | (unsigned long long)len);
+    long long prefix = 0;
+    long long k = u - 1;
+    for (;;) {
+        const long long idx = k - lane;
+        unsigned long long v = (idx >= 0) ? ld_acquire(&lb[idx]) : kFlagInc;
+        const unsigned long long fl = v & ~kValMask;
+        const unsigned inc = __ballot_sync(0xffffffffu, fl == kFlagInc);
+        const unsigned nrd = __ballot_sync(0xffffffffu, fl == 0);
+        const int first_inc = inc ? __ffs(inc) - 1 : 32;
+        const unsigned need = first_inc >= 31 ? 0xffffffffu : ((2u << first_inc) - 1u);
+        if (nrd & need) {       // a predecessor before the nearest INC is not ready
+            __nanosleep(32);
+            continue;
+        }
+        unsigned long long part = (lane <= first_inc) ? (v & kValMask) : 0ULL;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        prefix += (long long)part;
+        if (inc) break;
+        k -= 32;
+    }
+    if (lane == 0) st_release(&lb[u], kFlagInc | (unsigned long long)(prefix + len));
+    return prefix;
+}
+
 // status words: [0] min non-finite index, [1] min (block << 8 | code) error
 // key, [2] total output bytes / misc, [3] error detail
 __device__ __forceinline__ void report_error(unsigned long long* status, long long block, int code) {
     atomicMin(&status[1], ((unsigned long long)block << 8) | (unsigned)code);
+}
+
+// ---------------------------------------------------------------------------
+// byte copies from a 4-aligned word source (smem or global) to an arbitrary
+// global byte range; bytes outside [dst, dst+len) are never written.
+// ---------------------------------------------------------------------------
+template <bool SRC_SHARED>
+__device__ void copy_out(uint8_t* dst, const uint32_t* src, long long len) {
+    if (len <= 0) return;
+    const int tid = threadIdx.x;
+    uintptr_t d0 = (uintptr_t)dst;
+    long long head = (long long)((16 - (d0 & 15)) & 15);
+    if (head > len) head = len;
+    const uint8_t* sb = (const uint8_t*)src;
+    for (long long i = tid; i < head; i += blockDim.x) dst[i] = sb[i];
+    long long body = (len - head) & ~15LL;
+    long long nchunks = body >> 4;
+    uint4* d16 = (uint4*)(dst + head);
+    const uint32_t sh = (uint32_t)(head & 3) * 8;
+    const long long wbase = head >> 2;
+    for (long long c = tid; c < nchunks; c += blockDim.x) {
+        long long w = wbase + 4 * c;
+        uint32_t a0 = src[w], a1 = src[w + 1], a2 = src[w + 2], a3 = src[w + 3], a4 = src[w + 4];
+        uint4 v;
+        v.x = __funnelshift_r(a0, a1, sh);
+        v.y = __funnelshift_r(a1, a2, sh);
+        v.z = __funnelshift_r(a2, a3, sh);
+        v.w = __funnelshift_r(a3, a4, sh);
+        d16[c] = v;
+    }
+    for (long long i = head + body + tid; i < len; i += blockDim.x) dst[i] = sb[i];
 }
 
 }  // namespace apax

@@ -306,37 +306,6 @@ __device__ __forceinline__ void cta_scan_jee(uint32_t f, unsigned bits, uint32_t
 }
 
 // ---------------------------------------------------------------------------
-// byte copies from a 4-aligned word source (smem or global) to an arbitrary
-// global byte range; bytes outside [dst, dst+len) are never written.
-// ---------------------------------------------------------------------------
-template <bool SRC_SHARED>
-__device__ void copy_out(uint8_t* dst, const uint32_t* src, long long len) {
-    if (len <= 0) return;
-    const int tid = threadIdx.x;
-    uintptr_t d0 = (uintptr_t)dst;
-    long long head = (long long)((16 - (d0 & 15)) & 15);
-    if (head > len) head = len;
-    const uint8_t* sb = (const uint8_t*)src;
-    for (long long i = tid; i < head; i += kNT) dst[i] = sb[i];
-    long long body = (len - head) & ~15LL;
-    long long nchunks = body >> 4;
-    uint4* d16 = (uint4*)(dst + head);
-    const uint32_t sh = (uint32_t)(head & 3) * 8;
-    const long long wbase = head >> 2;
-    for (long long c = tid; c < nchunks; c += kNT) {
-        long long w = wbase + 4 * c;
-        uint32_t a0 = src[w], a1 = src[w + 1], a2 = src[w + 2], a3 = src[w + 3], a4 = src[w + 4];
-        uint4 v;
-        v.x = __funnelshift_r(a0, a1, sh);
-        v.y = __funnelshift_r(a1, a2, sh);
-        v.z = __funnelshift_r(a2, a3, sh);
-        v.w = __funnelshift_r(a3, a4, sh);
-        d16[c] = v;
-    }
-    for (long long i = head + body + tid; i < len; i += kNT) dst[i] = sb[i];
-}
-
-// ---------------------------------------------------------------------------
 // the encoder kernel
 // ---------------------------------------------------------------------------
 template <int DT>
@@ -932,27 +901,15 @@ __global__ void __launch_bounds__(kNT) encode_kernel(EncParams P) {
         }
 
         // ---------------- placement: decoupled look-back ----------------
-        if (tid == 0) {
+        if (tid < 32) {
             const long long L = S->unit_len;
-            long long prefix = 0;
-            if (u == 0) {
-                st_release(&P.lookback[0], kFlagInc | (unsigned long long)L);
-            } else {
-                st_release(&P.lookback[u], kFlagAgg | (unsigned long long)L);
-                long long k = u - 1;
-                while (k >= 0) {
-                    unsigned long long v = ld_acquire(&P.lookback[k]);
-                    unsigned long long fl = v & ~kValMask;
-                    if (fl == kFlagInc) { prefix += (long long)(v & kValMask); break; }
-                    if (fl == kFlagAgg) { prefix += (long long)(v & kValMask); k--; continue; }
-                    __nanosleep(64);
+            const long long prefix = warp_lookback(P.lookback, u, L);
+            if (tid == 0) {
+                S->prefix = prefix;
+                if (u == P.n_units - 1) {
+                    P.status[2] = (unsigned long long)(kFileHeader + prefix + L);
+                    if (P.block_offsets) P.block_offsets[P.n_blocks] = kFileHeader + prefix + L;
                 }
-                st_release(&P.lookback[u], kFlagInc | (unsigned long long)(prefix + L));
-            }
-            S->prefix = prefix;
-            if (u == P.n_units - 1) {
-                P.status[2] = (unsigned long long)(kFileHeader + prefix + L);
-                if (P.block_offsets) P.block_offsets[P.n_blocks] = kFileHeader + prefix + L;
             }
         }
         __syncthreads();

@@ -1,0 +1,1104 @@
+// apax_encode_v2.cu -- instruction-lean B200 encoder for block sizes
+// 128..4096 (powers of two): the hot path of every BASELINE config.
+//
+// Same contract and byte-exact output as apax_encode.cu (reference
+// encode_stream, pkg/src/apax/codec.py:258-285 / encode_block :192-255); the
+// v1 kernel remains the general path (any block size 64..16384).
+//
+// Per CTA (256 threads, persistent, ticketed units of consecutive blocks):
+//   * TMA bulk copies (cp.async.bulk + mbarrier) double-buffer the next
+//     block's samples into shared memory while the current one is coded;
+//   * phase A  block peak (|x| bit-max) and, for fixed quality, numpy's
+//              pairwise sum of x^2 (8 lanes per 128-sample leaf, exactly the
+//              association tree of np.add.reduce; codec.py:159,248);
+//   * scalar   thread 0: gain / scale code / float block exponent.  max|q|
+//              equals rint(peak*s) exactly, so the overflow-retry loop of
+//              codec.py:126-131 runs on scalars only;
+//   * phase B  fixed quality: quantize + dequantize (Markstein quotient with a
+//              per-block reciprocal, bit-identical to IEEE division) + the
+//              pairwise residual power; other modes quantize in phase C;
+//   * phase C  16 contiguous samples per thread in registers: d1/d2
+//              (transform.py:86-91), group widths via bit_length((v<<1)^v)
+//              OR-accumulated per group (= entropy.py:38-55), the three costs
+//              (transform.py:94-97) and the ordered sign-change monitor
+//              (transform.py:67-83);
+//   * phase D  JEE greedy pairing as a CTA scan of 2-state transfer
+//              functions (entropy.py:63-88) fused with the mantissa bit
+//              offsets; MSB-first packing into a shared-memory window
+//              (entropy.py:194-240); whole 16-byte chunks are flushed after
+//              every block, so the window only holds one block plus a tail;
+//   * placement  decoupled look-back over unit byte lengths, then the unit's
+//              bytes move from its scratch slot to their final offset.
+// Blocks whose streams need 64-bit differences (max|q| >= 2^29) take a
+// recomputing 64-bit path; f64 blocks whose quantized samples leave int32
+// (|x| >= ~2^188) are handled there too.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "apax_device.cuh"
+#include "apax_kernels.cuh"
+
+namespace apax {
+namespace v2 {
+
+constexpr int NT = 256;
+constexpr int NW = NT / 32;
+constexpr int SPT = 16;          // samples per thread in the contiguous mapping
+constexpr int MAXBS = 4096;
+constexpr int LEAF_STRIDE = 136; // padded 128-sample leaf in qbuf (bank spread)
+
+struct St {
+    // CodecState (codec.py:66-82)
+    double att;
+    long long p1, p2;
+    long long pc[3];
+    long long emitted;
+    int has_pc, initialized;
+    // per-block broadcast
+    double a, s, rs, aq, ra, px, pd, peak_d;
+    long long qpk;
+    int code, fbe, sel, wide, zero, gate, bad, nonfinite;
+    long long sum_e[3];
+    long long blen, jee_nib, bits;
+    long long last1, last2;     // q[np-1], q[np-2] of the block
+    // window / slot
+    long long win_base;
+    int tail_len;
+    uint32_t tail[4];
+    long long unit_len, unit, prefix;
+    int direct;
+    // reductions
+    double pxw[NW], pdw[NW];
+    unsigned long long pkw[NW];
+    int sew[3][NW];
+    int monc[NW], monf[NW];
+    unsigned emaxw[NW];
+    uint32_t scf[NW], scb[NW];
+    uint32_t pre_f[NW], pre_b[NW];
+    unsigned long long mbar[2];
+};
+
+// ---------------------------------------------------------------------------
+// TMA bulk copy + mbarrier
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t sa(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(sa(b)) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t bytes,
+                                         unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 :: "r"(sa(bar)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(sa(dst)), "l"(src), "r"(bytes), "r"(sa(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phase) {
+    uint32_t ok = 0;
+    while (!ok) {
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(ok) : "r"(sa(bar)), "r"(phase) : "memory");
+    }
+}
+
+// ---------------------------------------------------------------------------
+// small helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int bitlen32(unsigned v) { return 32 - __clz((int)v); }
+__device__ __forceinline__ int bitlen64(unsigned long long v) { return 64 - __clzll((long long)v); }
+__device__ __forceinline__ unsigned wbits32(int v) { return (unsigned)((v << 1) ^ v); }
+__device__ __forceinline__ unsigned long long wbits64(long long v) {
+    return (unsigned long long)((v << 1) ^ v);
+}
+
+__device__ __forceinline__ double clamp_att(double att, double lo) {
+    double m = (lo > att) ? lo : att;
+    return (0.0 < m) ? 0.0 : m;
+}
+__device__ __forceinline__ double att_to_a(double att) {
+    double p = pow(10.0, att / 20.0);
+    double m = (4.656612873077393e-10 > p) ? 4.656612873077393e-10 : p;
+    return (1.0 < m) ? 1.0 : m;
+}
+__device__ __forceinline__ double clamp_step(double d) {
+    double m = (d < 6.0) ? d : 6.0;
+    return (m > -6.0) ? m : -6.0;
+}
+
+// JEE transfer functions (see apax_encode.cu): bit0 out(S), bit1 out(C),
+// bits 2..16 nibbles from S, 17..31 nibbles from C
+__device__ __forceinline__ uint32_t jf_pack(int o0, int o1, int n0, int n1) {
+    return (uint32_t)o0 | ((uint32_t)o1 << 1) | ((uint32_t)n0 << 2) | ((uint32_t)n1 << 17);
+}
+__device__ __forceinline__ uint32_t jf_compose(uint32_t a, uint32_t b) {  // a then b
+    uint32_t ao0 = a & 1u, ao1 = (a >> 1) & 1u;
+    uint32_t bo0 = b & 1u, bo1 = (b >> 1) & 1u;
+    uint32_t bn0 = (b >> 2) & 0x7fffu, bn1 = (b >> 17) & 0x7fffu;
+    uint32_t r_o0 = ao0 ? bo1 : bo0, r_o1 = ao1 ? bo1 : bo0;
+    uint32_t r_n0 = ((a >> 2) & 0x7fffu) + (ao0 ? bn1 : bn0);
+    uint32_t r_n1 = ((a >> 17) & 0x7fffu) + (ao1 ? bn1 : bn0);
+    return r_o0 | (r_o1 << 1) | (r_n0 << 2) | (r_n1 << 17);
+}
+constexpr uint32_t kJfId = 2u;  // out(S)=S(0), out(C)=C(1), 0 nibbles
+
+// generic pairwise sum (numpy), sequential on one thread, term(i) on the fly.
+// Iterative (explicit stack) so no device recursion / stack frames are needed.
+template <typename F>
+__device__ double pw_leaf(F& term, int s, int n) {
+    if (n < 8) {
+        double r = -0.0;
+        for (int i = 0; i < n; i++) r += term(s + i);
+        return r;
+    }
+    double r[8];
+    for (int j = 0; j < 8; j++) r[j] = term(s + j);
+    int i = 8;
+    for (; i < n - (n % 8); i += 8)
+        for (int j = 0; j < 8; j++) r[j] += term(s + i + j);
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; i++) res += term(s + i);
+    return res;
+}
+template <typename F>
+__device__ double pw_seq(F& term, int s0, int n0) {
+    // frames: (start, len, stage, left partial)
+    int fs[16], fn[16], fst[16];
+    double fl[16];
+    int sp = 0;
+    fs[0] = s0; fn[0] = n0; fst[0] = 0; sp = 1;
+    double val = 0.0;
+    bool have = false;
+    while (sp > 0) {
+        const int t = sp - 1;
+        if (have) {               // deliver val to frame t
+            if (fst[t] == 1) {    // left done -> start right
+                fl[t] = val;
+                fst[t] = 2;
+                int n2 = fn[t] / 2;
+                n2 -= n2 % 8;
+                fs[sp] = fs[t] + n2; fn[sp] = fn[t] - n2; fst[sp] = 0; sp++;
+                have = false;
+            } else {              // right done
+                val = fl[t] + val;
+                sp--;
+            }
+            continue;
+        }
+        if (fn[t] <= 128) {
+            val = pw_leaf(term, fs[t], fn[t]);
+            have = true;
+            sp--;
+            continue;
+        }
+        // descend left
+        fst[t] = 1;
+        int n2 = fn[t] / 2;
+        n2 -= n2 % 8;
+        fs[sp] = fs[t]; fn[sp] = n2; fst[sp] = 0; sp++;
+    }
+    return val;
+}
+
+__device__ __forceinline__ int qaddr(int i) { return (i >> 7) * LEAF_STRIDE + (i & 127); }
+
+// ---------------------------------------------------------------------------
+// the kernel
+// ---------------------------------------------------------------------------
+template <int DT>
+__global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
+    using Tr = DT_<DT>;
+    using T = typename Tr::T;
+    constexpr bool F = Tr::F;
+    constexpr int HS = Tr::HDR;
+    // x^2 is exact in double for 8/16-bit ints and f32
+    constexpr bool SQ_EXACT = (DT == 0 || DT == 1 || DT == 3);
+
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int bs = P.bs;
+    const bool FQ = (P.mode == 2);
+
+    St* S = (St*)smem;
+    size_t off = (sizeof(St) + 127) & ~(size_t)127;
+    T* xbuf[2];
+    xbuf[0] = (T*)(smem + off);
+    off += ((size_t)MAXBS * sizeof(T) + 127) & ~(size_t)127;
+    xbuf[1] = (T*)(smem + off);
+    off += ((size_t)MAXBS * sizeof(T) + 127) & ~(size_t)127;
+    int* qbuf = (int*)(smem + off);
+    if (FQ) off += ((size_t)32 * LEAF_STRIDE * 4 + 127) & ~(size_t)127;
+    uint32_t* es32 = (uint32_t*)(smem + off);
+    off += ((size_t)(NT + 2) * 4 + 127) & ~(size_t)127;
+    uint32_t* win = (uint32_t*)(smem + off);
+    const int win_words = P.stage_bytes / 4;
+
+    uint8_t* slot = P.slots + (long long)blockIdx.x * P.slot_bytes;
+
+    if (tid == 0) {
+        mbar_init(&S->mbar[0]);
+        mbar_init(&S->mbar[1]);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    uint32_t phase[2] = {0u, 0u};
+
+    for (;;) {
+        if (tid == 0) S->unit = (long long)atomicAdd(P.ticket, 1u);
+        __syncthreads();
+        const long long u = S->unit;
+        if (u >= P.n_units) break;
+        const long long b0 = u * P.unit_blocks;
+        const long long b1 = (b0 + P.unit_blocks < P.n_blocks) ? b0 + P.unit_blocks : P.n_blocks;
+        if (tid == 0) {
+            S->att = 0.0; S->p1 = 0; S->p2 = 0; S->has_pc = 0; S->initialized = 0;
+            S->emitted = 0; S->win_base = 0; S->tail_len = 0; S->unit_len = 0;
+            S->tail[0] = S->tail[1] = S->tail[2] = S->tail[3] = 0u;
+            S->direct = (u == 0);
+            S->prefix = 0;
+            if (P.halo && b0 > 1) {  // history entering block b0-1 (App. C E2)
+                const T* xh = (const T*)P.x + (b0 - 1) * (long long)bs;
+                S->p1 = (long long)xh[-1];
+                S->p2 = (long long)xh[-2];
+            }
+        }
+        // pass list: [halo] | [warm1, warm2] then the unit's blocks
+        const bool halo = P.halo && b0 > 0;
+        const bool warm = !P.halo && P.policy == 1 && P.mode == 1;
+        const int npre = halo ? 1 : (warm ? 2 : 0);
+        const long long npass = npre + (b1 - b0);
+        auto pass_block = [&](long long k) -> long long {
+            if (halo) return k == 0 ? b0 - 1 : b0 + k - 1;
+            if (warm) return k < 2 ? b0 : b0 + k - 2;
+            return b0 + k;
+        };
+        auto block_n = [&](long long b) -> int {
+            long long r = P.n - b * (long long)bs;
+            return (int)(r < bs ? r : bs);
+        };
+        auto tma_ok = [&](long long b) -> bool {
+            const T* src = (const T*)P.x + b * (long long)bs;
+            long long bytes = (long long)block_n(b) * (long long)sizeof(T);
+            return ((((uintptr_t)src) & 15) == 0) && ((bytes & 15) == 0);
+        };
+        // issue the load of the first pass's block
+        long long loaded_b = -1;
+        int cur = 0;
+        __syncthreads();
+        {
+            long long bfirst = pass_block(0);
+            if (tma_ok(bfirst) && tid == 0) {
+                fence_proxy_async();
+                tma_load(xbuf[0], (const T*)P.x + bfirst * (long long)bs,
+                         (uint32_t)(block_n(bfirst) * sizeof(T)), &S->mbar[0]);
+            }
+        }
+        long long inflight_b = pass_block(0);
+        int inflight_buf = 0;
+
+        for (long long k = 0; k < npass; k++) {
+            const long long b = pass_block(k);
+            const int kind = halo ? (k == 0 ? 1 : 0) : (warm ? (k == 0 ? 2 : (k == 1 ? 3 : 0)) : 0);
+            // kind: 0 emit, 1 halo costs, 2 warm pass 1 (a = 1), 3 warm pass 2 (a = a(att0))
+            const int n = block_n(b);
+            const int G = (n + 3) >> 2;
+            const int np = 4 * G;
+            // ---------------- make block b's samples available ----------------
+            if (b != loaded_b) {
+                if (inflight_b == b) {
+                    cur = inflight_buf;
+                    if (tma_ok(b)) {
+                        mbar_wait(&S->mbar[cur], phase[cur]);
+                        phase[cur] ^= 1u;
+                    } else {
+                        const T* src = (const T*)P.x + b * (long long)bs;
+                        for (int i = tid; i < n; i += NT) xbuf[cur][i] = src[i];
+                    }
+                } else {
+                    cur ^= 1;
+                    const T* src = (const T*)P.x + b * (long long)bs;
+                    for (int i = tid; i < n; i += NT) xbuf[cur][i] = src[i];
+                }
+                loaded_b = b;
+                inflight_b = -1;
+                // prefetch the next distinct block of the unit
+                long long nb = -1;
+                for (long long kk = k + 1; kk < npass; kk++) {
+                    long long bb = pass_block(kk);
+                    if (bb != b) { nb = bb; break; }
+                }
+                __syncthreads();  // previous users of the other buffer are done
+                if (nb >= 0) {
+                    inflight_b = nb;
+                    inflight_buf = cur ^ 1;
+                    if (tma_ok(nb) && tid == 0) {
+                        fence_proxy_async();
+                        tma_load(xbuf[inflight_buf], (const T*)P.x + nb * (long long)bs,
+                                 (uint32_t)(block_n(nb) * sizeof(T)), &S->mbar[inflight_buf]);
+                    }
+                }
+            }
+            const T* xs = xbuf[cur];
+            // window: restore the carried tail, zero the rest (emit passes)
+            if (kind == 0) {
+                for (int i = 4 + tid; i < win_words + 4; i += NT) win[i] = 0u;
+                if (tid < 4) win[tid] = S->tail[tid];
+            }
+
+            // ================= phase A: peak (+ px) =================
+            const int leaf = warp * 4 + (lane >> 3);
+            const int jj = lane & 7;
+            const int L = n >> 7;                     // full leaves
+            const bool regular = (n == bs) && (n >= 128);
+            {
+                unsigned long long pk = 0;            // max |x| bit pattern / magnitude
+                double pxs = 0.0;
+                // every thread scans a strided slice for the peak (floats:
+                // scale; i32: 64-bit stream decision)
+                if (F || DT == 2) for (int i = tid; i < n; i += NT) {
+                    if (F) {
+                        unsigned long long bits;
+                        if (DT == 3) bits = (unsigned)__float_as_uint((float)xs[i]) & 0x7fffffffu;
+                        else bits = (unsigned long long)__double_as_longlong((double)xs[i]) & 0x7fffffffffffffffULL;
+                        pk = bits > pk ? bits : pk;
+                    } else {
+                        long long v = (long long)xs[i];
+                        unsigned long long av = (unsigned long long)(v < 0 ? -v : v);
+                        pk = av > pk ? av : pk;
+                    }
+                }
+                if (FQ && regular) {
+                    // 8-lane pairwise leaves (numpy order); warps beyond the
+                    // leaf count shuffle zeros
+                    if (warp * 4 < L) {
+                        double r = 0.0;
+                        if (leaf < L) {
+                            const int base = leaf * 128 + jj;
+                            double v = (double)xs[base];
+                            r = v * v;
+#pragma unroll
+                            for (int i = 1; i < 16; i++) {
+                                double w = (double)xs[base + 8 * i];
+                                if (SQ_EXACT) r = __fma_rn(w, w, r);
+                                else r = r + w * w;
+                            }
+                        }
+                        r += __shfl_xor_sync(0xffffffffu, r, 1);
+                        r += __shfl_xor_sync(0xffffffffu, r, 2);
+                        r += __shfl_xor_sync(0xffffffffu, r, 4);
+                        if (L >= 2) r += __shfl_xor_sync(0xffffffffu, r, 8);
+                        if (L >= 4) r += __shfl_xor_sync(0xffffffffu, r, 16);
+                        pxs = r;
+                    }
+                }
+                unsigned long long pkr = pk;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    unsigned long long t = __shfl_xor_sync(0xffffffffu, pkr, o);
+                    pkr = t > pkr ? t : pkr;
+                }
+                if (lane == 0) { S->pkw[warp] = pkr; S->pxw[warp] = pxs; }
+            }
+            __syncthreads();  // B1
+            // ================= scalar: gain, code, scale =================
+            if (tid == 0) {
+                unsigned long long pk = 0;
+                for (int w = 0; w < NW; w++) pk = S->pkw[w] > pk ? S->pkw[w] : pk;
+                double px = 0.0;
+                if (FQ) {
+                    if (regular) {
+                        const int nwd = (L + 3) / 4;
+                        double v[NW];
+                        for (int w = 0; w < nwd; w++) v[w] = S->pxw[w];
+                        for (int st = 1; st < nwd; st <<= 1)
+                            for (int w = 0; w + st < nwd; w += 2 * st) v[w] = v[w] + v[w + st];
+                        px = v[0];
+                    } else {
+                        auto t2 = [&](int i) { double v = (double)xs[i]; return v * v; };
+                        px = pw_seq(t2, 0, n);
+                    }
+                    S->px = px;
+                }
+                double peak;
+                bool nonfin = false;
+                if (F) {
+                    if (DT == 3) {
+                        nonfin = pk >= 0x7f800000ULL;
+                        peak = (double)__uint_as_float((unsigned)pk);
+                    } else {
+                        nonfin = pk >= 0x7ff0000000000000ULL;
+                        peak = __longlong_as_double((long long)pk);
+                    }
+                } else {
+                    peak = (double)pk;
+                }
+                S->nonfinite = nonfin;
+                if (nonfin) {
+                    for (int i = 0; i < n; i++) {
+                        if (!isfinite((double)xs[i])) {
+                            atomicMin(&P.status[0], (unsigned long long)(b * (long long)bs + i));
+                            break;
+                        }
+                    }
+                }
+                // gain
+                if (kind == 0 && !S->initialized) {
+                    if (FQ) {  // _init_attenuation (codec.py:155-168)
+                        double rms = sqrt(px / (double)n);
+                        double att0 = 0.0;
+                        if (rms != 0.0) {
+                            double rqa = F ? (1073741824.0 * rms) / peak : rms;
+                            double a0 = P.pow10_t20 / (P.sqrt12 * rqa);
+                            double m = (1e-300 > a0) ? 1e-300 : a0;
+                            att0 = 20.0 * log10(m);
+                        }
+                        S->att = clamp_att(att0, P.att_lo);
+                    }
+                    S->initialized = 1;
+                }
+                double a;
+                if (kind == 1 || kind == 2) a = 1.0;
+                else if (kind == 3) a = S->a;
+                else if (P.mode == 0) a = 1.0;
+                else a = att_to_a(S->att);
+                S->a = a;
+                int bad = 0, zero = 0, fbe = 0, code;
+                double s = 1.0, aq = 1.0;
+                long long qpk;
+                if (!F) {
+                    code = encode_scale_code(a);
+                    aq = decode_scale_code(code);
+                    qpk = (aq == 1.0) ? (long long)peak : (long long)rint(peak * aq);
+                } else if (nonfin || peak == 0.0) {
+                    code = kScaleCodeOne; zero = 1; qpk = 0;
+                } else {
+                    double s_des = (a * 1073741824.0) / peak;
+                    if (!isfinite(s_des)) {
+                        bad = APAX_ERR_OVERFLOW; code = kScaleCodeOne; zero = 1; qpk = 0;
+                    } else {
+                        long long l2 = floor_log2_rn(s_des);
+                        long long fb = (-31 <= l2 && l2 <= 31) ? 0 : l2 - 31;
+                        fb = fb < -127 ? -127 : (fb > 127 ? 127 : fb);
+                        double rem = ldexp(s_des, (int)-fb);
+                        const double nxt = 8589934591.999999;
+                        double mm = (nxt < rem) ? nxt : rem;
+                        rem = (mm > 4.656612873077393e-10) ? mm : 4.656612873077393e-10;
+                        code = encode_scale_code(rem);
+                        // overflow guard (codec.py:126-131): max|q| = rint(peak*s)
+                        for (;;) {
+                            s = decode_scale_code(code) * ldexp(1.0, (int)fb);
+                            double qm = rint(peak * s);
+                            if (qm < 2147483648.0 || fb <= -127) { qpk = qm < 9.2e18 ? (long long)qm : (1LL << 62); break; }
+                            fb -= 1;
+                        }
+                        fbe = (int)fb;
+                    }
+                }
+                S->code = code; S->fbe = fbe; S->s = s; S->aq = aq; S->zero = zero;
+                S->rs = F ? __ddiv_rn(1.0, s) : (aq == 1.0 ? 1.0 : __ddiv_rn(1.0, aq));
+                S->qpk = qpk;
+                // 64-bit streams needed when |d2| could reach 2^31
+                S->wide = (qpk >= (1LL << 29)) ? 1 : 0;
+                S->bad = bad;
+            }
+            __syncthreads();  // B2
+            const double s = S->s, rs = S->rs, aq = S->aq;
+            const bool zero = F && S->zero;
+            const bool wide = S->wide;
+            const bool fq_emit = FQ && kind == 0;
+
+            auto quant = [&](T xv) -> long long {
+                if (F) {
+                    if (zero) return 0;
+                    return f2i64(rint((double)xv * s));
+                } else {
+                    long long v = (long long)xv;
+                    if (aq == 1.0) return v;
+                    return f2i64(rint((double)v * aq));
+                }
+            };
+            // dequantize one sample (codec.py:135-146) as the dtype's value in double
+            auto deq = [&](long long q) -> double {
+                const double r = (double)q;
+                if (F) {
+                    double y0 = r * rs;
+                    double e = __fma_rn(-s, y0, r);
+                    double y = __fma_rn(e, rs, y0);
+                    return (DT == 3) ? (double)__double2float_rn(y) : y;
+                } else {
+                    long long yi;
+                    if (aq == 1.0) yi = q;
+                    else {
+                        double y0 = r * rs;
+                        double e = __fma_rn(-aq, y0, r);
+                        yi = f2i64(rint(__fma_rn(e, rs, y0)));
+                    }
+                    yi = yi < Tr::LO ? Tr::LO : (yi > Tr::HI ? Tr::HI : yi);
+                    return (double)yi;
+                }
+            };
+
+            // ================= phase B: fixed-quality quantize + residual =================
+            if (fq_emit) {
+                double pds = 0.0;
+                if (regular) {
+                    if (warp * 4 < L) {
+                        double r = 0.0;
+                        if (leaf < L) {
+                            const int base = leaf * 128 + jj;
+                            int* qrow = qbuf + leaf * LEAF_STRIDE + jj;
+#pragma unroll 4
+                            for (int i = 0; i < 16; i++) {
+                                T xv = xs[base + 8 * i];
+                                long long q = quant(xv);
+                                qrow[8 * i] = (int)q;
+                                double d = (double)xv - deq(q);
+                                double d2 = d * d;
+                                r = (i == 0) ? d2 : r + d2;
+                            }
+                        }
+                        r += __shfl_xor_sync(0xffffffffu, r, 1);
+                        r += __shfl_xor_sync(0xffffffffu, r, 2);
+                        r += __shfl_xor_sync(0xffffffffu, r, 4);
+                        if (L >= 2) r += __shfl_xor_sync(0xffffffffu, r, 8);
+                        if (L >= 4) r += __shfl_xor_sync(0xffffffffu, r, 16);
+                        pds = r;
+                    }
+                } else {
+                    for (int i = tid; i < n; i += NT) qbuf[qaddr(i)] = (int)quant(xs[i]);
+                }
+                if (lane == 0) S->pdw[warp] = pds;
+                // padding samples of a partial block are zero
+                for (int i = n + tid; i < np; i += NT) qbuf[qaddr(i)] = 0;
+                __syncthreads();  // B3
+                if (tid == 0) {
+                    double pd;
+                    if (regular) {
+                        const int nwd = (L + 3) / 4;
+                        double v[NW];
+                        for (int w = 0; w < nwd; w++) v[w] = S->pdw[w];
+                        for (int st = 1; st < nwd; st <<= 1)
+                            for (int w = 0; w + st < nwd; w += 2 * st) v[w] = v[w] + v[w + st];
+                        pd = v[0];
+                    } else {
+                        auto td = [&](int i) {
+                            double d = (double)xs[i] - deq((long long)qbuf[qaddr(i)]);
+                            return d * d;
+                        };
+                        pd = pw_seq(td, 0, n);
+                    }
+                    S->pd = pd;
+                }
+            }
+
+            // ================= phase C: streams, widths, costs, monitor =================
+            const int t0 = SPT * tid;                // first sample of this thread
+            const bool active = t0 < np;
+            int q[SPT];
+            long long hq1, hq2;                      // q[t0-1], q[t0-2]
+            const long long hp1 = S->p1, hp2 = S->p2;
+            uint32_t epk[3] = {0u, 0u, 0u};          // per stream: 4 group widths packed
+            int se[3] = {0, 0, 0};
+            unsigned emax = 0;
+            int mon_ch = 0, mon_first = 0, mon_last = 0;
+            if (!wide) {
+                if (active) {
+                    if (fq_emit) {
+                        const int4* qp = (const int4*)(qbuf + qaddr(t0));
+#pragma unroll
+                        for (int c = 0; c < 4; c++) {
+                            int4 v4 = qp[c];
+                            q[4 * c] = v4.x; q[4 * c + 1] = v4.y; q[4 * c + 2] = v4.z; q[4 * c + 3] = v4.w;
+                        }
+                        hq1 = t0 >= 1 ? qbuf[qaddr(t0 - 1)] : hp1;
+                        hq2 = t0 >= 2 ? qbuf[qaddr(t0 - 2)] : (t0 == 1 ? hp1 : hp2);
+                    } else {
+#pragma unroll
+                        for (int k2 = 0; k2 < SPT; k2++) {
+                            int i = t0 + k2;
+                            q[k2] = (i < n) ? (int)quant(xs[i]) : 0;
+                        }
+                        hq1 = t0 >= 1 ? quant(xs[t0 - 1]) : hp1;
+                        hq2 = t0 >= 2 ? quant(xs[t0 - 2]) : hp2;
+                    }
+                    int m1 = (int)hq1, dprev = (int)(hq1 - hq2);
+                    int lastv = 0;
+#pragma unroll
+                    for (int g = 0; g < 4; g++) {
+                        unsigned o0 = 0, o1 = 0, o2 = 0;
+#pragma unroll
+                        for (int kk = 0; kk < 4; kk++) {
+                            const int v0 = q[4 * g + kk];
+                            const int v1 = v0 - m1;
+                            const int v2 = v1 - dprev;
+                            o0 |= wbits32(v0); o1 |= wbits32(v1); o2 |= wbits32(v2);
+                            m1 = v0; dprev = v1;
+                            if (v0) {
+                                if (lastv) mon_ch += ((v0 ^ lastv) < 0);
+                                else mon_first = v0;
+                                lastv = v0;
+                            }
+                        }
+                        const bool gv = (t0 + 4 * g) < np;
+                        const int w0 = gv ? bitlen32(o0) : 0, w1 = gv ? bitlen32(o1) : 0,
+                                  w2 = gv ? bitlen32(o2) : 0;
+                        epk[0] |= (uint32_t)w0 << (8 * g);
+                        epk[1] |= (uint32_t)w1 << (8 * g);
+                        epk[2] |= (uint32_t)w2 << (8 * g);
+                        se[0] += w0; se[1] += w1; se[2] += w2;
+                    }
+                    mon_last = lastv;
+#pragma unroll
+                    for (int k2 = 0; k2 < SPT; k2++) {
+                        if (t0 + k2 == np - 1) S->last1 = q[k2];
+                        if (t0 + k2 == np - 2) S->last2 = q[k2];
+                    }
+                }
+            } else {
+                // 64-bit streams, samples recomputed from x (rare path)
+                if (active) {
+                    auto qat = [&](int i) -> long long {
+                        if (i < 0) return i == -1 ? hp1 : hp2;
+                        if (i >= n) return 0;
+                        return quant(xs[i]);
+                    };
+                    long long m1 = qat(t0 - 1), m2 = qat(t0 - 2);
+                    long long dprev = (long long)((unsigned long long)m1 - (unsigned long long)m2);
+                    long long lastv = 0;
+                    for (int g = 0; g < 4; g++) {
+                        unsigned long long o0 = 0, o1 = 0, o2 = 0;
+                        for (int kk = 0; kk < 4; kk++) {
+                            const long long v0 = qat(t0 + 4 * g + kk);
+                            const long long v1 = (long long)((unsigned long long)v0 - (unsigned long long)m1);
+                            const long long v2 = (long long)((unsigned long long)v1 - (unsigned long long)dprev);
+                            o0 |= wbits64(v0); o1 |= wbits64(v1); o2 |= wbits64(v2);
+                            // width of values beyond 2^62 (pathological f64): force > 34
+                            if (v0 >= (1LL << 62) || v0 < -(1LL << 62)) o0 |= 1ULL << 63;
+                            if (v1 >= (1LL << 62) || v1 < -(1LL << 62)) o1 |= 1ULL << 63;
+                            if (v2 >= (1LL << 62) || v2 < -(1LL << 62)) o2 |= 1ULL << 63;
+                            m1 = v0; dprev = v1;
+                            if (v0) {
+                                if (lastv) mon_ch += ((v0 ^ lastv) < 0);
+                                else mon_first = v0 > 0 ? 1 : -1;
+                                lastv = v0;
+                            }
+                        }
+                        const bool gv = (t0 + 4 * g) < np;
+                        int w0 = gv ? bitlen64(o0) : 0, w1 = gv ? bitlen64(o1) : 0, w2 = gv ? bitlen64(o2) : 0;
+                        unsigned wm = (unsigned)max(w0, max(w1, w2));
+                        emax = wm > emax ? wm : emax;
+                        w0 = min(w0, 255); w1 = min(w1, 255); w2 = min(w2, 255);
+                        epk[0] |= (uint32_t)w0 << (8 * g);
+                        epk[1] |= (uint32_t)w1 << (8 * g);
+                        epk[2] |= (uint32_t)w2 << (8 * g);
+                        se[0] += w0; se[1] += w1; se[2] += w2;
+                    }
+                    mon_last = lastv > 0 ? 1 : (lastv < 0 ? -1 : 0);
+                    if (t0 <= np - 1 && np - 1 < t0 + SPT) {
+                        S->last1 = qat(np - 1);
+                        S->last2 = qat(np - 2);
+                    }
+                }
+            }
+            // signs only
+            int fs = mon_first > 0 ? 1 : (mon_first < 0 ? -1 : 0);
+            int ls = mon_last > 0 ? 1 : (mon_last < 0 ? -1 : 0);
+            // ---- reductions: sums (redux), emax, ordered monitor ----
+            {
+                int s0 = __reduce_add_sync(0xffffffffu, se[0]);
+                int s1 = __reduce_add_sync(0xffffffffu, se[1]);
+                int s2 = __reduce_add_sync(0xffffffffu, se[2]);
+                unsigned em = __reduce_max_sync(0xffffffffu, emax);
+                int ch = mon_ch, f = fs, l = ls;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    int och = __shfl_down_sync(0xffffffffu, ch, o);
+                    int ofl = __shfl_down_sync(0xffffffffu, (f + 1) | ((l + 1) << 2), o);
+                    if (((lane & (2 * o - 1)) == 0) && lane + o < 32) {
+                        int of = (ofl & 3) - 1, ol = ((ofl >> 2) & 3) - 1;
+                        ch += och + ((l != 0 && of != 0 && l != of) ? 1 : 0);
+                        if (!f) f = of;
+                        if (ol) l = ol;
+                    }
+                }
+                if (lane == 0) {
+                    S->sew[0][warp] = s0; S->sew[1][warp] = s1; S->sew[2][warp] = s2;
+                    S->emaxw[warp] = em;
+                    S->monc[warp] = ch;
+                    S->monf[warp] = (f + 1) | ((l + 1) << 2);
+                }
+            }
+            __syncthreads();  // B4
+            if (tid == 0) {
+                long long t[3] = {0, 0, 0};
+                unsigned em = 0;
+                int ch = 0, f = 0, l = 0;
+                for (int w = 0; w < NW; w++) {
+                    t[0] += S->sew[0][w]; t[1] += S->sew[1][w]; t[2] += S->sew[2][w];
+                    em = S->emaxw[w] > em ? S->emaxw[w] : em;
+                    int of = (S->monf[w] & 3) - 1, ol = ((S->monf[w] >> 2) & 3) - 1;
+                    ch += S->monc[w] + ((l != 0 && of != 0 && l != of) ? 1 : 0);
+                    if (!f) f = of;
+                    if (ol) l = ol;
+                }
+                S->sum_e[0] = t[0]; S->sum_e[1] = t[1]; S->sum_e[2] = t[2];
+                if (em > (unsigned)kMaxExponent && !S->bad) S->bad = APAX_ERR_INTERNAL;
+                // centre-frequency gate cf > 1/3 (transform.py:75-83, 110-111)
+                double cf = (double)ch / (2.0 * (double)(np - 1));
+                S->gate = cf > 1.0 / 3.0;
+                int sel = 0;
+                if (S->has_pc && !S->gate) {
+                    if (S->pc[1] < S->pc[sel]) sel = 1;
+                    if (S->pc[2] < S->pc[sel]) sel = 2;
+                }
+                S->sel = sel;
+            }
+            if (kind != 0) {
+                // cost-only passes (lossless halo / warm_self)
+                __syncthreads();
+                if (tid == 0) {
+                    const long long g4 = 4LL * G;
+                    if (kind == 1) {
+                        S->has_pc = 1;
+                        for (int c = 0; c < 3; c++) S->pc[c] = 4 * S->sum_e[c] + g4;
+                        S->p1 = S->last1; S->p2 = S->last2;
+                        S->emitted = 1; S->initialized = 1;
+                    } else if (kind == 2) {
+                        long long mn = S->sum_e[0];
+                        mn = S->sum_e[1] < mn ? S->sum_e[1] : mn;
+                        mn = S->sum_e[2] < mn ? S->sum_e[2] : mn;
+                        double bps0 = (double)(4 * mn + g4 + 8LL * HS) / (double)bs;
+                        double att0 = clamp_att(0.0 - 6.02 * (bps0 - P.target), P.att_lo);
+                        S->att = att0;
+                        S->a = att_to_a(att0);
+                    } else {
+                        S->has_pc = 1;
+                        for (int c = 0; c < 3; c++) S->pc[c] = 4 * S->sum_e[c] + g4;
+                    }
+                    if (S->bad) report_error(P.status, b, S->bad);
+                }
+                __syncthreads();
+                continue;
+            }
+            __syncthreads();  // B5
+            // ================= phase D: JEE + mantissa =================
+            const int sel = S->sel;
+            const uint32_t es = sel == 0 ? epk[0] : (sel == 1 ? epk[1] : epk[2]);
+            es32[tid + 1] = es;
+            if (tid == 0) { es32[0] = 0u; es32[NT + 1] = 0u; }
+            __syncthreads();  // B6
+            const int g0 = 4 * tid;                  // first group of this thread
+            int ev[5];
+            ev[0] = (int)(es32[tid] >> 24);          // e[g0-1]
+#pragma unroll
+            for (int g = 0; g < 4; g++) ev[g + 1] = (int)((es >> (8 * g)) & 0xffu);
+            const int enext = (int)(es32[tid + 2] & 0xffu);
+            int pair = 0, single = 0;                // bit k: position g0+k
+#pragma unroll
+            for (int k2 = 0; k2 < 4; k2++) {
+                const int p = g0 + k2;
+                const int d = ev[k2 + 1] - ev[k2];
+                const int dn = (k2 < 3 ? ev[k2 + 2] : enext) - ev[k2 + 1];
+                const bool s1 = (unsigned)(d + 1) <= 2u, s1n = (unsigned)(dn + 1) <= 2u;
+                const bool s2 = (unsigned)(d + 2) <= 4u;
+                if (p != 0 && p + 1 < G && s1 && s1n) pair |= 1 << k2;
+                if (p != 0 && s2) single |= 1 << k2;
+            }
+            const int nvalid = (g0 < G) ? min(4, G - g0) : 0;
+            uint32_t f = kJfId;
+            unsigned mbits = 0;
+            if (nvalid > 0) {
+                int o[2], nb[2];
+#pragma unroll
+                for (int s0 = 0; s0 < 2; s0++) {
+                    int st = s0, cnt = 0;
+#pragma unroll
+                    for (int k2 = 0; k2 < 4; k2++) {
+                        if (k2 >= nvalid) break;
+                        if (st) { st = 0; continue; }
+                        if ((pair >> k2) & 1) { cnt += 1; st = 1; }
+                        else cnt += ((single >> k2) & 1) ? 1 : 3;
+                    }
+                    o[s0] = st; nb[s0] = cnt;
+                }
+                f = jf_pack(o[0], o[1], nb[0], nb[1]);
+#pragma unroll
+                for (int g = 0; g < 4; g++) mbits += (g < nvalid) ? 4u * (unsigned)ev[g + 1] : 0u;
+            }
+            // CTA exclusive scan of (f, mbits)
+            uint32_t fi = f;
+            unsigned bi = mbits;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                uint32_t of = __shfl_up_sync(0xffffffffu, fi, d);
+                unsigned ob = __shfl_up_sync(0xffffffffu, bi, d);
+                if (lane >= d) { fi = jf_compose(of, fi); bi += ob; }
+            }
+            uint32_t fx = __shfl_up_sync(0xffffffffu, fi, 1);
+            unsigned bx = __shfl_up_sync(0xffffffffu, bi, 1);
+            if (lane == 0) { fx = kJfId; bx = 0; }
+            if (lane == 31) { S->scf[warp] = fi; S->scb[warp] = bi; }
+            __syncthreads();  // B7
+            if (tid == 0) {
+                uint32_t acc = kJfId;
+                unsigned accb = 0;
+                for (int w = 0; w < NW; w++) {
+                    S->pre_f[w] = acc; S->pre_b[w] = accb;
+                    acc = jf_compose(acc, S->scf[w]);
+                    accb += S->scb[w];
+                }
+                const long long nib = (acc >> 2) & 0x7fff;
+                S->jee_nib = nib;
+                S->bits = accb;
+                S->blen = HS + ((nib + 1) >> 1) + ((long long)accb + 7) / 8;
+            }
+            __syncthreads();  // B8
+            const uint32_t fpre = jf_compose(S->pre_f[warp], fx);
+            const unsigned bpre = S->pre_b[warp] + bx;
+            const long long wb = S->tail_len;            // window byte of block start
+            const long long jee_bytes = (S->jee_nib + 1) >> 1;
+            if (nvalid > 0 && !S->bad) {
+                // JEE nibbles
+                BitWriter bw;
+                bw.init(win, 8 * (wb + HS) + 4LL * ((fpre >> 2) & 0x7fff));
+                int st = fpre & 1;
+#pragma unroll
+                for (int k2 = 0; k2 < 4; k2++) {
+                    if (k2 >= nvalid) break;
+                    if (st) { st = 0; continue; }
+                    const int e = ev[k2 + 1];
+                    const int d = e - ev[k2];
+                    if ((pair >> k2) & 1) {
+                        const int dn = (k2 < 3 ? ev[k2 + 2] : enext) - e;
+                        bw.put32((uint32_t)((d + 1) * 3 + (dn + 1)), 4);
+                        st = 1;
+                    } else if ((single >> k2) & 1) {
+                        bw.put32((uint32_t)(11 + d), 4);
+                    } else {
+                        bw.put32(0xF00u | (uint32_t)e, 12);
+                    }
+                }
+                bw.flush();
+                // mantissa bits
+                BitWriter mw;
+                mw.init(win, 8 * (wb + HS + jee_bytes) + (long long)bpre);
+                if (!wide) {
+                    int m1 = (int)hq1, dprev = (int)(hq1 - hq2);
+#pragma unroll
+                    for (int g = 0; g < 4; g++) {
+                        int vs[4];
+#pragma unroll
+                        for (int kk = 0; kk < 4; kk++) {
+                            const int v0 = q[4 * g + kk];
+                            const int v1 = v0 - m1;
+                            const int v2 = v1 - dprev;
+                            m1 = v0; dprev = v1;
+                            vs[kk] = sel == 0 ? v0 : (sel == 1 ? v1 : v2);
+                        }
+                        const int w = ev[g + 1];
+                        if (g >= nvalid || w == 0) continue;
+                        if (w <= 8) {
+                            const uint32_t m = (1u << w) - 1u;
+                            uint32_t c = ((uint32_t)vs[0] & m) << (3 * w) | ((uint32_t)vs[1] & m) << (2 * w) |
+                                         ((uint32_t)vs[2] & m) << w | ((uint32_t)vs[3] & m);
+                            mw.put32(c, 4 * w);
+                        } else if (w <= 16) {
+                            const uint32_t m = (1u << w) - 1u;
+                            mw.put32(((uint32_t)vs[0] & m) << w | ((uint32_t)vs[1] & m), 2 * w);
+                            mw.put32(((uint32_t)vs[2] & m) << w | ((uint32_t)vs[3] & m), 2 * w);
+                        } else {
+#pragma unroll
+                            for (int kk = 0; kk < 4; kk++) mw.put32((uint32_t)vs[kk] & (0xffffffffu >> (32 - w)), w);
+                        }
+                    }
+                } else {
+                    auto qat = [&](int i) -> long long {
+                        if (i < 0) return i == -1 ? hp1 : hp2;
+                        if (i >= n) return 0;
+                        return quant(xs[i]);
+                    };
+                    long long m1 = qat(t0 - 1), m2 = qat(t0 - 2);
+                    long long dprev = (long long)((unsigned long long)m1 - (unsigned long long)m2);
+                    for (int g = 0; g < 4; g++) {
+                        const int w = ev[g + 1];
+                        for (int kk = 0; kk < 4; kk++) {
+                            const long long v0 = qat(t0 + 4 * g + kk);
+                            const long long v1 = (long long)((unsigned long long)v0 - (unsigned long long)m1);
+                            const long long v2 = (long long)((unsigned long long)v1 - (unsigned long long)dprev);
+                            m1 = v0; dprev = v1;
+                            if (g < nvalid && w) mw.put((unsigned long long)(sel == 0 ? v0 : (sel == 1 ? v1 : v2)), w);
+                        }
+                    }
+                }
+                mw.flush();
+            }
+            if (tid == 0) {
+                // block header (dtypes.py:156-165)
+                const int restart = (S->emitted == 0);
+                const int code = S->code;
+                uint32_t hb[6] = {(uint32_t)((sel & 3) | (restart ? 4 : 0)), (uint32_t)(code & 0xFF),
+                                  (uint32_t)((code >> 8) & 0xFF), 0u,
+                                  (uint32_t)(uint8_t)(int8_t)S->fbe, 0u};
+                for (int k2 = 0; k2 < HS; k2++) {
+                    const long long bp = wb + k2;
+                    atomicOr(&win[bp >> 2], hb[k2] << (8 * (bp & 3)));
+                }
+            }
+            __syncthreads();  // B9
+            // ---- flush whole 16-byte chunks; keep the tail ----
+            {
+                const long long total = wb + S->blen;
+                const long long full = total & ~15LL;
+                if (S->direct) {
+                    copy_out<true>(P.out + kFileHeader + S->win_base, win, full);
+                } else {
+                    uint4* dst = (uint4*)(slot + S->win_base);
+                    const uint4* src = (const uint4*)win;
+                    for (long long c = tid; c < (full >> 4); c += NT) dst[c] = src[c];
+                }
+                if (tid == 0) {
+                    const int w0 = (int)(full >> 2);
+                    S->tail[0] = win[w0]; S->tail[1] = win[w0 + 1];
+                    S->tail[2] = win[w0 + 2]; S->tail[3] = win[w0 + 3];
+                    // bookkeeping (codec.py:220-254)
+                    if (P.block_offsets) P.block_offsets[b] = S->win_base + wb;  // unit-relative
+                    if (P.trace) {
+                        double* tr = P.trace + 10 * b;
+                        tr[0] = S->att; tr[1] = S->a; tr[2] = S->code; tr[3] = S->fbe; tr[4] = sel;
+                        tr[5] = (double)(4 * S->sum_e[0] + 4LL * G); tr[6] = (double)(4 * S->sum_e[1] + 4LL * G);
+                        tr[7] = (double)(4 * S->sum_e[2] + 4LL * G); tr[8] = (double)S->blen;
+                        tr[9] = (S->emitted == 0);
+                    }
+                    if (S->bad) report_error(P.status, b, S->bad);
+                    S->has_pc = 1;
+                    for (int c = 0; c < 3; c++) S->pc[c] = 4 * S->sum_e[c] + 4LL * G;
+                    S->p1 = S->last1;
+                    S->p2 = S->last2;
+                    if (P.mode == 1) {
+                        if (S->emitted == 0) {
+                            long long mn = S->pc[0] < S->pc[1] ? S->pc[0] : S->pc[1];
+                            mn = S->pc[2] < mn ? S->pc[2] : mn;
+                            double bps0 = (double)(mn + 8LL * HS) / (double)bs;
+                            S->att = clamp_att(S->att - 6.02 * (bps0 - P.target), P.att_lo);
+                        } else {
+                            double err = (double)(S->blen * 8) / (double)bs - P.target;
+                            S->att = clamp_att(S->att - clamp_step(0.75 * err), P.att_lo);
+                        }
+                    } else if (P.mode == 2) {
+                        double px = S->px / (double)n, pd = S->pd / (double)n;
+                        if (px > 0.0) {
+                            double measured = (pd == 0.0) ? INFINITY : 10.0 * log10(px / pd);
+                            if (isfinite(measured))
+                                S->att = clamp_att(S->att - clamp_step(0.5 * (measured - P.target)), P.att_lo);
+                        }
+                    }
+                    S->emitted += 1;
+                    S->unit_len += S->blen;
+                    S->win_base += full;
+                    S->tail_len = (int)(total - full);
+                }
+            }
+            __syncthreads();  // B10
+        }
+
+        // ---------------- unit end: last tail, look-back, placement ----------------
+        if (S->tail_len > 0) {
+            if (S->direct) {
+                if (tid < S->tail_len)
+                    P.out[kFileHeader + S->win_base + tid] = ((const uint8_t*)S->tail)[tid];
+            } else if (tid == 0) {
+                uint4 t4 = make_uint4(S->tail[0], S->tail[1], S->tail[2], S->tail[3]);
+                *(uint4*)(slot + S->win_base) = t4;
+            }
+        }
+        if (warp == 0) {
+            const long long Lu = S->unit_len;
+            const long long prefix = warp_lookback(P.lookback, u, Lu);
+            if (lane == 0) {
+                S->prefix = prefix;
+                if (u == P.n_units - 1) {
+                    P.status[2] = (unsigned long long)(kFileHeader + prefix + Lu);
+                    if (P.block_offsets) P.block_offsets[P.n_blocks] = kFileHeader + prefix + Lu;
+                }
+            }
+        }
+        __syncthreads();
+        const long long prefix = S->prefix;
+        if (!S->direct) {
+            __threadfence_block();
+            copy_out<false>(P.out + kFileHeader + prefix, (const uint32_t*)slot, S->unit_len);
+        }
+        if (u == 0 && tid < kFileHeader) {
+            unsigned char h[kFileHeader];
+            h[0] = 'A'; h[1] = 'P'; h[2] = 'A'; h[3] = 'X';
+            h[4] = 1; h[5] = (unsigned char)DT; h[6] = (unsigned char)P.mode; h[7] = 0;
+            for (int k2 = 0; k2 < 4; k2++) h[8 + k2] = (unsigned char)((unsigned)bs >> (8 * k2));
+            for (int k2 = 0; k2 < 8; k2++) h[12 + k2] = (unsigned char)((unsigned long long)P.n >> (8 * k2));
+            unsigned long long tb = (unsigned long long)__double_as_longlong(P.target);
+            for (int k2 = 0; k2 < 8; k2++) h[20 + k2] = (unsigned char)(tb >> (8 * k2));
+            P.out[tid] = h[tid];
+        }
+        if (P.block_offsets) {
+            for (long long bb = b0 + tid; bb < b1; bb += NT) P.block_offsets[bb] += kFileHeader + prefix;
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace v2
+
+size_t encode_v2_smem_bytes(int dt, int mode, int window_bytes) {
+    auto al = [](size_t v) { return (v + 127) & ~(size_t)127; };
+    size_t w = (size_t)dt_width(dt);
+    size_t s = al(sizeof(v2::St)) + 2 * al((size_t)v2::MAXBS * w);
+    if (mode == 2) s += al((size_t)32 * v2::LEAF_STRIDE * 4);
+    s += al((size_t)(v2::NT + 2) * 4);
+    s += (size_t)window_bytes + 16 + 16;
+    return s;
+}
+
+bool encode_v2_supported(int bs) {
+    return bs >= 128 && bs <= v2::MAXBS && (bs & (bs - 1)) == 0;
+}
+
+template <int DT>
+static void* v2_fn() { return (void*)v2::encode_v2_kernel<DT>; }
+
+static void* v2_kernel(int dt) {
+    switch (dt) {
+        case 0: return v2_fn<0>();
+        case 1: return v2_fn<1>();
+        case 2: return v2_fn<2>();
+        case 3: return v2_fn<3>();
+        default: return v2_fn<4>();
+    }
+}
+
+int encode_v2_resident_ctas(int dt, size_t smem) {
+    int dev = 0, nsm = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const void* fn = v2_kernel(dt);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, v2::NT, smem) != cudaSuccess || per < 1)
+        per = 1;
+    return per * (nsm > 0 ? nsm : 148);
+}
+
+int launch_encode_v2(int dt, const EncParams& P, int grid, size_t smem, cudaStream_t st) {
+    const void* fn = v2_kernel(dt);
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return APAX_ERR_CUDA;
+    EncParams p = P;
+    void* args[] = {&p};
+    if (cudaLaunchKernel(fn, dim3(grid), dim3(v2::NT), args, smem, st) != cudaSuccess) return APAX_ERR_CUDA;
+    return APAX_OK;
+}
+
+}  // namespace apax
