@@ -73,8 +73,11 @@ struct St {
     int sew[3][NW];
     int monc[NW], monf[NW];
     unsigned emaxw[NW];
-    uint32_t scf[NW], scb[NW];
-    uint32_t pre_f[NW], pre_b[NW];
+    int exact_mon;
+    uint32_t edge_first[NW], edge_last[NW];   // per stream first/last group width of each warp
+    uint32_t pw[32], ew[32], tw[32], xw[32], jw[32];
+    int nibpre[32];
+    unsigned mbw[NW], mbpre[NW];
     unsigned long long mbar[2];
 };
 
@@ -123,7 +126,7 @@ __device__ __forceinline__ double clamp_att(double att, double lo) {
     return (0.0 < m) ? 0.0 : m;
 }
 __device__ __forceinline__ double att_to_a(double att) {
-    double p = pow(10.0, att / 20.0);
+    double p = exp10(att / 20.0);  // 10.0 ** (att / 20.0) (dtypes.py:199)
     double m = (4.656612873077393e-10 > p) ? 4.656612873077393e-10 : p;
     return (1.0 < m) ? 1.0 : m;
 }
@@ -209,6 +212,22 @@ __device__ double pw_seq(F& term, int s0, int n0) {
 __device__ __forceinline__ int qaddr(int i) { return (i >> 7) * LEAF_STRIDE + (i & 127); }
 
 // ---------------------------------------------------------------------------
+// 32-position JEE words: C[i+1] = P[i] & ~C[i] (a position following a joint
+// token is consumed), solved with the odd-run carry trick (the escape-scanner
+// identity popularised by simdjson).  Returns consumed mask, *cout = C[32].
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t consumed_word(uint32_t P, uint32_t cin, uint32_t* cout) {
+    const uint32_t even = 0x55555555u;
+    const uint32_t P2 = P & ~cin;
+    const uint32_t follows = (P2 << 1) | cin;
+    const uint32_t odd_starts = P2 & ~even & ~follows;
+    unsigned long long s = (unsigned long long)odd_starts + P2;
+    *cout = (uint32_t)(s >> 32);
+    const uint32_t inv = (uint32_t)s << 1;
+    return (even ^ inv) & follows;
+}
+
+// ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
 template <int DT>
@@ -232,10 +251,6 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
     off += ((size_t)MAXBS * sizeof(T) + 127) & ~(size_t)127;
     xbuf[1] = (T*)(smem + off);
     off += ((size_t)MAXBS * sizeof(T) + 127) & ~(size_t)127;
-    int* qbuf = (int*)(smem + off);
-    if (FQ) off += ((size_t)32 * LEAF_STRIDE * 4 + 127) & ~(size_t)127;
-    uint32_t* es32 = (uint32_t*)(smem + off);
-    off += ((size_t)(NT + 2) * 4 + 127) & ~(size_t)127;
     uint32_t* win = (uint32_t*)(smem + off);
     const int win_words = P.stage_bytes / 4;
 
@@ -287,7 +302,6 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
             long long bytes = (long long)block_n(b) * (long long)sizeof(T);
             return ((((uintptr_t)src) & 15) == 0) && ((bytes & 15) == 0);
         };
-        // issue the load of the first pass's block
         long long loaded_b = -1;
         int cur = 0;
         __syncthreads();
@@ -304,12 +318,12 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
 
         for (long long k = 0; k < npass; k++) {
             const long long b = pass_block(k);
+            // kind: 0 emit, 1 halo costs, 2 warm pass 1 (a = 1), 3 warm pass 2
             const int kind = halo ? (k == 0 ? 1 : 0) : (warm ? (k == 0 ? 2 : (k == 1 ? 3 : 0)) : 0);
-            // kind: 0 emit, 1 halo costs, 2 warm pass 1 (a = 1), 3 warm pass 2 (a = a(att0))
             const int n = block_n(b);
             const int G = (n + 3) >> 2;
             const int np = 4 * G;
-            // ---------------- make block b's samples available ----------------
+            // ---------------- block b's samples -> smem ----------------
             if (b != loaded_b) {
                 if (inflight_b == b) {
                     cur = inflight_buf;
@@ -327,13 +341,12 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
                 }
                 loaded_b = b;
                 inflight_b = -1;
-                // prefetch the next distinct block of the unit
                 long long nb = -1;
                 for (long long kk = k + 1; kk < npass; kk++) {
                     long long bb = pass_block(kk);
                     if (bb != b) { nb = bb; break; }
                 }
-                __syncthreads();  // previous users of the other buffer are done
+                __syncthreads();  // the other buffer's readers are done
                 if (nb >= 0) {
                     inflight_b = nb;
                     inflight_buf = cur ^ 1;
@@ -345,48 +358,44 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
                 }
             }
             const T* xs = xbuf[cur];
-            // window: restore the carried tail, zero the rest (emit passes)
-            if (kind == 0) {
-                for (int i = 4 + tid; i < win_words + 4; i += NT) win[i] = 0u;
-                if (tid < 4) win[tid] = S->tail[tid];
+            if (kind == 0) {  // window: carried tail + zeros
+                uint4* w4 = (uint4*)win;
+                for (int i = 1 + tid; i < win_words / 4 + 2; i += NT) w4[i] = make_uint4(0u, 0u, 0u, 0u);
+                if (tid == 0) w4[0] = make_uint4(S->tail[0], S->tail[1], S->tail[2], S->tail[3]);
             }
 
-            // ================= phase A: peak (+ px) =================
+            // ================= phase A: peak (+ px, fixed quality) =================
             const int leaf = warp * 4 + (lane >> 3);
             const int jj = lane & 7;
-            const int L = n >> 7;                     // full leaves
-            const bool regular = (n == bs) && (n >= 128);
+            const int L = n >> 7;                      // full 128-sample leaves
+            const bool regular = (n == bs);            // bs is a power of two >= 128
             {
-                unsigned long long pk = 0;            // max |x| bit pattern / magnitude
+                unsigned long long pk = 0;             // max |x| (bit pattern for floats)
                 double pxs = 0.0;
-                // every thread scans a strided slice for the peak (floats:
-                // scale; i32: 64-bit stream decision)
-                if (F || DT == 2) for (int i = tid; i < n; i += NT) {
-                    if (F) {
-                        unsigned long long bits;
-                        if (DT == 3) bits = (unsigned)__float_as_uint((float)xs[i]) & 0x7fffffffu;
-                        else bits = (unsigned long long)__double_as_longlong((double)xs[i]) & 0x7fffffffffffffffULL;
-                        pk = bits > pk ? bits : pk;
-                    } else {
-                        long long v = (long long)xs[i];
-                        unsigned long long av = (unsigned long long)(v < 0 ? -v : v);
-                        pk = av > pk ? av : pk;
-                    }
-                }
+                auto absbits = [&](T v) -> unsigned long long {
+                    if (DT == 3) return (unsigned)__float_as_uint((float)v) & 0x7fffffffu;
+                    if (DT == 4) return (unsigned long long)__double_as_longlong((double)v) & 0x7fffffffffffffffULL;
+                    long long iv = (long long)v;
+                    return (unsigned long long)(iv < 0 ? -iv : iv);
+                };
                 if (FQ && regular) {
-                    // 8-lane pairwise leaves (numpy order); warps beyond the
-                    // leaf count shuffle zeros
+                    // pairwise x^2 over 8-lane leaves (numpy order) + peak
                     if (warp * 4 < L) {
                         double r = 0.0;
                         if (leaf < L) {
                             const int base = leaf * 128 + jj;
-                            double v = (double)xs[base];
+                            const T x0 = xs[base];
+                            const double v = (double)x0;
                             r = v * v;
+                            pk = absbits(x0);
 #pragma unroll
                             for (int i = 1; i < 16; i++) {
-                                double w = (double)xs[base + 8 * i];
+                                const T xi = xs[base + 8 * i];
+                                const double w = (double)xi;
                                 if (SQ_EXACT) r = __fma_rn(w, w, r);
                                 else r = r + w * w;
+                                const unsigned long long ab = absbits(xi);
+                                pk = ab > pk ? ab : pk;
                             }
                         }
                         r += __shfl_xor_sync(0xffffffffu, r, 1);
@@ -395,6 +404,23 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
                         if (L >= 2) r += __shfl_xor_sync(0xffffffffu, r, 8);
                         if (L >= 4) r += __shfl_xor_sync(0xffffffffu, r, 16);
                         pxs = r;
+                    }
+                } else if (F || DT == 2 || FQ) {
+                    // floats: scale from the peak; i32: 64-bit stream decision
+                    if (DT == 3 && (n & 3) == 0) {
+                        const uint4* x4 = (const uint4*)xs;
+                        unsigned m = 0;
+                        for (int i = tid; i < (n >> 2); i += NT) {
+                            uint4 v = x4[i];
+                            m = max(m, max(max(v.x & 0x7fffffffu, v.y & 0x7fffffffu),
+                                           max(v.z & 0x7fffffffu, v.w & 0x7fffffffu)));
+                        }
+                        pk = m;
+                    } else {
+                        for (int i = tid; i < n; i += NT) {
+                            const unsigned long long ab = absbits(xs[i]);
+                            pk = ab > pk ? ab : pk;
+                        }
                     }
                 }
                 unsigned long long pkr = pk;
@@ -406,7 +432,7 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
                 if (lane == 0) { S->pkw[warp] = pkr; S->pxw[warp] = pxs; }
             }
             __syncthreads();  // B1
-            // ================= scalar: gain, code, scale =================
+            // ================= scalar: gain, code, scale (thread 0) =================
             if (tid == 0) {
                 unsigned long long pk = 0;
                 for (int w = 0; w < NW; w++) pk = S->pkw[w] > pk ? S->pkw[w] : pk;
@@ -447,7 +473,6 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
                         }
                     }
                 }
-                // gain
                 if (kind == 0 && !S->initialized) {
                     if (FQ) {  // _init_attenuation (codec.py:155-168)
                         double rms = sqrt(px / (double)n);
@@ -494,7 +519,10 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
                         for (;;) {
                             s = decode_scale_code(code) * ldexp(1.0, (int)fb);
                             double qm = rint(peak * s);
-                            if (qm < 2147483648.0 || fb <= -127) { qpk = qm < 9.2e18 ? (long long)qm : (1LL << 62); break; }
+                            if (qm < 2147483648.0 || fb <= -127) {
+                                qpk = qm < 9.2e18 ? (long long)qm : (1LL << 62);
+                                break;
+                            }
                             fb -= 1;
                         }
                         fbe = (int)fb;
@@ -503,7 +531,7 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
                 S->code = code; S->fbe = fbe; S->s = s; S->aq = aq; S->zero = zero;
                 S->rs = F ? __ddiv_rn(1.0, s) : (aq == 1.0 ? 1.0 : __ddiv_rn(1.0, aq));
                 S->qpk = qpk;
-                // 64-bit streams needed when |d2| could reach 2^31
+                // 64-bit streams when |d2| could reach 2^31 (or q leaves int32)
                 S->wide = (qpk >= (1LL << 29)) ? 1 : 0;
                 S->bad = bad;
             }
@@ -512,18 +540,20 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
             const bool zero = F && S->zero;
             const bool wide = S->wide;
             const bool fq_emit = FQ && kind == 0;
+            const long long hp1 = S->p1, hp2 = S->p2;
 
-            auto quant = [&](T xv) -> long long {
-                if (F) {
-                    if (zero) return 0;
-                    return f2i64(rint((double)xv * s));
-                } else {
-                    long long v = (long long)xv;
-                    if (aq == 1.0) return v;
-                    return f2i64(rint((double)v * aq));
-                }
+            // quantize one sample (codec.py:94-132); fast form valid when |q| < 2^31
+            auto quant32 = [&](T xv) -> int {
+                if (F) return zero ? 0 : __double2int_rn((double)xv * s);
+                if (DT == 2) return aq == 1.0 ? (int)xv : __double2int_rn((double)xv * aq);
+                return aq == 1.0 ? (int)xv : __double2int_rn((double)(int)xv * aq);
             };
-            // dequantize one sample (codec.py:135-146) as the dtype's value in double
+            auto quant64 = [&](T xv) -> long long {
+                if (F) return zero ? 0 : f2i64(rint((double)xv * s));
+                const long long v = (long long)xv;
+                return aq == 1.0 ? v : f2i64(rint((double)v * aq));
+            };
+            // dequantize to the dtype's value in double (codec.py:135-146)
             auto deq = [&](long long q) -> double {
                 const double r = (double)q;
                 if (F) {
@@ -543,8 +573,13 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
                     return (double)yi;
                 }
             };
+            auto qat = [&](int i) -> long long {  // 64-bit q with block context
+                if (i < 0) return i == -1 ? hp1 : hp2;
+                if (i >= n) return 0;
+                return wide ? quant64(xs[i]) : (long long)quant32(xs[i]);
+            };
 
-            // ================= phase B: fixed-quality quantize + residual =================
+            // ================= phase B: fixed-quality residual power =================
             if (fq_emit) {
                 double pds = 0.0;
                 if (regular) {
@@ -552,14 +587,12 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
                         double r = 0.0;
                         if (leaf < L) {
                             const int base = leaf * 128 + jj;
-                            int* qrow = qbuf + leaf * LEAF_STRIDE + jj;
 #pragma unroll 4
                             for (int i = 0; i < 16; i++) {
-                                T xv = xs[base + 8 * i];
-                                long long q = quant(xv);
-                                qrow[8 * i] = (int)q;
-                                double d = (double)xv - deq(q);
-                                double d2 = d * d;
+                                const T xv = xs[base + 8 * i];
+                                const long long q = wide ? quant64(xv) : (long long)quant32(xv);
+                                const double d = (double)xv - deq(q);
+                                const double d2 = d * d;
                                 r = (i == 0) ? d2 : r + d2;
                             }
                         }
@@ -570,14 +603,132 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
                         if (L >= 4) r += __shfl_xor_sync(0xffffffffu, r, 16);
                         pds = r;
                     }
-                } else {
-                    for (int i = tid; i < n; i += NT) qbuf[qaddr(i)] = (int)quant(xs[i]);
                 }
                 if (lane == 0) S->pdw[warp] = pds;
-                // padding samples of a partial block are zero
-                for (int i = n + tid; i < np; i += NT) qbuf[qaddr(i)] = 0;
-                __syncthreads();  // B3
-                if (tid == 0) {
+            }
+
+            // ================= phase C: streams, widths, costs, sign flips =================
+            const int t0 = SPT * tid;
+            const bool active = t0 < np;
+            int q[SPT];
+            int hq1 = 0, hq2 = 0;
+            uint32_t epk[3] = {0u, 0u, 0u};
+            int se[3] = {0, 0, 0};
+            unsigned emax = 0;
+            int flips = 0;
+            if (!wide) {
+                if (active) {
+                    if (DT == 3 && t0 + SPT <= n) {
+                        const float4* x4 = (const float4*)(xs + t0);
+#pragma unroll
+                        for (int c = 0; c < SPT / 4; c++) {
+                            const float4 v = x4[c];
+                            q[4 * c] = quant32((T)v.x); q[4 * c + 1] = quant32((T)v.y);
+                            q[4 * c + 2] = quant32((T)v.z); q[4 * c + 3] = quant32((T)v.w);
+                        }
+                    } else {
+#pragma unroll
+                        for (int k2 = 0; k2 < SPT; k2++) {
+                            const int i = t0 + k2;
+                            q[k2] = (i < n) ? quant32(xs[i]) : 0;
+                        }
+                    }
+                    hq1 = t0 >= 1 ? quant32(xs[t0 - 1]) : (int)hp1;
+                    hq2 = t0 >= 2 ? quant32(xs[t0 - 2]) : (int)hp2;
+                    int m1 = hq1, dprev = hq1 - hq2;
+#pragma unroll
+                    for (int g = 0; g < 4; g++) {
+                        unsigned o0 = 0, o1 = 0, o2 = 0;
+#pragma unroll
+                        for (int kk = 0; kk < 4; kk++) {
+                            const int v0 = q[4 * g + kk];
+                            const int v1 = v0 - m1;
+                            const int v2 = v1 - dprev;
+                            o0 |= wbits32(v0); o1 |= wbits32(v1); o2 |= wbits32(v2);
+                            flips += (int)((unsigned)(v0 ^ m1) >> 31);
+                            m1 = v0; dprev = v1;
+                        }
+                        const bool gv = (t0 + 4 * g) < np;
+                        const int w0 = gv ? bitlen32(o0) : 0, w1 = gv ? bitlen32(o1) : 0,
+                                  w2 = gv ? bitlen32(o2) : 0;
+                        epk[0] |= (uint32_t)w0 << (8 * g);
+                        epk[1] |= (uint32_t)w1 << (8 * g);
+                        epk[2] |= (uint32_t)w2 << (8 * g);
+                        se[0] += w0; se[1] += w1; se[2] += w2;
+                    }
+                    if (t0 == 0) flips -= (int)((unsigned)(q[0] ^ hq1) >> 31);  // no predecessor in the block
+#pragma unroll
+                    for (int k2 = 0; k2 < SPT; k2++) {
+                        if (t0 + k2 == np - 1) S->last1 = q[k2];
+                        if (t0 + k2 == np - 2) S->last2 = q[k2];
+                    }
+                }
+            } else {
+                // 64-bit streams, samples recomputed from x (rare path)
+                if (active) {
+                    long long m1 = qat(t0 - 1), m2 = qat(t0 - 2);
+                    long long dprev = (long long)((unsigned long long)m1 - (unsigned long long)m2);
+                    for (int g = 0; g < 4; g++) {
+                        unsigned long long o0 = 0, o1 = 0, o2 = 0;
+                        for (int kk = 0; kk < 4; kk++) {
+                            const long long v0 = qat(t0 + 4 * g + kk);
+                            const long long v1 = (long long)((unsigned long long)v0 - (unsigned long long)m1);
+                            const long long v2 = (long long)((unsigned long long)v1 - (unsigned long long)dprev);
+                            o0 |= wbits64(v0); o1 |= wbits64(v1); o2 |= wbits64(v2);
+                            if (v0 >= (1LL << 62) || v0 < -(1LL << 62)) o0 |= 1ULL << 63;
+                            if (v1 >= (1LL << 62) || v1 < -(1LL << 62)) o1 |= 1ULL << 63;
+                            if (v2 >= (1LL << 62) || v2 < -(1LL << 62)) o2 |= 1ULL << 63;
+                            if (t0 + 4 * g + kk > 0) flips += ((v0 ^ m1) < 0) ? 1 : 0;
+                            m1 = v0; dprev = v1;
+                        }
+                        const bool gv = (t0 + 4 * g) < np;
+                        int w0 = gv ? bitlen64(o0) : 0, w1 = gv ? bitlen64(o1) : 0, w2 = gv ? bitlen64(o2) : 0;
+                        const unsigned wm = (unsigned)max(w0, max(w1, w2));
+                        emax = wm > emax ? wm : emax;
+                        w0 = min(w0, 255); w1 = min(w1, 255); w2 = min(w2, 255);
+                        epk[0] |= (uint32_t)w0 << (8 * g);
+                        epk[1] |= (uint32_t)w1 << (8 * g);
+                        epk[2] |= (uint32_t)w2 << (8 * g);
+                        se[0] += w0; se[1] += w1; se[2] += w2;
+                    }
+                    if (t0 <= np - 1 && np - 1 < t0 + SPT) {
+                        S->last1 = qat(np - 1);
+                        S->last2 = qat(np - 2);
+                    }
+                }
+            }
+            {
+                const int s0 = __reduce_add_sync(0xffffffffu, se[0]);
+                const int s1 = __reduce_add_sync(0xffffffffu, se[1]);
+                const int s2 = __reduce_add_sync(0xffffffffu, se[2]);
+                const unsigned em = __reduce_max_sync(0xffffffffu, emax);
+                const int fl = __reduce_add_sync(0xffffffffu, flips);
+                if (lane == 0) {
+                    S->sew[0][warp] = s0; S->sew[1][warp] = s1; S->sew[2][warp] = s2;
+                    S->emaxw[warp] = em;
+                    S->monc[warp] = fl;
+                    S->edge_first[warp] = epk[0] & 0xffu | ((epk[1] & 0xffu) << 8) | ((epk[2] & 0xffu) << 16);
+                }
+                if (lane == 31) S->edge_last[warp] = (epk[0] >> 24) | ((epk[1] >> 24) << 8) | ((epk[2] >> 24) << 16);
+            }
+            __syncthreads();  // B4
+            if (tid == 0) {
+                long long tt[3] = {0, 0, 0};
+                unsigned em = 0;
+                int fl = 0;
+                for (int w = 0; w < NW; w++) {
+                    tt[0] += S->sew[0][w]; tt[1] += S->sew[1][w]; tt[2] += S->sew[2][w];
+                    em = S->emaxw[w] > em ? S->emaxw[w] : em;
+                    fl += S->monc[w];
+                }
+                S->sum_e[0] = tt[0]; S->sum_e[1] = tt[1]; S->sum_e[2] = tt[2];
+                if (em > (unsigned)kMaxExponent && !S->bad) S->bad = APAX_ERR_INTERNAL;
+                // every sign change of the nonzero subsequence is witnessed by a
+                // distinct sign-bit flip between neighbours, so cf <= flips /
+                // (2 (np-1)); the exact monitor is only needed above the gate
+                S->exact_mon = (3LL * fl > 2LL * (np - 1)) ? 1 : 0;
+                S->gate = 0;
+                if (fq_emit) {
                     double pd;
                     if (regular) {
                         const int nwd = (L + 3) / 4;
@@ -588,7 +739,7 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
                         pd = v[0];
                     } else {
                         auto td = [&](int i) {
-                            double d = (double)xs[i] - deq((long long)qbuf[qaddr(i)]);
+                            const double d = (double)xs[i] - deq(qat(i));
                             return d * d;
                         };
                         pd = pw_seq(td, 0, n);
@@ -596,173 +747,56 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
                     S->pd = pd;
                 }
             }
-
-            // ================= phase C: streams, widths, costs, monitor =================
-            const int t0 = SPT * tid;                // first sample of this thread
-            const bool active = t0 < np;
-            int q[SPT];
-            long long hq1, hq2;                      // q[t0-1], q[t0-2]
-            const long long hp1 = S->p1, hp2 = S->p2;
-            uint32_t epk[3] = {0u, 0u, 0u};          // per stream: 4 group widths packed
-            int se[3] = {0, 0, 0};
-            unsigned emax = 0;
-            int mon_ch = 0, mon_first = 0, mon_last = 0;
-            if (!wide) {
+            __syncthreads();  // B5
+            if (S->exact_mon) {
+                // exact monitor (transform.py:67-83): ordered sign-change count
+                int ch = 0, fs = 0, lsg = 0;
                 if (active) {
-                    if (fq_emit) {
-                        const int4* qp = (const int4*)(qbuf + qaddr(t0));
-#pragma unroll
-                        for (int c = 0; c < 4; c++) {
-                            int4 v4 = qp[c];
-                            q[4 * c] = v4.x; q[4 * c + 1] = v4.y; q[4 * c + 2] = v4.z; q[4 * c + 3] = v4.w;
-                        }
-                        hq1 = t0 >= 1 ? qbuf[qaddr(t0 - 1)] : hp1;
-                        hq2 = t0 >= 2 ? qbuf[qaddr(t0 - 2)] : (t0 == 1 ? hp1 : hp2);
-                    } else {
-#pragma unroll
-                        for (int k2 = 0; k2 < SPT; k2++) {
-                            int i = t0 + k2;
-                            q[k2] = (i < n) ? (int)quant(xs[i]) : 0;
-                        }
-                        hq1 = t0 >= 1 ? quant(xs[t0 - 1]) : hp1;
-                        hq2 = t0 >= 2 ? quant(xs[t0 - 2]) : hp2;
-                    }
-                    int m1 = (int)hq1, dprev = (int)(hq1 - hq2);
-                    int lastv = 0;
-#pragma unroll
-                    for (int g = 0; g < 4; g++) {
-                        unsigned o0 = 0, o1 = 0, o2 = 0;
-#pragma unroll
-                        for (int kk = 0; kk < 4; kk++) {
-                            const int v0 = q[4 * g + kk];
-                            const int v1 = v0 - m1;
-                            const int v2 = v1 - dprev;
-                            o0 |= wbits32(v0); o1 |= wbits32(v1); o2 |= wbits32(v2);
-                            m1 = v0; dprev = v1;
-                            if (v0) {
-                                if (lastv) mon_ch += ((v0 ^ lastv) < 0);
-                                else mon_first = v0;
-                                lastv = v0;
-                            }
-                        }
-                        const bool gv = (t0 + 4 * g) < np;
-                        const int w0 = gv ? bitlen32(o0) : 0, w1 = gv ? bitlen32(o1) : 0,
-                                  w2 = gv ? bitlen32(o2) : 0;
-                        epk[0] |= (uint32_t)w0 << (8 * g);
-                        epk[1] |= (uint32_t)w1 << (8 * g);
-                        epk[2] |= (uint32_t)w2 << (8 * g);
-                        se[0] += w0; se[1] += w1; se[2] += w2;
-                    }
-                    mon_last = lastv;
-#pragma unroll
                     for (int k2 = 0; k2 < SPT; k2++) {
-                        if (t0 + k2 == np - 1) S->last1 = q[k2];
-                        if (t0 + k2 == np - 2) S->last2 = q[k2];
-                    }
-                }
-            } else {
-                // 64-bit streams, samples recomputed from x (rare path)
-                if (active) {
-                    auto qat = [&](int i) -> long long {
-                        if (i < 0) return i == -1 ? hp1 : hp2;
-                        if (i >= n) return 0;
-                        return quant(xs[i]);
-                    };
-                    long long m1 = qat(t0 - 1), m2 = qat(t0 - 2);
-                    long long dprev = (long long)((unsigned long long)m1 - (unsigned long long)m2);
-                    long long lastv = 0;
-                    for (int g = 0; g < 4; g++) {
-                        unsigned long long o0 = 0, o1 = 0, o2 = 0;
-                        for (int kk = 0; kk < 4; kk++) {
-                            const long long v0 = qat(t0 + 4 * g + kk);
-                            const long long v1 = (long long)((unsigned long long)v0 - (unsigned long long)m1);
-                            const long long v2 = (long long)((unsigned long long)v1 - (unsigned long long)dprev);
-                            o0 |= wbits64(v0); o1 |= wbits64(v1); o2 |= wbits64(v2);
-                            // width of values beyond 2^62 (pathological f64): force > 34
-                            if (v0 >= (1LL << 62) || v0 < -(1LL << 62)) o0 |= 1ULL << 63;
-                            if (v1 >= (1LL << 62) || v1 < -(1LL << 62)) o1 |= 1ULL << 63;
-                            if (v2 >= (1LL << 62) || v2 < -(1LL << 62)) o2 |= 1ULL << 63;
-                            m1 = v0; dprev = v1;
-                            if (v0) {
-                                if (lastv) mon_ch += ((v0 ^ lastv) < 0);
-                                else mon_first = v0 > 0 ? 1 : -1;
-                                lastv = v0;
-                            }
+                        const long long v = qat(t0 + k2 < np ? t0 + k2 : np + 4);
+                        const int sg = (v > 0) - (v < 0);
+                        if (sg) {
+                            if (lsg) ch += (sg != lsg);
+                            else fs = sg;
+                            lsg = sg;
                         }
-                        const bool gv = (t0 + 4 * g) < np;
-                        int w0 = gv ? bitlen64(o0) : 0, w1 = gv ? bitlen64(o1) : 0, w2 = gv ? bitlen64(o2) : 0;
-                        unsigned wm = (unsigned)max(w0, max(w1, w2));
-                        emax = wm > emax ? wm : emax;
-                        w0 = min(w0, 255); w1 = min(w1, 255); w2 = min(w2, 255);
-                        epk[0] |= (uint32_t)w0 << (8 * g);
-                        epk[1] |= (uint32_t)w1 << (8 * g);
-                        epk[2] |= (uint32_t)w2 << (8 * g);
-                        se[0] += w0; se[1] += w1; se[2] += w2;
-                    }
-                    mon_last = lastv > 0 ? 1 : (lastv < 0 ? -1 : 0);
-                    if (t0 <= np - 1 && np - 1 < t0 + SPT) {
-                        S->last1 = qat(np - 1);
-                        S->last2 = qat(np - 2);
                     }
                 }
-            }
-            // signs only
-            int fs = mon_first > 0 ? 1 : (mon_first < 0 ? -1 : 0);
-            int ls = mon_last > 0 ? 1 : (mon_last < 0 ? -1 : 0);
-            // ---- reductions: sums (redux), emax, ordered monitor ----
-            {
-                int s0 = __reduce_add_sync(0xffffffffu, se[0]);
-                int s1 = __reduce_add_sync(0xffffffffu, se[1]);
-                int s2 = __reduce_add_sync(0xffffffffu, se[2]);
-                unsigned em = __reduce_max_sync(0xffffffffu, emax);
-                int ch = mon_ch, f = fs, l = ls;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
-                    int och = __shfl_down_sync(0xffffffffu, ch, o);
-                    int ofl = __shfl_down_sync(0xffffffffu, (f + 1) | ((l + 1) << 2), o);
+                    const int och = __shfl_down_sync(0xffffffffu, ch, o);
+                    const int ofl = __shfl_down_sync(0xffffffffu, (fs + 1) | ((lsg + 1) << 2), o);
                     if (((lane & (2 * o - 1)) == 0) && lane + o < 32) {
-                        int of = (ofl & 3) - 1, ol = ((ofl >> 2) & 3) - 1;
-                        ch += och + ((l != 0 && of != 0 && l != of) ? 1 : 0);
+                        const int of = (ofl & 3) - 1, ol = ((ofl >> 2) & 3) - 1;
+                        ch += och + ((lsg != 0 && of != 0 && lsg != of) ? 1 : 0);
+                        if (!fs) fs = of;
+                        if (ol) lsg = ol;
+                    }
+                }
+                if (lane == 0) { S->monc[warp] = ch; S->monf[warp] = (fs + 1) | ((lsg + 1) << 2); }
+                __syncthreads();
+                if (tid == 0) {
+                    int ch2 = 0, f = 0, l = 0;
+                    for (int w = 0; w < NW; w++) {
+                        const int of = (S->monf[w] & 3) - 1, ol = ((S->monf[w] >> 2) & 3) - 1;
+                        ch2 += S->monc[w] + ((l != 0 && of != 0 && l != of) ? 1 : 0);
                         if (!f) f = of;
                         if (ol) l = ol;
                     }
+                    const double cf = (double)ch2 / (2.0 * (double)(np - 1));
+                    S->gate = cf > 1.0 / 3.0;
                 }
-                if (lane == 0) {
-                    S->sew[0][warp] = s0; S->sew[1][warp] = s1; S->sew[2][warp] = s2;
-                    S->emaxw[warp] = em;
-                    S->monc[warp] = ch;
-                    S->monf[warp] = (f + 1) | ((l + 1) << 2);
-                }
+                __syncthreads();
             }
-            __syncthreads();  // B4
             if (tid == 0) {
-                long long t[3] = {0, 0, 0};
-                unsigned em = 0;
-                int ch = 0, f = 0, l = 0;
-                for (int w = 0; w < NW; w++) {
-                    t[0] += S->sew[0][w]; t[1] += S->sew[1][w]; t[2] += S->sew[2][w];
-                    em = S->emaxw[w] > em ? S->emaxw[w] : em;
-                    int of = (S->monf[w] & 3) - 1, ol = ((S->monf[w] >> 2) & 3) - 1;
-                    ch += S->monc[w] + ((l != 0 && of != 0 && l != of) ? 1 : 0);
-                    if (!f) f = of;
-                    if (ol) l = ol;
-                }
-                S->sum_e[0] = t[0]; S->sum_e[1] = t[1]; S->sum_e[2] = t[2];
-                if (em > (unsigned)kMaxExponent && !S->bad) S->bad = APAX_ERR_INTERNAL;
-                // centre-frequency gate cf > 1/3 (transform.py:75-83, 110-111)
-                double cf = (double)ch / (2.0 * (double)(np - 1));
-                S->gate = cf > 1.0 / 3.0;
                 int sel = 0;
                 if (S->has_pc && !S->gate) {
                     if (S->pc[1] < S->pc[sel]) sel = 1;
                     if (S->pc[2] < S->pc[sel]) sel = 2;
                 }
                 S->sel = sel;
-            }
-            if (kind != 0) {
-                // cost-only passes (lossless halo / warm_self)
-                __syncthreads();
-                if (tid == 0) {
+                if (kind != 0) {
+                    // cost-only passes (lossless halo / warm_self)
                     const long long g4 = 4LL * G;
                     if (kind == 1) {
                         S->has_pc = 1;
@@ -773,8 +807,8 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
                         long long mn = S->sum_e[0];
                         mn = S->sum_e[1] < mn ? S->sum_e[1] : mn;
                         mn = S->sum_e[2] < mn ? S->sum_e[2] : mn;
-                        double bps0 = (double)(4 * mn + g4 + 8LL * HS) / (double)bs;
-                        double att0 = clamp_att(0.0 - 6.02 * (bps0 - P.target), P.att_lo);
+                        const double bps0 = (double)(4 * mn + g4 + 8LL * HS) / (double)bs;
+                        const double att0 = clamp_att(0.0 - 6.02 * (bps0 - P.target), P.att_lo);
                         S->att = att0;
                         S->a = att_to_a(att0);
                     } else {
@@ -783,113 +817,144 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
                     }
                     if (S->bad) report_error(P.status, b, S->bad);
                 }
-                __syncthreads();
-                continue;
             }
-            __syncthreads();  // B5
-            // ================= phase D: JEE + mantissa =================
+            __syncthreads();  // B6
+            if (kind != 0) continue;
+
+            // ================= phase D: JEE (bitmask) + mantissa offsets =================
             const int sel = S->sel;
             const uint32_t es = sel == 0 ? epk[0] : (sel == 1 ? epk[1] : epk[2]);
-            es32[tid + 1] = es;
-            if (tid == 0) { es32[0] = 0u; es32[NT + 1] = 0u; }
-            __syncthreads();  // B6
             const int g0 = 4 * tid;                  // first group of this thread
             int ev[5];
-            ev[0] = (int)(es32[tid] >> 24);          // e[g0-1]
+            int enext;
+            {
+                const uint32_t up = __shfl_up_sync(0xffffffffu, es, 1);
+                const uint32_t dn = __shfl_down_sync(0xffffffffu, es, 1);
+                ev[0] = lane > 0 ? (int)(up >> 24)
+                                 : (warp > 0 ? (int)((S->edge_last[warp - 1] >> (8 * sel)) & 0xffu) : 0);
 #pragma unroll
-            for (int g = 0; g < 4; g++) ev[g + 1] = (int)((es >> (8 * g)) & 0xffu);
-            const int enext = (int)(es32[tid + 2] & 0xffu);
-            int pair = 0, single = 0;                // bit k: position g0+k
-#pragma unroll
-            for (int k2 = 0; k2 < 4; k2++) {
-                const int p = g0 + k2;
-                const int d = ev[k2 + 1] - ev[k2];
-                const int dn = (k2 < 3 ? ev[k2 + 2] : enext) - ev[k2 + 1];
-                const bool s1 = (unsigned)(d + 1) <= 2u, s1n = (unsigned)(dn + 1) <= 2u;
-                const bool s2 = (unsigned)(d + 2) <= 4u;
-                if (p != 0 && p + 1 < G && s1 && s1n) pair |= 1 << k2;
-                if (p != 0 && s2) single |= 1 << k2;
-            }
-            const int nvalid = (g0 < G) ? min(4, G - g0) : 0;
-            uint32_t f = kJfId;
-            unsigned mbits = 0;
-            if (nvalid > 0) {
-                int o[2], nb[2];
-#pragma unroll
-                for (int s0 = 0; s0 < 2; s0++) {
-                    int st = s0, cnt = 0;
-#pragma unroll
-                    for (int k2 = 0; k2 < 4; k2++) {
-                        if (k2 >= nvalid) break;
-                        if (st) { st = 0; continue; }
-                        if ((pair >> k2) & 1) { cnt += 1; st = 1; }
-                        else cnt += ((single >> k2) & 1) ? 1 : 3;
-                    }
-                    o[s0] = st; nb[s0] = cnt;
-                }
-                f = jf_pack(o[0], o[1], nb[0], nb[1]);
-#pragma unroll
-                for (int g = 0; g < 4; g++) mbits += (g < nvalid) ? 4u * (unsigned)ev[g + 1] : 0u;
-            }
-            // CTA exclusive scan of (f, mbits)
-            uint32_t fi = f;
-            unsigned bi = mbits;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                uint32_t of = __shfl_up_sync(0xffffffffu, fi, d);
-                unsigned ob = __shfl_up_sync(0xffffffffu, bi, d);
-                if (lane >= d) { fi = jf_compose(of, fi); bi += ob; }
-            }
-            uint32_t fx = __shfl_up_sync(0xffffffffu, fi, 1);
-            unsigned bx = __shfl_up_sync(0xffffffffu, bi, 1);
-            if (lane == 0) { fx = kJfId; bx = 0; }
-            if (lane == 31) { S->scf[warp] = fi; S->scb[warp] = bi; }
-            __syncthreads();  // B7
-            if (tid == 0) {
-                uint32_t acc = kJfId;
-                unsigned accb = 0;
-                for (int w = 0; w < NW; w++) {
-                    S->pre_f[w] = acc; S->pre_b[w] = accb;
-                    acc = jf_compose(acc, S->scf[w]);
-                    accb += S->scb[w];
-                }
-                const long long nib = (acc >> 2) & 0x7fff;
-                S->jee_nib = nib;
-                S->bits = accb;
-                S->blen = HS + ((nib + 1) >> 1) + ((long long)accb + 7) / 8;
-            }
-            __syncthreads();  // B8
-            const uint32_t fpre = jf_compose(S->pre_f[warp], fx);
-            const unsigned bpre = S->pre_b[warp] + bx;
-            const long long wb = S->tail_len;            // window byte of block start
-            const long long jee_bytes = (S->jee_nib + 1) >> 1;
-            if (nvalid > 0 && !S->bad) {
-                // JEE nibbles
-                BitWriter bw;
-                bw.init(win, 8 * (wb + HS) + 4LL * ((fpre >> 2) & 0x7fff));
-                int st = fpre & 1;
+                for (int g = 0; g < 4; g++) ev[g + 1] = (int)((es >> (8 * g)) & 0xffu);
+                enext = lane < 31 ? (int)(dn & 0xffu)
+                                  : (warp < NW - 1 ? (int)((S->edge_first[warp + 1] >> (8 * sel)) & 0xffu) : 0);
+                int pb = 0, eb = 0;
 #pragma unroll
                 for (int k2 = 0; k2 < 4; k2++) {
-                    if (k2 >= nvalid) break;
-                    if (st) { st = 0; continue; }
+                    const int p = g0 + k2;
+                    const int d = ev[k2 + 1] - ev[k2];
+                    const int dn2 = (k2 < 3 ? ev[k2 + 2] : enext) - ev[k2 + 1];
+                    const bool s1 = (unsigned)(d + 1) <= 2u, s1n = (unsigned)(dn2 + 1) <= 2u;
+                    const bool s2 = (unsigned)(d + 2) <= 4u;
+                    const bool pr = p != 0 && p + 1 < G && s1 && s1n;
+                    if (pr) pb |= 1 << k2;
+                    else if (p == 0 || !s2) eb |= 1 << k2;
+                }
+                // 32-position words: 8 lanes x 4 positions
+                const int sh = 4 * (lane & 7);
+                uint32_t pw = (uint32_t)pb << sh, ew = (uint32_t)eb << sh;
+                pw |= __shfl_xor_sync(0xffffffffu, pw, 1);
+                ew |= __shfl_xor_sync(0xffffffffu, ew, 1);
+                pw |= __shfl_xor_sync(0xffffffffu, pw, 2);
+                ew |= __shfl_xor_sync(0xffffffffu, ew, 2);
+                pw |= __shfl_xor_sync(0xffffffffu, pw, 4);
+                ew |= __shfl_xor_sync(0xffffffffu, ew, 4);
+                if ((lane & 7) == 0) { S->pw[warp * 4 + (lane >> 3)] = pw; S->ew[warp * 4 + (lane >> 3)] = ew; }
+            }
+            // mantissa bits of this thread and warp-inclusive prefix
+            unsigned mb = 0;
+#pragma unroll
+            for (int g = 0; g < 4; g++) mb += (g0 + g < G) ? 4u * (unsigned)ev[g + 1] : 0u;
+            unsigned mbi = mb;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const unsigned o = __shfl_up_sync(0xffffffffu, mbi, d);
+                if (lane >= d) mbi += o;
+            }
+            if (lane == 31) S->mbw[warp] = mbi;
+            __syncthreads();  // B7
+            if (warp == 0) {
+                // word m = positions 32m .. 32m+31
+                const int m = lane;
+                const uint32_t Pm = S->pw[m], Em = S->ew[m];
+                const int lo = 32 * m;
+                const uint32_t V = (G >= lo + 32) ? 0xffffffffu : (G > lo ? ((1u << (G - lo)) - 1u) : 0u);
+                uint32_t c0, c1;
+                const uint32_t C0 = consumed_word(Pm, 0u, &c0);
+                const uint32_t C1 = consumed_word(Pm, 1u, &c1);
+                // carry scan of 1-bit transfer functions f(c) = c ? c1 : c0
+                uint32_t f0 = c0, f1 = c1;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t o0 = __shfl_up_sync(0xffffffffu, f0, d);
+                    const uint32_t o1 = __shfl_up_sync(0xffffffffu, f1, d);
+                    if (lane >= d) {
+                        const uint32_t n0 = o0 ? f1 : f0, n1 = o1 ? f1 : f0;
+                        f0 = n0; f1 = n1;
+                    }
+                }
+                uint32_t cin = __shfl_up_sync(0xffffffffu, f0, 1);  // exclusive, applied to 0
+                if (lane == 0) cin = 0u;
+                const uint32_t Cm = cin ? C1 : C0;
+                const uint32_t Tm = V & ~Cm;          // token starts
+                const uint32_t Xm = Tm & Em;          // escapes
+                const int nibm = __popc(Tm) + 2 * __popc(Xm);
+                int ni = nibm;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int o = __shfl_up_sync(0xffffffffu, ni, d);
+                    if (lane >= d) ni += o;
+                }
+                S->tw[m] = Tm; S->xw[m] = Xm; S->jw[m] = Tm & Pm;
+                S->nibpre[m] = ni - nibm;
+                unsigned mbx = 0, mbt = 0;
+                if (lane < NW) mbx = S->mbw[lane];
+                unsigned mbs = mbx;
+#pragma unroll
+                for (int d = 1; d < NW; d <<= 1) {
+                    const unsigned o = __shfl_up_sync(0xffffffffu, mbs, d);
+                    if (lane >= d) mbs += o;
+                }
+                mbt = __shfl_sync(0xffffffffu, mbs, NW - 1);
+                if (lane < NW) S->mbpre[lane] = mbs - mbx;
+                const int nib_total = __shfl_sync(0xffffffffu, ni, 31);
+                if (lane == 0) {
+                    S->jee_nib = nib_total;
+                    S->bits = mbt;
+                    S->blen = HS + ((nib_total + 1) >> 1) + ((long long)mbt + 7) / 8;
+                }
+            }
+            __syncthreads();  // B8
+            const long long wb = S->tail_len;            // window byte of block start
+            const long long jee_bytes = (S->jee_nib + 1) >> 1;
+            if (g0 < G && !S->bad) {
+                const int w = tid >> 3, sh = 4 * (tid & 7);
+                const uint32_t below = (1u << sh) - 1u;
+                const uint32_t Tw = S->tw[w], Xw = S->xw[w], Jw = S->jw[w];
+                const int nib_off = S->nibpre[w] + __popc(Tw & below) + 2 * __popc(Xw & below);
+                const int Tb = (Tw >> sh) & 15, Xb = (Xw >> sh) & 15, Jb = (Jw >> sh) & 15;
+                BitWriter bw;
+                bw.init(win, 8 * (wb + HS) + 4LL * nib_off);
+#pragma unroll
+                for (int k2 = 0; k2 < 4; k2++) {
+                    if (!((Tb >> k2) & 1)) continue;
                     const int e = ev[k2 + 1];
                     const int d = e - ev[k2];
-                    if ((pair >> k2) & 1) {
-                        const int dn = (k2 < 3 ? ev[k2 + 2] : enext) - e;
-                        bw.put32((uint32_t)((d + 1) * 3 + (dn + 1)), 4);
-                        st = 1;
-                    } else if ((single >> k2) & 1) {
-                        bw.put32((uint32_t)(11 + d), 4);
-                    } else {
+                    if ((Jb >> k2) & 1) {
+                        const int dn2 = (k2 < 3 ? ev[k2 + 2] : enext) - e;
+                        bw.put32((uint32_t)((d + 1) * 3 + (dn2 + 1)), 4);
+                    } else if ((Xb >> k2) & 1) {
                         bw.put32(0xF00u | (uint32_t)e, 12);
+                    } else {
+                        bw.put32((uint32_t)(11 + d), 4);
                     }
                 }
                 bw.flush();
-                // mantissa bits
+            }
+            if (g0 < G && !S->bad) {
+                const unsigned mbx = S->mbpre[warp] + (mbi - mb);
                 BitWriter mw;
-                mw.init(win, 8 * (wb + HS + jee_bytes) + (long long)bpre);
+                mw.init(win, 8 * (wb + HS + jee_bytes) + (long long)mbx);
                 if (!wide) {
-                    int m1 = (int)hq1, dprev = (int)(hq1 - hq2);
+                    int m1 = hq1, dprev = hq1 - hq2;
 #pragma unroll
                     for (int g = 0; g < 4; g++) {
                         int vs[4];
@@ -902,11 +967,11 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
                             vs[kk] = sel == 0 ? v0 : (sel == 1 ? v1 : v2);
                         }
                         const int w = ev[g + 1];
-                        if (g >= nvalid || w == 0) continue;
+                        if (g0 + g >= G || w == 0) continue;
                         if (w <= 8) {
                             const uint32_t m = (1u << w) - 1u;
-                            uint32_t c = ((uint32_t)vs[0] & m) << (3 * w) | ((uint32_t)vs[1] & m) << (2 * w) |
-                                         ((uint32_t)vs[2] & m) << w | ((uint32_t)vs[3] & m);
+                            const uint32_t c = ((uint32_t)vs[0] & m) << (3 * w) | ((uint32_t)vs[1] & m) << (2 * w) |
+                                               ((uint32_t)vs[2] & m) << w | ((uint32_t)vs[3] & m);
                             mw.put32(c, 4 * w);
                         } else if (w <= 16) {
                             const uint32_t m = (1u << w) - 1u;
@@ -918,11 +983,6 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
                         }
                     }
                 } else {
-                    auto qat = [&](int i) -> long long {
-                        if (i < 0) return i == -1 ? hp1 : hp2;
-                        if (i >= n) return 0;
-                        return quant(xs[i]);
-                    };
                     long long m1 = qat(t0 - 1), m2 = qat(t0 - 2);
                     long long dprev = (long long)((unsigned long long)m1 - (unsigned long long)m2);
                     for (int g = 0; g < 4; g++) {
@@ -932,7 +992,7 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
                             const long long v1 = (long long)((unsigned long long)v0 - (unsigned long long)m1);
                             const long long v2 = (long long)((unsigned long long)v1 - (unsigned long long)dprev);
                             m1 = v0; dprev = v1;
-                            if (g < nvalid && w) mw.put((unsigned long long)(sel == 0 ? v0 : (sel == 1 ? v1 : v2)), w);
+                            if (g0 + g < G && w) mw.put((unsigned long long)(sel == 0 ? v0 : (sel == 1 ? v1 : v2)), w);
                         }
                     }
                 }
@@ -942,9 +1002,9 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
                 // block header (dtypes.py:156-165)
                 const int restart = (S->emitted == 0);
                 const int code = S->code;
-                uint32_t hb[6] = {(uint32_t)((sel & 3) | (restart ? 4 : 0)), (uint32_t)(code & 0xFF),
-                                  (uint32_t)((code >> 8) & 0xFF), 0u,
-                                  (uint32_t)(uint8_t)(int8_t)S->fbe, 0u};
+                const uint32_t hb[6] = {(uint32_t)((sel & 3) | (restart ? 4 : 0)), (uint32_t)(code & 0xFF),
+                                        (uint32_t)((code >> 8) & 0xFF), 0u,
+                                        (uint32_t)(uint8_t)(int8_t)S->fbe, 0u};
                 for (int k2 = 0; k2 < HS; k2++) {
                     const long long bp = wb + k2;
                     atomicOr(&win[bp >> 2], hb[k2] << (8 * (bp & 3)));
@@ -984,16 +1044,16 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
                         if (S->emitted == 0) {
                             long long mn = S->pc[0] < S->pc[1] ? S->pc[0] : S->pc[1];
                             mn = S->pc[2] < mn ? S->pc[2] : mn;
-                            double bps0 = (double)(mn + 8LL * HS) / (double)bs;
+                            const double bps0 = (double)(mn + 8LL * HS) / (double)bs;
                             S->att = clamp_att(S->att - 6.02 * (bps0 - P.target), P.att_lo);
                         } else {
-                            double err = (double)(S->blen * 8) / (double)bs - P.target;
+                            const double err = (double)(S->blen * 8) / (double)bs - P.target;
                             S->att = clamp_att(S->att - clamp_step(0.75 * err), P.att_lo);
                         }
                     } else if (P.mode == 2) {
-                        double px = S->px / (double)n, pd = S->pd / (double)n;
+                        const double px = S->px / (double)n, pd = S->pd / (double)n;
                         if (px > 0.0) {
-                            double measured = (pd == 0.0) ? INFINITY : 10.0 * log10(px / pd);
+                            const double measured = (pd == 0.0) ? INFINITY : 10.0 * log10(px / pd);
                             if (isfinite(measured))
                                 S->att = clamp_att(S->att - clamp_step(0.5 * (measured - P.target)), P.att_lo);
                         }
@@ -1013,7 +1073,7 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
                 if (tid < S->tail_len)
                     P.out[kFileHeader + S->win_base + tid] = ((const uint8_t*)S->tail)[tid];
             } else if (tid == 0) {
-                uint4 t4 = make_uint4(S->tail[0], S->tail[1], S->tail[2], S->tail[3]);
+                const uint4 t4 = make_uint4(S->tail[0], S->tail[1], S->tail[2], S->tail[3]);
                 *(uint4*)(slot + S->win_base) = t4;
             }
         }
@@ -1030,17 +1090,14 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
         }
         __syncthreads();
         const long long prefix = S->prefix;
-        if (!S->direct) {
-            __threadfence_block();
-            copy_out<false>(P.out + kFileHeader + prefix, (const uint32_t*)slot, S->unit_len);
-        }
+        if (!S->direct) copy_out<false>(P.out + kFileHeader + prefix, (const uint32_t*)slot, S->unit_len);
         if (u == 0 && tid < kFileHeader) {
             unsigned char h[kFileHeader];
             h[0] = 'A'; h[1] = 'P'; h[2] = 'A'; h[3] = 'X';
             h[4] = 1; h[5] = (unsigned char)DT; h[6] = (unsigned char)P.mode; h[7] = 0;
             for (int k2 = 0; k2 < 4; k2++) h[8 + k2] = (unsigned char)((unsigned)bs >> (8 * k2));
             for (int k2 = 0; k2 < 8; k2++) h[12 + k2] = (unsigned char)((unsigned long long)P.n >> (8 * k2));
-            unsigned long long tb = (unsigned long long)__double_as_longlong(P.target);
+            const unsigned long long tb = (unsigned long long)__double_as_longlong(P.target);
             for (int k2 = 0; k2 < 8; k2++) h[20 + k2] = (unsigned char)(tb >> (8 * k2));
             P.out[tid] = h[tid];
         }
@@ -1055,12 +1112,9 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
 
 size_t encode_v2_smem_bytes(int dt, int mode, int window_bytes) {
     auto al = [](size_t v) { return (v + 127) & ~(size_t)127; };
+    (void)mode;
     size_t w = (size_t)dt_width(dt);
-    size_t s = al(sizeof(v2::St)) + 2 * al((size_t)v2::MAXBS * w);
-    if (mode == 2) s += al((size_t)32 * v2::LEAF_STRIDE * 4);
-    s += al((size_t)(v2::NT + 2) * 4);
-    s += (size_t)window_bytes + 16 + 16;
-    return s;
+    return al(sizeof(v2::St)) + 2 * al((size_t)v2::MAXBS * w) + (size_t)window_bytes + 32;
 }
 
 bool encode_v2_supported(int bs) {
