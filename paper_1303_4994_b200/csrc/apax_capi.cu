@@ -100,6 +100,7 @@ int plan_encode(long long n, int dt, int mode, int bs, long long seg, EncPlan* p
 struct DecPlan {
     long long n_blocks;
     int payload_cap;
+    int v2;
     size_t smem;
     int grid;
     long long ws_carry, ws_ticket, ws_offsets, ws_total;
@@ -113,8 +114,15 @@ int plan_decode(long long n, int dt, int bs, DecPlan* p) {
     p->n_blocks = (n + bs - 1) / bs;
     long long cap = max_block_bytes(dt, bs) + 64;
     p->payload_cap = (int)((cap + 15) & ~15LL);
-    p->smem = decode_smem_bytes(dt, bs, p->payload_cap);
-    int resident = decode_resident_ctas(dt, p->smem);
+    p->v2 = decode_v2_supported(bs) && env_int("APAX_FORCE_V1", 0) == 0;
+    int resident;
+    if (p->v2) {
+        p->smem = decode_v2_smem_bytes(dt, bs, p->payload_cap);
+        resident = decode_v2_resident_ctas(dt, p->smem);
+    } else {
+        p->smem = decode_smem_bytes(dt, bs, p->payload_cap);
+        resident = decode_resident_ctas(dt, p->smem);
+    }
     long long g = p->n_blocks < resident ? p->n_blocks : resident;
     p->grid = (int)(g < 1 ? 1 : g);
     p->ws_carry = 0;
@@ -280,6 +288,7 @@ int apax_decode(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, int b
     P.carry = (unsigned long long*)(w + p.ws_carry);
     P.ticket = (unsigned int*)(w + p.ws_ticket);
     P.payload_cap = p.payload_cap;
+    if (p.v2) return launch_decode_v2(dtype, P, p.grid, p.smem, s);
     return launch_decode(dtype, P, p.grid, p.smem, s);
 }
 

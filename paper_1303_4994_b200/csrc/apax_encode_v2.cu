@@ -5,7 +5,7 @@
 // encode_stream, pkg/src/apax/codec.py:258-285 / encode_block :192-255); the
 // v1 kernel remains the general path (any block size 64..16384).
 //
-// Per CTA (256 threads, persistent, ticketed units of consecutive blocks):
+// Per CTA (256 threads, persistent, round-robin units of consecutive blocks):
 //   * TMA bulk copies (cp.async.bulk + mbarrier) double-buffer the next
 //     block's samples into shared memory while the current one is coded;
 //   * phase A  block peak (|x| bit-max) and, for fixed quality, numpy's
@@ -81,35 +81,7 @@ struct St {
     unsigned long long mbar[2];
 };
 
-// ---------------------------------------------------------------------------
-// TMA bulk copy + mbarrier
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t sa(const void* p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(unsigned long long* b) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(sa(b)) : "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t bytes,
-                                         unsigned long long* bar) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
-                 :: "r"(sa(bar)), "r"(bytes) : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 :: "r"(sa(dst)), "l"(src), "r"(bytes), "r"(sa(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phase) {
-    uint32_t ok = 0;
-    while (!ok) {
-        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                     : "=r"(ok) : "r"(sa(bar)), "r"(phase) : "memory");
-    }
-}
+using namespace apax::tma;
 
 // ---------------------------------------------------------------------------
 // small helpers
@@ -264,11 +236,24 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
     __syncthreads();
     uint32_t phase[2] = {0u, 0u};
 
-    for (;;) {
-        if (tid == 0) S->unit = (long long)atomicAdd(P.ticket, 1u);
-        __syncthreads();
-        const long long u = S->unit;
-        if (u >= P.n_units) break;
+    auto block_n = [&](long long b) -> int {
+        long long r = P.n - b * (long long)bs;
+        return (int)(r < bs ? r : bs);
+    };
+    auto tma_ok = [&](long long b) -> bool {
+        const T* src = (const T*)P.x + b * (long long)bs;
+        long long bytes = (long long)block_n(b) * (long long)sizeof(T);
+        return ((((uintptr_t)src) & 15) == 0) && ((bytes & 15) == 0);
+    };
+    auto first_block = [&](long long uu) -> long long {
+        const long long bb = uu * P.unit_blocks;
+        return (P.halo && bb > 0) ? bb - 1 : bb;
+    };
+    long long loaded_b = -1, inflight_b = -1;
+    int cur = 0, inflight_buf = 0;
+    // units are assigned round-robin; the launch is cooperative, so every
+    // unit's predecessor is on a co-resident CTA (look-back cannot deadlock)
+    for (long long u = blockIdx.x; u < P.n_units; u += gridDim.x) {
         const long long b0 = u * P.unit_blocks;
         const long long b1 = (b0 + P.unit_blocks < P.n_blocks) ? b0 + P.unit_blocks : P.n_blocks;
         if (tid == 0) {
@@ -293,28 +278,19 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
             if (warm) return k < 2 ? b0 : b0 + k - 2;
             return b0 + k;
         };
-        auto block_n = [&](long long b) -> int {
-            long long r = P.n - b * (long long)bs;
-            return (int)(r < bs ? r : bs);
-        };
-        auto tma_ok = [&](long long b) -> bool {
-            const T* src = (const T*)P.x + b * (long long)bs;
-            long long bytes = (long long)block_n(b) * (long long)sizeof(T);
-            return ((((uintptr_t)src) & 15) == 0) && ((bytes & 15) == 0);
-        };
-        long long loaded_b = -1;
-        int cur = 0;
         __syncthreads();
         {
-            long long bfirst = pass_block(0);
-            if (tma_ok(bfirst) && tid == 0) {
-                fence_proxy_async();
-                tma_load(xbuf[0], (const T*)P.x + bfirst * (long long)bs,
-                         (uint32_t)(block_n(bfirst) * sizeof(T)), &S->mbar[0]);
+            const long long bfirst = pass_block(0);
+            if (bfirst != loaded_b && bfirst != inflight_b) {
+                inflight_b = bfirst;
+                inflight_buf = cur ^ 1;
+                if (tma_ok(bfirst) && tid == 0) {
+                    fence_proxy_async();
+                    tma_load(xbuf[inflight_buf], (const T*)P.x + bfirst * (long long)bs,
+                             (uint32_t)(block_n(bfirst) * sizeof(T)), &S->mbar[inflight_buf]);
+                }
             }
         }
-        long long inflight_b = pass_block(0);
-        int inflight_buf = 0;
 
         for (long long k = 0; k < npass; k++) {
             const long long b = pass_block(k);
@@ -345,6 +321,10 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
                 for (long long kk = k + 1; kk < npass; kk++) {
                     long long bb = pass_block(kk);
                     if (bb != b) { nb = bb; break; }
+                }
+                if (nb < 0 && u + gridDim.x < P.n_units) {  // next unit's first block
+                    const long long bb = first_block(u + gridDim.x);
+                    if (bb != b) nb = bb;
                 }
                 __syncthreads();  // the other buffer's readers are done
                 if (nb >= 0) {
@@ -1151,7 +1131,10 @@ int launch_encode_v2(int dt, const EncParams& P, int grid, size_t smem, cudaStre
         return APAX_ERR_CUDA;
     EncParams p = P;
     void* args[] = {&p};
-    if (cudaLaunchKernel(fn, dim3(grid), dim3(v2::NT), args, smem, st) != cudaSuccess) return APAX_ERR_CUDA;
+    // cooperative: co-residency of all CTAs (round-robin units look back at
+    // their predecessors' CTAs)
+    if (cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(v2::NT), args, smem, st) != cudaSuccess)
+        return APAX_ERR_CUDA;
     return APAX_OK;
 }
 

@@ -58,6 +58,10 @@ bool encode_v2_supported(int bs);
 int encode_v2_resident_ctas(int dt, size_t smem);
 int launch_encode_v2(int dt, const EncParams& P, int grid, size_t smem, cudaStream_t st);
 int launch_decode(int dt, const DecParams& P, int grid, size_t smem, cudaStream_t st);
+size_t decode_v2_smem_bytes(int dt, int bs, int payload_cap);
+bool decode_v2_supported(int bs);
+int decode_v2_resident_ctas(int dt, size_t smem);
+int launch_decode_v2(int dt, const DecParams& P, int grid, size_t smem, cudaStream_t st);
 int launch_walk(const uint8_t* blob, long long nbytes, long long n, int bs, int dt, long long n_blocks,
                 long long* offsets, unsigned long long* status, cudaStream_t st);
 
