@@ -93,7 +93,7 @@ int plan_encode(long long n, int dt, int mode, int bs, long long seg, EncPlan* p
     p->ws_lookback = 0;
     p->ws_ticket = (p->n_units * 8 + 255) & ~255LL;
     p->ws_slots = p->ws_ticket + 256;
-    p->ws_total = p->ws_slots + (long long)p->grid * p->slot_bytes;
+    p->ws_total = p->ws_slots + (long long)p->grid * p->slot_bytes * (p->v2 ? 2 : 1);
     return APAX_OK;
 }
 

@@ -480,7 +480,7 @@ __global__ void __launch_bounds__(NT, 2) decode_v2_kernel(DecParams P) {
             }
         }
         __syncthreads();
-        if (tid == 0) {
+        if (warp == 0) {
             const unsigned long long L1 = (unsigned long long)S->l1;
             const unsigned long long L2 = (unsigned long long)S->l2;
             const unsigned long long unp = (unsigned long long)np;
@@ -490,36 +490,67 @@ __global__ void __launch_bounds__(NT, 2) decode_v2_kernel(DecParams P) {
             else M = {unp + 1, 0ULL - unp, unp, 0ULL - (unp - 1), L1, L2};
             unsigned long long in1 = 0, in2 = 0;
             if (sel != 0 && !S->restart && b > 0) {
-                cw[1] = M.m11; cw[2] = M.m12; cw[3] = M.m21; cw[4] = M.m22; cw[5] = M.c1; cw[6] = M.c2;
-                __threadfence();
-                st_release(&cw[0], kFlagAgg);
-                Aff acc = {1, 0, 0, 1, 0, 0};
-                long long k = b - 1;
+                if (lane == 0) {
+                    cw[1] = M.m11; cw[2] = M.m12; cw[3] = M.m21; cw[4] = M.m22; cw[5] = M.c1; cw[6] = M.c2;
+                    __threadfence();
+                    st_release(&cw[0], kFlagAgg);
+                }
+                // warp-parallel look-back: lane l examines block b-1-l
+                Aff acc = {1, 0, 0, 1, 0, 0};   // composition of the blocks passed so far
+                long long base = b - 1;
                 for (;;) {
-                    const unsigned long long* ck = P.carry + 16 * k;
-                    const unsigned long long fl = ld_acquire(&ck[0]);
-                    if (fl == kFlagInc) {
-                        const unsigned long long q1 = __ldcg(&ck[8]), q2 = __ldcg(&ck[9]);
-                        in1 = acc.m11 * q1 + acc.m12 * q2 + acc.c1;
-                        in2 = acc.m21 * q1 + acc.m22 * q2 + acc.c2;
+                    const long long k = base - lane;
+                    unsigned long long fl = kFlagInc;
+                    const unsigned long long* ck = P.carry + 16 * (k >= 0 ? k : 0);
+                    if (k >= 0) fl = ld_acquire(&ck[0]);
+                    const unsigned inc = __ballot_sync(0xffffffffu, fl == kFlagInc);
+                    const unsigned nrd = __ballot_sync(0xffffffffu, fl != kFlagInc && fl != kFlagAgg);
+                    const int first_inc = inc ? __ffs(inc) - 1 : 32;
+                    const unsigned need = first_inc >= 31 ? 0xffffffffu : ((2u << first_inc) - 1u);
+                    if (nrd & need) { __nanosleep(32); continue; }
+                    Aff Ml = {1, 0, 0, 1, 0, 0};
+                    if (lane < first_inc) {
+                        Ml = {__ldcg(&ck[1]), __ldcg(&ck[2]), __ldcg(&ck[3]), __ldcg(&ck[4]),
+                              __ldcg(&ck[5]), __ldcg(&ck[6])};
+                    } else if (lane == first_inc) {
+                        Ml = {0, 0, 0, 0, (k >= 0 ? __ldcg(&ck[8]) : 0ULL), (k >= 0 ? __ldcg(&ck[9]) : 0ULL)};
+                    }
+                    // ordered tree: lane 0 ends with M_0 o M_1 o ... o M_31
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        Aff O;
+                        O.m11 = __shfl_down_sync(0xffffffffu, Ml.m11, d);
+                        O.m12 = __shfl_down_sync(0xffffffffu, Ml.m12, d);
+                        O.m21 = __shfl_down_sync(0xffffffffu, Ml.m21, d);
+                        O.m22 = __shfl_down_sync(0xffffffffu, Ml.m22, d);
+                        O.c1 = __shfl_down_sync(0xffffffffu, Ml.c1, d);
+                        O.c2 = __shfl_down_sync(0xffffffffu, Ml.c2, d);
+                        if ((lane & (2 * d - 1)) == 0 && lane + d < 32) Ml = aff_compose(Ml, O);
+                    }
+                    Aff tot;
+                    tot.m11 = __shfl_sync(0xffffffffu, Ml.m11, 0);
+                    tot.m12 = __shfl_sync(0xffffffffu, Ml.m12, 0);
+                    tot.m21 = __shfl_sync(0xffffffffu, Ml.m21, 0);
+                    tot.m22 = __shfl_sync(0xffffffffu, Ml.m22, 0);
+                    tot.c1 = __shfl_sync(0xffffffffu, Ml.c1, 0);
+                    tot.c2 = __shfl_sync(0xffffffffu, Ml.c2, 0);
+                    acc = aff_compose(acc, tot);
+                    if (inc) {  // acc is constant now (ends in a concrete history)
+                        in1 = acc.c1;
+                        in2 = acc.c2;
                         break;
                     }
-                    if (fl == kFlagAgg) {
-                        const Aff Mk = {__ldcg(&ck[1]), __ldcg(&ck[2]), __ldcg(&ck[3]),
-                                        __ldcg(&ck[4]), __ldcg(&ck[5]), __ldcg(&ck[6])};
-                        acc = aff_compose(acc, Mk);
-                        k--;
-                        continue;
-                    }
-                    __nanosleep(32);
+                    base -= 32;
                 }
             }
-            cw[8] = M.m11 * in1 + M.m12 * in2 + M.c1;
-            cw[9] = M.m21 * in1 + M.m22 * in2 + M.c2;
-            __threadfence();
-            st_release(&cw[0], kFlagInc);
-            S->p1 = (long long)in1;
-            S->p2 = (long long)in2;
+            if (lane == 0) {
+                cw[8] = M.m11 * in1 + M.m12 * in2 + M.c1;
+                cw[9] = M.m21 * in1 + M.m22 * in2 + M.c2;
+                __threadfence();
+                st_release(&cw[0], kFlagInc);
+                S->p1 = (long long)in1;
+                S->p2 = (long long)in2;
+            }
         }
         __syncthreads();
         // ---- finalize, dequantize, store ----

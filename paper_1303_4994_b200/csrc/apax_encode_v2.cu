@@ -79,6 +79,9 @@ struct St {
     int nibpre[32];
     unsigned mbw[NW], mbpre[NW];
     unsigned long long mbar[2];
+    // deferred placement of the previous unit (look-back + copy-out)
+    long long pend_u, pend_len, pend_b0, pend_b1, pend_k, pend_acc, pend_prefix;
+    int pend_slot, pend_ready;
 };
 
 using namespace apax::tma;
@@ -226,15 +229,74 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
     uint32_t* win = (uint32_t*)(smem + off);
     const int win_words = P.stage_bytes / 4;
 
-    uint8_t* slot = P.slots + (long long)blockIdx.x * P.slot_bytes;
+    uint8_t* slots2[2];
+    slots2[0] = P.slots + (long long)blockIdx.x * 2 * P.slot_bytes;
+    slots2[1] = slots2[0] + P.slot_bytes;
+    int cur_slot = 0;
+    uint8_t* slot = slots2[0];
 
     if (tid == 0) {
         mbar_init(&S->mbar[0]);
         mbar_init(&S->mbar[1]);
         fence_mbar_init();
+        S->pend_u = -1;
+        S->pend_ready = 0;
     }
     __syncthreads();
     uint32_t phase[2] = {0u, 0u};
+
+    // ---- deferred placement helpers ----
+    // one look-back window (32 predecessors) for the pending unit; warp 0.
+    auto lookback_try = [&](bool blocking) {
+        if (S->pend_u < 0 || S->pend_ready) return;
+        for (;;) {
+            const long long kq = S->pend_k;
+            const long long idx = kq - lane;
+            unsigned long long vq = (idx >= 0) ? ld_acquire(&P.lookback[idx]) : kFlagInc;
+            const unsigned long long fl = vq & ~kValMask;
+            const unsigned inc = __ballot_sync(0xffffffffu, fl == kFlagInc);
+            const unsigned nrd = __ballot_sync(0xffffffffu, fl == 0);
+            const int first_inc = inc ? __ffs(inc) - 1 : 32;
+            const int first_nrd = nrd ? __ffs(nrd) - 1 : 32;
+            // consume the ready prefix of the window (up to the first INC)
+            const int upto = first_inc < first_nrd ? first_inc : first_nrd - 1;  // inclusive
+            unsigned long long part = (lane <= upto) ? (vq & kValMask) : 0ULL;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+            __syncwarp();
+            if (lane == 0) {
+                S->pend_acc += (long long)part;
+                S->pend_k -= (upto + 1);
+            }
+            __syncwarp();
+            if (first_inc < first_nrd) {  // resolved
+                if (lane == 0) {
+                    const long long prefix = S->pend_acc;
+                    st_release(&P.lookback[S->pend_u], kFlagInc | (unsigned long long)(prefix + S->pend_len));
+                    S->pend_prefix = prefix;
+                    S->pend_ready = 1;
+                    if (S->pend_u == P.n_units - 1) {
+                        P.status[2] = (unsigned long long)(kFileHeader + prefix + S->pend_len);
+                        if (P.block_offsets) P.block_offsets[P.n_blocks] = kFileHeader + prefix + S->pend_len;
+                    }
+                }
+                __syncwarp();
+                return;
+            }
+            if (!blocking) return;
+            if (first_nrd < 32) __nanosleep(64);
+        }
+    };
+    // copy the resolved pending unit to its final place (all threads)
+    auto place_pending = [&]() {
+        const long long prefix = S->pend_prefix;
+        copy_out<false>(P.out + kFileHeader + prefix, (const uint32_t*)slots2[S->pend_slot], S->pend_len);
+        if (P.block_offsets)
+            for (long long bb = S->pend_b0 + tid; bb < S->pend_b1; bb += NT) P.block_offsets[bb] += kFileHeader + prefix;
+        __syncthreads();
+        if (tid == 0) { S->pend_u = -1; S->pend_ready = 0; }
+        __syncthreads();
+    };
 
     auto block_n = [&](long long b) -> int {
         long long r = P.n - b * (long long)bs;
@@ -1044,10 +1106,12 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
                     S->tail_len = (int)(total - full);
                 }
             }
+            if (warp == NW - 1) lookback_try(false);
             __syncthreads();  // B10
+            if (S->pend_ready) place_pending();
         }
 
-        // ---------------- unit end: last tail, look-back, placement ----------------
+        // ---------------- unit end: last tail, publish, defer placement ----------------
         if (S->tail_len > 0) {
             if (S->direct) {
                 if (tid < S->tail_len)
@@ -1057,35 +1121,46 @@ __global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
                 *(uint4*)(slot + S->win_base) = t4;
             }
         }
-        if (warp == 0) {
+        // at most one unit pending: finish the previous one first
+        if (warp == NW - 1) lookback_try(true);
+        __syncthreads();
+        if (S->pend_ready) place_pending();
+        if (tid == 0) {
             const long long Lu = S->unit_len;
-            const long long prefix = warp_lookback(P.lookback, u, Lu);
-            if (lane == 0) {
-                S->prefix = prefix;
-                if (u == P.n_units - 1) {
-                    P.status[2] = (unsigned long long)(kFileHeader + prefix + Lu);
-                    if (P.block_offsets) P.block_offsets[P.n_blocks] = kFileHeader + prefix + Lu;
+            if (u == 0) {
+                st_release(&P.lookback[0], kFlagInc | (unsigned long long)Lu);
+                if (P.n_units == 1) {
+                    P.status[2] = (unsigned long long)(kFileHeader + Lu);
+                    if (P.block_offsets) P.block_offsets[P.n_blocks] = kFileHeader + Lu;
                 }
+            } else {
+                st_release(&P.lookback[u], kFlagAgg | (unsigned long long)Lu);
+                S->pend_u = u; S->pend_len = Lu; S->pend_b0 = b0; S->pend_b1 = b1;
+                S->pend_k = u - 1; S->pend_acc = 0; S->pend_slot = cur_slot; S->pend_ready = 0;
             }
         }
-        __syncthreads();
-        const long long prefix = S->prefix;
-        if (!S->direct) copy_out<false>(P.out + kFileHeader + prefix, (const uint32_t*)slot, S->unit_len);
-        if (u == 0 && tid < kFileHeader) {
-            unsigned char h[kFileHeader];
-            h[0] = 'A'; h[1] = 'P'; h[2] = 'A'; h[3] = 'X';
-            h[4] = 1; h[5] = (unsigned char)DT; h[6] = (unsigned char)P.mode; h[7] = 0;
-            for (int k2 = 0; k2 < 4; k2++) h[8 + k2] = (unsigned char)((unsigned)bs >> (8 * k2));
-            for (int k2 = 0; k2 < 8; k2++) h[12 + k2] = (unsigned char)((unsigned long long)P.n >> (8 * k2));
-            const unsigned long long tb = (unsigned long long)__double_as_longlong(P.target);
-            for (int k2 = 0; k2 < 8; k2++) h[20 + k2] = (unsigned char)(tb >> (8 * k2));
-            P.out[tid] = h[tid];
+        if (u == 0) {
+            if (tid < kFileHeader) {
+                unsigned char h[kFileHeader];
+                h[0] = 'A'; h[1] = 'P'; h[2] = 'A'; h[3] = 'X';
+                h[4] = 1; h[5] = (unsigned char)DT; h[6] = (unsigned char)P.mode; h[7] = 0;
+                for (int k2 = 0; k2 < 4; k2++) h[8 + k2] = (unsigned char)((unsigned)bs >> (8 * k2));
+                for (int k2 = 0; k2 < 8; k2++) h[12 + k2] = (unsigned char)((unsigned long long)P.n >> (8 * k2));
+                const unsigned long long tb = (unsigned long long)__double_as_longlong(P.target);
+                for (int k2 = 0; k2 < 8; k2++) h[20 + k2] = (unsigned char)(tb >> (8 * k2));
+                P.out[tid] = h[tid];
+            }
+            if (P.block_offsets)
+                for (long long bb = b0 + tid; bb < b1; bb += NT) P.block_offsets[bb] += kFileHeader;
         }
-        if (P.block_offsets) {
-            for (long long bb = b0 + tid; bb < b1; bb += NT) P.block_offsets[bb] += kFileHeader + prefix;
-        }
+        cur_slot ^= 1;
+        slot = slots2[cur_slot];
         __syncthreads();
     }
+    // drain the last pending unit
+    if (warp == NW - 1) lookback_try(true);
+    __syncthreads();
+    if (S->pend_ready) place_pending();
 }
 
 }  // namespace v2
