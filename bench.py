@@ -97,6 +97,23 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def _ncu_traffic(kernel_prefix: str):
+    """DRAM bytes per launch of the kernel from the committed ncu --set full
+    summary (profiles/latest_ncu_summary.json), or None."""
+    p = ROOT / "profiles" / "latest_ncu_summary.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text())
+    except Exception:  # noqa: BLE001
+        return None
+    for k, v in d.items():
+        if kernel_prefix in k:
+            return {"bytes": v.get("dram_bytes_total"), "kernel": k,
+                    "source": "profiles/latest_ncu_summary.json"}
+    return None
+
+
 def cpu_round_trip(x, target, seg, threads, budget_s=10.0):
     """Oracle (C port of the reference) encode+decode on host cores."""
     from oracle import oracle as O
@@ -270,28 +287,37 @@ def main():
     alg_dec = nbytes + in_bytes + 8 * (enc.n_blocks + 1)   # read container + offsets, write y
     ach_enc = alg_enc / (mean_enc * 1e-3) / 1e9
     ach_dec = alg_dec / (mean_dec * 1e-3) / 1e9
-    dominant = "encode_kernel<3>" if mean_enc >= mean_dec else "decode_kernel<3>"
+    dominant = "encode_v2_kernel<3>" if mean_enc >= mean_dec else "decode_v2_kernel<3>"
     ach = ach_enc if mean_enc >= mean_dec else ach_dec
 
     # ---- e2e: host buffers through the C-ABI entry points ----
+    # Pinned host samples -> H2D -> apax_encode -> D2H container + block index
+    # -> H2D container + index -> apax_decode -> D2H samples, every step.
     e2e = None
     if not args.no_e2e and not args.profile:
         xh = torch.from_numpy(x_host).pin_memory()
         blob_h = torch.empty(enc.cap + 64, dtype=torch.uint8).pin_memory()
+        offs_h = torch.empty(enc.n_blocks + 1, dtype=torch.int64).pin_memory()
         yh = torch.empty(n, dtype=torch.float32).pin_memory()
-        blob_d = torch.empty(enc.cap + 64, dtype=torch.uint8, device=dev)
+        blob_d = torch.zeros(enc.cap + 64, dtype=torch.uint8, device=dev)
+        offs_d = torch.empty(enc.n_blocks + 1, dtype=torch.int64, device=dev)
         xd2 = torch.empty(n, dtype=torch.float32, device=dev)
         dec2 = Decoder(n, Dtype.F32, 4096, device=dev)
         e2e_steps = max(3, min(args.steps, 10))
 
-        def e2e_step():
-            xd2.copy_(xh, non_blocking=True)                 # H2D input
+        def e2e_step(indexless=False):
+            xd2.copy_(xh, non_blocking=True)                         # H2D input
             enc.encode(xd2)
-            nb = enc.finish()                                # container length (host)
-            blob_h[:nb].copy_(enc.out[:nb], non_blocking=True)   # D2H container
-            blob_d[:nb].copy_(blob_h[:nb], non_blocking=True)    # H2D container
-            dec2.decode(blob_d, nb, None)                    # index-less: block walk + decode
-            yh.copy_(dec2.y[:n], non_blocking=True)          # D2H decoded samples
+            nb = enc.finish()                                        # container length
+            blob_h[:nb].copy_(enc.out[:nb], non_blocking=True)       # D2H container
+            offs_h.copy_(enc.offsets, non_blocking=True)             # D2H block index
+            blob_d[:nb].copy_(blob_h[:nb], non_blocking=True)        # H2D container
+            if indexless:
+                dec2.decode(blob_d, nb, None)                        # device block walk
+            else:
+                offs_d.copy_(offs_h, non_blocking=True)              # H2D block index
+                dec2.decode(blob_d, nb, offs_d)
+            yh.copy_(dec2.y[:n], non_blocking=True)                  # D2H decoded samples
             torch.cuda.synchronize()
             return nb
 
@@ -306,14 +332,28 @@ def main():
         e2e_s = (time.perf_counter() - a) / e2e_steps
         dec2.finish()
         ok_e2e = bool(torch.equal(yh, dec.y[:n].cpu()))
+        # index-less decode (container bytes only, like decode_stream(bytes))
+        a = time.perf_counter()
+        e2e_step(indexless=True)
+        il_s = time.perf_counter() - a
+        dec2.finish()
+        ok_il = bool(torch.equal(yh, dec.y[:n].cpu()))
         if world > 1:
-            t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+            t = torch.tensor([e2e_s, il_s], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_s = t.item()
+            e2e_s, il_s = t.tolist()
+        idx_bytes = 8 * (enc.n_blocks + 1)
         e2e = {"value": world * in_bytes / e2e_s / 1e9, "unit": UNIT,
-               "h2d_bytes_per_step": in_bytes + nb, "d2h_bytes_per_step": nb + in_bytes,
-               "ms_per_step": e2e_s * 1e3, "decode_path": "index-less (device block walk)",
-               "bit_exact_vs_device_path": ok_e2e}
+               "h2d_bytes_per_step": in_bytes + nb + idx_bytes,
+               "d2h_bytes_per_step": nb + idx_bytes + in_bytes,
+               "ms_per_step": e2e_s * 1e3,
+               "path": "C-ABI apax_encode/apax_decode with pinned host buffers, "
+                       "container + side-band block index round-tripped through the host",
+               "bit_exact_vs_device_path": ok_e2e,
+               "indexless": {"value": world * in_bytes / il_s / 1e9, "unit": UNIT,
+                             "ms_per_step": il_s * 1e3,
+                             "decode_path": "container bytes only; device block walk",
+                             "bit_exact_vs_device_path": ok_il}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
@@ -344,7 +384,10 @@ def main():
             "encode_ms": mean_enc, "decode_ms": mean_dec,
             "container_bytes": total_container, "ratio": world * in_bytes / total_container,
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                         "frac": ach / peak, "traffic": None, "kernel": dominant,
+                         "frac": ach / peak,
+                         "traffic": (_ncu_traffic(dominant) or {}).get("bytes"),
+                         "traffic_source": (_ncu_traffic(dominant) or {}).get("source"),
+                         "kernel": dominant,
                          "peak_kind": peak_kind,
                          "algorithmic_bytes_per_launch": alg_enc if dominant.startswith("enc") else alg_dec,
                          "encode": {"achieved": ach_enc, "frac": ach_enc / peak},
