@@ -10,7 +10,10 @@ import ctypes
 import pathlib
 
 _HERE = pathlib.Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libapax_b200.so"
+import os as _os
+
+# APAX_LIB_PATH overrides the in-tree library (tuning experiments only)
+LIB_PATH = pathlib.Path(_os.environ.get("APAX_LIB_PATH", str(_HERE / "libapax_b200.so")))
 
 
 class ExtensionMissing(ImportError):

@@ -25,6 +25,10 @@
 #include "apax_kernels.cuh"
 #include "apax_jee.cuh"
 
+#ifndef APAX_DEC_MINB
+#define APAX_DEC_MINB 3
+#endif
+
 namespace apax {
 
 
@@ -130,7 +134,7 @@ __device__ __forceinline__ Aff aff_compose(const Aff& A, const Aff& B) {  // A a
 }
 
 template <int DT>
-__global__ void __launch_bounds__(NT, 2) decode_v2_kernel(DecParams P) {
+__global__ void __launch_bounds__(NT, APAX_DEC_MINB) decode_v2_kernel(DecParams P) {
     using Tr = DT_<DT>;
     using T = typename Tr::T;
     constexpr int HS = Tr::HDR;

@@ -38,6 +38,10 @@
 #include "apax_device.cuh"
 #include "apax_kernels.cuh"
 
+#ifndef APAX_ENC_MINB
+#define APAX_ENC_MINB 4
+#endif
+
 namespace apax {
 namespace v2 {
 
@@ -206,7 +210,7 @@ __device__ __forceinline__ uint32_t consumed_word(uint32_t P, uint32_t cin, uint
 // the kernel
 // ---------------------------------------------------------------------------
 template <int DT>
-__global__ void __launch_bounds__(NT, 3) encode_v2_kernel(EncParams P) {
+__global__ void __launch_bounds__(NT, APAX_ENC_MINB) encode_v2_kernel(EncParams P) {
     using Tr = DT_<DT>;
     using T = typename Tr::T;
     constexpr bool F = Tr::F;
