@@ -25,7 +25,7 @@ struct EncPlan {
     int halo;
     int stage_bytes;
     int x_in_smem;
-    int v2;
+    int v2, v3;
     size_t smem;
     int grid;
     long long slot_bytes;
@@ -63,15 +63,27 @@ int plan_encode(long long n, int dt, int mode, int bs, long long seg, EncPlan* p
     if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess ||
         optin <= 0)
         optin = 227 * 1024;
-    p->v2 = encode_v2_supported(bs) && env_int("APAX_FORCE_V1", 0) == 0;
-    if (p->v2) {
+    const int ver = env_int("APAX_ENC_VER", 0);   // 0 = best available; 1/2/3 force
+    p->v3 = encode_v3_supported(dt, bs) && (ver == 0 || ver == 3) && env_int("APAX_FORCE_V1", 0) == 0;
+    if (p->v3) {
+        p->stage_bytes = encode_v3_stage_bytes(dt, bs);
+        p->x_in_smem = 1;
+        p->smem = encode_v3_smem_bytes(dt, bs, p->stage_bytes);
+        if (p->smem > (size_t)optin) p->v3 = 0;
+    }
+    p->v2 = !p->v3 && encode_v2_supported(bs) && (ver == 0 || ver == 2) && env_int("APAX_FORCE_V1", 0) == 0;
+    if (p->v3) {
+        int resident = encode_v3_resident_ctas(dt, p->smem);
+        p->grid = (int)(p->n_units < resident ? p->n_units : resident);
+    } else if (p->v2) {
         // v2: the window holds one block plus a <16-byte tail
         p->stage_bytes = (int)((mbb + 64 + 15) & ~15LL);
         p->x_in_smem = 1;
         p->smem = encode_v2_smem_bytes(dt, mode, p->stage_bytes);
         if (p->smem > (size_t)optin) p->v2 = 0;
     }
-    if (p->v2) {
+    if (p->v3) {
+    } else if (p->v2) {
         int resident = encode_v2_resident_ctas(dt, p->smem);
         p->grid = (int)(p->n_units < resident ? p->n_units : resident);
     } else {
@@ -89,11 +101,11 @@ int plan_encode(long long n, int dt, int mode, int bs, long long seg, EncPlan* p
         p->grid = (int)(p->n_units < resident ? p->n_units : resident);
     }
     if (p->grid < 1) p->grid = 1;
-    p->slot_bytes = (p->n_units > 1) ? ((p->unit_blocks * mbb + 64 + 255) & ~255LL) : 0;
+    p->slot_bytes = (p->n_units > 1 || p->v3) ? ((p->unit_blocks * mbb + 64 + 255) & ~255LL) : 0;
     p->ws_lookback = 0;
     p->ws_ticket = (p->n_units * 8 + 255) & ~255LL;
     p->ws_slots = p->ws_ticket + 256;
-    p->ws_total = p->ws_slots + (long long)p->grid * p->slot_bytes * (p->v2 ? 2 : 1);
+    p->ws_total = p->ws_slots + (long long)p->grid * p->slot_bytes * ((p->v2 || p->v3) ? 2 : 1);
     return APAX_OK;
 }
 
@@ -230,6 +242,7 @@ int apax_encode(const void* x, int64_t n, int dtype, int mode, double target, in
     P.pow10_t20 = pow(10.0, target / 20.0);
     P.sqrt12 = sqrt(12.0);
     P.trace = trace;
+    if (p.v3) return launch_encode_v3(dtype, P, p.grid, p.smem, s);
     if (p.v2) return launch_encode_v2(dtype, P, p.grid, p.smem, s);
     return launch_encode(dtype, P, p.grid, p.smem, s);
 }

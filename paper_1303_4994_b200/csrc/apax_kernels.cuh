@@ -57,6 +57,11 @@ size_t encode_v2_smem_bytes(int dt, int mode, int window_bytes);
 bool encode_v2_supported(int bs);
 int encode_v2_resident_ctas(int dt, size_t smem);
 int launch_encode_v2(int dt, const EncParams& P, int grid, size_t smem, cudaStream_t st);
+size_t encode_v3_smem_bytes(int dt, int bs, int stage_bytes);
+int encode_v3_stage_bytes(int dt, int bs);
+bool encode_v3_supported(int dt, int bs);
+int encode_v3_resident_ctas(int dt, size_t smem);
+int launch_encode_v3(int dt, const EncParams& P, int grid, size_t smem, cudaStream_t st);
 int launch_decode(int dt, const DecParams& P, int grid, size_t smem, cudaStream_t st);
 size_t decode_v2_smem_bytes(int dt, int bs, int payload_cap);
 bool decode_v2_supported(int bs);
