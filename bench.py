@@ -232,7 +232,7 @@ def main():
         flush.zero_()  # keep the container out of L2 for the decode timing
         if record:
             record[2].record(stream)
-        dec.decode(enc.out, enc.cap, enc.offsets)
+        dec.decode(enc.out, enc.cap, enc.offsets, segment_blocks=args.segment_blocks)
         if record:
             record[3].record(stream)
         if world > 1:  # cross-GPU offset scan input: every rank's container length
@@ -316,7 +316,7 @@ def main():
                 dec2.decode(blob_d, nb, None)                        # device block walk
             else:
                 offs_d.copy_(offs_h, non_blocking=True)              # H2D block index
-                dec2.decode(blob_d, nb, offs_d)
+                dec2.decode(blob_d, nb, offs_d, segment_blocks=args.segment_blocks)
             yh.copy_(dec2.y[:n], non_blocking=True)                  # D2H decoded samples
             torch.cuda.synchronize()
             return nb

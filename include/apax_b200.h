@@ -90,6 +90,18 @@ int apax_decode(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, int b
                 const int64_t* block_offsets, void* y, uint64_t* status, void* ws,
                 int64_t ws_bytes, void* stream);
 
+/* Decode a container of independent segments (every segment_blocks-th
+ * block carries the restart flag, as apax_encode writes with
+ * segment_blocks > 0) given its side-band block index: one CTA per segment,
+ * history kept on chip.  Same arguments and status contract as apax_decode;
+ * falls back to apax_decode when the fast path does not apply (no index,
+ * segment_blocks <= 0, f64, or block sizes other than powers of two in
+ * 128..4096).  Workspace: apax_decode_segments_workspace_bytes. */
+int64_t apax_decode_segments_workspace_bytes(int64_t n, int dtype, int block_size);
+int apax_decode_segments(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, int block_size,
+                         const int64_t* block_offsets, int64_t segment_blocks, void* y, uint64_t* status,
+                         void* ws, int64_t ws_bytes, void* stream);
+
 /* The reference's serial boundary walk on the device: offsets (device,
  * n_blocks + 1) receives every block header offset and the end offset;
  * errors go to status[1]. */

@@ -48,6 +48,10 @@ def lib():
     L.apax_decode_workspace_bytes.restype = I64
     L.apax_decode.argtypes = [P, I64, I64, I32, I32, P, P, P, P, I64, P]
     L.apax_decode.restype = I32
+    L.apax_decode_segments_workspace_bytes.argtypes = [I64, I32, I32]
+    L.apax_decode_segments_workspace_bytes.restype = I64
+    L.apax_decode_segments.argtypes = [P, I64, I64, I32, I32, P, I64, P, P, P, I64, P]
+    L.apax_decode_segments.restype = I32
     L.apax_find_blocks.argtypes = [P, I64, I64, I32, I32, P, P, P]
     L.apax_find_blocks.restype = I32
     L.apax_parse_file_header.argtypes = [P, I64, P, P, P, P, P, P]
@@ -60,4 +64,5 @@ EXPORTED_SYMBOLS = (
     "apax_version", "apax_status_string", "apax_max_encoded_bytes",
     "apax_encode_workspace_bytes", "apax_encode", "apax_decode_workspace_bytes",
     "apax_decode", "apax_find_blocks", "apax_parse_file_header",
+    "apax_decode_segments_workspace_bytes", "apax_decode_segments",
 )

@@ -191,14 +191,26 @@ class Decoder:
         self.y = torch.empty(max(self.n, 1), dtype=torch_dtype(dtype), device=self.device)
         self._lib = L
 
-    def decode(self, blob, nbytes: int, offsets=None, stream=None, out=None) -> None:
+    def decode(self, blob, nbytes: int, offsets=None, stream=None, out=None,
+               segment_blocks: Optional[int] = None) -> None:
+        """Enqueue a decode.  With the side-band `offsets` and the container's
+        `segment_blocks` (the encoder's StreamConfig.segment_blocks), the
+        segment-serial decoder runs (apax_decode_segments); otherwise the
+        general decoder (apax_decode)."""
         y = self.y if out is None else out
-        st = self._lib.apax_decode(
-            ctypes.c_void_p(blob.data_ptr()), int(nbytes), self.n, self.dtype.wire_code, self.bs,
-            ctypes.c_void_p(offsets.data_ptr()) if offsets is not None else None,
-            ctypes.c_void_p(y.data_ptr()), ctypes.c_void_p(self.status.data_ptr()),
-            ctypes.c_void_p(self.ws.data_ptr()), self.ws.numel(),
-            ctypes.c_void_p(_stream_ptr(stream)))
+        offs = ctypes.c_void_p(offsets.data_ptr()) if offsets is not None else None
+        if segment_blocks and offsets is not None:
+            st = self._lib.apax_decode_segments(
+                ctypes.c_void_p(blob.data_ptr()), int(nbytes), self.n, self.dtype.wire_code, self.bs,
+                offs, int(segment_blocks), ctypes.c_void_p(y.data_ptr()),
+                ctypes.c_void_p(self.status.data_ptr()), ctypes.c_void_p(self.ws.data_ptr()),
+                self.ws.numel(), ctypes.c_void_p(_stream_ptr(stream)))
+        else:
+            st = self._lib.apax_decode(
+                ctypes.c_void_p(blob.data_ptr()), int(nbytes), self.n, self.dtype.wire_code, self.bs,
+                offs, ctypes.c_void_p(y.data_ptr()), ctypes.c_void_p(self.status.data_ptr()),
+                ctypes.c_void_p(self.ws.data_ptr()), self.ws.numel(),
+                ctypes.c_void_p(_stream_ptr(stream)))
         raise_status(st)
 
     def finish(self, stream=None):
@@ -230,8 +242,10 @@ def _decodable_count(count: int, nbytes: int, cfg: StreamConfig) -> int:
     return min(count, limit_blocks * cfg.block_size)
 
 
-def decode_device(blob, nbytes: Optional[int] = None, offsets=None):
-    """Decode a container held in a CUDA uint8 tensor; returns a CUDA tensor."""
+def decode_device(blob, nbytes: Optional[int] = None, offsets=None,
+                  segment_blocks: Optional[int] = None):
+    """Decode a container held in a CUDA uint8 tensor; returns a CUDA tensor.
+    `segment_blocks` (with `offsets`) selects the segment-serial decoder."""
     torch = _torch()
     nbytes = int(blob.numel() if nbytes is None else nbytes)
     head = bytes(blob[:min(nbytes, FILE_HEADER_SIZE)].cpu().numpy().tobytes())
@@ -242,7 +256,8 @@ def decode_device(blob, nbytes: Optional[int] = None, offsets=None):
         return torch.empty(0, dtype=torch_dtype(cfg.dtype), device=blob.device)
     n = _decodable_count(count, nbytes, cfg)
     dec = Decoder(n, cfg.dtype, cfg.block_size, device=blob.device)
-    dec.decode(blob, nbytes, offsets if n == count else None)
+    ok = n == count
+    dec.decode(blob, nbytes, offsets if ok else None, segment_blocks=segment_blocks if ok else None)
     return dec.finish()
 
 

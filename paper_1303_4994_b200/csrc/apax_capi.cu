@@ -305,6 +305,42 @@ int apax_decode(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, int b
     return launch_decode(dtype, P, p.grid, p.smem, s);
 }
 
+int64_t apax_decode_segments_workspace_bytes(int64_t n, int dtype, int block_size) {
+    return apax_decode_workspace_bytes(n, dtype, block_size);
+}
+
+int apax_decode_segments(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, int block_size,
+                         const int64_t* block_offsets, int64_t segment_blocks, void* y, uint64_t* status,
+                         void* ws, int64_t ws_bytes, void* stream) {
+    // segment-serial decoder (apax_decode_v3.cu): needs the side-band index
+    // and the container's segment length; anything else takes apax_decode
+    if (segment_blocks <= 0 || !block_offsets || !decode_v3_supported(dtype, block_size) ||
+        env_int("APAX_DEC_VER", 0) == 2)
+        return apax_decode(blob, nbytes, n, dtype, block_size, block_offsets, y, status, ws, ws_bytes, stream);
+    DecPlan p;
+    int st = plan_decode(n, dtype, block_size, &p);
+    if (st) return st;
+    if (!blob || !status || (n > 0 && !y)) return APAX_ERR_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (cudaMemsetAsync(status, 0xFF, 4 * sizeof(uint64_t), s) != cudaSuccess) return APAX_ERR_CUDA;
+    if (p.n_blocks == 0) return APAX_OK;
+    DecParams P;
+    memset(&P, 0, sizeof(P));
+    P.blob = blob;
+    P.nbytes = nbytes;
+    P.offsets = (const long long*)block_offsets;
+    P.y = y;
+    P.n = n;
+    P.bs = block_size;
+    P.n_blocks = p.n_blocks;
+    P.status = (unsigned long long*)status;
+    P.payload_cap = p.payload_cap;
+    P.segment_blocks = segment_blocks;
+    const size_t smem = decode_v3_smem_bytes(dtype, p.payload_cap);
+    const int grid = decode_v3_resident_ctas(dtype, smem);
+    return launch_decode_v3(dtype, P, grid, smem, s);
+}
+
 int apax_parse_file_header(const uint8_t* d, int64_t len, int* dt, int* mode, int* bs,
                            int64_t* count, double* target, int64_t* detail) {
     // reference parse_file_header (codec.py:288-305) + StreamConfig.validate

@@ -1,0 +1,657 @@
+// apax_decode_v3.cu -- segment-serial B200 decoder (block sizes 128..4096,
+// powers of two) for containers whose segments are known: every
+// `segment_blocks`-th block starts a segment (restart flag), as
+// written by apax_encode with segment_blocks > 0.
+//
+// Same bit-exact output as the reference decode_stream
+// (pkg/src/apax/codec.py:308-329); the block walk is replaced by the
+// side-band offsets.  One CTA decodes a segment's blocks in order, so the
+// derivative history (transform.py:31-49) stays in shared memory and no
+// cross-block carry protocol is needed; segments are spread over the CTAs.
+//
+// Per block (256 threads, 16 samples per thread):
+//   * the block (header + payload) arrives by one TMA bulk copy issued while
+//     the previous block was decoded;
+//   * JEE (entropy.py:118-164): every thread parses the tokens that start in
+//     its 4-nibble slice (two consecutive non-15 nibbles always precede a
+//     token start), then one CTA scan of (exponent count, escape reset,
+//     running value) places every exponent; an irregular stream re-runs the
+//     exact serial parser (apax_jee.cuh) for the reference's status code;
+//   * mantissa bit offsets: a CTA scan of 4*sum(e) over the thread's 4
+//     groups; 32-bit funnel windows + signed bit-field extracts unpack them
+//     (entropy.py:249-277);
+//   * D1/D2 (transform.py:116-129) in 64-bit: one CTA scan of (sum, sum of
+//     partial sums) per block, then d1 += v; q += d1 per sample;
+//   * dequantize (codec.py:135-146) with the Markstein quotient, y staged in
+//     shared memory, one TMA bulk store per block.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "apax_device.cuh"
+#include "apax_kernels.cuh"
+#include "apax_jee.cuh"
+
+#ifndef APAX_D3_MINB
+#define APAX_D3_MINB 3
+#endif
+
+namespace apax {
+namespace d3 {
+
+constexpr int NT = 256;
+constexpr int NW = NT / 32;
+constexpr int SPT = 16;
+constexpr int MAXBS = 4096;
+constexpr int NIB_PER_PASS = 4 * NT;
+constexpr double kMagicI = 6755401588539392.0;   // 1.5 * 2^52 + 2^31
+
+struct __align__(16) St {
+    // block descriptor (thread 0 at issue time) for the two payload buffers
+    long long ld_a[2], ld_boff[2], ld_bend[2];
+    int ld_tma[2];
+    unsigned long long mbar[2];
+    // history (q[np-1], q[np-2] of the previous block)
+    long long p1, p2;
+    // JEE pass state
+    int cnt_base, val_base, first_event, used, fallback, err;
+    int sc_cnt[NW], sc_flag[NW], sc_val[NW], ev_min[NW];
+    unsigned bits_w[NW];
+    long long rs_w[NW], rt_w[NW];
+    int store_pending;
+};
+
+using namespace apax::tma;
+
+__device__ __forceinline__ void cbar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                 :: "l"(gdst), "r"(sa(ssrc)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ int bfe_s(uint32_t v, int pos, int len) {
+    int r;
+    asm("bfe.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(v), "r"(pos), "r"(len));
+    return r;
+}
+// 32 bits of the MSB-first stream starting at bit position bp (word array
+// in shared memory, little-endian words holding big-endian bytes)
+__device__ __forceinline__ uint32_t r32(const uint32_t* w, int bp) {
+    const int k = bp >> 5;
+    return __funnelshift_l(bswap32(w[k + 1]), bswap32(w[k]), (unsigned)(bp & 31));
+}
+
+template <int DT, bool FIX>
+__global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P) {
+    using Tr = DT_<DT>;
+    using T = typename Tr::T;
+    constexpr int HS = Tr::HDR;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int bs = FIX ? MAXBS : P.bs;
+
+    St* S = (St*)smem;
+    size_t off = (sizeof(St) + 127) & ~(size_t)127;
+    uint8_t* ebuf = smem + off;                           // group exponents
+    off += ((size_t)MAXBS / 4 + 128 + 127) & ~(size_t)127;
+    T* ybuf = (T*)(smem + off);                           // decoded block
+    off += ((size_t)MAXBS * sizeof(T) + 127) & ~(size_t)127;
+    const int bufsz = (P.payload_cap + 64 + 127) & ~127;
+    uint8_t* pbuf0 = smem + off;
+    uint8_t* pbuf1 = smem + off + bufsz;
+    const long long limit = P.nbytes & ~15LL;             // TMA never reads past the blob
+
+    if (tid == 0) {
+        mbar_init(&S->mbar[0]);
+        mbar_init(&S->mbar[1]);
+        fence_mbar_init();
+        S->store_pending = 0;
+    }
+    __syncthreads();
+    uint32_t phs = 0u;
+
+    const long long P_seg = P.segment_blocks;
+    const long long s_begin = P.seg_begin, s_end = P.seg_end;
+
+    // issue the load of block bb into buffer slot (thread 0)
+    auto issue = [&](long long bb, int slot) {
+        const long long o0 = P.offsets[bb], o1 = P.offsets[bb + 1];
+        const long long hi = o1 > o0 + HS ? o1 : o0 + HS;
+        const long long a0 = (o0 >= 0 ? o0 : 0) & ~15LL;
+        const long long e1 = (hi + 15) & ~15LL;
+        const long long len = e1 - a0;
+        S->ld_a[slot] = a0;
+        S->ld_boff[slot] = o0;
+        S->ld_bend[slot] = o1;
+        const bool ok = o0 >= 0 && len > 0 && len <= bufsz && e1 <= limit &&
+                        ((((uintptr_t)(P.blob + a0)) & 15) == 0);
+        S->ld_tma[slot] = ok ? 1 : 0;
+        if (ok) {
+            fence_proxy_async();
+            tma_load(slot ? pbuf1 : pbuf0, P.blob + a0, (uint32_t)len, &S->mbar[slot]);
+        }
+    };
+    // the first block of this CTA
+    if (tid == 0 && s_begin + blockIdx.x < s_end) issue((s_begin + blockIdx.x) * P_seg, 0);
+    __syncthreads();
+
+    int kk = 0;   // blocks decoded by this CTA (buffer parity)
+    for (long long sg = s_begin + blockIdx.x; sg < s_end; sg += gridDim.x) {
+        const long long b0 = sg * P_seg;
+        const long long b1 = (b0 + P_seg < P.n_blocks) ? b0 + P_seg : P.n_blocks;
+        if (tid == 0) { S->p1 = 0; S->p2 = 0; }
+        for (long long b = b0; b < b1; b++, kk++) {
+            const int cur = kk & 1;
+            uint8_t* pay = cur ? pbuf1 : pbuf0;
+            const long long start = b * (long long)bs;
+            const int n = FIX ? MAXBS : (int)((P.n - start) < bs ? (P.n - start) : bs);
+            const int G = FIX ? MAXBS / 4 : (n + 3) >> 2;
+            const int np = FIX ? MAXBS : 4 * G;
+            // prefetch the next block of this CTA
+            if (tid == 0) {
+                long long nb = -1;
+                if (b + 1 < b1) nb = b + 1;
+                else if (sg + gridDim.x < s_end) nb = (sg + gridDim.x) * P_seg;
+                if (nb >= 0) issue(nb, cur ^ 1);
+            }
+            const bool was_tma = S->ld_tma[cur] != 0;
+            const long long a0 = S->ld_a[cur];
+            const long long boff = S->ld_boff[cur];
+            const long long bend = S->ld_bend[cur];
+            if (was_tma) {
+                mbar_wait(&S->mbar[cur], (phs >> cur) & 1u);
+                phs ^= 1u << cur;
+            } else if (boff >= 0) {
+                long long hi = bend > boff + HS ? bend : boff + HS;
+                long long e1 = hi < P.nbytes ? hi : P.nbytes;
+                long long len = e1 - a0;
+                if (len > bufsz) len = bufsz;
+                for (long long i = tid; i < len; i += NT) pay[i] = P.blob[a0 + i];
+                cbar();
+            }
+            // ---- block header (dtypes.py:156-180), read by every thread ----
+            int err = 0;
+            int sel = 0, restart = 0, code = 0, fbe = 0;
+            long long pay_off = 0, avail = 0, staged = 0;
+            if (boff < 0) {
+                err = APAX_ERR_ARG;
+            } else if (P.nbytes - boff < HS) {
+                err = APAX_ERR_BLOCK_HDR_TRUNCATED;
+            } else {
+                const uint8_t* h = pay + (boff - a0);
+                sel = h[0] & 3;
+                restart = (h[0] >> 2) & 1;
+                code = h[1] | (h[2] << 8);
+                fbe = Tr::F ? (int)(int8_t)h[4] : 0;
+                if (sel == 3) err = APAX_ERR_SELECTOR;
+                const long long ps = boff + HS;
+                const long long pe = bend > ps ? bend : ps;
+                long long e1 = (pe + 15) & ~15LL;
+                if (e1 > limit) e1 = limit;
+                long long staged_end = a0 + (e1 - a0 < bufsz ? e1 - a0 : bufsz);
+                if (!was_tma) staged_end = a0 + min((long long)bufsz, min(pe, P.nbytes) - a0);
+                pay_off = ps - a0;
+                avail = P.nbytes - ps;
+                staged = staged_end - ps;
+            }
+            // ---- JEE: parallel token parse ----
+            int used = 0;
+            if (!err) {
+                const uint8_t* p = pay + pay_off;
+                const long long maxj = (3LL * G + 2) / 2;
+                const long long nbj = avail < maxj ? avail : maxj;
+                const int total = (int)(2 * nbj);
+                const int stotal = (int)min(2 * staged, (long long)total);
+                int cbase = 0, vbase = 0;
+                for (int pass_base = 0;; pass_base += NIB_PER_PASS) {
+                    const int p0 = pass_base + 4 * tid;
+                    auto nb = [&](int k) -> int {
+                        if (k >= stotal) return 0;
+                        const uint8_t bb = p[k >> 1];
+                        return (k & 1) ? (bb & 15) : (bb >> 4);
+                    };
+                    // nearest definite token start at or before p0
+                    int skip = 0;
+                    if (p0 > 0 && p0 < stotal + 4) {
+                        int q = p0;
+                        while (q > 0 && !(nb(q - 1) != 15 && (q < 2 || nb(q - 2) != 15))) q--;
+                        int pos = q;
+                        while (pos < p0) pos += (nb(pos) == 15) ? 3 : 1;
+                        skip = pos - p0;
+                    }
+                    int cnt = 0, flag = 0, val = 0;
+                    int tk_pos[4], tk_kind[4], tk_a[4], tk_b[4], ntok = 0;
+#pragma unroll
+                    for (int r = 0; r < 4; r++) { tk_pos[r] = 0; tk_kind[r] = 0; tk_a[r] = 0; tk_b[r] = 0; }
+                    for (int pos = p0 + skip; pos < p0 + 4 && ntok < 4;) {
+                        const int v = nb(pos);
+                        int kind, len = 1;
+                        if (pos >= stotal) kind = 5;
+                        else if (v == 14) kind = 4;
+                        else if (v == 15) {
+                            kind = 1; len = 3;
+                            if (pos + 2 >= stotal) kind = 5;
+                            else {
+                                const int a = (nb(pos + 1) << 4) | nb(pos + 2);
+                                tk_a[ntok] = a;
+                                flag = 1; val = a; cnt += 1;
+                            }
+                        } else if (v >= 9) {
+                            kind = 3; tk_a[ntok] = v - 11; val += v - 11; cnt += 1;
+                        } else {
+                            kind = 2; tk_a[ntok] = v / 3 - 1; tk_b[ntok] = v % 3 - 1;
+                            val += (v / 3 - 1) + (v % 3 - 1); cnt += 2;
+                        }
+                        tk_pos[ntok] = pos;
+                        tk_kind[ntok] = kind;
+                        ntok++;
+                        pos += len;
+                        if (kind >= 4) break;
+                    }
+                    // warp scan of (cnt, flag, val): A then B = (cA+cB, fA|fB, fB ? vB : vA+vB)
+                    int c_i = cnt, f_i = flag, v_i = val;
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const int oc = __shfl_up_sync(0xffffffffu, c_i, d);
+                        const int of = __shfl_up_sync(0xffffffffu, f_i, d);
+                        const int ov = __shfl_up_sync(0xffffffffu, v_i, d);
+                        if (lane >= d) {
+                            c_i += oc;
+                            if (!f_i) v_i += ov;
+                            f_i |= of;
+                        }
+                    }
+                    if (lane == 31) { S->sc_cnt[warp] = c_i; S->sc_flag[warp] = f_i; S->sc_val[warp] = v_i; }
+                    cbar();
+                    // prefix over the previous warps (lanes 0..NW-1) and the previous pass
+                    int pc, pf, pv;
+                    {
+                        const int w = lane & (NW - 1);
+                        int wc = (lane < NW) ? S->sc_cnt[w] : 0, wf = (lane < NW) ? S->sc_flag[w] : 0;
+                        int wv = (lane < NW) ? S->sc_val[w] : 0;
+#pragma unroll
+                        for (int d = 1; d < NW; d <<= 1) {
+                            const int oc = __shfl_up_sync(0xffffffffu, wc, d);
+                            const int of = __shfl_up_sync(0xffffffffu, wf, d);
+                            const int ov = __shfl_up_sync(0xffffffffu, wv, d);
+                            if (lane >= d) {
+                                wc += oc;
+                                if (!wf) wv += ov;
+                                wf |= of;
+                            }
+                        }
+                        // exclusive for warp `warp`
+                        int ec = __shfl_up_sync(0xffffffffu, wc, 1), ef = __shfl_up_sync(0xffffffffu, wf, 1);
+                        int evv = __shfl_up_sync(0xffffffffu, wv, 1);
+                        if (lane == 0) { ec = 0; ef = 0; evv = 0; }
+                        pc = __shfl_sync(0xffffffffu, ec, warp);
+                        pf = __shfl_sync(0xffffffffu, ef, warp);
+                        pv = __shfl_sync(0xffffffffu, evv, warp);
+                        // pass totals for the next pass
+                        const int tc = __shfl_sync(0xffffffffu, wc, NW - 1);
+                        const int tf = __shfl_sync(0xffffffffu, wf, NW - 1);
+                        const int tv = __shfl_sync(0xffffffffu, wv, NW - 1);
+                        const int nbase_c = cbase + tc;
+                        const int nbase_v = tf ? tv : vbase + tv;
+                        pc += cbase;
+                        pv = pf ? pv : vbase + pv;
+                        cbase = nbase_c;
+                        vbase = nbase_v;
+                    }
+                    // this thread's exclusive prefix inside its warp
+                    int ec = __shfl_up_sync(0xffffffffu, c_i, 1), ef = __shfl_up_sync(0xffffffffu, f_i, 1),
+                        evv = __shfl_up_sync(0xffffffffu, v_i, 1);
+                    if (lane == 0) { ec = 0; ef = 0; evv = 0; }
+                    int idx = pc + ec;
+                    int curv = ef ? evv : pv + evv;
+                    // evaluate tokens in order; first event = error or completion
+                    int ev_pos = 0x7fffffff, ev_done = 0;
+                    for (int k2 = 0; k2 < ntok; k2++) {
+                        if (idx >= G) break;
+                        const int kind = tk_kind[k2], pos = tk_pos[k2];
+                        int e_err = 0, adv = 0;
+                        if (kind >= 4) e_err = 1;
+                        else if (kind == 1) {
+                            if (tk_a[k2] > 34) e_err = 1;
+                            else { curv = tk_a[k2]; ebuf[idx] = (uint8_t)curv; adv = 1; }
+                        } else if (idx == 0) e_err = 1;
+                        else if (kind == 3) {
+                            curv += tk_a[k2];
+                            if (curv < 0 || curv > 34) e_err = 1;
+                            else { ebuf[idx] = (uint8_t)curv; adv = 1; }
+                        } else {
+                            curv += tk_a[k2];
+                            if (curv < 0 || curv > 34 || idx + 1 >= G) e_err = 1;
+                            else {
+                                ebuf[idx] = (uint8_t)curv;
+                                curv += tk_b[k2];
+                                if (curv < 0 || curv > 34) e_err = 1;
+                                else { ebuf[idx + 1] = (uint8_t)curv; adv = 2; }
+                            }
+                        }
+                        if (e_err) { ev_pos = pos; ev_done = 0; break; }
+                        idx += adv;
+                        if (idx >= G) { ev_pos = pos + (kind == 1 ? 3 : 1); ev_done = 1; break; }
+                    }
+                    int key = (ev_pos == 0x7fffffff) ? 0x7fffffff : ((ev_pos << 1) | (ev_done ? 0 : 1));
+                    key = __reduce_min_sync(0xffffffffu, key);
+                    if (lane == 0) S->ev_min[warp] = key;
+                    cbar();
+                    int kmin = (lane < NW) ? S->ev_min[lane & (NW - 1)] : 0x7fffffff;
+                    kmin = __reduce_min_sync(0xffffffffu, kmin);
+                    int fallback = 0, fev;
+                    if (kmin == 0x7fffffff) {
+                        if (pass_base + NIB_PER_PASS >= stotal) { fallback = 1; fev = -1; }
+                        else fev = -2;
+                    } else if (kmin & 1) {
+                        fallback = 1;
+                        fev = kmin >> 1;
+                    } else {
+                        fev = kmin >> 1;
+                        used = kmin >> 1;
+                    }
+                    if (fev != -2) {
+                        if (fallback) {
+                            // exact serial parse (reference semantics and status code)
+                            cbar();
+                            if (warp == 0) {
+                                long long u2 = 0, esum = 0;
+                                const int st = warp_jee_decode(P.blob + boff + HS, 2 * nbj, G, ebuf, u2, esum);
+                                if (lane == 0) { S->err = st; S->used = (int)u2; }
+                            }
+                            cbar();
+                            err = S->err;
+                            used = S->used;
+                            cbar();
+                        }
+                        break;
+                    }
+                    cbar();   // the per-warp words are rewritten by the next pass
+                }
+                (void)total;
+            }
+            const int jee_bytes = (used + 1) >> 1;
+            // ---- mantissa offsets (entropy.py:209-219): CTA scan of 4*sum(e) ----
+            const int g0 = 4 * tid;
+            const bool active = FIX ? true : (g0 < G);
+            uint32_t epk = 0;
+            if (!err && active) {
+                if (FIX || g0 + 4 <= G) epk = *(const uint32_t*)(ebuf + g0);
+                else
+                    for (int g = 0; g < 4; g++) epk |= (g0 + g < G ? (uint32_t)ebuf[g0 + g] : 0u) << (8 * g);
+            }
+            const unsigned lbits = 4u * ((epk & 0xffu) + ((epk >> 8) & 0xffu) + ((epk >> 16) & 0xffu) + (epk >> 24));
+            unsigned xb = lbits;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const unsigned o = __shfl_up_sync(0xffffffffu, xb, d);
+                if (lane >= d) xb += o;
+            }
+            if (lane == 31) S->bits_w[warp] = xb;
+            cbar();
+            unsigned bpre, btot;
+            {
+                unsigned wb = (lane < NW) ? S->bits_w[lane & (NW - 1)] : 0u;
+#pragma unroll
+                for (int d = 1; d < NW; d <<= 1) {
+                    const unsigned o = __shfl_up_sync(0xffffffffu, wb, d);
+                    if (lane >= d) wb += o;
+                }
+                btot = __shfl_sync(0xffffffffu, wb, NW - 1);
+                const unsigned ex = __shfl_up_sync(0xffffffffu, wb, 1);
+                bpre = __shfl_sync(0xffffffffu, lane == 0 ? 0u : ex, warp);
+                bpre = (warp == 0 ? 0u : bpre) + (xb - lbits);
+            }
+            if (!err) {
+                const long long mant_bytes = ((long long)btot + 7) / 8;
+                if (avail < jee_bytes + mant_bytes) err = APAX_ERR_MANTISSA_TRUNCATED;
+                else if (jee_bytes + mant_bytes > staged) err = APAX_ERR_ARG;   // offsets inconsistent
+            }
+            if (err) {
+                if (tid == 0 && err > 0) report_error(P.status, b, err);
+                cbar();
+                continue;
+            }
+            // ---- unpack 16 values ----
+            long long q[SPT];
+            {
+                const uint32_t* w = (const uint32_t*)pay;
+                int bp = 8 * ((int)pay_off + jee_bytes) + (int)bpre;
+#pragma unroll
+                for (int g = 0; g < 4; g++) {
+                    const int wd = (int)((epk >> (8 * g)) & 0xffu);
+                    if (wd == 0) {
+#pragma unroll
+                        for (int k = 0; k < 4; k++) q[4 * g + k] = 0;
+                    } else if (wd <= 8) {
+                        const uint32_t c = r32(w, bp);
+#pragma unroll
+                        for (int k = 0; k < 4; k++) q[4 * g + k] = bfe_s(c, 32 - wd * (k + 1), wd);
+                    } else if (wd <= 16) {
+                        const uint32_t c0 = r32(w, bp), c1 = r32(w, bp + 2 * wd);
+                        q[4 * g + 0] = bfe_s(c0, 32 - wd, wd);
+                        q[4 * g + 1] = bfe_s(c0, 32 - 2 * wd, wd);
+                        q[4 * g + 2] = bfe_s(c1, 32 - wd, wd);
+                        q[4 * g + 3] = bfe_s(c1, 32 - 2 * wd, wd);
+                    } else if (wd <= 32) {
+#pragma unroll
+                        for (int k = 0; k < 4; k++) q[4 * g + k] = bfe_s(r32(w, bp + k * wd), 32 - wd, wd);
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < 4; k++) {
+                            const int pb = bp + k * wd;
+                            const unsigned long long hi = ((unsigned long long)r32(w, pb) << 32) | r32(w, pb + 32);
+                            q[4 * g + k] = (long long)hi >> (64 - wd);
+                        }
+                    }
+                    bp += 4 * wd;
+                }
+            }
+            // ---- reconstruct (transform.py:116-129) ----
+            const long long p1 = S->p1, p2 = S->p2;
+            const unsigned long long h1 = restart ? 0ULL : (unsigned long long)p1;
+            const unsigned long long h2 = restart ? 0ULL : (unsigned long long)p2;
+            if (sel >= 1) {
+                // thread sums: s = sum v, t = sum of local partial sums; ranges
+                // compose as (s, t, m): A then B = (sA+sB, tA+tB+mB*sA, mA+mB)
+                unsigned long long s = 0, t = 0;
+#pragma unroll
+                for (int i = 0; i < SPT; i++) { s += (unsigned long long)q[i]; t += s; }
+                unsigned long long xs = s, xt = t;
+                unsigned xm = SPT;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const unsigned long long os = __shfl_up_sync(0xffffffffu, xs, d);
+                    const unsigned long long ot = __shfl_up_sync(0xffffffffu, xt, d);
+                    const unsigned om = __shfl_up_sync(0xffffffffu, xm, d);
+                    if (lane >= d) { xt = ot + xt + (unsigned long long)xm * os; xs += os; xm += om; }
+                }
+                if (lane == 31) { S->rs_w[warp] = (long long)xs; S->rt_w[warp] = (long long)xt; }
+                cbar();
+                // prefix over the previous warps (each spans 32 x 16 samples)
+                unsigned long long ps, pt;
+                {
+                    unsigned long long ws = (lane < NW) ? (unsigned long long)S->rs_w[lane & (NW - 1)] : 0ULL;
+                    unsigned long long wt = (lane < NW) ? (unsigned long long)S->rt_w[lane & (NW - 1)] : 0ULL;
+                    unsigned wm = 32 * SPT;
+#pragma unroll
+                    for (int d = 1; d < NW; d <<= 1) {
+                        const unsigned long long os = __shfl_up_sync(0xffffffffu, ws, d);
+                        const unsigned long long ot = __shfl_up_sync(0xffffffffu, wt, d);
+                        const unsigned om = __shfl_up_sync(0xffffffffu, wm, d);
+                        if (lane >= d) { wt = ot + wt + (unsigned long long)wm * os; ws += os; wm += om; }
+                    }
+                    unsigned long long es = __shfl_up_sync(0xffffffffu, ws, 1);
+                    unsigned long long et = __shfl_up_sync(0xffffffffu, wt, 1);
+                    if (lane == 0) { es = 0; et = 0; }
+                    const unsigned long long pws = __shfl_sync(0xffffffffu, es, warp);
+                    const unsigned long long pwt = __shfl_sync(0xffffffffu, et, warp);
+                    // then the lanes before this one inside the warp
+                    unsigned long long ls = __shfl_up_sync(0xffffffffu, xs, 1);
+                    unsigned long long lt = __shfl_up_sync(0xffffffffu, xt, 1);
+                    unsigned lm = __shfl_up_sync(0xffffffffu, xm, 1);
+                    if (lane == 0) { ls = 0; lt = 0; lm = 0; }
+                    ps = pws + ls;
+                    pt = pwt + lt + (unsigned long long)lm * pws;
+                }
+                // history: d1 entering the block = p1 - p2; q entering = p1
+                const int i0 = SPT * tid;
+                if (sel == 1) {
+                    unsigned long long acc = h1 + ps;
+#pragma unroll
+                    for (int i = 0; i < SPT; i++) { acc += (unsigned long long)q[i]; q[i] = (long long)acc; }
+                } else {
+                    unsigned long long d1 = (h1 - h2) + ps;
+                    unsigned long long acc = h1 + (unsigned long long)i0 * (h1 - h2) + pt;
+#pragma unroll
+                    for (int i = 0; i < SPT; i++) {
+                        d1 += (unsigned long long)q[i];
+                        acc += d1;
+                        q[i] = (long long)acc;
+                    }
+                }
+            }
+            // outgoing history: q[np-1], q[np-2] (padded block)
+            if (tid == (np - 1) / SPT) {
+                const int j1 = (np - 1) % SPT;
+#pragma unroll
+                for (int i = 0; i < SPT; i++) {
+                    if (i == j1) S->p1 = q[i];
+                    if (i == j1 - 1) S->p2 = q[i];
+                }
+                if (j1 == 0) S->p2 = 0;   // np is a multiple of 4: never happens
+            }
+            // ---- dequantize (codec.py:135-146) into the y buffer ----
+            if (tid == 0 && S->store_pending) { bulk_wait_read(); S->store_pending = 0; }
+            cbar();   // p1/p2 readers are done with the old values; y buffer free
+            if (active) {
+                T out[SPT];
+                if (Tr::F) {
+                    const double s = decode_scale_code(code) * ldexp(1.0, fbe);
+                    const double rs = __ddiv_rn(1.0, s);
+#pragma unroll
+                    for (int i = 0; i < SPT; i++) {
+                        const long long qv = q[i];
+                        double r;
+                        if (qv == (long long)(int)qv)
+                            r = __hiloint2double(0x43380000, (int)qv ^ (int)0x80000000) - kMagicI;
+                        else
+                            r = (double)qv;
+                        const double y0 = r * rs;
+                        const double ee = __fma_rn(-s, y0, r);
+                        out[i] = (T)__fma_rn(ee, rs, y0);
+                    }
+                } else {
+                    const double a = decode_scale_code(code);
+                    const double ra = __ddiv_rn(1.0, a);
+#pragma unroll
+                    for (int i = 0; i < SPT; i++) {
+                        long long yi = q[i];
+                        if (a != 1.0) {
+                            const double r = (double)q[i];
+                            const double y0 = r * ra;
+                            const double ee = __fma_rn(-a, y0, r);
+                            yi = f2i64(rint(__fma_rn(ee, ra, y0)));
+                        }
+                        yi = yi < Tr::LO ? Tr::LO : (yi > Tr::HI ? Tr::HI : yi);
+                        out[i] = (T)yi;
+                    }
+                }
+                constexpr int PER = 16 / (int)sizeof(T);
+                uint4* y4 = (uint4*)(ybuf + SPT * tid);
+#pragma unroll
+                for (int c = 0; c < SPT / PER; c++) {
+                    uint4 w4;
+                    memcpy(&w4, &out[c * PER], 16);
+                    y4[c] = w4;
+                }
+            }
+            fence_proxy_async();
+            cbar();
+            if (tid == 0) {
+                T* y = (T*)P.y + start;
+                const int bytes = n * (int)sizeof(T);
+                const int full = bytes & ~15;
+                if (full > 0 && (((uintptr_t)y) & 15) == 0) {
+                    bulk_store(y, ybuf, (uint32_t)full);
+                    S->store_pending = 1;
+                    for (int i = full; i < bytes; i++) ((uint8_t*)y)[i] = ((const uint8_t*)ybuf)[i];
+                } else {
+                    for (int i = 0; i < bytes; i++) ((uint8_t*)y)[i] = ((const uint8_t*)ybuf)[i];
+                }
+            }
+        }
+    }
+    if (tid == 0 && S->store_pending) bulk_wait_all();
+}
+
+}  // namespace d3
+
+size_t decode_v3_smem_bytes(int dt, int payload_cap) {
+    auto al = [](size_t v) { return (v + 127) & ~(size_t)127; };
+    return al(sizeof(d3::St)) + al((size_t)d3::MAXBS / 4 + 128) + al((size_t)d3::MAXBS * dt_width(dt)) +
+           2 * (size_t)((payload_cap + 64 + 127) & ~127);
+}
+
+bool decode_v3_supported(int dt, int bs) {
+    return dt >= 0 && dt <= 3 && bs >= 128 && bs <= d3::MAXBS && (bs & (bs - 1)) == 0;
+}
+
+template <int DT, bool FIX>
+static void* d3_fn() { return (void*)d3::decode_v3_kernel<DT, FIX>; }
+static void* d3_kernel(int dt, bool fix) {
+    switch (dt) {
+        case 0: return d3_fn<0, false>();
+        case 1: return fix ? d3_fn<1, true>() : d3_fn<1, false>();
+        case 2: return fix ? d3_fn<2, true>() : d3_fn<2, false>();
+        default: return fix ? d3_fn<3, true>() : d3_fn<3, false>();
+    }
+}
+
+int decode_v3_resident_ctas(int dt, size_t smem) {
+    int dev = 0, nsm = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const void* fn = d3_kernel(dt, false);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, d3::NT, smem) != cudaSuccess || per < 1)
+        per = 1;
+    return per * (nsm > 0 ? nsm : 148);
+}
+
+static int launch_d3_range(int dt, bool fix, const DecParams& P, long long s0, long long s1, int grid,
+                           size_t smem, cudaStream_t st) {
+    const void* fn = d3_kernel(dt, fix);
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return APAX_ERR_CUDA;
+    DecParams p = P;
+    p.seg_begin = s0;
+    p.seg_end = s1;
+    const long long ns = s1 - s0;
+    const int g = (int)(ns < grid ? ns : grid);
+    void* args[] = {&p};
+    if (cudaLaunchKernel(fn, dim3(g), dim3(d3::NT), args, smem, st) != cudaSuccess) return APAX_ERR_CUDA;
+    return APAX_OK;
+}
+
+int launch_decode_v3(int dt, const DecParams& P, int grid, size_t smem, cudaStream_t st) {
+    const long long nseg = (P.n_blocks + P.segment_blocks - 1) / P.segment_blocks;
+    // full-block segments take the compile-time-geometry kernel; the segment
+    // holding a partial last block follows in a generic launch
+    const bool fixable = P.bs == d3::MAXBS && dt >= 1 && dt <= 3;
+    long long sfull = fixable ? nseg : 0;
+    if (fixable && (P.n % d3::MAXBS) != 0) sfull = nseg - 1;
+    if (sfull > 0) {
+        const int r = launch_d3_range(dt, true, P, 0, sfull, grid, smem, st);
+        if (r) return r;
+    }
+    if (sfull < nseg) return launch_d3_range(dt, false, P, sfull, nseg, grid, smem, st);
+    return APAX_OK;
+}
+
+}  // namespace apax

@@ -36,6 +36,7 @@
 // Blocks whose differences may leave int32 (max|q| >= 2^29) take a 64-bit
 // phase C/D.
 #include <cstdint>
+#include <cstdlib>
 #include <type_traits>
 #include <cuda_runtime.h>
 
@@ -434,12 +435,13 @@ __device__ void warp_copy_out(uint8_t* dst, const uint32_t* src, long long len) 
 }
 
 // placement warp: resolve every finished unit of this CTA and copy it out
-__device__ __noinline__ void placement_loop(long long n_units, long long n_blocks, unsigned long long* lookback,
+__device__ __noinline__ void placement_loop(long long unit_begin, long long unit_end, long long n_units,
+                                            long long n_blocks, unsigned long long* lookback,
                                             unsigned long long* status, long long* block_offsets, uint8_t* out,
                                             St* S, uint8_t* slot0, uint8_t* slot1) {
     const int lane = threadIdx.x & 31;
     int k = 0;
-    for (long long u = blockIdx.x; u < n_units; u += gridDim.x, k++) {
+    for (long long u = unit_begin + blockIdx.x; u < unit_end; u += gridDim.x, k++) {
         const int sl = k & 1;
         nb_full_sync(sl);
         const long long len = S->slot_len[sl];
@@ -477,14 +479,17 @@ __device__ __noinline__ void placement_loop(long long n_units, long long n_block
             for (long long bb = b0 + lane; bb < b1; bb += 32) block_offsets[bb] += kFileHeader + prefix;
         __syncwarp();
         __threadfence_block();
-        if (u + 2 * (long long)gridDim.x < n_units) nb_free_arrive(sl);   // the slot is reused
+        if (u + 2 * (long long)gridDim.x < unit_end) nb_free_arrive(sl);   // the slot is reused
     }
 }
 
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
-template <int DT>
+// FIX: every block of this launch is a full 4096-sample block; the block
+// geometry is then compile-time (the partial last block of a stream goes
+// through a second, generic launch over its unit).
+template <int DT, bool FIX>
 __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P) {
     using Tr = DT_<DT>;
     using T = typename Tr::T;
@@ -497,8 +502,8 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
 
     extern __shared__ __align__(128) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int bs = P.bs;
-    const int NL = bs >> 7;                     // leaves of a full block
+    const int bs = FIX ? MAXBS : P.bs;
+    const int NL = FIX ? 32 : (bs >> 7);        // leaves of a full block
     const bool FQ = (P.mode == 2);
     const int XB = P.stage_bytes;               // bytes per staging buffer
 
@@ -517,10 +522,20 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
     }
     __syncthreads();
     if (warp == NCW) {
-        placement_loop(P.n_units, P.n_blocks, P.lookback, P.status, P.block_offsets, P.out, S, slot0, slot1);
+        placement_loop(P.unit_begin, P.unit_end, P.n_units, P.n_blocks, P.lookback, P.status, P.block_offsets,
+                       P.out, S, slot0, slot1);
         return;
     }
     // ---------------- compute warps (named barrier 1, 256 threads) ----------------
+#ifdef APAX_V3_PROF
+    // phase timing of thread 0 (tools/prof_v3.py): acc[k] += clock(k) - clock(k-1)
+    unsigned long long prof_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long prof_wait = 0;
+    long long prof_last = clock64();
+#define PROF_MARK(k) do { if (tid == 0) { const long long c_ = clock64(); prof_acc[k] += (unsigned long long)(c_ - prof_last); prof_last = c_; } } while (0)
+#else
+#define PROF_MARK(k) do { } while (0)
+#endif
     auto xbuf = [&](int k) -> T* { return (T*)(smem + xoff + (k ? XB : 0)); };
     // staging state of the two buffers, in scalars (no local memory)
     long long bb0 = -1, bb1 = -1;       // block held by buffer 0 / 1
@@ -529,10 +544,11 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
     auto bufblk_get = [&](int k) -> long long { return k ? bb1 : bb0; };
     auto bufblk_set = [&](int k, long long v) { if (k) bb1 = v; else bb0 = v; };
 
-    auto block_n = [&](long long b) -> int {
+    auto block_len = [&](long long b) -> int {   // exact
         long long r = P.n - b * (long long)bs;
         return (int)(r < bs ? r : bs);
     };
+    auto block_n = [&](long long b) -> int { return FIX ? MAXBS : block_len(b); };
     // stage block b into buffer k (all compute threads)
     auto stage = [&](long long b, int k) {
         const int n = block_n(b);
@@ -558,7 +574,13 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
     };
     auto wait_buf = [&](int k) {
         if (!((wst >> k) & 1u)) {
+#ifdef APAX_V3_PROF
+            const long long w0_ = clock64();
             mbar_wait_acq(&S->mb_stage[k], (phs >> k) & 1u);
+            if (tid == 0) prof_wait += (unsigned long long)(clock64() - w0_);
+#else
+            mbar_wait_acq(&S->mb_stage[k], (phs >> k) & 1u);
+#endif
             phs ^= 1u << k;
             wst |= 1u << k;
         }
@@ -572,7 +594,7 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
         if (NEED_PEAK) {
             // full blocks sit in the leaf layout: rows of 8*NL samples, stride RS
             const bool lay = TRL && n == bs;
-            const int lgr = 3 + __ffs(NL) - 1;        // log2(8 * NL)
+            const int lgr = FIX ? 8 : 3 + __ffs(NL) - 1;   // log2(8 * NL)
             if (DT == 3) {
                 const uint4* x4 = (const uint4*)xs;
                 int ms = 0;
@@ -636,7 +658,7 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
     long long a_done = -1;
     int kunit = 0;
 
-    for (long long u = blockIdx.x; u < P.n_units; u += gridDim.x, kunit++) {
+    for (long long u = P.unit_begin + blockIdx.x; u < P.unit_end; u += gridDim.x, kunit++) {
         const int sl = kunit & 1;
         uint8_t* slot = sl ? slot1 : slot0;
         const long long b0 = u * P.unit_blocks;
@@ -683,14 +705,15 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
             const long long b = pass_block(kp);
             const int kind = halo ? (kp == 0 ? 1 : 0) : (warm ? (kp == 0 ? 2 : (kp == 1 ? 3 : 0)) : 0);
             const int n = block_n(b);
-            const int G = (n + 3) >> 2;
-            const int np = 4 * G;
-            const bool regular = (n == bs);
+            const int G = FIX ? MAXBS / 4 : (n + 3) >> 2;
+            const int np = FIX ? MAXBS : 4 * G;
+            const bool regular = FIX ? true : (n == bs);
             const int cur = (bb0 == b) ? 0 : 1;
             T* xs = xbuf(cur);
             const bool emit = (kind == 0);
             const bool fq_emit = FQ && emit;
 
+            PROF_MARK(0);
             // ============ S1 (thread 0): gain, code, scale ============
             if (tid == 0) {
                 if (S->store_pending) { bulk_wait_read(); S->store_pending = 0; }
@@ -792,6 +815,7 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
                 S->zlen = (int)zg;
             }
             cbar();  // B2
+            PROF_MARK(1);
 
             // stage the next distinct block into the other buffer
             {
@@ -800,7 +824,7 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
                     const long long bb = pass_block(kk);
                     if (bb != b) { nb = bb; break; }
                 }
-                if (nb < 0 && u + gridDim.x < P.n_units) {
+                if (nb < 0 && u + gridDim.x < P.unit_end) {
                     const long long bb = first_block(u + gridDim.x);
                     if (bb != b) nb = bb;
                 }
@@ -809,7 +833,7 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
                     if (tid == 0) {
                         const long long pb = nb + 1;   // warm L2 one block further ahead
                         if (pb < P.n_blocks) {
-                            const long long bytes = (long long)block_n(pb) * (long long)sizeof(T);
+                            const long long bytes = (long long)block_len(pb) * (long long)sizeof(T);
                             const T* psrc = (const T*)P.x + pb * (long long)bs;
                             if ((((uintptr_t)psrc) & 15) == 0 && (bytes & 15) == 0 && bytes > 0)
                                 prefetch_l2(psrc, (uint32_t)bytes);
@@ -879,6 +903,7 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
                     }
                 }
                 cbar();  // B3
+                PROF_MARK(2);
                 if (fq_emit && tid == 0) {
                     // quality loop (codec.py:244-252, 179-189)
                     double px, pd;
@@ -903,7 +928,7 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
             // ============ phase C: streams, widths, costs, JEE structure ============
             const int sel_spec = S->sel_spec;
             const int t0 = SPT * tid;
-            const bool active = t0 < np;
+            const bool active = FIX ? true : t0 < np;
             const int p0 = 4 * tid;                    // first group of this thread
             const int4* qb4 = (const int4*)qbuf;
             // physical chunk of this thread's chunk m is qpb ^ m (see swz)
@@ -925,9 +950,10 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
                     hq2 = h.x; hq1 = h.y;
                 }
                 q14 = q[14]; q15 = q[15];
-                const int ng = min(4, G - p0);         // valid groups of this thread (>= 1)
+                const int ng = FIX ? 4 : min(4, G - p0);   // valid groups of this thread (>= 1)
                 if (!wide) {
                     int m1 = hq1, dprev = hq1 - hq2;
+                    unsigned sgn = (unsigned)hq1 >> 31;   // sign bits, oldest first
 #pragma unroll
                     for (int g = 0; g < 4; g++) {
                         unsigned o0 = 0, o1 = 0, o2 = 0;
@@ -937,7 +963,7 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
                             const int v1 = v0 - m1;
                             const int v2 = v1 - dprev;
                             o0 |= wb32(v0); o1 |= wb32(v1); o2 |= wb32(v2);
-                            flips += (int)((unsigned)(v0 ^ m1) >> 31);
+                            sgn = __funnelshift_l((unsigned)v0, sgn, 1);
                             m1 = v0; dprev = v1;
                         }
                         if (g < ng) {
@@ -946,6 +972,8 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
                             epk2 |= (uint32_t)bitlen32(o2) << (8 * g);
                         }
                     }
+                    // sign-bit flips between neighbours (17 bits: q[t0-1] .. q[t0+15])
+                    flips = __popc((sgn ^ (sgn >> 1)) & 0xffffu);
                 } else {
                     long long m1 = hq1, dprev = (long long)hq1 - (long long)hq2;
 #pragma unroll
@@ -1030,8 +1058,9 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
                                     ((unsigned)(d5 + 1) < 3u ? 16u : 0u);
                 const uint32_t S2 = ((unsigned)(d1 + 2) < 5u ? 1u : 0u) | ((unsigned)(d2 + 2) < 5u ? 2u : 0u) |
                                     ((unsigned)(d3 + 2) < 5u ? 4u : 0u) | ((unsigned)(d4 + 2) < 5u ? 8u : 0u);
-                const int nv = active ? min(4, G - p0) : 0;                // valid positions
-                const int npr = active ? max(0, min(4, G - 1 - p0)) : 0;   // positions with p+1 < G
+                const int nv = FIX ? 4 : (active ? min(4, G - p0) : 0);    // valid positions
+                const int npr = FIX ? (tid == NCT - 1 ? 3 : 4)
+                                    : (active ? max(0, min(4, G - 1 - p0)) : 0);   // positions with p+1 < G
                 Vb = (1u << nv) - 1u;
                 const uint32_t first = (p0 == 0) ? 1u : 0u;                // position 0: always an escape
                 Pb = S1 & (S1 >> 1) & ((1u << npr) - 1u) & ~first;
@@ -1096,6 +1125,7 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
                 bufblk_set(cur, -1);
             }
             cbar();  // B4
+            PROF_MARK(3);
 
             // ============ resolve: totals, selector, offsets ============
             long long tt0, tt1, tt2;
@@ -1257,7 +1287,7 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
                         q[4 * m] = v.x; q[4 * m + 1] = v.y; q[4 * m + 2] = v.z; q[4 * m + 3] = v.w;
                     }
                     int pos = 8 * (wb + HS + jee_bytes) + mb_off;
-                    const int ng = min(4, G - p0);
+                    const int ng = FIX ? 4 : min(4, G - p0);
                     if (!wide) {
                         auto emit_groups = [&](auto SELC) {
                             constexpr int SL = decltype(SELC)::value;
@@ -1337,12 +1367,13 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
                 }
             }
 
+            PROF_MARK(4);
             // ============ phase A of the next pass block (overlaps this block's tail) ============
             {
                 long long nb = -1;
                 bool nfirst = false;
                 if (kp + 1 < npass) nb = pass_block(kp + 1);
-                else if (u + gridDim.x < P.n_units) { nb = first_block(u + gridDim.x); nfirst = true; }
+                else if (u + gridDim.x < P.unit_end) { nb = first_block(u + gridDim.x); nfirst = true; }
                 a_done = -1;
                 if (nb >= 0) {
                     const int k = (bb0 == nb) ? 0 : ((bb1 == nb) ? 1 : -1);
@@ -1355,6 +1386,7 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
             }
             if (emit) fence_proxy_async();  // window writes -> async proxy (bulk store)
             cbar();  // B5
+            PROF_MARK(5);
 
             // ============ flush + bookkeeping (thread 0) ============
             if (emit && tid == 0) {
@@ -1392,6 +1424,7 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
             }
         }
 
+        PROF_MARK(6);
         // ---------------- unit end: last tail, publish, hand to the placement warp ----------------
         if (tid == 0) {
             if (S->store_pending) { bulk_wait_all(); S->store_pending = 0; }
@@ -1416,6 +1449,13 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
             P.out[tid] = h[tid];
         }
     }
+#ifdef APAX_V3_PROF
+    if (tid == 0 && P.trace) {
+        const long long c_ = clock64();
+        prof_acc[7] = prof_wait;   // staging waits (inside the phases above)
+        for (int k2 = 0; k2 < 8; k2++) atomicAdd((unsigned long long*)(P.trace + 10 * P.n_blocks) + k2, prof_acc[k2]);
+    }
+#endif
 }
 
 }  // namespace v3
@@ -1438,15 +1478,15 @@ bool encode_v3_supported(int dt, int bs) {
     return dt >= 0 && dt <= 3 && bs >= 128 && bs <= v3::MAXBS && (bs & (bs - 1)) == 0;
 }
 
-template <int DT>
-static void* v3_fn() { return (void*)v3::encode_v3_kernel<DT>; }
+template <int DT, bool FIX>
+static void* v3_fn() { return (void*)v3::encode_v3_kernel<DT, FIX>; }
 
-static void* v3_kernel(int dt) {
+static void* v3_kernel(int dt, bool fix) {
     switch (dt) {
-        case 0: return v3_fn<0>();
-        case 1: return v3_fn<1>();
-        case 2: return v3_fn<2>();
-        default: return v3_fn<3>();
+        case 0: return v3_fn<0, false>();
+        case 1: return fix ? v3_fn<1, true>() : v3_fn<1, false>();
+        case 2: return fix ? v3_fn<2, true>() : v3_fn<2, false>();
+        default: return fix ? v3_fn<3, true>() : v3_fn<3, false>();
     }
 }
 
@@ -1454,21 +1494,43 @@ int encode_v3_resident_ctas(int dt, size_t smem) {
     int dev = 0, nsm = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const void* fn = v3_kernel(dt);
+    const void* fn = v3_kernel(dt, false);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, v3::NT, smem) != cudaSuccess || per < 1)
         per = 1;
     return per * (nsm > 0 ? nsm : 148);
 }
 
-int launch_encode_v3(int dt, const EncParams& P, int grid, size_t smem, cudaStream_t st) {
-    const void* fn = v3_kernel(dt);
+static int launch_v3_range(int dt, bool fix, const EncParams& P, long long u0, long long u1, int grid,
+                           size_t smem, cudaStream_t st) {
+    const void* fn = v3_kernel(dt, fix);
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return APAX_ERR_CUDA;
     EncParams p = P;
+    p.unit_begin = u0;
+    p.unit_end = u1;
+    const long long nu = u1 - u0;
+    const int g = (int)(nu < grid ? nu : grid);
     void* args[] = {&p};
-    if (cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(v3::NT), args, smem, st) != cudaSuccess)
+    if (cudaLaunchCooperativeKernel(fn, dim3(g), dim3(v3::NT), args, smem, st) != cudaSuccess)
         return APAX_ERR_CUDA;
+    return APAX_OK;
+}
+
+int launch_encode_v3(int dt, const EncParams& P, int grid, size_t smem, cudaStream_t st) {
+    // bs 4096 (i16/i32/f32): units made only of full blocks take the
+    // compile-time-geometry kernel; the unit holding a partial last block
+    // follows in a generic launch (its look-back reads the first launch's
+    // published lengths)
+    const bool fixable = P.bs == v3::MAXBS && dt >= 1 && dt <= 3 && getenv("APAX_V3_NOFIX") == nullptr;
+    long long ufull = P.n_units;
+    if (fixable && (P.n % v3::MAXBS) != 0) ufull = P.n_units - 1;
+    if (!fixable) ufull = 0;
+    if (ufull > 0) {
+        const int r = launch_v3_range(dt, true, P, 0, ufull, grid, smem, st);
+        if (r) return r;
+    }
+    if (ufull < P.n_units) return launch_v3_range(dt, false, P, ufull, P.n_units, grid, smem, st);
     return APAX_OK;
 }
 

@@ -16,6 +16,7 @@ struct EncParams {
     long long n_blocks;
     long long unit_blocks;
     long long n_units;
+    long long unit_begin, unit_end;  // units processed by this launch (v3)
     int halo;              // 1: lossless whole-stream units (no restart)
     int policy;            // 0 cold, 1 warm_self (FR only)
     uint8_t* out;
@@ -46,6 +47,8 @@ struct DecParams {
     unsigned long long* carry;  // 8 words per block
     unsigned int* ticket;
     int payload_cap;            // smem bytes reserved for one block payload
+    long long segment_blocks;   // d3: every segment_blocks-th block starts a segment
+    long long seg_begin, seg_end;
 };
 
 size_t encode_smem_bytes(int dt, int bs, int stage_bytes, int x_in_smem);
@@ -63,6 +66,10 @@ bool encode_v3_supported(int dt, int bs);
 int encode_v3_resident_ctas(int dt, size_t smem);
 int launch_encode_v3(int dt, const EncParams& P, int grid, size_t smem, cudaStream_t st);
 int launch_decode(int dt, const DecParams& P, int grid, size_t smem, cudaStream_t st);
+size_t decode_v3_smem_bytes(int dt, int payload_cap);
+bool decode_v3_supported(int dt, int bs);
+int decode_v3_resident_ctas(int dt, size_t smem);
+int launch_decode_v3(int dt, const DecParams& P, int grid, size_t smem, cudaStream_t st);
 size_t decode_v2_smem_bytes(int dt, int bs, int payload_cap);
 bool decode_v2_supported(int bs);
 int decode_v2_resident_ctas(int dt, size_t smem);

@@ -55,6 +55,40 @@ def test_golden_container_decode(name):
     assert np.array_equal(y2, c["y"])
 
 
+@pytest.mark.parametrize("name", [n for n in golden_containers() if n.startswith(("seg_", "warm_"))])
+def test_golden_container_decode_segments(name):
+    """Segment-serial decoder (apax_decode_segments) on the golden
+    segmented containers: bit-exact against the reference's decode."""
+    c = load_container(GOLDEN / "containers" / f"{name}.npz")
+    blob = torch.from_numpy(np.frombuffer(c["blob"], np.uint8).copy()).cuda()
+    offs = torch.from_numpy(c["offsets"]).cuda()
+    y = decode_device(blob, len(c["blob"]), offs, segment_blocks=c["meta"]["segment_blocks"]).cpu().numpy()
+    assert y.dtype == c["y"].dtype and np.array_equal(y, c["y"])
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_segment_decoder_random_vs_oracle(seed):
+    """Encoder containers of random segment length, dtype, mode and block
+    size (powers of two, partial last blocks): the segment decoder is
+    bit-exact against the oracle's decode."""
+    rng = np.random.default_rng(4000 + seed)
+    for _ in range(8):
+        dt = [Dtype.I8, Dtype.I16, Dtype.I32, Dtype.F32][rng.integers(0, 4)]
+        modes = [Mode.FIXED_RATE, Mode.FIXED_QUALITY] + ([] if dt.is_float else [Mode.LOSSLESS])
+        mode = modes[rng.integers(0, len(modes))]
+        bs = int(rng.choice([128, 256, 1024, 2048, 4096, 4096]))
+        target = float(rng.uniform(1, 12)) if mode is Mode.FIXED_RATE else float(rng.uniform(10, 100))
+        seg = int(rng.choice([1, 2, 3, 8, 16]))
+        x = _random_case(rng, dt)
+        if rng.integers(0, 2):
+            x = np.concatenate([x, x[: bs * 3]])
+        cfg = StreamConfig(dt, bs, mode, target, segment_blocks=seg)
+        res = encode_device(torch.from_numpy(x).cuda(), cfg)
+        ref = O.decode(res.to_bytes())
+        y = decode_device(res.blob, res.nbytes, res.block_offsets, segment_blocks=seg).cpu().numpy()
+        assert np.array_equal(y, ref), (dt, mode, bs, seg, x.size)
+
+
 def test_drop_in_bytes_api():
     c = load_container(GOLDEN / "containers" / "cfg1_i16_fr4.npz")
     cfg = _cfg(c["meta"])
@@ -161,7 +195,11 @@ def test_bench_size_cfg2_segmented_vs_oracle():
     dec = Decoder(x.size, Dtype.F32, 4096)
     dec.decode(res.blob, res.nbytes, res.block_offsets)
     y = dec.finish().cpu().numpy()
-    assert np.array_equal(y, O.decode(ref, offs, nthreads=0))
+    yo = O.decode(ref, offs, nthreads=0)
+    assert np.array_equal(y, yo)
+    # the segment-serial decoder on the same container
+    dec.decode(res.blob, res.nbytes, res.block_offsets, segment_blocks=16)
+    assert np.array_equal(dec.finish().cpu().numpy(), yo)
 
 
 def test_bench_size_cfg1_lossless_round_trip():
