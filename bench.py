@@ -3,8 +3,10 @@
 
 Workload (N=1 line): BASELINE configs[1] = cfg2, float32 AR(2) 2^26 samples,
 fixed-quality at the reference profiler's recommended SRR target, encoded as a
-container of independent 16-block segments (cold policy: every segment is
+container of independent P-block segments (cold policy: every segment is
 byte-identical to the reference encode_stream of that slice), then decoded.
+P defaults to the one-wave length (every resident encoder CTA one segment:
+37 blocks on a 148-SM B200); `--segment-blocks` fixes it.
 One step = encode of the whole array + decode of the resulting container,
 inputs resident in HBM.  `value` = input bytes / step time (GB/s).
 
@@ -137,6 +139,18 @@ def cpu_round_trip(x, target, seg, threads, budget_s=10.0):
             "dec_gbs": nb * reps / dec_t / 1e9, "reps": reps, "seconds": enc_t + dec_t}
 
 
+def workload_segment_blocks(args, n):
+    """P of the workload: --segment-blocks, else the one-wave length of this
+    device (the library query), else 37 (its value on B200)."""
+    if args.segment_blocks > 0:
+        return args.segment_blocks
+    try:
+        from paper_1303_4994_b200 import Dtype, Mode, wave_segment_blocks
+        return wave_segment_blocks(n, Dtype.F32, Mode.FIXED_QUALITY, 4096)
+    except Exception:  # noqa: BLE001
+        return 37
+
+
 def run_reference(args, rank):
     """--impl reference: the reference algorithm (C oracle port) on all host
     threads, same metric/config; rank 0 only."""
@@ -144,16 +158,17 @@ def run_reference(args, rank):
         return
     from paper_1303_4994_b200 import workloads as W
     threads = os.cpu_count() or 1
+    seg = workload_segment_blocks(args, 1 << args.n_log2)
     n = 1 << 22
     x = W.cfg2_ar2_f32(n)
     from oracle import oracle as O
     for _ in range(max(args.warmup, 1)):
-        blob, offs, _ = O.encode(x, 3, 2, W.CFG2_TARGET_DB, 4096, segment_blocks=16,
+        blob, offs, _ = O.encode(x, 3, 2, W.CFG2_TARGET_DB, 4096, segment_blocks=seg,
                                  nthreads=threads)
     times = []
     for _ in range(args.steps):
         a = time.perf_counter()
-        blob, offs, _ = O.encode(x, 3, 2, W.CFG2_TARGET_DB, 4096, segment_blocks=16,
+        blob, offs, _ = O.encode(x, 3, 2, W.CFG2_TARGET_DB, 4096, segment_blocks=seg,
                                  nthreads=threads)
         O.decode(blob, offs, nthreads=threads)
         times.append(time.perf_counter() - a)
@@ -164,9 +179,9 @@ def run_reference(args, rank):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "cfg2: f32 AR(2) x1e3, FQ at profiler SRR target, 16-block "
+        "config": {"workload": f"cfg2: f32 AR(2) x1e3, FQ at profiler SRR target, {seg}-block "
                                "cold segments, bs 4096 (bounded 2^22-sample sample)",
-                   "n_samples": x.size, "segment_blocks": 16, "block_size": 4096},
+                   "n_samples": x.size, "segment_blocks": seg, "block_size": 4096},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"cfg2 first 2^22 samples (16 MiB f32) encode+decode, "
                                    f"{args.steps} steps, OpenMP over segments"},
@@ -181,7 +196,8 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--segment-blocks", type=int, default=16)
+    ap.add_argument("--segment-blocks", type=int, default=0,
+                    help="blocks per segment; 0 = one-wave (every resident encoder CTA one segment)")
     ap.add_argument("--n-log2", type=int, default=26)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -210,6 +226,7 @@ def main():
     from paper_1303_4994_b200 import workloads as W
 
     n = 1 << args.n_log2
+    args.segment_blocks = workload_segment_blocks(args, n)
     x_host = W.cfg2_ar2_f32(n, seed=2 + rank)
     target = W.CFG2_TARGET_DB
     cfg = StreamConfig(Dtype.F32, 4096, Mode.FIXED_QUALITY, target,
@@ -287,7 +304,7 @@ def main():
     alg_dec = nbytes + in_bytes + 8 * (enc.n_blocks + 1)   # read container + offsets, write y
     ach_enc = alg_enc / (mean_enc * 1e-3) / 1e9
     ach_dec = alg_dec / (mean_dec * 1e-3) / 1e9
-    dominant = "encode_v2_kernel<3>" if mean_enc >= mean_dec else "decode_v2_kernel<3>"
+    dominant = "encode_v3_kernel<3" if mean_enc >= mean_dec else "decode_v3_kernel<3"
     ach = ach_enc if mean_enc >= mean_dec else ach_dec
 
     # ---- e2e: host buffers through the C-ABI entry points ----
@@ -373,7 +390,7 @@ def main():
             "dtype": "f32", "data": "synthetic",
             "config": {
                 "workload": "cfg2: f32 AR(2) r=0.98 x1e3, 2^26 samples/GPU, fixed-quality at "
-                            "the reference profiler's SRR target, 16-block cold segments, "
+                            f"the reference profiler's SRR target, {args.segment_blocks}-block cold segments, "
                             "bs 4096; step = encode + decode (device-resident)",
                 "n_samples_per_gpu": n, "block_size": 4096,
                 "segment_blocks": args.segment_blocks, "srr_target_db": target,

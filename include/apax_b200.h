@@ -50,6 +50,12 @@ const char* apax_status_string(int code);
 /* Worst-case container size for n samples (28-byte file header included). */
 int64_t apax_max_encoded_bytes(int64_t n, int dtype, int block_size);
 
+/* Segment length (blocks) that gives every resident encoder CTA of this
+ * device exactly one segment of n samples: the one-wave schedule.  A
+ * convenience for choosing segment_blocks; the container depends only on
+ * the value passed to apax_encode. */
+int64_t apax_encode_wave_segment_blocks(int64_t n, int dtype, int mode, int block_size);
+
 /* Device workspace needed by apax_encode for these arguments. */
 int64_t apax_encode_workspace_bytes(int64_t n, int dtype, int mode, int block_size,
                                     int64_t segment_blocks);

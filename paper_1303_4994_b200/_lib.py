@@ -48,6 +48,8 @@ def lib():
     L.apax_decode_workspace_bytes.restype = I64
     L.apax_decode.argtypes = [P, I64, I64, I32, I32, P, P, P, P, I64, P]
     L.apax_decode.restype = I32
+    L.apax_encode_wave_segment_blocks.argtypes = [I64, I32, I32, I32]
+    L.apax_encode_wave_segment_blocks.restype = I64
     L.apax_decode_segments_workspace_bytes.argtypes = [I64, I32, I32]
     L.apax_decode_segments_workspace_bytes.restype = I64
     L.apax_decode_segments.argtypes = [P, I64, I64, I32, I32, P, I64, P, P, P, I64, P]
@@ -65,4 +67,5 @@ EXPORTED_SYMBOLS = (
     "apax_encode_workspace_bytes", "apax_encode", "apax_decode_workspace_bytes",
     "apax_decode", "apax_find_blocks", "apax_parse_file_header",
     "apax_decode_segments_workspace_bytes", "apax_decode_segments",
+    "apax_encode_wave_segment_blocks",
 )

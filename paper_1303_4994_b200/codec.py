@@ -92,6 +92,16 @@ def parse_file_header(data) -> Tuple[StreamConfig, int]:
     return cfg, int(count.value) & _U64_MAX
 
 
+def wave_segment_blocks(n: int, dtype: Dtype, mode: Mode, block_size: int) -> int:
+    """Segment length giving every resident encoder CTA of the current
+    device one segment (apax_encode_wave_segment_blocks)."""
+    _, L = _require_cuda()
+    v = int(L.apax_encode_wave_segment_blocks(int(n), dtype.wire_code, mode.value, int(block_size)))
+    if v < 1:
+        raise InvalidConfig("invalid arguments")
+    return v
+
+
 def max_encoded_bytes(n: int, dtype: Dtype, block_size: int) -> int:
     return int(_lib.lib().apax_max_encoded_bytes(int(n), dtype.wire_code, int(block_size)))
 

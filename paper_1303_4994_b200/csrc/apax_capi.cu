@@ -305,6 +305,18 @@ int apax_decode(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, int b
     return launch_decode(dtype, P, p.grid, p.smem, s);
 }
 
+int64_t apax_encode_wave_segment_blocks(int64_t n, int dtype, int mode, int block_size) {
+    // segment length that gives every resident encoder CTA one segment
+    // (a one-wave schedule); the container then depends on this value only
+    EncPlan p;
+    if (plan_encode(n, dtype, mode, block_size, 1, &p)) return -1;
+    int resident = p.grid;
+    if (p.v3) resident = encode_v3_resident_ctas(dtype, p.smem);
+    else if (p.v2) resident = encode_v2_resident_ctas(dtype, p.smem);
+    if (resident < 1) resident = 1;
+    return (p.n_blocks + resident - 1) / resident;
+}
+
 int64_t apax_decode_segments_workspace_bytes(int64_t n, int dtype, int block_size) {
     return apax_decode_workspace_bytes(n, dtype, block_size);
 }

@@ -49,6 +49,9 @@ struct __align__(16) St {
     // block descriptor (thread 0 at issue time) for the two payload buffers
     long long ld_a[2], ld_boff[2], ld_bend[2];
     int ld_tma[2];
+    // per-slot header geometry (thread 0 at issue time): pre-header error,
+    // header offset in the buffer, payload offset, bytes available / staged
+    int ld_err[2], ld_hoff[2], ld_payoff[2], ld_avail[2], ld_staged[2];
     unsigned long long mbar[2];
     // history (q[np-1], q[np-2] of the previous block)
     long long p1, p2;
@@ -131,6 +134,26 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
         const bool ok = o0 >= 0 && len > 0 && len <= bufsz && e1 <= limit &&
                         ((((uintptr_t)(P.blob + a0)) & 15) == 0);
         S->ld_tma[slot] = ok ? 1 : 0;
+        {
+            int derr = 0, hoff = 0, payoff = 0, av = 0, stg = 0;
+            if (o0 < 0) derr = APAX_ERR_ARG;
+            else if (P.nbytes - o0 < HS) derr = APAX_ERR_BLOCK_HDR_TRUNCATED;
+            else {
+                const long long ps = o0 + HS;
+                const long long pe = o1 > ps ? o1 : ps;
+                long long ee = (pe + 15) & ~15LL;
+                if (ee > limit) ee = limit;
+                long long staged_end = a0 + (ee - a0 < bufsz ? ee - a0 : bufsz);
+                if (!ok) staged_end = a0 + min((long long)bufsz, min(pe, P.nbytes) - a0);
+                hoff = (int)(o0 - a0);
+                payoff = (int)(ps - a0);
+                const long long avl = P.nbytes - ps;
+                av = (int)(avl < (1LL << 30) ? avl : (1LL << 30));
+                stg = (int)(staged_end - ps);
+            }
+            S->ld_err[slot] = derr; S->ld_hoff[slot] = hoff; S->ld_payoff[slot] = payoff;
+            S->ld_avail[slot] = av; S->ld_staged[slot] = stg;
+        }
         if (ok) {
             fence_proxy_async();
             tma_load(slot ? pbuf1 : pbuf0, P.blob + a0, (uint32_t)len, &S->mbar[slot]);
@@ -175,38 +198,25 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                 cbar();
             }
             // ---- block header (dtypes.py:156-180), read by every thread ----
-            int err = 0;
+            int err = S->ld_err[cur];
             int sel = 0, restart = 0, code = 0, fbe = 0;
-            long long pay_off = 0, avail = 0, staged = 0;
-            if (boff < 0) {
-                err = APAX_ERR_ARG;
-            } else if (P.nbytes - boff < HS) {
-                err = APAX_ERR_BLOCK_HDR_TRUNCATED;
-            } else {
-                const uint8_t* h = pay + (boff - a0);
+            const int pay_off = S->ld_payoff[cur], avail = S->ld_avail[cur], staged = S->ld_staged[cur];
+            if (!err) {
+                const uint8_t* h = pay + S->ld_hoff[cur];
                 sel = h[0] & 3;
                 restart = (h[0] >> 2) & 1;
                 code = h[1] | (h[2] << 8);
                 fbe = Tr::F ? (int)(int8_t)h[4] : 0;
                 if (sel == 3) err = APAX_ERR_SELECTOR;
-                const long long ps = boff + HS;
-                const long long pe = bend > ps ? bend : ps;
-                long long e1 = (pe + 15) & ~15LL;
-                if (e1 > limit) e1 = limit;
-                long long staged_end = a0 + (e1 - a0 < bufsz ? e1 - a0 : bufsz);
-                if (!was_tma) staged_end = a0 + min((long long)bufsz, min(pe, P.nbytes) - a0);
-                pay_off = ps - a0;
-                avail = P.nbytes - ps;
-                staged = staged_end - ps;
             }
             // ---- JEE: parallel token parse ----
             int used = 0;
             if (!err) {
                 const uint8_t* p = pay + pay_off;
-                const long long maxj = (3LL * G + 2) / 2;
-                const long long nbj = avail < maxj ? avail : maxj;
-                const int total = (int)(2 * nbj);
-                const int stotal = (int)min(2 * staged, (long long)total);
+                const int maxj = (3 * G + 2) / 2;
+                const int nbj = avail < maxj ? avail : maxj;
+                const int total = 2 * nbj;
+                const int stotal = min(2 * staged, total);
                 int cbase = 0, vbase = 0;
                 for (int pass_base = 0;; pass_base += NIB_PER_PASS) {
                     const int p0 = pass_base + 4 * tid;
@@ -215,43 +225,78 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                         const uint8_t bb = p[k >> 1];
                         return (k & 1) ? (bb & 15) : (bb >> 4);
                     };
-                    // nearest definite token start at or before p0
+                    // nibbles p0-4 .. p0+11 of the JEE stream in one 64-bit window
+                    // (zero beyond the staged nibbles)
+                    unsigned long long W = 0ULL;
+                    if (p0 - 4 < stotal) {   // (beyond: no nibbles, and no reads past the buffer)
+                        const int byte0 = (int)pay_off + (p0 >> 1) - 2;   // pay_off >= HS >= 4
+                        const uint32_t* pw = (const uint32_t*)pay;
+                        const int wi = byte0 >> 2;
+                        const unsigned sh = (unsigned)(byte0 & 3) * 8u;
+                        const uint32_t w0 = bswap32(pw[wi]), w1 = bswap32(pw[wi + 1]), w2 = bswap32(pw[wi + 2]);
+                        W = ((unsigned long long)__funnelshift_l(w1, w0, sh) << 32) | __funnelshift_l(w2, w1, sh);
+                        const int rem = stotal - (p0 - 4);
+                        if (rem < 16) W = rem <= 0 ? 0ULL : (W & (~0ULL << (4 * (16 - rem))));
+                    }
+                    auto nw = [&](int k) -> int { return (int)((W >> (4 * (11 - k))) & 15ULL); };   // k in -4..11
+                    // leading positions covered by an escape that started before p0:
+                    // two consecutive non-15 nibbles are always followed by a token start
                     int skip = 0;
                     if (p0 > 0 && p0 < stotal + 4) {
-                        int q = p0;
-                        while (q > 0 && !(nb(q - 1) != 15 && (q < 2 || nb(q - 2) != 15))) q--;
-                        int pos = q;
-                        while (pos < p0) pos += (nb(pos) == 15) ? 3 : 1;
-                        skip = pos - p0;
-                    }
-                    int cnt = 0, flag = 0, val = 0;
-                    int tk_pos[4], tk_kind[4], tk_a[4], tk_b[4], ntok = 0;
-#pragma unroll
-                    for (int r = 0; r < 4; r++) { tk_pos[r] = 0; tk_kind[r] = 0; tk_a[r] = 0; tk_b[r] = 0; }
-                    for (int pos = p0 + skip; pos < p0 + 4 && ntok < 4;) {
-                        const int v = nb(pos);
-                        int kind, len = 1;
-                        if (pos >= stotal) kind = 5;
-                        else if (v == 14) kind = 4;
-                        else if (v == 15) {
-                            kind = 1; len = 3;
-                            if (pos + 2 >= stotal) kind = 5;
-                            else {
-                                const int a = (nb(pos + 1) << 4) | nb(pos + 2);
-                                tk_a[ntok] = a;
-                                flag = 1; val = a; cnt += 1;
-                            }
-                        } else if (v >= 9) {
-                            kind = 3; tk_a[ntok] = v - 11; val += v - 11; cnt += 1;
-                        } else {
-                            kind = 2; tk_a[ntok] = v / 3 - 1; tk_b[ntok] = v % 3 - 1;
-                            val += (v / 3 - 1) + (v % 3 - 1); cnt += 2;
+                        const bool f1 = nw(-1) == 15, f2 = nw(-2) == 15, f3 = nw(-3) == 15, f4 = nw(-4) == 15;
+                        if (!f1 && !f2) skip = 0;
+                        else if (!f2 && !f3) skip = f1 ? 2 : 0;
+                        else if (!f3 && !f4) skip = f2 ? 1 : (f1 ? 2 : 0);
+                        else {
+                            // long escape run: walk back to a definite start (rare)
+                            auto nb = [&](int k) -> int {
+                                if (k >= stotal) return 0;
+                                const uint8_t bb = p[k >> 1];
+                                return (k & 1) ? (bb & 15) : (bb >> 4);
+                            };
+                            int q = p0;
+                            while (q > 0 && !(nb(q - 1) != 15 && (q < 2 || nb(q - 2) != 15))) q--;
+                            int pos = q;
+                            while (pos < p0) pos += (nb(pos) == 15) ? 3 : 1;
+                            skip = pos - p0;
                         }
-                        tk_pos[ntok] = pos;
-                        tk_kind[ntok] = kind;
-                        ntok++;
-                        pos += len;
-                        if (kind >= 4) break;
+                    }
+                    // token starts among this thread's 4 positions
+                    const bool n0f = nw(0) == 15, n1f = nw(1) == 15, n2f = nw(2) == 15;
+                    const bool st0 = skip == 0;
+                    const bool st1 = skip == 1 || (st0 && !n0f);
+                    const bool st2 = skip == 2 || (st1 && !n1f);
+                    const bool st3 = (st2 && !n2f) || (st0 && n0f);
+                    const bool stv[4] = {st0, st1, st2, st3};
+                    int cnt = 0, flag = 0, val = 0;
+                    int tkind[4], ta[4], tb[4];
+                    bool tok[4];
+                    bool stop = p0 >= stotal + 4;   // nothing of this slice is staged
+#pragma unroll
+                    for (int k = 0; k < 4; k++) {
+                        const int pos = p0 + k;
+                        const int v = nw(k);
+                        int kd, av = 0, bv = 0;
+                        if (pos >= stotal) kd = 5;
+                        else if (v == 14) kd = 4;
+                        else if (v == 15) {
+                            kd = 1;
+                            if (pos + 2 >= stotal) kd = 5;
+                            else av = (nw(k + 1) << 4) | nw(k + 2);
+                        } else if (v >= 9) {
+                            kd = 3; av = v - 11;
+                        } else {
+                            const int v3 = (v * 11) >> 5;   // v / 3 for v <= 8
+                            kd = 2; av = v3 - 1; bv = v - 3 * v3 - 1;
+                        }
+                        const bool sk = stv[k] && !stop;
+                        tok[k] = sk; tkind[k] = kd; ta[k] = av; tb[k] = bv;
+                        if (sk) {
+                            if (kd == 1) { flag = 1; val = av; cnt += 1; }
+                            else if (kd == 3) { val += av; cnt += 1; }
+                            else if (kd == 2) { val += av + bv; cnt += 2; }
+                            else stop = true;
+                        }
                     }
                     // warp scan of (cnt, flag, val): A then B = (cA+cB, fA|fB, fB ? vB : vA+vB)
                     int c_i = cnt, f_i = flag, v_i = val;
@@ -311,32 +356,35 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                     int curv = ef ? evv : pv + evv;
                     // evaluate tokens in order; first event = error or completion
                     int ev_pos = 0x7fffffff, ev_done = 0;
-                    for (int k2 = 0; k2 < ntok; k2++) {
-                        if (idx >= G) break;
-                        const int kind = tk_kind[k2], pos = tk_pos[k2];
+                    bool fin = false;
+#pragma unroll
+                    for (int k = 0; k < 4; k++) {
+                        if (!tok[k] || fin) continue;
+                        if (idx >= G) { fin = true; continue; }
+                        const int kind = tkind[k], pos = p0 + k;
                         int e_err = 0, adv = 0;
                         if (kind >= 4) e_err = 1;
                         else if (kind == 1) {
-                            if (tk_a[k2] > 34) e_err = 1;
-                            else { curv = tk_a[k2]; ebuf[idx] = (uint8_t)curv; adv = 1; }
+                            if (ta[k] > 34) e_err = 1;
+                            else { curv = ta[k]; ebuf[idx] = (uint8_t)curv; adv = 1; }
                         } else if (idx == 0) e_err = 1;
                         else if (kind == 3) {
-                            curv += tk_a[k2];
+                            curv += ta[k];
                             if (curv < 0 || curv > 34) e_err = 1;
                             else { ebuf[idx] = (uint8_t)curv; adv = 1; }
                         } else {
-                            curv += tk_a[k2];
+                            curv += ta[k];
                             if (curv < 0 || curv > 34 || idx + 1 >= G) e_err = 1;
                             else {
                                 ebuf[idx] = (uint8_t)curv;
-                                curv += tk_b[k2];
+                                curv += tb[k];
                                 if (curv < 0 || curv > 34) e_err = 1;
                                 else { ebuf[idx + 1] = (uint8_t)curv; adv = 2; }
                             }
                         }
-                        if (e_err) { ev_pos = pos; ev_done = 0; break; }
+                        if (e_err) { ev_pos = pos; ev_done = 0; fin = true; continue; }
                         idx += adv;
-                        if (idx >= G) { ev_pos = pos + (kind == 1 ? 3 : 1); ev_done = 1; break; }
+                        if (idx >= G) { ev_pos = pos + (kind == 1 ? 3 : 1); ev_done = 1; fin = true; }
                     }
                     int key = (ev_pos == 0x7fffffff) ? 0x7fffffff : ((ev_pos << 1) | (ev_done ? 0 : 1));
                     key = __reduce_min_sync(0xffffffffu, key);
@@ -361,7 +409,7 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                             cbar();
                             if (warp == 0) {
                                 long long u2 = 0, esum = 0;
-                                const int st = warp_jee_decode(P.blob + boff + HS, 2 * nbj, G, ebuf, u2, esum);
+                                const int st = warp_jee_decode(P.blob + boff + HS, 2LL * nbj, G, ebuf, u2, esum);
                                 if (lane == 0) { S->err = st; S->used = (int)u2; }
                             }
                             cbar();
@@ -422,34 +470,37 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
             {
                 const uint32_t* w = (const uint32_t*)pay;
                 int bp = 8 * ((int)pay_off + jee_bytes) + (int)bpre;
+                const unsigned wmax4 = epk;   // bytes: widths
+                const unsigned wm = max(max(wmax4 & 0xffu, (wmax4 >> 8) & 0xffu),
+                                        max((wmax4 >> 16) & 0xffu, wmax4 >> 24));
+                if (!__any_sync(0xffffffffu, wm > 16)) {
+                    // every group of the warp fits two 32-bit windows
 #pragma unroll
-                for (int g = 0; g < 4; g++) {
-                    const int wd = (int)((epk >> (8 * g)) & 0xffu);
-                    if (wd == 0) {
-#pragma unroll
-                        for (int k = 0; k < 4; k++) q[4 * g + k] = 0;
-                    } else if (wd <= 8) {
-                        const uint32_t c = r32(w, bp);
-#pragma unroll
-                        for (int k = 0; k < 4; k++) q[4 * g + k] = bfe_s(c, 32 - wd * (k + 1), wd);
-                    } else if (wd <= 16) {
+                    for (int g = 0; g < 4; g++) {
+                        const int wd = (int)((epk >> (8 * g)) & 0xffu);
                         const uint32_t c0 = r32(w, bp), c1 = r32(w, bp + 2 * wd);
-                        q[4 * g + 0] = bfe_s(c0, 32 - wd, wd);
-                        q[4 * g + 1] = bfe_s(c0, 32 - 2 * wd, wd);
-                        q[4 * g + 2] = bfe_s(c1, 32 - wd, wd);
-                        q[4 * g + 3] = bfe_s(c1, 32 - 2 * wd, wd);
-                    } else if (wd <= 32) {
+                        q[4 * g + 0] = wd ? bfe_s(c0, 32 - wd, wd) : 0;
+                        q[4 * g + 1] = wd ? bfe_s(c0, 32 - 2 * wd, wd) : 0;
+                        q[4 * g + 2] = wd ? bfe_s(c1, 32 - wd, wd) : 0;
+                        q[4 * g + 3] = wd ? bfe_s(c1, 32 - 2 * wd, wd) : 0;
+                        bp += 4 * wd;
+                    }
+                } else {
 #pragma unroll
-                        for (int k = 0; k < 4; k++) q[4 * g + k] = bfe_s(r32(w, bp + k * wd), 32 - wd, wd);
-                    } else {
+                    for (int g = 0; g < 4; g++) {
+                        const int wd = (int)((epk >> (8 * g)) & 0xffu);
 #pragma unroll
                         for (int k = 0; k < 4; k++) {
                             const int pb = bp + k * wd;
-                            const unsigned long long hi = ((unsigned long long)r32(w, pb) << 32) | r32(w, pb + 32);
-                            q[4 * g + k] = (long long)hi >> (64 - wd);
+                            if (wd == 0) q[4 * g + k] = 0;
+                            else if (wd <= 32) q[4 * g + k] = bfe_s(r32(w, pb), 32 - wd, wd);
+                            else {
+                                const unsigned long long hi = ((unsigned long long)r32(w, pb) << 32) | r32(w, pb + 32);
+                                q[4 * g + k] = (long long)hi >> (64 - wd);
+                            }
                         }
+                        bp += 4 * wd;
                     }
-                    bp += 4 * wd;
                 }
             }
             // ---- reconstruct (transform.py:116-129) ----
