@@ -114,6 +114,39 @@ int apax_decode_segments(const uint8_t* blob, int64_t nbytes, int64_t n, int dty
 int apax_find_blocks(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, int block_size,
                      int64_t* offsets, uint64_t* status, void* stream);
 
+/* ---- profiler statistics (reference pkg/src/apax/profiler.py) ----
+ * x, y: device arrays of n samples of `dtype` (input and decoded output);
+ * d = x - y in double precision.  Every call writes per-CTA partials
+ * (apax_profile_grid() of them) that the caller sums in CTA order, so
+ * results are run-to-run deterministic. */
+int apax_profile_grid(void);
+
+/* pass 0: partials[g*8 + k] = sums over CTA g of
+ *   k = 0 x, 1 y, 2 d, 3 x^2, 4 y^2, 5 d^2, 6 x*y      (pearson_r :40-48,
+ *   window2_metrics :127-159); counts[0] += #(x == 0 and d != 0),
+ *   counts[1] += #(d == 0) (caller zeroes counts).
+ * pass 1 (centred, for the two-pass std): k = 3 (x-mean_x)^2,
+ *   4 (y-mean_y)^2, 5 (d-mean_d)^2. */
+int apax_profile_sums(const void* x, const void* y, int64_t n, int dtype, int pass, double mean_x, double mean_y,
+                      double mean_d, double* partials, uint64_t* counts, void* stream);
+
+/* Welch power sums (welch_spectrum :61-74): frames of `seg` samples (power
+ * of two, 2..4096) at hop seg/2; partials[g*(seg/2+1) + k] = sum over the
+ * frames of CTA g of |FFT(hann * frame)_k|^2.  which: 0 x, 1 y, 2 d.
+ * tables (device): seg/2 twiddles exp(-2 pi i k/seg) as (re, im) pairs,
+ * then the seg window values. */
+int apax_profile_welch(const void* x, const void* y, int64_t n, int dtype, int which, int seg,
+                       const double* tables, double* partials, void* stream);
+
+/* One pass of the radix multi-select over the per-sample ratio keys
+ * (s2r_distribution :105-124): key = bits of |x| / |d| (d == 0: +inf,
+ * x == 0 != d: 0), d = x - y when y_is_output, else y itself is d.
+ * Pass p (0..15) counts the 4-bit digit p (most significant first) of
+ * every key whose higher 4p bits equal one of the sorted, unique
+ * `prefixes`: hist[j*16 + digit] (caller zeroes hist). */
+int apax_profile_select(const void* x, const void* y, int64_t n, int dtype, int pass, const uint64_t* prefixes,
+                        int n_prefixes, uint64_t* hist, int y_is_output, void* stream);
+
 /* Host-side parse of the 28-byte file header (host pointer).  Returns an
  * apax_status code; *detail carries the offending value for messages. */
 int apax_parse_file_header(const uint8_t* host_blob, int64_t len, int* dtype, int* mode,

@@ -4,19 +4,20 @@ Drop-in for the reference package's hot path (reference
 `pkg/src/apax/__init__.py:9-21`): the same `encode_stream`, `decode_stream`,
 `StreamConfig`, `Dtype`, `Mode` names, container bitstream and exceptions,
 with every sample-level operation running in hand-written sm_100a kernels
-behind the C ABI in include/apax_b200.h.  `profile` / `ProfileSession` come
-in a later round.
+behind the C ABI in include/apax_b200.h.  `profile` / `ProfileSession`
+(reference profiler.py) run their statistics in csrc/apax_profile.cu.
 """
 from .codec import (Decoder, EncodedStream, Encoder, decode_device, decode_stream,
                     encode_device, encode_stream, max_encoded_bytes, parse_file_header,
                     wave_segment_blocks)
 from .dtypes import BlockHeader, Dtype, Mode, StreamConfig, decode_scale_code, encode_scale_code
 from . import errors
+from .profiler import ProfileSession, profile
 
 __all__ = [
     "Dtype", "Mode", "StreamConfig", "BlockHeader", "encode_stream", "decode_stream",
     "parse_file_header", "encode_device", "decode_device", "Encoder", "Decoder",
-    "EncodedStream", "max_encoded_bytes", "wave_segment_blocks", "encode_scale_code", "decode_scale_code", "errors",
+    "EncodedStream", "max_encoded_bytes", "wave_segment_blocks", "profile", "ProfileSession", "encode_scale_code", "decode_scale_code", "errors",
 ]
 
 __version__ = "0.1.0"

@@ -54,6 +54,14 @@ def lib():
     L.apax_decode_segments_workspace_bytes.restype = I64
     L.apax_decode_segments.argtypes = [P, I64, I64, I32, I32, P, I64, P, P, P, I64, P]
     L.apax_decode_segments.restype = I32
+    L.apax_profile_grid.argtypes = []
+    L.apax_profile_grid.restype = I32
+    L.apax_profile_sums.argtypes = [P, P, I64, I32, I32, D, D, D, P, P, P]
+    L.apax_profile_sums.restype = I32
+    L.apax_profile_welch.argtypes = [P, P, I64, I32, I32, I32, P, P, P]
+    L.apax_profile_welch.restype = I32
+    L.apax_profile_select.argtypes = [P, P, I64, I32, I32, P, I32, P, I32, P]
+    L.apax_profile_select.restype = I32
     L.apax_find_blocks.argtypes = [P, I64, I64, I32, I32, P, P, P]
     L.apax_find_blocks.restype = I32
     L.apax_parse_file_header.argtypes = [P, I64, P, P, P, P, P, P]
@@ -67,5 +75,6 @@ EXPORTED_SYMBOLS = (
     "apax_encode_workspace_bytes", "apax_encode", "apax_decode_workspace_bytes",
     "apax_decode", "apax_find_blocks", "apax_parse_file_header",
     "apax_decode_segments_workspace_bytes", "apax_decode_segments",
-    "apax_encode_wave_segment_blocks",
+    "apax_encode_wave_segment_blocks", "apax_profile_grid", "apax_profile_sums", "apax_profile_welch",
+    "apax_profile_select",
 )

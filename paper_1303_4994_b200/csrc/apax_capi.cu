@@ -353,6 +353,46 @@ int apax_decode_segments(const uint8_t* blob, int64_t nbytes, int64_t n, int dty
     return launch_decode_v3(dtype, P, grid, smem, s);
 }
 
+// ---------------------------------------------------------------------------
+// profiler statistics (reference profiler.py): per-CTA partials, summed by
+// the caller in CTA order
+// ---------------------------------------------------------------------------
+int apax_profile_grid(void) {
+    int dev = 0, nsm = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || nsm <= 0) nsm = 148;
+    return 2 * nsm;
+}
+
+int apax_profile_sums(const void* x, const void* y, int64_t n, int dtype, int pass, double mean_x, double mean_y,
+                      double mean_d, double* partials, uint64_t* counts, void* stream) {
+    if (!valid_dtype(dtype) || n < 0 || !x || !y || !partials || !counts || pass < 0 || pass > 1)
+        return APAX_ERR_ARG;
+    return profile_sums(x, y, n, dtype, pass, mean_x, mean_y, mean_d, partials,
+                        (unsigned long long*)counts, apax_profile_grid(), (cudaStream_t)stream);
+}
+
+int apax_profile_welch(const void* x, const void* y, int64_t n, int dtype, int which, int seg,
+                       const double* tables, double* partials, void* stream) {
+    if (!valid_dtype(dtype) || !x || !tables || !partials || which < 0 || which > 2 || (which && !y))
+        return APAX_ERR_ARG;
+    if (seg < 2 || seg > 4096 || (seg & (seg - 1)) || n < seg) return APAX_ERR_ARG;
+    int lg = 0;
+    while ((1 << lg) < seg) lg++;
+    const long long nframes = (n - seg) / (seg / 2) + 1;
+    return profile_welch(x, y ? y : x, n, dtype, which, seg, lg, nframes, tables, partials, apax_profile_grid(),
+                         (cudaStream_t)stream);
+}
+
+int apax_profile_select(const void* x, const void* y, int64_t n, int dtype, int pass, const uint64_t* prefixes,
+                        int n_prefixes, uint64_t* hist, int y_is_output, void* stream) {
+    if (!valid_dtype(dtype) || !x || !y || !prefixes || !hist || pass < 0 || pass > 15 || n_prefixes < 1 ||
+        n_prefixes > 1024)
+        return APAX_ERR_ARG;
+    return profile_select(x, y, n, dtype, pass, (const unsigned long long*)prefixes, n_prefixes,
+                          (unsigned long long*)hist, y_is_output ? 1 : 0, apax_profile_grid(), (cudaStream_t)stream);
+}
+
 int apax_parse_file_header(const uint8_t* d, int64_t len, int* dt, int* mode, int* bs,
                            int64_t* count, double* target, int64_t* detail) {
     // reference parse_file_header (codec.py:288-305) + StreamConfig.validate

@@ -74,6 +74,14 @@ size_t decode_v2_smem_bytes(int dt, int bs, int payload_cap);
 bool decode_v2_supported(int bs);
 int decode_v2_resident_ctas(int dt, size_t smem);
 int launch_decode_v2(int dt, const DecParams& P, int grid, size_t smem, cudaStream_t st);
+int profile_sums(const void* x, const void* y, long long n, int dt, int pass, double mx, double my,
+                 double md, double* partials, unsigned long long* counts, int grid, cudaStream_t st);
+size_t profile_welch_smem(int seg);
+int profile_welch(const void* x, const void* y, long long n, int dt, int which, int seg, int lg,
+                  long long nframes, const double* tw, double* partials, int grid, cudaStream_t st);
+int profile_select(const void* x, const void* y, long long n, int dt, int pass,
+                   const unsigned long long* prefixes, int npre, unsigned long long* hist, int ydiff, int grid,
+                   cudaStream_t st);
 int launch_walk(const uint8_t* blob, long long nbytes, long long n, int bs, int dt, long long n_blocks,
                 long long* offsets, unsigned long long* status, cudaStream_t st);
 
