@@ -1,0 +1,129 @@
+"""Multi-GPU sharding of the codec and the profiler statistics
+(SURVEY.md §8(e)): one process per GPU, torch.distributed for the plumbing.
+
+Encode: the stream's segments (independent: every segment starts with a
+restart block) are split into contiguous ranges, one per rank.
+Each rank encodes its samples into a container body; the only data-path
+exchange is an all-gather of the R body lengths (int64), whose exclusive
+scan places every body after the 28-byte file header of the concatenated
+stream.  Bodies stay sharded (gathering a multi-GB container would cost
+more than the encode); `global_block_offsets` maps a rank's side-band index
+into the concatenated stream.
+
+Decode: a rank decodes its own body (a container of its segments).
+
+Profiler: per-rank sums are all-gathered and added in rank order, so the
+result is deterministic and independent of the collective's reduction tree.
+
+The byte-level assembly is independent of which encoder produced a body;
+the CPU tests drive it with gloo and the oracle.
+"""
+from __future__ import annotations
+
+import struct
+from dataclasses import dataclass
+from typing import Optional, Sequence, Tuple
+
+import numpy as np
+
+FILE_HEADER_FMT = "<4sBBBBIQd"   # reference codec.py:53-56
+FILE_HEADER_SIZE = 28
+
+
+def shard_samples(n: int, block_size: int, segment_blocks: int, world: int, rank: int) -> Tuple[int, int]:
+    """[start, end) samples of `rank`'s contiguous range of whole segments
+    (segments split as evenly as possible; a rank may get none)."""
+    if segment_blocks < 1:
+        raise ValueError("sharding needs segment_blocks >= 1")
+    n_blocks = (n + block_size - 1) // block_size
+    n_seg = (n_blocks + segment_blocks - 1) // segment_blocks
+    s0 = (n_seg * rank) // world
+    s1 = (n_seg * (rank + 1)) // world
+    seg_samples = segment_blocks * block_size
+    return min(n, s0 * seg_samples), min(n, s1 * seg_samples)
+
+
+def file_header(dtype_wire: int, mode: int, block_size: int, count: int, target: float) -> bytes:
+    """The 28-byte container header of the concatenated stream."""
+    return struct.pack(FILE_HEADER_FMT, b"APAX", 1, dtype_wire, mode, 0, block_size, count, float(target))
+
+
+def _all_gather_i64(value: int, group=None, device=None):
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    t = torch.tensor([int(value)], dtype=torch.int64, device=device)
+    out = torch.empty(world, dtype=torch.int64, device=device)
+    dist.all_gather_into_tensor(out, t, group=group)
+    return [int(v) for v in out.cpu().tolist()]
+
+
+@dataclass
+class ShardPlacement:
+    """Where a rank's body sits in the concatenated container."""
+
+    rank: int
+    body_offset: int              # byte offset of this rank's body in the stream
+    total_bytes: int              # length of the concatenated container
+    body_lengths: Tuple[int, ...]
+
+
+def place_bodies(body_len: int, group=None, device=None) -> ShardPlacement:
+    """All-gather of the body lengths + exclusive scan (the cross-GPU offset
+    scan of SURVEY.md §8(e))."""
+    import torch.distributed as dist
+    lens = _all_gather_i64(body_len, group, device)
+    rank = dist.get_rank(group)
+    off = FILE_HEADER_SIZE + sum(lens[:rank])
+    return ShardPlacement(rank, off, FILE_HEADER_SIZE + sum(lens), tuple(lens))
+
+
+def global_block_offsets(local_offsets: np.ndarray, placement: ShardPlacement) -> np.ndarray:
+    """Side-band index of a rank's blocks in the concatenated stream: local
+    offsets (relative to the rank's own container, header included) shifted
+    by the body's global position; the last entry is the body end."""
+    lo = np.asarray(local_offsets, dtype=np.int64)
+    return lo - FILE_HEADER_SIZE + placement.body_offset
+
+
+def gather_container(body: bytes, header: bytes, group=None) -> Optional[bytes]:
+    """Concatenated container on rank 0 (tests and small streams only)."""
+    import torch.distributed as dist
+    parts = [None] * dist.get_world_size(group)
+    dist.all_gather_object(parts, body, group=group)
+    if dist.get_rank(group) != 0:
+        return None
+    return header + b"".join(parts)
+
+
+def merge_sums(local: Sequence[float], group=None, device=None) -> np.ndarray:
+    """Rank-ordered sum of per-rank statistic vectors (deterministic)."""
+    import torch
+    import torch.distributed as dist
+    v = torch.tensor(np.asarray(local, dtype=np.float64), device=device)
+    world = dist.get_world_size(group)
+    out = torch.empty(world * v.numel(), dtype=torch.float64, device=device)
+    dist.all_gather_into_tensor(out, v, group=group)
+    parts = out.cpu().numpy().reshape(world, -1)
+    acc = np.zeros(parts.shape[1])
+    for r in range(world):
+        acc = acc + parts[r]
+    return acc
+
+
+def sharded_encode(x_local, config, group=None):
+    """Encode this rank's contiguous whole-segment range on its GPU; returns
+    (body bytes, ShardPlacement, global block offsets).  `config` must be
+    segmented (StreamConfig.segment_blocks > 0) so every body starts with a
+    restart block."""
+    import torch
+    from .codec import encode_device
+    if not config.segment_blocks:
+        raise ValueError("sharded_encode needs a segmented StreamConfig")
+    res = encode_device(x_local, config)
+    body_len = res.nbytes - FILE_HEADER_SIZE
+    dev = x_local.device if isinstance(x_local, torch.Tensor) else None
+    place = place_bodies(body_len, group, dev)
+    body = bytes(res.blob[FILE_HEADER_SIZE:res.nbytes].cpu().numpy().tobytes())
+    offs = global_block_offsets(res.block_offsets.cpu().numpy(), place)
+    return body, place, offs
