@@ -115,7 +115,7 @@ struct DecPlan {
     int v2;
     size_t smem;
     int grid;
-    long long ws_carry, ws_ticket, ws_offsets, ws_total;
+    long long ws_carry, ws_ticket, ws_offsets, ws_k5, ws_total;
 };
 
 int plan_decode(long long n, int dt, int bs, DecPlan* p) {
@@ -140,7 +140,8 @@ int plan_decode(long long n, int dt, int bs, DecPlan* p) {
     p->ws_carry = 0;
     p->ws_ticket = (p->n_blocks * 128 + 255) & ~255LL;
     p->ws_offsets = p->ws_ticket + 256;
-    p->ws_total = p->ws_offsets + (((p->n_blocks + 1) * 8 + 255) & ~255LL);
+    p->ws_k5 = p->ws_offsets + (((p->n_blocks + 1) * 8 + 255) & ~255LL);
+    p->ws_total = p->ws_k5 + (long long)find_blocks_k5_ws_bytes(p->n_blocks);
     return APAX_OK;
 }
 
@@ -263,8 +264,16 @@ int apax_find_blocks(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, 
     if (cudaMemsetAsync(status, 0xFF, 4 * sizeof(uint64_t), s) != cudaSuccess) return APAX_ERR_CUDA;
     if (cudaMemsetAsync(offsets, 0xFF, (size_t)(nb + 1) * 8, s) != cudaSuccess) return APAX_ERR_CUDA;
     if (nb == 0) return APAX_OK;
-    return launch_walk(blob, nbytes, n, block_size, dtype, nb, (long long*)offsets,
-                       (unsigned long long*)status, s);
+    if (nb < 2 || !env_int("APAX_K5", 1))
+        return launch_walk(blob, nbytes, n, block_size, dtype, nb, (long long*)offsets,
+                           (unsigned long long*)status, s);
+    // K5 scratch from the stream-ordered pool (this entry point takes no workspace)
+    void* ws = nullptr;
+    if (cudaMallocAsync(&ws, find_blocks_k5_ws_bytes(nb), s) != cudaSuccess) return APAX_ERR_CUDA;
+    int st = launch_find_blocks_k5(blob, nbytes, n, block_size, dtype, nb, (long long*)offsets,
+                                   (unsigned long long*)status, ws, s);
+    if (cudaFreeAsync(ws, s) != cudaSuccess && st == APAX_OK) st = APAX_ERR_CUDA;
+    return st;
 }
 
 int apax_decode(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, int block_size,
@@ -284,7 +293,11 @@ int apax_decode(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, int b
     if (!offs) {
         long long* wo = (long long*)(w + p.ws_offsets);
         if (cudaMemsetAsync(wo, 0xFF, (size_t)(p.n_blocks + 1) * 8, s) != cudaSuccess) return APAX_ERR_CUDA;
-        st = launch_walk(blob, nbytes, n, block_size, dtype, p.n_blocks, wo, (unsigned long long*)status, s);
+        if (p.n_blocks >= 2 && env_int("APAX_K5", 1))
+            st = launch_find_blocks_k5(blob, nbytes, n, block_size, dtype, p.n_blocks, wo,
+                                       (unsigned long long*)status, w + p.ws_k5, s);
+        else
+            st = launch_walk(blob, nbytes, n, block_size, dtype, p.n_blocks, wo, (unsigned long long*)status, s);
         if (st) return st;
         offs = wo;
     }

@@ -316,15 +316,29 @@ __global__ void __launch_bounds__(kNT) decode_kernel(DecParams P) {
 // each block's header + JEE + mantissa length.  offsets[b] = header offset,
 // offsets[nb] = end.  Stops at the first error (status key).
 // ---------------------------------------------------------------------------
+// After K5 (apax_k5.cu, `k5_fail` non-null): on success only the last block
+// is parsed (its group count may be short); on failure the offsets K5 wrote
+// are reset and the full walk runs, reporting the reference's exact error.
 __global__ void walk_kernel(const uint8_t* blob, long long nbytes, long long n, int bs, int dt,
-                            long long n_blocks, long long* offsets, unsigned long long* status) {
+                            long long n_blocks, long long* offsets, unsigned long long* status,
+                            const int* k5_fail) {
     extern __shared__ __align__(16) unsigned char smem_w[];
     uint8_t* e = smem_w;
     const int lane = threadIdx.x & 31;
     if (threadIdx.x >= 32) return;
     const int hs = hdr_size(dt);
     long long pos = kFileHeader;
-    for (long long b = 0; b < n_blocks; b++) {
+    long long b0 = 0;
+    if (k5_fail) {
+        if (*k5_fail == 0) {
+            b0 = n_blocks - 1;
+            pos = offsets[b0];
+        } else {
+            for (long long b = lane; b <= n_blocks; b += 32) offsets[b] = -1;
+            __syncwarp();
+        }
+    }
+    for (long long b = b0; b < n_blocks; b++) {
         const long long start = b * (long long)bs;
         const int nn = (int)((n - start) < bs ? (n - start) : bs);
         const int G = (nn + 3) >> 2;
@@ -396,7 +410,14 @@ int launch_decode(int dt, const DecParams& P, int grid, size_t smem, cudaStream_
 int launch_walk(const uint8_t* blob, long long nbytes, long long n, int bs, int dt, long long n_blocks,
                 long long* offsets, unsigned long long* status, cudaStream_t st) {
     size_t smem = (size_t)(bs / 4) + 64;
-    walk_kernel<<<1, 32, smem, st>>>(blob, nbytes, n, bs, dt, n_blocks, offsets, status);
+    walk_kernel<<<1, 32, smem, st>>>(blob, nbytes, n, bs, dt, n_blocks, offsets, status, nullptr);
+    return cudaGetLastError() == cudaSuccess ? APAX_OK : APAX_ERR_CUDA;
+}
+
+int launch_walk_after_k5(const uint8_t* blob, long long nbytes, long long n, int bs, int dt, long long n_blocks,
+                         long long* offsets, unsigned long long* status, const int* k5_fail, cudaStream_t st) {
+    size_t smem = (size_t)(bs / 4) + 64;
+    walk_kernel<<<1, 32, smem, st>>>(blob, nbytes, n, bs, dt, n_blocks, offsets, status, k5_fail);
     return cudaGetLastError() == cudaSuccess ? APAX_OK : APAX_ERR_CUDA;
 }
 

@@ -84,5 +84,11 @@ int profile_select(const void* x, const void* y, long long n, int dt, int pass,
                    cudaStream_t st);
 int launch_walk(const uint8_t* blob, long long nbytes, long long n, int bs, int dt, long long n_blocks,
                 long long* offsets, unsigned long long* status, cudaStream_t st);
+int launch_walk_after_k5(const uint8_t* blob, long long nbytes, long long n, int bs, int dt, long long n_blocks,
+                         long long* offsets, unsigned long long* status, const int* k5_fail, cudaStream_t st);
+// K5 index-less block discovery (apax_k5.cu); ws of find_blocks_k5_ws_bytes
+size_t find_blocks_k5_ws_bytes(long long n_blocks);
+int launch_find_blocks_k5(const uint8_t* blob, long long nbytes, long long n, int bs, int dt, long long n_blocks,
+                          long long* offsets, unsigned long long* status, void* ws, cudaStream_t st);
 
 }  // namespace apax
