@@ -201,6 +201,7 @@ def main():
     ap.add_argument("--n-log2", type=int, default=26)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-chunks", type=int, default=4, help="pipeline chunks of the e2e round trip")
     ap.add_argument("--profile", action="store_true",
                     help="short run for ncu: no e2e, no cpu baseline, no clocks")
     args = ap.parse_args()
@@ -309,68 +310,64 @@ def main():
 
     # ---- e2e: host buffers through the C-ABI entry points ----
     # Pinned host samples -> H2D -> apax_encode -> D2H container + block index
-    # -> H2D container + index -> apax_decode -> D2H samples, every step.
+    # -> H2D container + index -> apax_decode_segments -> D2H samples, every
+    # step, pipelined over chunks of whole segments on copy-in / compute /
+    # copy-out streams (paper_1303_4994_b200/pipeline.py).
     e2e = None
     if not args.no_e2e and not args.profile:
+        from paper_1303_4994_b200.pipeline import HostRoundTrip
+        rt = HostRoundTrip(n, cfg, chunks=args.e2e_chunks, device=dev)
         xh = torch.from_numpy(x_host).pin_memory()
-        blob_h = torch.empty(enc.cap + 64, dtype=torch.uint8).pin_memory()
+        blob_h = torch.empty(rt.blob_d.numel(), dtype=torch.uint8).pin_memory()
         offs_h = torch.empty(enc.n_blocks + 1, dtype=torch.int64).pin_memory()
         yh = torch.empty(n, dtype=torch.float32).pin_memory()
-        blob_d = torch.zeros(enc.cap + 64, dtype=torch.uint8, device=dev)
-        offs_d = torch.empty(enc.n_blocks + 1, dtype=torch.int64, device=dev)
-        xd2 = torch.empty(n, dtype=torch.float32, device=dev)
-        dec2 = Decoder(n, Dtype.F32, 4096, device=dev)
         e2e_steps = max(3, min(args.steps, 10))
-
-        def e2e_step(indexless=False):
-            xd2.copy_(xh, non_blocking=True)                         # H2D input
-            enc.encode(xd2)
-            nb = enc.finish()                                        # container length
-            blob_h[:nb].copy_(enc.out[:nb], non_blocking=True)       # D2H container
-            offs_h.copy_(enc.offsets, non_blocking=True)             # D2H block index
-            blob_d[:nb].copy_(blob_h[:nb], non_blocking=True)        # H2D container
-            if indexless:
-                dec2.decode(blob_d, nb, None)                        # device block walk
-            else:
-                offs_d.copy_(offs_h, non_blocking=True)              # H2D block index
-                dec2.decode(blob_d, nb, offs_d, segment_blocks=args.segment_blocks)
-            yh.copy_(dec2.y[:n], non_blocking=True)                  # D2H decoded samples
-            torch.cuda.synchronize()
-            return nb
-
         for _ in range(2):
-            e2e_step()
+            rt.run(xh, blob_h, offs_h, yh)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         a = time.perf_counter()
         for _ in range(e2e_steps):
-            nb = e2e_step()
+            nb = rt.run(xh, blob_h, offs_h, yh)
         e2e_s = (time.perf_counter() - a) / e2e_steps
-        dec2.finish()
-        ok_e2e = bool(torch.equal(yh, dec.y[:n].cpu()))
-        # index-less decode (container bytes only, like decode_stream(bytes))
+        ok_e2e = bool(torch.equal(yh, dec.y[:n].cpu())) and \
+            bool(torch.equal(blob_h[:nb], enc.out[:nb].cpu())) and \
+            bool(torch.equal(offs_h, enc.offsets.cpu()))
+        # index-less decode of the host container (like decode_stream(bytes)):
+        # H2D container -> K5 block discovery -> decode -> D2H samples
+        blob_d = torch.zeros(rt.blob_d.numel(), dtype=torch.uint8, device=dev)
+        dec2 = Decoder(n, Dtype.F32, 4096, device=dev)
+
+        def indexless():
+            blob_d[:nb].copy_(blob_h[:nb], non_blocking=True)
+            dec2.decode(blob_d, nb, None)
+            yh.copy_(dec2.y[:n], non_blocking=True)
+            torch.cuda.synchronize()
+        indexless()
         a = time.perf_counter()
-        e2e_step(indexless=True)
-        il_s = time.perf_counter() - a
+        for _ in range(3):
+            indexless()
+        il_s = (time.perf_counter() - a) / 3
         dec2.finish()
         ok_il = bool(torch.equal(yh, dec.y[:n].cpu()))
         if world > 1:
             t = torch.tensor([e2e_s, il_s], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s, il_s = t.tolist()
-        idx_bytes = 8 * (enc.n_blocks + 1)
         e2e = {"value": world * in_bytes / e2e_s / 1e9, "unit": UNIT,
-               "h2d_bytes_per_step": in_bytes + nb + idx_bytes,
-               "d2h_bytes_per_step": nb + idx_bytes + in_bytes,
+               "h2d_bytes_per_step": rt.h2d_bytes,
+               "d2h_bytes_per_step": rt.d2h_bytes,
                "ms_per_step": e2e_s * 1e3,
-               "path": "C-ABI apax_encode/apax_decode with pinned host buffers, "
-                       "container + side-band block index round-tripped through the host",
+               "path": f"C-ABI apax_encode/apax_decode_segments with pinned host buffers, container + "
+                       f"side-band block index round-tripped through the host, pipelined over "
+                       f"{len(rt.ranges)} chunks of whole segments (copy-in/compute/copy-out streams)",
                "bit_exact_vs_device_path": ok_e2e,
-               "indexless": {"value": world * in_bytes / il_s / 1e9, "unit": UNIT,
-                             "ms_per_step": il_s * 1e3,
-                             "decode_path": "container bytes only; device block walk",
-                             "bit_exact_vs_device_path": ok_il}}
+               "indexless_decode": {"value": world * in_bytes / il_s / 1e9, "unit": UNIT,
+                                    "ms_per_step": il_s * 1e3,
+                                    "path": "host container bytes only: H2D, K5 parallel block "
+                                            "discovery, apax_decode, D2H samples",
+                                    "bit_exact_vs_device_path": ok_il}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:

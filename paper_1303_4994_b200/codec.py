@@ -189,7 +189,7 @@ class Encoder:
 class Decoder:
     """Preallocated decode plan for containers of (n, dtype, block_size)."""
 
-    def __init__(self, n: int, dtype: Dtype, block_size: int, device=None):
+    def __init__(self, n: int, dtype: Dtype, block_size: int, device=None, alloc_y: bool = True):
         torch, L = _require_cuda()
         self.n, self.dtype, self.bs = int(n), dtype, int(block_size)
         self.device = torch.device(device or "cuda")
@@ -198,7 +198,7 @@ class Decoder:
             raise InvalidConfig("invalid decode arguments")
         self.ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device=self.device)
         self.status = torch.empty(4, dtype=torch.int64, device=self.device)
-        self.y = torch.empty(max(self.n, 1), dtype=torch_dtype(dtype), device=self.device)
+        self.y = torch.empty(max(self.n, 1) if alloc_y else 1, dtype=torch_dtype(dtype), device=self.device)
         self._lib = L
 
     def decode(self, blob, nbytes: int, offsets=None, stream=None, out=None,
@@ -208,6 +208,8 @@ class Decoder:
         segment-serial decoder runs (apax_decode_segments); otherwise the
         general decoder (apax_decode)."""
         y = self.y if out is None else out
+        if y.numel() < self.n:
+            raise InvalidConfig("decode output buffer smaller than the element count")
         offs = ctypes.c_void_p(offsets.data_ptr()) if offsets is not None else None
         if segment_blocks and offsets is not None:
             st = self._lib.apax_decode_segments(
@@ -309,6 +311,8 @@ def encode_stream(samples, config: StreamConfig) -> bytes:
         raise InvalidConfig("element_count must be >= 1")
     torch, _ = _require_cuda()
     x = _as_config_dtype(x, config.dtype)
+    if not x.flags.writeable:
+        x = x.copy()
     xd = torch.from_numpy(x).to("cuda", non_blocking=False)
     enc = Encoder(x.size, config, with_offsets=False)
     enc.encode(xd)

@@ -1,0 +1,225 @@
+"""Copy/compute-overlapped host round trip: pinned host samples -> container
+bytes + side-band block index in pinned host memory -> decoded samples in
+pinned host memory, through the same C-ABI calls as the device API.
+
+A whole-stream host round trip is PCIe-bound (the kernels take < 1 ms of a
+~13 ms round trip for cfg2), so the stream is cut into chunks of whole
+segments and each chunk flows through
+
+    H2D samples -> apax_encode -> D2H container + index
+                -> H2D container + index -> apax_decode_segments -> D2H samples
+
+on three CUDA streams (copy-in, compute, copy-out), so host->device and
+device->host copies of different chunks run at the same time on the two
+copy directions while the kernels run in between.  Segments are independent
+(every segment starts with a restart block), so the chunk
+containers' bodies concatenate into exactly the bytes of one encode of the
+whole stream with the same segment length (the same property the multi-GPU
+sharding uses, distributed.py); the host blob carries the whole-stream file
+header.
+
+The host must learn each chunk's container length before its D2H: one
+event wait per chunk, issued after the next chunk's copy and encode are
+already queued, so the GPU never idles on it.
+"""
+from __future__ import annotations
+
+import struct
+from typing import List, Optional
+
+import numpy as np
+
+from .codec import FILE_HEADER_FMT, FILE_HEADER_SIZE, Decoder, Encoder, _check_status, torch_dtype
+from .dtypes import StreamConfig
+from .errors import InvalidConfig
+
+
+class HostRoundTrip:
+    """Reusable pipelined host encode+decode plan for (n, config).
+
+    `config.segment_blocks` must be set (chunks are whole segments).
+    `chunks` is the number of pipeline chunks (rounded to segment
+    boundaries)."""
+
+    def __init__(self, n: int, config: StreamConfig, chunks: int = 8, device=None, depth: int = 3):
+        import torch
+        if not config.segment_blocks:
+            raise InvalidConfig("HostRoundTrip needs a segmented StreamConfig")
+        config.validate()
+        self.n, self.config = int(n), config
+        self.device = torch.device(device or "cuda")
+        bs, P = config.block_size, int(config.segment_blocks)
+        seg_samples = bs * P
+        n_seg = (self.n + seg_samples - 1) // seg_samples
+        k = max(1, min(int(chunks), n_seg))
+        bounds = [min(self.n, ((n_seg * i) // k) * seg_samples) for i in range(k + 1)]
+        self.ranges = [(a, b) for a, b in zip(bounds, bounds[1:]) if b > a]
+        self.depth = max(2, min(depth, len(self.ranges)))
+        # one encoder / decoder per in-flight slot (buffers reused round-robin)
+        lens = [b - a for a, b in self.ranges]
+        nmax = max(lens)
+        self.enc = [Encoder(nmax, config, device=self.device) for _ in range(self.depth)]
+        self._enc_by_len = {}
+        self.dec = {}
+        for m in set(lens):
+            self.dec[m] = Decoder(m, config.dtype, bs, device=self.device, alloc_y=False)
+            if m != nmax:
+                self._enc_by_len[m] = [Encoder(m, config, device=self.device) for _ in range(self.depth)]
+        self.n_blocks = (self.n + bs - 1) // bs
+        cap = sum(self.enc[0].cap for _ in self.ranges) + 64
+        self.blob_d = torch.empty(cap, dtype=torch.uint8, device=self.device)   # decode-side container
+        self.offs_d = torch.empty(self.n_blocks + len(self.ranges), dtype=torch.int64, device=self.device)
+        self.status_log = torch.empty(len(self.ranges), 2, 4, dtype=torch.int64, device=self.device)
+        self.nb_h = torch.empty(len(self.ranges), 4, dtype=torch.int64).pin_memory()
+        self.offs_stage = torch.empty(self.n_blocks + len(self.ranges), dtype=torch.int64).pin_memory()
+        self.s_in = torch.cuda.Stream(self.device)
+        self.s_cmp = torch.cuda.Stream(self.device)
+        self.s_out = torch.cuda.Stream(self.device)
+        self.h2d_bytes = 0
+        self.d2h_bytes = 0
+
+    def _encoder(self, j: int, m: int) -> Encoder:
+        pool = self.enc if m == self.enc[0].n else self._enc_by_len[m]
+        return pool[j % self.depth]
+
+    def header(self) -> bytes:
+        c = self.config
+        return struct.pack(FILE_HEADER_FMT, b"APAX", 1, c.dtype.wire_code, c.mode.value, 0, c.block_size,
+                           self.n, float(c.target))
+
+    def run(self, x_h, blob_h, offs_h, y_h) -> int:
+        """One pipelined round trip.  x_h, y_h: pinned CPU tensors of the
+        config dtype and length n; blob_h: pinned uint8 (>= container
+        length); offs_h: pinned int64 (n_blocks + 1) receiving the global
+        side-band index.  Returns the container length; raises the
+        reference exception on any device status."""
+        import torch
+        P = int(self.config.segment_blocks)
+        bs = self.config.block_size
+        K = len(self.ranges)
+        ev_slot_free = [None] * self.depth        # D2H of slot's container done
+        ev_enc: List[Optional[torch.cuda.Event]] = [None] * K
+        hdr = np.frombuffer(self.header(), np.uint8)
+        blob_h[:FILE_HEADER_SIZE].copy_(torch.from_numpy(hdr.copy()))
+        h2d = d2h = 0
+        bodies = []
+
+        def launch_encode(j):
+            nonlocal h2d
+            a, b = self.ranges[j]
+            m = b - a
+            e = self._encoder(j, m)
+            slot = j % self.depth
+            # the slot's input buffer doubles as staging: decode output lands in y_h directly
+            xd = self._xbuf(slot, m)
+            with torch.cuda.stream(self.s_in):
+                if ev_slot_free[slot] is not None:
+                    self.s_in.wait_event(ev_slot_free[slot])
+                xd.copy_(x_h[a:b], non_blocking=True)
+                ev_x = torch.cuda.Event()
+                ev_x.record(self.s_in)
+            h2d += m * x_h.element_size()
+            self.s_cmp.wait_event(ev_x)
+            e.encode(xd, stream=self.s_cmp)
+            with torch.cuda.stream(self.s_cmp):
+                self.nb_h[j].copy_(e.status, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.s_cmp)
+            ev_enc[j] = ev
+
+        goff = FILE_HEADER_SIZE
+        blk = 0
+        ev_done = []
+        launch_encode(0)
+        for j in range(K):
+            if j + 1 < K:
+                launch_encode(j + 1)
+            a, b = self.ranges[j]
+            m = b - a
+            e = self._encoder(j, m)
+            slot = j % self.depth
+            ev_enc[j].synchronize()
+            st = self.nb_h[j].numpy().view(np.uint64)
+            _check_status(st)
+            nb = int(st[2])
+            body = nb - FILE_HEADER_SIZE
+            nblk = (m + bs - 1) // bs
+            # D2H container body + local index (device -> pinned host)
+            with torch.cuda.stream(self.s_out):
+                self.s_out.wait_event(ev_enc[j])
+                blob_h[goff:goff + body].copy_(e.out[FILE_HEADER_SIZE:nb], non_blocking=True)
+                stage = self.offs_stage[blk + j: blk + j + nblk + 1]
+                stage.copy_(e.offsets[:nblk + 1], non_blocking=True)
+                ev_c = torch.cuda.Event()
+                ev_c.record(self.s_out)
+                ev_slot_free[slot] = ev_c
+            d2h += body + 8 * (nblk + 1)
+            # H2D container body + index back; decode from the host copy
+            base = goff - FILE_HEADER_SIZE        # chunk's container view starts 28 B before its body
+            with torch.cuda.stream(self.s_in):
+                self.s_in.wait_event(ev_c)
+                self.blob_d[goff:goff + body].copy_(blob_h[goff:goff + body], non_blocking=True)
+                od = self.offs_d[blk + j: blk + j + nblk + 1]
+                od.copy_(stage, non_blocking=True)
+                ev_ci = torch.cuda.Event()
+                ev_ci.record(self.s_in)
+            h2d += body + 8 * (nblk + 1)
+            self.s_cmp.wait_event(ev_ci)
+            d = self.dec[m]
+            yd = self._ybuf(slot, m)
+            d.decode(self.blob_d[base:], nb, od, stream=self.s_cmp, out=yd, segment_blocks=P)
+            with torch.cuda.stream(self.s_cmp):
+                self.status_log[j, 1].copy_(d.status)
+                ev_d = torch.cuda.Event()
+                ev_d.record(self.s_cmp)
+            with torch.cuda.stream(self.s_out):
+                self.s_out.wait_event(ev_d)
+                y_h[a:b].copy_(yd[:m], non_blocking=True)
+                ev_y = torch.cuda.Event()
+                ev_y.record(self.s_out)
+            d2h += m * y_h.element_size()
+            ev_done.append(ev_y)
+            # next chunk's input copy may reuse this slot's buffers only after
+            # its decode output left the device
+            ev_slot_free[slot] = ev_y
+            bodies.append(body)
+            goff += body
+            blk += nblk
+        for ev in ev_done:
+            ev.synchronize()
+        # global side-band index: local offsets shifted to the body positions
+        # (host arithmetic on the small index, after the copies landed)
+        self._globalize(offs_h, bodies)
+        for j in range(K):
+            _check_status(self.status_log[j, 1].cpu().numpy().view(np.uint64))
+        self.h2d_bytes, self.d2h_bytes = h2d, d2h
+        return goff
+
+    # ---- buffers ------------------------------------------------------
+    def _xbuf(self, slot, m):
+        import torch
+        if not hasattr(self, "_xb"):
+            nmax = max(b - a for a, b in self.ranges)
+            self._xb = [torch.empty(nmax, dtype=torch_dtype(self.config.dtype), device=self.device)
+                        for _ in range(self.depth)]
+        return self._xb[slot][:m]
+
+    def _ybuf(self, slot, m):
+        import torch
+        if not hasattr(self, "_yb"):
+            nmax = max(b - a for a, b in self.ranges)
+            self._yb = [torch.empty(nmax, dtype=torch_dtype(self.config.dtype), device=self.device)
+                        for _ in range(self.depth)]
+        return self._yb[slot][:m]
+
+    def _globalize(self, offs_h, bodies) -> None:
+        bs = self.config.block_size
+        o = offs_h.numpy()
+        st = self.offs_stage.numpy()
+        goff = FILE_HEADER_SIZE
+        blk = 0
+        for j, (a, b) in enumerate(self.ranges):
+            nblk = (b - a + bs - 1) // bs
+            o[blk:blk + nblk + 1] = st[blk + j: blk + j + nblk + 1] + (goff - FILE_HEADER_SIZE)
+            goff += bodies[j]
+            blk += nblk
