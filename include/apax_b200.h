@@ -90,7 +90,8 @@ int64_t apax_decode_workspace_bytes(int64_t n, int dtype, int block_size);
  * `nbytes` bytes (file header included; the caller parsed the header with
  * apax_parse_file_header for n / dtype / block_size).  block_offsets
  * (device, nullable): n_blocks + 1 offsets from apax_encode or
- * apax_find_blocks; NULL runs the block walk first.  y (device) receives n
+ * apax_find_blocks; NULL runs block discovery (K5, see apax_find_blocks)
+ * first.  y (device) receives n
  * samples of dtype. */
 int apax_decode(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, int block_size,
                 const int64_t* block_offsets, void* y, uint64_t* status, void* ws,
@@ -108,9 +109,15 @@ int apax_decode_segments(const uint8_t* blob, int64_t nbytes, int64_t n, int dty
                          const int64_t* block_offsets, int64_t segment_blocks, void* y, uint64_t* status,
                          void* ws, int64_t ws_bytes, void* stream);
 
-/* The reference's serial boundary walk on the device: offsets (device,
+/* Block boundaries of a container without a side-band index (replaces the
+ * reference's serial walk, codec.py:317-323): offsets (device,
  * n_blocks + 1) receives every block header offset and the end offset;
- * errors go to status[1]. */
+ * errors go to status[1] with the walk's block index.  Runs K5 (parallel
+ * signature candidates + per-candidate JEE parse + exact verification of
+ * the walk recurrence, apax_k5.cu) with the serial walk as the exact
+ * fallback; APAX_K5=0 in the environment forces the serial walk.  Scratch
+ * comes from the stream-ordered allocator (cudaMallocAsync).  apax_decode
+ * with block_offsets == NULL runs the same discovery in its workspace. */
 int apax_find_blocks(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, int block_size,
                      int64_t* offsets, uint64_t* status, void* stream);
 
