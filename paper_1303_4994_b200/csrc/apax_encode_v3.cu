@@ -128,6 +128,12 @@ __device__ __forceinline__ unsigned long long wb64(long long v) {
 __device__ __forceinline__ int swz(int k) { return k ^ (((k >> 3) & 3) ^ (((k >> 5) & 3) << 1)); }
 __device__ __forceinline__ int qw(int s) { return (swz(s >> 2) << 2) | (s & 3); }
 
+// decode_scale_code (dtypes.py:124-128) built from the bits: (1 + f/1024) *
+// 2^(e-31) is a normal double for every code
+__device__ __forceinline__ double scale_code_value(int code) {
+    const unsigned long long e = (unsigned long long)(code >> 10), f = (unsigned long long)(code & 0x3FF);
+    return __longlong_as_double((long long)(((e + 992ull) << 52) | (f << 42)));
+}
 __device__ __forceinline__ double clamp_att(double att, double lo) {
     double m = (lo > att) ? lo : att;
     return (0.0 < m) ? 0.0 : m;
@@ -219,6 +225,15 @@ __device__ __forceinline__ void put_bits(uint32_t* win, int pos, uint32_t c, int
     uint32_t* w = win + (pos >> 5);
     atomicOr(w, bswap32(a >> sh));
     if (sh + nb > 32) atomicOr(w + 1, bswap32(a << (32 - sh)));
+}
+// the same for a piece of 1..64 bits (at most three words)
+__device__ __forceinline__ void put_bits64(uint32_t* win, int pos, unsigned long long c, int nb) {
+    const unsigned long long a = c << (64 - nb);  // left-aligned
+    const int sh = pos & 31;
+    uint32_t* w = win + (pos >> 5);
+    atomicOr(w, bswap32((uint32_t)(a >> (32 + sh))));
+    if (sh + nb > 32) atomicOr(w + 1, bswap32((uint32_t)(a >> sh)));
+    if (sh + nb > 64) atomicOr(w + 2, bswap32((uint32_t)(a << (32 - sh))));
 }
 
 // ---------------------------------------------------------------------------
@@ -766,7 +781,7 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
                 long long qpk;
                 if (!F) {
                     code = encode_scale_code(a);
-                    aq = decode_scale_code(code);
+                    aq = scale_code_value(code);
                     qpk = (aq == 1.0) ? (long long)peak : (long long)rint(peak * aq);
                 } else if (nonfin || peak == 0.0) {
                     code = kScaleCodeOne; zero = 1; qpk = 0;
@@ -775,16 +790,21 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
                     if (!isfinite(s_des)) {
                         bad = APAX_ERR_OVERFLOW; code = kScaleCodeOne; zero = 1; qpk = 0;
                     } else {
-                        long long l2 = floor_log2_rn(s_des);
+                        // floor(log2 s_des) from the bits; only mantissas within
+                        // 2^-40 of 2 can round up (floor_log2_rn decides those)
+                        const unsigned long long sb = (unsigned long long)__double_as_longlong(s_des);
+                        const long long l2 = ((sb & 0xFFFFFFFFFFFFFull) < 0xFFFFFFFFFF000ull && (sb >> 52) != 0)
+                                                 ? (long long)(sb >> 52) - 1023
+                                                 : floor_log2_rn(s_des);
                         long long fb = (-31 <= l2 && l2 <= 31) ? 0 : l2 - 31;
                         fb = fb < -127 ? -127 : (fb > 127 ? 127 : fb);
-                        double rem = ldexp(s_des, (int)-fb);
+                        double rem = fb ? ldexp(s_des, (int)-fb) : s_des;
                         const double nxt = 8589934591.999999;
                         double mm = (nxt < rem) ? nxt : rem;
                         rem = (mm > 4.656612873077393e-10) ? mm : 4.656612873077393e-10;
                         code = encode_scale_code(rem);
                         for (;;) {  // overflow guard (codec.py:126-131)
-                            s = decode_scale_code(code) * ldexp(1.0, (int)fb);
+                            s = fb ? decode_scale_code(code) * ldexp(1.0, (int)fb) : scale_code_value(code);
                             double qm = rint(peak * s);
                             if (qm < 2147483648.0 || fb <= -127) {
                                 qpk = qm < 9.2e18 ? (long long)qm : (1LL << 62);
@@ -937,7 +957,6 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
             int flips = 0;
             unsigned emax = 0;
             int hq1 = hp1, hq2 = hp2;                  // q[t0-1], q[t0-2]
-            int q14 = 0, q15 = 0;                      // q[t0+14], q[t0+15]
             if (active) {
                 int q[SPT];
 #pragma unroll
@@ -949,7 +968,6 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
                     const int2 h = *(const int2*)&qbuf[(swz(4 * tid - 1) << 2) + 2];
                     hq2 = h.x; hq1 = h.y;
                 }
-                q14 = q[14]; q15 = q[15];
                 const int ng = FIX ? 4 : min(4, G - p0);   // valid groups of this thread (>= 1)
                 if (!wide) {
                     int m1 = hq1, dprev = hq1 - hq2;
@@ -1001,7 +1019,7 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
                 if (t0 == 0) flips -= (int)((unsigned)(q[0] ^ hq1) >> 31);  // no predecessor in the block
             }
             // byte sums of the packed widths
-            auto bsum = [](uint32_t e) -> int { return (int)((e & 0xffu) + ((e >> 8) & 0xffu) + ((e >> 16) & 0xffu) + (e >> 24)); };
+            auto bsum = [](uint32_t e) -> int { return (int)__dp4a(e, 0x01010101u, 0u); };
             // width of the group starting at sample i0 of stream sl2 (boundary lanes only)
             auto edge_w32 = [&](int sl2, int4 a, int m1, int m2) -> int {
                 const int v[4] = {a.x, a.y, a.z, a.w};
@@ -1041,14 +1059,18 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
                 esel = es;
                 eprev = __shfl_up_sync(0xffffffffu, (int)(es >> 24), 1);
                 enext = __shfl_down_sync(0xffffffffu, (int)(es & 0xffu), 1);
-                if (lane == 0 && active && p0 > 0) {   // previous warp's last group
-                    const int4 a = qb4[swz(4 * tid - 1)];
-                    const int2 h = *(const int2*)&qbuf[(swz(4 * tid - 2) << 2) + 2];
-                    eprev = wide ? edge_w(sl2, a, h.y, h.x) : edge_w32(sl2, a, h.y, h.x);
-                }
-                if (lane == 31 && active && p0 + 4 < G) {   // next warp's first group
-                    const int4 a = qb4[swz(4 * tid + 4)];
-                    enext = wide ? edge_w(sl2, a, q15, q14) : edge_w32(sl2, a, q15, q14);
+                // lane 0: the previous warp's last group; lane 31: the next
+                // warp's first group -- one divergent pass for both lanes
+                const bool ed0 = lane == 0 && active && p0 > 0;
+                const bool ed31 = lane == 31 && active && p0 + 4 < G;
+                if (ed0 || ed31) {
+                    const int4 a = qb4[swz(ed0 ? 4 * tid - 1 : 4 * tid + 4)];
+                    // the two samples before that group: chunk 4t-2 (lane 0) or
+                    // this thread's own last chunk (lane 31: q14, q15)
+                    const int2 h = *(const int2*)&qbuf[(swz(ed0 ? 4 * tid - 2 : 4 * tid + 3) << 2) + 2];
+                    const int ew = wide ? edge_w(sl2, a, h.y, h.x) : edge_w32(sl2, a, h.y, h.x);
+                    if (ed0) eprev = ew;
+                    else enext = ew;
                 }
                 const int e1 = (int)(es & 0xffu), e2 = (int)((es >> 8) & 0xffu);
                 const int e3 = (int)((es >> 16) & 0xffu), e4 = (int)(es >> 24);
@@ -1306,17 +1328,13 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
                                 const int w = (int)((esel >> (8 * g)) & 0xffu);
                                 if (g >= ng || w == 0) continue;
                                 const uint32_t m = 0xffffffffu >> (32 - w);
-                                if (w <= 8) {
+                                if (w <= 16) {
+                                    // one uniform path for every width <= 16: the group's
+                                    // 4w bits as one 64-bit piece (no <=8 / <=16 divergence)
                                     const uint32_t pw = 1u << w;
-                                    uint32_t c = (uint32_t)vs[0] & m;
-                                    c = c * pw + ((uint32_t)vs[1] & m);
-                                    c = c * pw + ((uint32_t)vs[2] & m);
-                                    c = c * pw + ((uint32_t)vs[3] & m);
-                                    put_bits(win, pos, c, 4 * w);
-                                } else if (w <= 16) {
-                                    const uint32_t pw = 1u << w;
-                                    put_bits(win, pos, ((uint32_t)vs[0] & m) * pw + ((uint32_t)vs[1] & m), 2 * w);
-                                    put_bits(win, pos + 2 * w, ((uint32_t)vs[2] & m) * pw + ((uint32_t)vs[3] & m), 2 * w);
+                                    const uint32_t hi = ((uint32_t)vs[0] & m) * pw + ((uint32_t)vs[1] & m);
+                                    const uint32_t lo = ((uint32_t)vs[2] & m) * pw + ((uint32_t)vs[3] & m);
+                                    put_bits64(win, pos, ((unsigned long long)hi << (2 * w)) | lo, 4 * w);
                                 } else {
 #pragma unroll
                                     for (int kk = 0; kk < 4; kk++) put_bits(win, pos + kk * w, (uint32_t)vs[kk] & m, w);
