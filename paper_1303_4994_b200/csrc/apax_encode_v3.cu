@@ -85,6 +85,7 @@ struct __align__(16) St {
     int mbw[NCW];          // mantissa bits of the warp
     int monc[NCW], monf[NCW];
     long long blen;
+    int tl_next;
     // window / unit bookkeeping
     long long win_base;
     int tail_len;
@@ -689,7 +690,7 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
         };
         if (tid == 0) {
             S->att = 0.0; S->p1 = 0; S->p2 = 0; S->has_pc = 0; S->initialized = 0;
-            S->emitted = 0; S->win_base = 0; S->tail_len = 0; S->unit_len = 0; S->blen = 0;
+            S->emitted = 0; S->win_base = 0; S->tail_len = 0; S->unit_len = 0; S->blen = 0; S->tl_next = 0;
             S->tail[0] = S->tail[1] = S->tail[2] = S->tail[3] = 0u;
             if (P.halo && b0 > 1) {  // history entering block b0-1 (App. C E2)
                 const T* xh = (const T*)P.x + (b0 - 1) * (long long)bs;
@@ -704,7 +705,7 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
                 int k = (bb0 == bf) ? 0 : ((bb1 == bf) ? 1 : -1);
                 cbar();
                 if (k < 0) {
-                    if (tid == 0 && S->store_pending) { bulk_wait_read(); S->store_pending = 0; }
+                    if (tid == 32 && S->store_pending) { bulk_wait_read(); S->store_pending = 0; }
                     cbar();
                     k = (bb0 == -1) ? 0 : ((bb1 == -1) ? 1 : 0);
                     stage(bf, k);
@@ -730,8 +731,10 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
 
             PROF_MARK(0);
             // ============ S1 (thread 0): gain, code, scale ============
+            // the previous block's bulk store must have read its window
+            // before B2 (this block stages into that buffer after B2)
+            if (tid == 32 && S->store_pending) { bulk_wait_read(); S->store_pending = 0; }
             if (tid == 0) {
-                if (S->store_pending) { bulk_wait_read(); S->store_pending = 0; }
                 unsigned pks = 0, pku = 0;
                 for (int w = 0; w < NCW; w++) {
                     pks = max(pks, S->pkw[w]);
@@ -829,9 +832,12 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
                 }
                 S->sel_spec = sel;
                 // window bytes to zero: a guess from the previous block, fixed up after B4
-                long long zg = S->tail_len + HS + (S->blen + (S->blen >> 2)) + 256;
+                // (tl_next: the window tail after this block's flush, which
+                // thread 32 may be writing to S->tail_len right now)
+                const long long pbl = S->blen;
+                long long zg = S->tl_next + HS + (pbl + (pbl >> 2)) + 256;
                 zg = (zg + 15) & ~15LL;
-                if (!S->blen || zg > XB) zg = XB;
+                if (!pbl || zg > XB) zg = XB;
                 S->zlen = (int)zg;
             }
             cbar();  // B2
@@ -1253,6 +1259,7 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
                 // FR loop needs this block's exact byte count (codec.py:228-243)
                 if (tid == 0) {
                     S->blen = blen;
+                    S->tl_next = (int)((wb + blen) & 15);
                     S->gate = gate;
                     if (P.mode == 1) {
                         const long long g4 = 4LL * G;
@@ -1406,22 +1413,31 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
             cbar();  // B5
             PROF_MARK(5);
 
-            // ============ flush + bookkeeping (thread 0) ============
-            if (emit && tid == 0) {
+            // ============ flush (thread 32) || bookkeeping + next S1 (thread 0) ============
+            // Thread 32 owns the window bytes: bulk store, tail, offsets,
+            // win_base / tail_len, and the store's read wait before the next
+            // barrier; thread 0 goes straight on to the next block's S1.
+            if (emit && tid == 32) {
                 const int wb = S->tail_len;
                 const long long blen = S->blen;
                 const uint32_t* win = (const uint32_t*)xs;
                 const long long total = wb + blen;
                 const long long full = total & ~15LL;
+                const long long wbase = S->win_base;
                 if (full > 0) {
-                    bulk_store(slot + S->win_base, win, (uint32_t)full);
+                    bulk_store(slot + wbase, win, (uint32_t)full);
                     S->store_pending = 1;
                 }
                 const int w0 = (int)(full >> 2);
                 S->tail[0] = win[w0]; S->tail[1] = win[w0 + 1];
                 S->tail[2] = win[w0 + 2]; S->tail[3] = win[w0 + 3];
+                if (P.block_offsets) P.block_offsets[b] = wbase + wb;  // unit-relative
+                S->win_base = wbase + full;
+                S->tail_len = (int)(total - full);
+            }
+            if (emit && tid == 0) {
+                const long long blen = S->blen;
                 const int sel = S->gate ? 0 : S->sel_spec;
-                if (P.block_offsets) P.block_offsets[b] = S->win_base + wb;  // unit-relative
                 if (P.trace) {
                     double* tr = P.trace + 10 * b;
                     tr[0] = S->att; tr[1] = S->a; tr[2] = S->code; tr[3] = S->fbe; tr[4] = sel;
@@ -1437,19 +1453,20 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
                 S->p2 = qbuf[qw(np - 2)];
                 S->emitted += 1;
                 S->unit_len += blen;
-                S->win_base += full;
-                S->tail_len = (int)(total - full);
             }
         }
 
         PROF_MARK(6);
         // ---------------- unit end: last tail, publish, hand to the placement warp ----------------
-        if (tid == 0) {
+        if (tid == 32) {
             if (S->store_pending) { bulk_wait_all(); S->store_pending = 0; }
             if (S->tail_len > 0) {
                 const uint4 t4 = make_uint4(S->tail[0], S->tail[1], S->tail[2], S->tail[3]);
                 *(uint4*)(slot + S->win_base) = t4;
             }
+        }
+        cbar();
+        if (tid == 0) {
             const long long Lu = S->unit_len;
             st_release(&P.lookback[u], (u == 0 ? kFlagInc : kFlagAgg) | (unsigned long long)Lu);
             S->slot_len[sl] = Lu; S->slot_b0[sl] = b0; S->slot_b1[sl] = b1;
