@@ -268,35 +268,33 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                     const bool st2 = skip == 2 || (st1 && !n1f);
                     const bool st3 = (st2 && !n2f) || (st0 && n0f);
                     const bool stv[4] = {st0, st1, st2, st3};
+                    // Branch-free token summary (count, escape flag, running value)
+                    // of the thread's starts from 16-entry nibble tables packed in
+                    // immediates (entropy.py:118-164 token alphabet):
+                    //   LUT_C  bit 3 = joint token (two exponents), bits 0-2 = delta sum + 2
+                    //   LUT_D1 first exponent's delta + 2;  LUT_D2 (2-bit) second delta + 1
+                    // Reserved nibbles, unstaged positions and range errors only raise
+                    // an error event (below); their contributions are never used.
+                    constexpr unsigned long long LUT_C = 0x43210cbaba9a98ull;
+                    constexpr unsigned long long LUT_D1 = 0x43210333222111ull;
+                    constexpr unsigned LUT_D2 = 0x24924u;
+                    const bool live = p0 < stotal + 4;   // any of this slice staged
                     int cnt = 0, flag = 0, val = 0;
-                    int tkind[4], ta[4], tb[4];
-                    bool tok[4];
-                    bool stop = p0 >= stotal + 4;   // nothing of this slice is staged
+                    int kv[4], kab[4];
 #pragma unroll
                     for (int k = 0; k < 4; k++) {
-                        const int pos = p0 + k;
                         const int v = nw(k);
-                        int kd, av = 0, bv = 0;
-                        if (pos >= stotal) kd = 5;
-                        else if (v == 14) kd = 4;
-                        else if (v == 15) {
-                            kd = 1;
-                            if (pos + 2 >= stotal) kd = 5;
-                            else av = (nw(k + 1) << 4) | nw(k + 2);
-                        } else if (v >= 9) {
-                            kd = 3; av = v - 11;
-                        } else {
-                            const int v3 = (v * 11) >> 5;   // v / 3 for v <= 8
-                            kd = 2; av = v3 - 1; bv = v - 3 * v3 - 1;
-                        }
-                        const bool sk = stv[k] && !stop;
-                        tok[k] = sk; tkind[k] = kd; ta[k] = av; tb[k] = bv;
-                        if (sk) {
-                            if (kd == 1) { flag = 1; val = av; cnt += 1; }
-                            else if (kd == 3) { val += av; cnt += 1; }
-                            else if (kd == 2) { val += av + bv; cnt += 2; }
-                            else stop = true;
-                        }
+                        const int ab = (int)((W >> (4 * (9 - k))) & 0xffULL);   // nibbles k+1, k+2
+                        kv[k] = v;
+                        kab[k] = ab;
+                        const int cd = (int)((LUT_C >> (4 * v)) & 15ull);
+                        const bool esc = v == 15;
+                        const int c = esc ? 1 : (cd >> 3) + 1;
+                        const int dv = (cd & 7) - 2;
+                        const bool t = stv[k] && live;
+                        cnt += t ? c : 0;
+                        val = t ? (esc ? ab : val + dv) : val;
+                        flag |= (t && esc) ? 1 : 0;
                     }
                     // warp scan of (cnt, flag, val): A then B = (cA+cB, fA|fB, fB ? vB : vA+vB)
                     int c_i = cnt, f_i = flag, v_i = val;
@@ -354,39 +352,36 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                     if (lane == 0) { ec = 0; ef = 0; evv = 0; }
                     int idx = pc + ec;
                     int curv = ef ? evv : pv + evv;
-                    // evaluate tokens in order; first event = error or completion
-                    int ev_pos = 0x7fffffff, ev_done = 0;
-                    bool fin = false;
+                    // evaluate the thread's tokens in order: exponents into ebuf, and the
+                    // first event (error, or the token that completes G exponents) as
+                    // key = position << 1 | is_error
+                    int key = 0x7fffffff;
 #pragma unroll
                     for (int k = 0; k < 4; k++) {
-                        if (!tok[k] || fin) continue;
-                        if (idx >= G) { fin = true; continue; }
-                        const int kind = tkind[k], pos = p0 + k;
-                        int e_err = 0, adv = 0;
-                        if (kind >= 4) e_err = 1;
-                        else if (kind == 1) {
-                            if (ta[k] > 34) e_err = 1;
-                            else { curv = ta[k]; ebuf[idx] = (uint8_t)curv; adv = 1; }
-                        } else if (idx == 0) e_err = 1;
-                        else if (kind == 3) {
-                            curv += ta[k];
-                            if (curv < 0 || curv > 34) e_err = 1;
-                            else { ebuf[idx] = (uint8_t)curv; adv = 1; }
-                        } else {
-                            curv += ta[k];
-                            if (curv < 0 || curv > 34 || idx + 1 >= G) e_err = 1;
-                            else {
-                                ebuf[idx] = (uint8_t)curv;
-                                curv += tb[k];
-                                if (curv < 0 || curv > 34) e_err = 1;
-                                else { ebuf[idx + 1] = (uint8_t)curv; adv = 2; }
-                            }
+                        const int pos = p0 + k;
+                        const int v = kv[k];
+                        const bool t = stv[k] && live && idx < G;   // tokens after the G-th exponent are not read
+                        const bool esc = v == 15;
+                        const int cd = (int)((LUT_C >> (4 * v)) & 15ull);
+                        const bool joint = !esc && (cd >> 3) != 0;
+                        const int e1 = esc ? kab[k] : curv + (int)((LUT_D1 >> (4 * v)) & 15ull) - 2;
+                        const int e2 = e1 + (int)((LUT_D2 >> (2 * v)) & 3u) - 1;
+                        bool bad = pos >= stotal || v == 14;
+                        bad |= esc && pos + 2 >= stotal;
+                        bad |= !esc && idx == 0;                     // stream must open with an escape
+                        bad |= (unsigned)e1 > 34u;
+                        bad |= joint && (idx + 1 >= G || (unsigned)e2 > 34u);
+                        const int nexp = joint ? 2 : 1;
+                        const bool done = idx + nexp >= G;
+                        if (t && !bad) {
+                            ebuf[idx] = (uint8_t)e1;
+                            if (joint) ebuf[idx + 1] = (uint8_t)e2;
                         }
-                        if (e_err) { ev_pos = pos; ev_done = 0; fin = true; continue; }
-                        idx += adv;
-                        if (idx >= G) { ev_pos = pos + (kind == 1 ? 3 : 1); ev_done = 1; fin = true; }
+                        const int kk2 = bad ? ((pos << 1) | 1) : (done ? ((pos + (esc ? 3 : 1)) << 1) : 0x7fffffff);
+                        key = t ? min(key, kk2) : key;
+                        curv = t ? (joint ? e2 : e1) : curv;
+                        idx += t ? nexp : 0;
                     }
-                    int key = (ev_pos == 0x7fffffff) ? 0x7fffffff : ((ev_pos << 1) | (ev_done ? 0 : 1));
                     key = __reduce_min_sync(0xffffffffu, key);
                     if (lane == 0) S->ev_min[warp] = key;
                     cbar();

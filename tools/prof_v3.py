@@ -24,7 +24,7 @@ def build():
     src = os.path.join(ROOT, "paper_1303_4994_b200", "csrc")
     objs = []
     for f in ["apax_encode.cu", "apax_encode_v2.cu", "apax_encode_v3.cu", "apax_decode.cu", "apax_decode_v2.cu",
-              "apax_capi.cu"]:
+              "apax_decode_v3.cu", "apax_profile.cu", "apax_k5.cu", "apax_capi.cu"]:
         o = os.path.join(OUT, f.replace(".cu", ".o"))
         subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fmad=false",
                         "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-DAPAX_V3_PROF",
