@@ -94,6 +94,7 @@ struct __align__(16) St {
     int store_pending;
     // slots handed to the placement warp
     long long slot_len[2], slot_b0[2], slot_b1[2];
+    long long fin_prefix;
     unsigned long long mb_stage[2];
 };
 
@@ -403,11 +404,11 @@ __device__ __noinline__ int cold_gw(const int* qbuf, int sl, int gi, int np, lon
     return bitlen64(o);
 }
 
-// placement warp: copy len bytes from a 4-aligned global word source to an
-// arbitrary byte offset (one warp)
-__device__ void warp_copy_out(uint8_t* dst, const uint32_t* src, long long len) {
+// copy len bytes from a 4-aligned global word source to an arbitrary byte
+// offset with `nth` threads (thread index `lane` in 0..nth-1): one warp in
+// the placement loop, the whole CTA for the CTA's last unit
+__device__ void group_copy_out(uint8_t* dst, const uint32_t* src, long long len, int lane, int nth) {
     if (len <= 0) return;
-    const int lane = threadIdx.x & 31;
     const uintptr_t d0 = (uintptr_t)dst;
     long long head = (long long)((16 - (d0 & 15)) & 15);
     if (head > len) head = len;
@@ -419,11 +420,11 @@ __device__ void warp_copy_out(uint8_t* dst, const uint32_t* src, long long len) 
     const uint32_t sh = (uint32_t)(head & 3) * 8;
     const long long wbase = head >> 2;
     long long c = lane;
-    for (; c + 96 < nchunks; c += 128) {
+    for (; c + 3 * nth < nchunks; c += 4 * nth) {
         uint32_t a[4][5];
 #pragma unroll
         for (int r = 0; r < 4; r++) {
-            const long long w = wbase + 4 * (c + 32 * r);
+            const long long w = wbase + 4 * (c + (long long)nth * r);
 #pragma unroll
             for (int k = 0; k < 5; k++) a[r][k] = src[w + k];
         }
@@ -434,10 +435,10 @@ __device__ void warp_copy_out(uint8_t* dst, const uint32_t* src, long long len) 
             v.y = __funnelshift_r(a[r][1], a[r][2], sh);
             v.z = __funnelshift_r(a[r][2], a[r][3], sh);
             v.w = __funnelshift_r(a[r][3], a[r][4], sh);
-            d16[c + 32 * r] = v;
+            d16[c + (long long)nth * r] = v;
         }
     }
-    for (; c < nchunks; c += 32) {
+    for (; c < nchunks; c += nth) {
         const long long w = wbase + 4 * c;
         const uint32_t a0 = src[w], a1 = src[w + 1], a2 = src[w + 2], a3 = src[w + 3], a4 = src[w + 4];
         uint4 v;
@@ -447,7 +448,35 @@ __device__ void warp_copy_out(uint8_t* dst, const uint32_t* src, long long len) 
         v.w = __funnelshift_r(a3, a4, sh);
         d16[c] = v;
     }
-    for (long long i = head + body + lane; i < len; i += 32) dst[i] = sb[i];
+    for (long long i = head + body + lane; i < len; i += nth) dst[i] = sb[i];
+}
+
+// decoupled look-back (one warp): exclusive byte prefix of unit u from the
+// predecessors' aggregate / inclusive flags
+__device__ __forceinline__ long long unit_prefix(unsigned long long* lookback, long long u) {
+    const int lane = threadIdx.x & 31;
+    long long prefix = 0;
+    long long kk = u - 1;
+    for (;;) {
+        const long long idx = kk - lane;
+        const unsigned long long v = (idx >= 0) ? ld_acquire(&lookback[idx]) : kFlagInc;
+        const unsigned long long fl = v & ~kValMask;
+        const unsigned inc = __ballot_sync(0xffffffffu, fl == kFlagInc);
+        const unsigned nrd = __ballot_sync(0xffffffffu, fl == 0);
+        const int first_inc = inc ? __ffs(inc) - 1 : 32;
+        const unsigned need = first_inc >= 31 ? 0xffffffffu : ((2u << first_inc) - 1u);
+        if (nrd & need) {
+            __nanosleep(400);
+            continue;
+        }
+        unsigned long long part = (lane <= first_inc) ? (v & kValMask) : 0ULL;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        prefix += (long long)part;
+        if (inc) break;
+        kk -= 32;
+    }
+    return prefix;
 }
 
 // placement warp: resolve every finished unit of this CTA and copy it out
@@ -457,46 +486,66 @@ __device__ __noinline__ void placement_loop(long long unit_begin, long long unit
                                             St* S, uint8_t* slot0, uint8_t* slot1) {
     const int lane = threadIdx.x & 31;
     int k = 0;
-    for (long long u = unit_begin + blockIdx.x; u < unit_end; u += gridDim.x, k++) {
+    // every unit of this CTA but the last (the whole CTA places that one,
+    // final_place)
+    for (long long u = unit_begin + blockIdx.x; u + (long long)gridDim.x < unit_end; u += gridDim.x, k++) {
         const int sl = k & 1;
         nb_full_sync(sl);
         const long long len = S->slot_len[sl];
         const long long b0 = S->slot_b0[sl], b1 = S->slot_b1[sl];
         long long prefix = 0;
         if (u > 0) {
-            long long kk = u - 1;
-            for (;;) {
-                const long long idx = kk - lane;
-                const unsigned long long v = (idx >= 0) ? ld_acquire(&lookback[idx]) : kFlagInc;
-                const unsigned long long fl = v & ~kValMask;
-                const unsigned inc = __ballot_sync(0xffffffffu, fl == kFlagInc);
-                const unsigned nrd = __ballot_sync(0xffffffffu, fl == 0);
-                const int first_inc = inc ? __ffs(inc) - 1 : 32;
-                const unsigned need = first_inc >= 31 ? 0xffffffffu : ((2u << first_inc) - 1u);
-                if (nrd & need) {
-                    __nanosleep(400);
-                    continue;
-                }
-                unsigned long long part = (lane <= first_inc) ? (v & kValMask) : 0ULL;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-                prefix += (long long)part;
-                if (inc) break;
-                kk -= 32;
-            }
+            prefix = unit_prefix(lookback, u);
             if (lane == 0) st_release(&lookback[u], kFlagInc | (unsigned long long)(prefix + len));
         }
         if (u == n_units - 1 && lane == 0) {
             status[2] = (unsigned long long)(kFileHeader + prefix + len);
             if (block_offsets) block_offsets[n_blocks] = kFileHeader + prefix + len;
         }
-        warp_copy_out(out + kFileHeader + prefix, (const uint32_t*)(sl ? slot1 : slot0), len);
+#ifndef APAX_V3_NOCOPY
+        group_copy_out(out + kFileHeader + prefix, (const uint32_t*)(sl ? slot1 : slot0), len, lane, 32);
+#endif
         if (block_offsets)
             for (long long bb = b0 + lane; bb < b1; bb += 32) block_offsets[bb] += kFileHeader + prefix;
         __syncwarp();
         __threadfence_block();
         if (u + 2 * (long long)gridDim.x < unit_end) nb_free_arrive(sl);   // the slot is reused
     }
+}
+
+// the CTA's last unit, placed by all NT threads once the compute warps have
+// published it and the placement warp has placed the earlier units: warp 0
+// resolves the prefix, everyone copies (a one-warp copy of the whole unit
+// was the tail of one-wave launches)
+__device__ __forceinline__ void fbar() { asm volatile("bar.sync 7, %0;" :: "n"(NT) : "memory"); }
+__device__ __noinline__ void final_place(long long u, int sl, long long n_units, long long n_blocks,
+                                        unsigned long long* lookback, unsigned long long* status,
+                                        long long* block_offsets, uint8_t* out, St* S, uint8_t* slot) {
+    const int tid = threadIdx.x;
+    fbar();
+    const long long len = S->slot_len[sl];
+    const long long b0 = S->slot_b0[sl], b1 = S->slot_b1[sl];
+    if (tid < 32) {
+        long long prefix = 0;
+        if (u > 0) {
+            prefix = unit_prefix(lookback, u);
+            if (tid == 0) st_release(&lookback[u], kFlagInc | (unsigned long long)(prefix + len));
+        }
+        if (tid == 0) {
+            S->fin_prefix = prefix;
+            if (u == n_units - 1) {
+                status[2] = (unsigned long long)(kFileHeader + prefix + len);
+                if (block_offsets) block_offsets[n_blocks] = kFileHeader + prefix + len;
+            }
+        }
+    }
+    fbar();
+    const long long prefix = S->fin_prefix;
+#ifndef APAX_V3_NOCOPY
+    group_copy_out(out + kFileHeader + prefix, (const uint32_t*)slot, len, tid, NT);
+#endif
+    if (block_offsets)
+        for (long long bb = b0 + tid; bb < b1; bb += NT) block_offsets[bb] += kFileHeader + prefix;
 }
 
 // ---------------------------------------------------------------------------
@@ -540,6 +589,13 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
     if (warp == NCW) {
         placement_loop(P.unit_begin, P.unit_end, P.n_units, P.n_blocks, P.lookback, P.status, P.block_offsets,
                        P.out, S, slot0, slot1);
+        const long long u0 = P.unit_begin + blockIdx.x;
+        if (u0 < P.unit_end) {   // this CTA's last unit, with the compute warps
+            const long long nu = (P.unit_end - u0 + gridDim.x - 1) / gridDim.x;
+            const int sll = (int)((nu - 1) & 1);
+            final_place(u0 + (nu - 1) * gridDim.x, sll, P.n_units, P.n_blocks, P.lookback, P.status,
+                        P.block_offsets, P.out, S, sll ? slot1 : slot0);
+        }
         return;
     }
     // ---------------- compute warps (named barrier 1, 256 threads) ----------------
@@ -1472,7 +1528,8 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
             S->slot_len[sl] = Lu; S->slot_b0[sl] = b0; S->slot_b1[sl] = b1;
             __threadfence_block();
         }
-        nb_full_arrive(sl);
+        const bool last_unit = u + (long long)gridDim.x >= P.unit_end;
+        if (!last_unit) nb_full_arrive(sl);
         if (u == 0 && tid < kFileHeader) {
             unsigned char h[kFileHeader];
             h[0] = 'A'; h[1] = 'P'; h[2] = 'A'; h[3] = 'X';
@@ -1483,6 +1540,8 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
             for (int k2 = 0; k2 < 8; k2++) h[20 + k2] = (unsigned char)(tb >> (8 * k2));
             P.out[tid] = h[tid];
         }
+        if (last_unit)
+            final_place(u, sl, P.n_units, P.n_blocks, P.lookback, P.status, P.block_offsets, P.out, S, slot);
     }
 #ifdef APAX_V3_PROF
     if (tid == 0 && P.trace) {

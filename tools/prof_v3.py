@@ -19,7 +19,8 @@ OUT = os.path.join(ROOT, "build_variants")
 SO = os.path.join(OUT, "libapax_prof.so")
 
 
-def build():
+def build(defs=("-DAPAX_V3_PROF",), so=None):
+    so = so or SO
     os.makedirs(OUT, exist_ok=True)
     src = os.path.join(ROOT, "paper_1303_4994_b200", "csrc")
     objs = []
@@ -27,16 +28,21 @@ def build():
               "apax_decode_v3.cu", "apax_profile.cu", "apax_k5.cu", "apax_capi.cu"]:
         o = os.path.join(OUT, f.replace(".cu", ".o"))
         subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fmad=false",
-                        "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-DAPAX_V3_PROF",
+                        "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", *defs,
                         "-c", os.path.join(src, f), "-o", o], check=True)
         objs.append(o)
-    subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static", "-o", SO]
+    subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static", "-o", so]
                    + objs, check=True)
 
 
 def main():
     if "--build" in sys.argv:
         build()
+        return
+    if "--variant" in sys.argv:   # --variant NAME -DX -DY ...: build_variants/libapax_NAME.so
+        i = sys.argv.index("--variant")
+        name, defs = sys.argv[i + 1], sys.argv[i + 2:]
+        build(tuple(defs), os.path.join(OUT, f"libapax_{name}.so"))
         return
     seg = int(sys.argv[1]) if len(sys.argv) > 1 else 16
     L = ctypes.CDLL(SO)
