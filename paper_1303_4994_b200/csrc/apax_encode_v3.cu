@@ -150,8 +150,22 @@ __device__ __forceinline__ double clamp_step(double d) {
     return (m > -6.0) ? m : -6.0;
 }
 
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst), "l"(src) : "memory");
+// L2 policies: the input streams through once (evict first); the unit slots
+// are re-read by the placement copy and then discarded (evict last), so the
+// slot round trip stays in L2 instead of DRAM
+__device__ __forceinline__ unsigned long long pol_evict_first() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ unsigned long long pol_evict_last() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, unsigned long long pol) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" :: "r"(dst), "l"(src), "l"(pol)
+                 : "memory");
 }
 // one net arrival per thread once its earlier cp.async copies have landed
 // (the inc form + a release arrive also publishes plain st.shared writes)
@@ -184,8 +198,8 @@ __device__ __forceinline__ void mbar_wait_sleep(unsigned long long* bar, uint32_
     }
 }
 __device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
-                 :: "l"(gdst), "r"(sa(ssrc)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
+                 :: "l"(gdst), "r"(sa(ssrc)), "r"(bytes), "l"(pol_evict_last()) : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 __device__ __forceinline__ void bulk_wait_read() {
@@ -195,8 +209,13 @@ __device__ __forceinline__ void bulk_wait_all() {
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
+// drop a 128-byte L2 line without writing it back (a consumed slot line)
+__device__ __forceinline__ void discard_l2(const void* p) {
+    asm volatile("discard.global.L2 [%0], 128;" :: "l"(p) : "memory");
+}
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" :: "l"(p), "r"(bytes),
+                 "l"(pol_evict_first()) : "memory");
 }
 
 // numpy's pairwise combine of nwd (1, 2, 4 or 8) per-warp leaf sums
@@ -505,6 +524,8 @@ __device__ __noinline__ void placement_loop(long long unit_begin, long long unit
 #ifndef APAX_V3_NOCOPY
         group_copy_out(out + kFileHeader + prefix, (const uint32_t*)(sl ? slot1 : slot0), len, lane, 32);
 #endif
+        __syncwarp();
+        for (long long l = (long long)lane * 128; l < len; l += 32 * 128) discard_l2((sl ? slot1 : slot0) + l);
         if (block_offsets)
             for (long long bb = b0 + lane; bb < b1; bb += 32) block_offsets[bb] += kFileHeader + prefix;
         __syncwarp();
@@ -544,6 +565,8 @@ __device__ __noinline__ void final_place(long long u, int sl, long long n_units,
 #ifndef APAX_V3_NOCOPY
     group_copy_out(out + kFileHeader + prefix, (const uint32_t*)slot, len, tid, NT);
 #endif
+    fbar();   // every thread has read its slot words: the lines are dead
+    for (long long l = (long long)tid * 128; l < len; l += (long long)NT * 128) discard_l2(slot + l);
     if (block_offsets)
         for (long long bb = b0 + tid; bb < b1; bb += NT) block_offsets[bb] += kFileHeader + prefix;
 }
@@ -628,11 +651,12 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
         T* dst = xbuf(k);
         if (n == bs && (((uintptr_t)P.x) & 15) == 0) {
             const uint32_t d0 = sa(dst);
+            const unsigned long long xpol = pol_evict_first();
             const int nch = bs / CH;
             for (int c = tid; c < nch; c += NCT) {
                 const int s0 = c * CH;
                 const int di = TRL ? ((s0 & 127) >> 3) * RS + 8 * (s0 >> 7) + (s0 & 7) : s0;
-                cp_async16(d0 + (uint32_t)di * (uint32_t)sizeof(T), src + s0);
+                cp_async16(d0 + (uint32_t)di * (uint32_t)sizeof(T), src + s0, xpol);
             }
         } else if (n == bs) {
             for (int i = tid; i < n; i += NCT)
