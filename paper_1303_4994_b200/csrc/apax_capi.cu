@@ -72,9 +72,19 @@ int plan_encode(long long n, int dt, int mode, int bs, long long seg, EncPlan* p
         if (p->smem > (size_t)optin) p->v3 = 0;
     }
     p->v2 = !p->v3 && encode_v2_supported(bs) && (ver == 0 || ver == 2) && env_int("APAX_FORCE_V1", 0) == 0;
+    long long v3_slots = 0;
     if (p->v3) {
-        int resident = encode_v3_resident_ctas(dt, p->smem);
-        p->grid = (int)(p->n_units < resident ? p->n_units : resident);
+        // one unit per CTA fits: the 256-thread one-wave kernel (one slot per
+        // CTA); else the persistent kernel with a placement warp (two slots)
+        const int rw = encode_v3_resident_ctas_wave(dt, p->smem);
+        const int resident = encode_v3_resident_ctas(dt, p->smem);
+        if (p->n_units <= rw) {
+            p->grid = (int)p->n_units;
+            v3_slots = p->n_units;
+        } else {
+            p->grid = (int)(p->n_units < resident ? p->n_units : resident);
+            v3_slots = 2LL * p->grid > rw ? 2LL * p->grid : rw;   // a sub-range may run one-wave
+        }
     } else if (p->v2) {
         // v2: the window holds one block plus a <16-byte tail
         p->stage_bytes = (int)((mbb + 64 + 15) & ~15LL);
@@ -105,7 +115,7 @@ int plan_encode(long long n, int dt, int mode, int bs, long long seg, EncPlan* p
     p->ws_lookback = 0;
     p->ws_ticket = (p->n_units * 8 + 255) & ~255LL;
     p->ws_slots = p->ws_ticket + 256;
-    p->ws_total = p->ws_slots + (long long)p->grid * p->slot_bytes * ((p->v2 || p->v3) ? 2 : 1);
+    p->ws_total = p->ws_slots + p->slot_bytes * (p->v3 ? v3_slots : (long long)p->grid * (p->v2 ? 2 : 1));
     return APAX_OK;
 }
 
@@ -324,7 +334,10 @@ int64_t apax_encode_wave_segment_blocks(int64_t n, int dtype, int mode, int bloc
     EncPlan p;
     if (plan_encode(n, dtype, mode, block_size, 1, &p)) return -1;
     int resident = p.grid;
-    if (p.v3) resident = encode_v3_resident_ctas(dtype, p.smem);
+    if (p.v3) {
+        resident = encode_v3_resident_ctas_wave(dtype, p.smem);
+        if (resident < 1) resident = encode_v3_resident_ctas(dtype, p.smem);
+    }
     else if (p.v2) resident = encode_v2_resident_ctas(dtype, p.smem);
     if (resident < 1) resident = 1;
     return (p.n_blocks + resident - 1) / resident;

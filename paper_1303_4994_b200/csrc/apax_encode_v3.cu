@@ -43,6 +43,9 @@
 #include "apax_device.cuh"
 #include "apax_kernels.cuh"
 
+#ifndef APAX_V3_MINB_NP
+#define APAX_V3_MINB_NP 4   // one-wave launches: no placement warp, 256 threads, 64 registers
+#endif
 #ifndef APAX_V3_MINB
 #define APAX_V3_MINB 3
 #endif
@@ -163,9 +166,11 @@ __device__ __forceinline__ unsigned long long pol_evict_last() {
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, unsigned long long pol) {
-    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" :: "r"(dst), "l"(src), "l"(pol)
-                 : "memory");
+// (no L2::cache_hint on the 16-byte copies: with a policy operand the 64-register
+// instantiations faulted with an illegal instruction on the LDGSTS descriptor;
+// the input's evict-first policy rides on the bulk L2 prefetch instead)
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst), "l"(src) : "memory");
 }
 // one net arrival per thread once its earlier cp.async copies have landed
 // (the inc form + a release arrive also publishes plain st.shared writes)
@@ -538,12 +543,14 @@ __device__ __noinline__ void placement_loop(long long unit_begin, long long unit
 // published it and the placement warp has placed the earlier units: warp 0
 // resolves the prefix, everyone copies (a one-warp copy of the whole unit
 // was the tail of one-wave launches)
-__device__ __forceinline__ void fbar() { asm volatile("bar.sync 7, %0;" :: "n"(NT) : "memory"); }
+template <int NTT>
+__device__ __forceinline__ void fbar() { asm volatile("bar.sync 7, %0;" :: "n"(NTT) : "memory"); }
+template <int NTT>
 __device__ __noinline__ void final_place(long long u, int sl, long long n_units, long long n_blocks,
                                         unsigned long long* lookback, unsigned long long* status,
                                         long long* block_offsets, uint8_t* out, St* S, uint8_t* slot) {
     const int tid = threadIdx.x;
-    fbar();
+    fbar<NTT>();
     const long long len = S->slot_len[sl];
     const long long b0 = S->slot_b0[sl], b1 = S->slot_b1[sl];
     if (tid < 32) {
@@ -560,15 +567,15 @@ __device__ __noinline__ void final_place(long long u, int sl, long long n_units,
             }
         }
     }
-    fbar();
+    fbar<NTT>();
     const long long prefix = S->fin_prefix;
 #ifndef APAX_V3_NOCOPY
-    group_copy_out(out + kFileHeader + prefix, (const uint32_t*)slot, len, tid, NT);
+    group_copy_out(out + kFileHeader + prefix, (const uint32_t*)slot, len, tid, NTT);
 #endif
-    fbar();   // every thread has read its slot words: the lines are dead
-    for (long long l = (long long)tid * 128; l < len; l += (long long)NT * 128) discard_l2(slot + l);
+    fbar<NTT>();   // every thread has read its slot words: the lines are dead
+    for (long long l = (long long)tid * 128; l < len; l += (long long)NTT * 128) discard_l2(slot + l);
     if (block_offsets)
-        for (long long bb = b0 + tid; bb < b1; bb += NT) block_offsets[bb] += kFileHeader + prefix;
+        for (long long bb = b0 + tid; bb < b1; bb += NTT) block_offsets[bb] += kFileHeader + prefix;
 }
 
 // ---------------------------------------------------------------------------
@@ -577,8 +584,11 @@ __device__ __noinline__ void final_place(long long u, int sl, long long n_units,
 // FIX: every block of this launch is a full 4096-sample block; the block
 // geometry is then compile-time (the partial last block of a stream goes
 // through a second, generic launch over its unit).
-template <int DT, bool FIX>
-__global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P) {
+// PW: a placement warp places finished units while the next ones are coded
+// (more units than resident CTAs).  Without it (one-wave launches: one unit
+// per CTA) the CTA is 256 threads and four fit on an SM.
+template <int DT, bool FIX, bool PW>
+__global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MINB_NP) encode_v3_kernel(EncParams P) {
     using Tr = DT_<DT>;
     using T = typename Tr::T;
     constexpr bool F = Tr::F;
@@ -598,7 +608,7 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
     St* S = (St*)smem;
     const int xoff = (int)((sizeof(St) + 127) & ~(size_t)127);
     int* qbuf = (int*)(smem + xoff + 2 * XB);
-    uint8_t* slot0 = P.slots + (long long)blockIdx.x * 2 * P.slot_bytes;
+    uint8_t* slot0 = P.slots + (long long)blockIdx.x * (PW ? 2 : 1) * P.slot_bytes;
     uint8_t* slot1 = slot0 + P.slot_bytes;
 
     if (tid == 0) {
@@ -609,15 +619,15 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
         S->tail_len = 0;
     }
     __syncthreads();
-    if (warp == NCW) {
+    if (PW && warp == NCW) {
         placement_loop(P.unit_begin, P.unit_end, P.n_units, P.n_blocks, P.lookback, P.status, P.block_offsets,
                        P.out, S, slot0, slot1);
         const long long u0 = P.unit_begin + blockIdx.x;
         if (u0 < P.unit_end) {   // this CTA's last unit, with the compute warps
             const long long nu = (P.unit_end - u0 + gridDim.x - 1) / gridDim.x;
             const int sll = (int)((nu - 1) & 1);
-            final_place(u0 + (nu - 1) * gridDim.x, sll, P.n_units, P.n_blocks, P.lookback, P.status,
-                        P.block_offsets, P.out, S, sll ? slot1 : slot0);
+            final_place<NT>(u0 + (nu - 1) * gridDim.x, sll, P.n_units, P.n_blocks, P.lookback, P.status,
+                            P.block_offsets, P.out, S, sll ? slot1 : slot0);
         }
         return;
     }
@@ -651,12 +661,11 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
         T* dst = xbuf(k);
         if (n == bs && (((uintptr_t)P.x) & 15) == 0) {
             const uint32_t d0 = sa(dst);
-            const unsigned long long xpol = pol_evict_first();
             const int nch = bs / CH;
             for (int c = tid; c < nch; c += NCT) {
                 const int s0 = c * CH;
                 const int di = TRL ? ((s0 & 127) >> 3) * RS + 8 * (s0 >> 7) + (s0 & 7) : s0;
-                cp_async16(d0 + (uint32_t)di * (uint32_t)sizeof(T), src + s0, xpol);
+                cp_async16(d0 + (uint32_t)di * (uint32_t)sizeof(T), src + s0);
             }
         } else if (n == bs) {
             for (int i = tid; i < n; i += NCT)
@@ -778,7 +787,7 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
                 S->p2 = (long long)xh[-2];
             }
         }
-        if (kunit >= 2) nb_free_sync(sl);   // the slot's previous unit has been placed
+        if (PW && kunit >= 2) nb_free_sync(sl);   // the slot's previous unit has been placed
         {
             const long long bf = pass_block(0);
             if (a_done != bf) {
@@ -1552,8 +1561,8 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
             S->slot_len[sl] = Lu; S->slot_b0[sl] = b0; S->slot_b1[sl] = b1;
             __threadfence_block();
         }
-        const bool last_unit = u + (long long)gridDim.x >= P.unit_end;
-        if (!last_unit) nb_full_arrive(sl);
+        const bool last_unit = !PW || u + (long long)gridDim.x >= P.unit_end;
+        if (PW && !last_unit) nb_full_arrive(sl);
         if (u == 0 && tid < kFileHeader) {
             unsigned char h[kFileHeader];
             h[0] = 'A'; h[1] = 'P'; h[2] = 'A'; h[3] = 'X';
@@ -1565,7 +1574,8 @@ __global__ void __launch_bounds__(NT, APAX_V3_MINB) encode_v3_kernel(EncParams P
             P.out[tid] = h[tid];
         }
         if (last_unit)
-            final_place(u, sl, P.n_units, P.n_blocks, P.lookback, P.status, P.block_offsets, P.out, S, slot);
+            final_place<PW ? NT : NCT>(u, sl, P.n_units, P.n_blocks, P.lookback, P.status, P.block_offsets, P.out,
+                                       S, slot);
     }
 #ifdef APAX_V3_PROF
     if (tid == 0 && P.trace) {
@@ -1597,40 +1607,58 @@ bool encode_v3_supported(int dt, int bs) {
 }
 
 template <int DT, bool FIX>
-static void* v3_fn() { return (void*)v3::encode_v3_kernel<DT, FIX>; }
+static void* v3_fn(bool pw) {
+    return pw ? (void*)v3::encode_v3_kernel<DT, FIX, true> : (void*)v3::encode_v3_kernel<DT, FIX, false>;
+}
 
-static void* v3_kernel(int dt, bool fix) {
+static void* v3_kernel(int dt, bool fix, bool pw) {
     switch (dt) {
-        case 0: return v3_fn<0, false>();
-        case 1: return fix ? v3_fn<1, true>() : v3_fn<1, false>();
-        case 2: return fix ? v3_fn<2, true>() : v3_fn<2, false>();
-        default: return fix ? v3_fn<3, true>() : v3_fn<3, false>();
+        case 0: return v3_fn<0, false>(pw);
+        case 1: return fix ? v3_fn<1, true>(pw) : v3_fn<1, false>(pw);
+        case 2: return fix ? v3_fn<2, true>(pw) : v3_fn<2, false>(pw);
+        default: return fix ? v3_fn<3, true>(pw) : v3_fn<3, false>(pw);
     }
 }
 
-int encode_v3_resident_ctas(int dt, size_t smem) {
+static int v3_resident(int dt, size_t smem, bool pw) {
     int dev = 0, nsm = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const void* fn = v3_kernel(dt, false);
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, v3::NT, smem) != cudaSuccess || per < 1)
-        per = 1;
-    return per * (nsm > 0 ? nsm : 148);
+    int r = nsm > 0 ? nsm : 148;
+    for (int f = 0; f < 2; f++) {   // both instantiations must fit (the FIX one may use fewer registers)
+        const void* fn = v3_kernel(dt, f == 1 && dt >= 1, pw);
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int p = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p, fn, pw ? v3::NT : v3::NCT, smem) != cudaSuccess || p < 1)
+            p = 1;
+        per = f == 0 ? p : (p < per ? p : per);
+    }
+    return per * r;
+}
+
+// resident CTAs with the placement warp (persistent multi-unit launches)
+int encode_v3_resident_ctas(int dt, size_t smem) { return v3_resident(dt, smem, true); }
+// resident CTAs of the one-wave variant (no placement warp)
+int encode_v3_resident_ctas_wave(int dt, size_t smem) {
+    if (getenv("APAX_V3_PW")) return 0;   // tuning: force the placement-warp kernel
+    return v3_resident(dt, smem, false);
 }
 
 static int launch_v3_range(int dt, bool fix, const EncParams& P, long long u0, long long u1, int grid,
                            size_t smem, cudaStream_t st) {
-    const void* fn = v3_kernel(dt, fix);
+    // one unit per CTA fits: the 256-thread kernel; otherwise the persistent
+    // kernel with its placement warp
+    const long long nu = u1 - u0;
+    const bool pw = nu > encode_v3_resident_ctas_wave(dt, smem);
+    const void* fn = v3_kernel(dt, fix, pw);
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return APAX_ERR_CUDA;
     EncParams p = P;
     p.unit_begin = u0;
     p.unit_end = u1;
-    const long long nu = u1 - u0;
-    const int g = (int)(nu < grid ? nu : grid);
+    const int g = pw ? (int)(nu < grid ? nu : grid) : (int)nu;
     void* args[] = {&p};
-    if (cudaLaunchCooperativeKernel(fn, dim3(g), dim3(v3::NT), args, smem, st) != cudaSuccess)
+    if (cudaLaunchCooperativeKernel(fn, dim3(g), dim3(pw ? v3::NT : v3::NCT), args, smem, st) != cudaSuccess)
         return APAX_ERR_CUDA;
     return APAX_OK;
 }

@@ -64,6 +64,7 @@ size_t encode_v3_smem_bytes(int dt, int bs, int stage_bytes);
 int encode_v3_stage_bytes(int dt, int bs);
 bool encode_v3_supported(int dt, int bs);
 int encode_v3_resident_ctas(int dt, size_t smem);
+int encode_v3_resident_ctas_wave(int dt, size_t smem);
 int launch_encode_v3(int dt, const EncParams& P, int grid, size_t smem, cudaStream_t st);
 int launch_decode(int dt, const DecParams& P, int grid, size_t smem, cudaStream_t st);
 size_t decode_v3_smem_bytes(int dt, int payload_cap);
