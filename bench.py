@@ -116,7 +116,7 @@ def _ncu_traffic(kernel_prefix: str):
     return None
 
 
-def cpu_round_trip(x, target, seg, threads, budget_s=10.0):
+def cpu_round_trip(x, target, seg, threads, budget_s=10.0, dt=3, mode=2, policy=0):
     """Oracle (C port of the reference) encode+decode on host cores."""
     from oracle import oracle as O
     O.lib()
@@ -125,7 +125,8 @@ def cpu_round_trip(x, target, seg, threads, budget_s=10.0):
     enc_t = dec_t = 0.0
     while True:
         a = time.perf_counter()
-        blob, offs, _ = O.encode(x, 3, 2, target, 4096, segment_blocks=seg, nthreads=threads)
+        blob, offs, _ = O.encode(x, dt, mode, target, 4096, segment_blocks=seg, policy=policy,
+                                 nthreads=threads)
         b = time.perf_counter()
         O.decode(blob, offs, nthreads=threads)
         c = time.perf_counter()
@@ -134,60 +135,127 @@ def cpu_round_trip(x, target, seg, threads, budget_s=10.0):
         reps += 1
         if time.perf_counter() - t0 > budget_s:
             break
-    nb = x.size * 4
+    nb = x.size * x.itemsize
     return {"gbs": nb * reps / (enc_t + dec_t) / 1e9, "enc_gbs": nb * reps / enc_t / 1e9,
             "dec_gbs": nb * reps / dec_t / 1e9, "reps": reps, "seconds": enc_t + dec_t}
 
+# BASELINE.json configs; the N=1 headline is cfg2.
+WORKLOADS = {
+    "cfg1": "cfg1: int16 8 sinusoids + N(0,20^2), 2^24 samples/GPU, fixed rate 4:1 (4 bps)",
+    "cfg2": "cfg2: f32 AR(2) r=0.98 x1e3, 2^26 samples/GPU, fixed-quality at the reference "
+            "profiler's SRR target",
+    "cfg3": "cfg3: f32 8192x8192 Gaussian random field k^-3 + U(+-1e-3 range), fixed rate 6:1",
+    "cfg4": "cfg4: f64 1024^3 (8 GiB) 64 Fourier modes + N(0,1e-4), fixed rate 3:1",
+    "cfg5": "cfg5: AR(1) rho=0.95 (int32 x1e6 or f32), fixed rate r:1 (bps = 32/r)",
+}
 
-def workload_segment_blocks(args, n):
+
+def make_workload(args, rank, dev):
+    """(x on the device, x on the host or None, StreamConfig, short name)."""
+    import torch
+    from paper_1303_4994_b200 import Dtype, Mode, StreamConfig
+    from paper_1303_4994_b200 import workloads as W
+    w = args.workload
+    if w == "cfg1":
+        xh = W.cfg1_sines_i16(1 << (args.n_log2 or 24), seed=1 + rank)
+        dt, mode, target = Dtype.I16, Mode.FIXED_RATE, 4.0
+    elif w == "cfg2":
+        xh = W.cfg2_ar2_f32(1 << (args.n_log2 or 26), seed=2 + rank)
+        dt, mode, target = Dtype.F32, Mode.FIXED_QUALITY, W.CFG2_TARGET_DB
+    elif w == "cfg3":
+        xh = W.cfg3_grf_f32(8192, seed=3 + rank)
+        dt, mode, target = Dtype.F32, Mode.FIXED_RATE, 32.0 / 6.0
+    elif w == "cfg4":
+        xd = W.cfg4_modes_f64(1024, seed=4 + rank, device=dev)
+        dt, mode, target = Dtype.F64, Mode.FIXED_RATE, 64.0 / 3.0
+        return xd, None, dt, mode, target
+    elif w == "cfg5":
+        xh = W.cfg5_ar1(1 << (args.n_log2 or 26), args.cfg5_dtype, seed=5 + rank)
+        dt = Dtype.I32 if args.cfg5_dtype == "i32" else Dtype.F32
+        mode, target = Mode.FIXED_RATE, 32.0 / args.rate
+    else:
+        raise SystemExit(f"unknown workload {w}")
+    return torch.from_numpy(xh).to(dev), xh, dt, mode, target
+
+
+
+def workload_segment_blocks(args, n, dt=None, mode=None):
     """P of the workload: --segment-blocks, else the one-wave length of this
     device (the library query), else 37 (its value on B200)."""
     if args.segment_blocks > 0:
         return args.segment_blocks
     try:
         from paper_1303_4994_b200 import Dtype, Mode, wave_segment_blocks
-        return wave_segment_blocks(n, Dtype.F32, Mode.FIXED_QUALITY, 4096)
+        return wave_segment_blocks(n, dt or Dtype.F32, mode or Mode.FIXED_QUALITY, 4096)
     except Exception:  # noqa: BLE001
         return 37
 
 
 def run_reference(args, rank):
     """--impl reference: the reference algorithm (C oracle port) on all host
-    threads, same metric/config; rank 0 only."""
+    threads, same metric/config, on a bounded sample of the workload; rank 0
+    only."""
     if rank != 0:
         return
+    from paper_1303_4994_b200 import Dtype, Mode
     from paper_1303_4994_b200 import workloads as W
     threads = os.cpu_count() or 1
-    seg = workload_segment_blocks(args, 1 << args.n_log2)
-    n = 1 << 22
-    x = W.cfg2_ar2_f32(n)
+    w = args.workload
+    if w == "cfg1":
+        x, dt, mode, target = W.cfg1_sines_i16(1 << 22), Dtype.I16, Mode.FIXED_RATE, 4.0
+    elif w == "cfg3":
+        x, dt, mode, target = W.cfg3_grf_f32(2048), Dtype.F32, Mode.FIXED_RATE, 32.0 / 6.0
+    elif w == "cfg4":
+        x = W.cfg4_modes_f64(160, device="cpu").numpy()
+        dt, mode, target = Dtype.F64, Mode.FIXED_RATE, 64.0 / 3.0
+    elif w == "cfg5":
+        x = W.cfg5_ar1(1 << 22, args.cfg5_dtype)
+        dt = Dtype.I32 if args.cfg5_dtype == "i32" else Dtype.F32
+        mode, target = Mode.FIXED_RATE, 32.0 / args.rate
+    else:
+        x, dt, mode, target = W.cfg2_ar2_f32(1 << 22), Dtype.F32, Mode.FIXED_QUALITY, W.CFG2_TARGET_DB
+    full_n = {"cfg1": 1 << 24, "cfg3": 1 << 26, "cfg4": 1 << 30}.get(w, 1 << (args.n_log2 or 26))
+    # the GPU arm's segment length for the full-size workload
+    seg = args.segment_blocks if args.segment_blocks > 0 else _wave_p(full_n, dt, mode)
+    pol = {"cold": 0, "warm_self": 1}.get(args.policy, 1 if mode == Mode.FIXED_RATE else 0)
     from oracle import oracle as O
     for _ in range(max(args.warmup, 1)):
-        blob, offs, _ = O.encode(x, 3, 2, W.CFG2_TARGET_DB, 4096, segment_blocks=seg,
-                                 nthreads=threads)
+        blob, offs, _ = O.encode(x, dt.wire_code, mode.value, target, 4096, segment_blocks=seg,
+                                 policy=pol, nthreads=threads)
     times = []
     for _ in range(args.steps):
         a = time.perf_counter()
-        blob, offs, _ = O.encode(x, 3, 2, W.CFG2_TARGET_DB, 4096, segment_blocks=seg,
-                                 nthreads=threads)
+        blob, offs, _ = O.encode(x, dt.wire_code, mode.value, target, 4096, segment_blocks=seg,
+                                 policy=pol, nthreads=threads)
         O.decode(blob, offs, nthreads=threads)
         times.append(time.perf_counter() - a)
     t = sum(times) / len(times)
-    v = x.size * 4 / t / 1e9
+    v = x.size * x.itemsize / t / 1e9
+    sample = (f"{w} bounded sample: {x.size} samples ({x.nbytes >> 20} MiB {dt.code}) encode+decode, "
+              f"{args.steps} steps, OpenMP over segments")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"cfg2: f32 AR(2) x1e3, FQ at profiler SRR target, {seg}-block "
-                               "cold segments, bs 4096 (bounded 2^22-sample sample)",
-                   "n_samples": x.size, "segment_blocks": seg, "block_size": 4096},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"cfg2 first 2^22 samples (16 MiB f32) encode+decode, "
-                                   f"{args.steps} steps, OpenMP over segments"},
+        "vs_baseline": None, "dtype": dt.code, "data": "synthetic",
+        "config": {"workload": WORKLOADS[w] + f"; {seg}-block {['cold', 'warm_self'][pol]} segments, "
+                               "bs 4096 (bounded sample)",
+                   "name": w, "n_samples": x.size, "segment_blocks": seg, "block_size": 4096},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def _wave_p(n, dt, mode):
+    """One-wave segment length of a B200 (148 SMs x the encoder's resident
+    CTAs) without touching a GPU: the reference arm runs on host cores."""
+    nb = (n + 4095) // 4096
+    try:
+        from paper_1303_4994_b200 import wave_segment_blocks
+        return wave_segment_blocks(n, dt, mode, 4096)
+    except Exception:  # noqa: BLE001
+        return max(1, (nb + 591) // 592)
 
 
 def main():
@@ -198,7 +266,13 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--segment-blocks", type=int, default=0,
                     help="blocks per segment; 0 = one-wave (every resident encoder CTA one segment)")
-    ap.add_argument("--n-log2", type=int, default=26)
+    ap.add_argument("--n-log2", type=int, default=0, help="samples per GPU = 2^n (cfg1/2/5; 0 = config default)")
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS),
+                    help="BASELINE config (the N=1 headline is cfg2; the others are reported beside it)")
+    ap.add_argument("--cfg5-dtype", default="i32", choices=["i32", "f32"])
+    ap.add_argument("--rate", type=float, default=4.0, help="cfg5 compression ratio r (bps = 32/r)")
+    ap.add_argument("--policy", default="auto", choices=["auto", "cold", "warm_self"],
+                    help="segment policy; auto = warm_self for fixed rate, cold for fixed quality")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=4, help="pipeline chunks of the e2e round trip")
@@ -226,16 +300,17 @@ def main():
     from paper_1303_4994_b200 import Decoder, Dtype, Encoder, Mode, StreamConfig
     from paper_1303_4994_b200 import workloads as W
 
-    n = 1 << args.n_log2
-    args.segment_blocks = workload_segment_blocks(args, n)
-    x_host = W.cfg2_ar2_f32(n, seed=2 + rank)
-    target = W.CFG2_TARGET_DB
-    cfg = StreamConfig(Dtype.F32, 4096, Mode.FIXED_QUALITY, target,
-                       segment_blocks=args.segment_blocks)
     dev = torch.device("cuda", local)
-    x = torch.from_numpy(x_host).to(dev)
+    x, x_host, wdt, wmode, target = make_workload(args, rank, dev)
+    n = x.numel()
+    args.segment_blocks = workload_segment_blocks(args, n, wdt, wmode)
+    policy = args.policy if args.policy != "auto" else (
+        "warm_self" if wmode == Mode.FIXED_RATE else "cold")
+    cfg = StreamConfig(wdt, 4096, wmode, target, segment_blocks=args.segment_blocks,
+                       segment_policy=policy)
+    width = wdt.width_bytes
     enc = Encoder(n, cfg, device=dev)
-    dec = Decoder(n, Dtype.F32, 4096, device=dev)
+    dec = Decoder(n, wdt, 4096, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
     nbytes_dev = enc.status[2:3]
@@ -296,7 +371,7 @@ def main():
     else:
         total_container = nbytes
 
-    in_bytes = n * 4
+    in_bytes = n * width
     value = world * in_bytes / (mean_step * 1e-3) / 1e9
     enc_gbs = in_bytes / (mean_enc * 1e-3) / 1e9
     dec_gbs = in_bytes / (mean_dec * 1e-3) / 1e9
@@ -305,8 +380,10 @@ def main():
     alg_dec = nbytes + in_bytes + 8 * (enc.n_blocks + 1)   # read container + offsets, write y
     ach_enc = alg_enc / (mean_enc * 1e-3) / 1e9
     ach_dec = alg_dec / (mean_dec * 1e-3) / 1e9
-    dominant = "encode_v3_kernel<3" if mean_enc >= mean_dec else "decode_v3_kernel<3"
-    ach = ach_enc if mean_enc >= mean_dec else ach_dec
+    enc_k = (f"encode_v3_kernel<{wdt.wire_code}" if wdt.wire_code <= 3 else f"encode_v2_kernel<{wdt.wire_code}")
+    dec_k = (f"decode_v3_kernel<{wdt.wire_code}" if wdt.wire_code <= 3 else f"decode_v2_kernel<{wdt.wire_code}")
+    dominant = enc_k if mean_enc >= mean_dec else dec_k
+    ach = ach_enc if mean_enc >= mean_dec else ach_dec  # noqa: E501
 
     # ---- e2e: host buffers through the C-ABI entry points ----
     # Pinned host samples -> H2D -> apax_encode -> D2H container + block index
@@ -314,13 +391,13 @@ def main():
     # step, pipelined over chunks of whole segments on copy-in / compute /
     # copy-out streams (paper_1303_4994_b200/pipeline.py).
     e2e = None
-    if not args.no_e2e and not args.profile:
+    if not args.no_e2e and not args.profile and x_host is not None:
         from paper_1303_4994_b200.pipeline import HostRoundTrip
         rt = HostRoundTrip(n, cfg, chunks=args.e2e_chunks, device=dev)
         xh = torch.from_numpy(x_host).pin_memory()
         blob_h = torch.empty(rt.blob_d.numel(), dtype=torch.uint8).pin_memory()
         offs_h = torch.empty(enc.n_blocks + 1, dtype=torch.int64).pin_memory()
-        yh = torch.empty(n, dtype=torch.float32).pin_memory()
+        yh = torch.empty(n, dtype=x.dtype).pin_memory()
         e2e_steps = max(3, min(args.steps, 10))
         for _ in range(2):
             rt.run(xh, blob_h, offs_h, yh)
@@ -337,7 +414,7 @@ def main():
         # index-less decode of the host container (like decode_stream(bytes)):
         # H2D container -> K5 block discovery -> decode -> D2H samples
         blob_d = torch.zeros(rt.blob_d.numel(), dtype=torch.uint8, device=dev)
-        dec2 = Decoder(n, Dtype.F32, 4096, device=dev)
+        dec2 = Decoder(n, wdt, 4096, device=dev)
 
         def indexless():
             blob_d[:nb].copy_(blob_h[:nb], non_blocking=True)
@@ -372,10 +449,13 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
         threads = os.cpu_count() or 1
-        xs = x_host[:1 << 22]
-        r = cpu_round_trip(xs, target, args.segment_blocks, threads, budget_s=12.0)
+        ns = max(1, (1 << 22) // (args.segment_blocks * 4096)) * args.segment_blocks * 4096
+        xs = x[:ns].cpu().numpy()
+        r = cpu_round_trip(xs, target, args.segment_blocks, threads, budget_s=12.0,
+                           dt=wdt.wire_code, mode=wmode.value, policy=1 if policy == "warm_self" else 0)
         cpu = {"value": r["gbs"], "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"cfg2 first 2^22 samples (16 MiB) encode+decode x{r['reps']}, "
+               "sample": f"{args.workload} first {xs.size} samples ({xs.nbytes >> 20} MiB, whole "
+                         f"segments) encode+decode x{r['reps']}, "
                          f"C oracle (restatement of the reference), OpenMP over segments",
                "encode_gbs": r["enc_gbs"], "decode_gbs": r["dec_gbs"]}
 
@@ -384,15 +464,20 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32", "data": "synthetic",
+            "dtype": wdt.code, "data": "synthetic",
             "config": {
-                "workload": "cfg2: f32 AR(2) r=0.98 x1e3, 2^26 samples/GPU, fixed-quality at "
-                            f"the reference profiler's SRR target, {args.segment_blocks}-block cold segments, "
-                            "bs 4096; step = encode + decode (device-resident)",
+                "workload": WORKLOADS[args.workload] +
+                            (f" ({args.cfg5_dtype}, r={args.rate:g}, 2^{(n).bit_length() - 1} samples)"
+                             if args.workload == "cfg5" else "") +
+                            f"; {args.segment_blocks}-block {policy} segments, bs 4096; step = encode + "
+                            "decode (device-resident)",
+                "name": args.workload,
                 "n_samples_per_gpu": n, "block_size": 4096,
-                "segment_blocks": args.segment_blocks, "srr_target_db": target,
+                "segment_blocks": args.segment_blocks, "segment_policy": policy,
+                "mode": wmode.name, "target": target,
                 "parallelism": f"dp{world} (segment shards)",
-                "l2": "inputs (256 MiB) larger than L2; L2 flushed between encode and decode",
+                "l2": f"inputs ({in_bytes >> 20} MiB) {'larger' if in_bytes > (126 << 20) else 'smaller'} "
+                      "than L2; L2 flushed (256 MiB write) between encode and decode and after decode",
             },
             "encode_gbs": enc_gbs * world, "decode_gbs": dec_gbs * world,
             "encode_ms": mean_enc, "decode_ms": mean_dec,
@@ -403,7 +488,7 @@ def main():
                          "traffic_source": (_ncu_traffic(dominant) or {}).get("source"),
                          "kernel": dominant,
                          "peak_kind": peak_kind,
-                         "algorithmic_bytes_per_launch": alg_enc if dominant.startswith("enc") else alg_dec,
+                         "algorithmic_bytes_per_launch": alg_enc if dominant == enc_k else alg_dec,
                          "encode": {"achieved": ach_enc, "frac": ach_enc / peak},
                          "decode": {"achieved": ach_dec, "frac": ach_dec / peak}},
             "cpu_baseline": cpu,

@@ -32,7 +32,7 @@
 #include "apax_jee.cuh"
 
 #ifndef APAX_D3_MINB
-#define APAX_D3_MINB 3
+#define APAX_D3_MINB 4
 #endif
 
 namespace apax {

@@ -11,7 +11,7 @@ from __future__ import annotations
 import numpy as np
 
 __all__ = ["cfg1_sines_i16", "cfg2_ar2_f32", "cfg3_grf_f32", "cfg4_modes_f64",
-           "cfg5_ar1", "CFG2_TARGET_DB"]
+           "cfg4_modes_f64_np", "cfg5_ar1", "CFG2_TARGET_DB"]
 
 # FQ target for cfg2: the reference profiler's recommended SRR target
 # (profile(x, Dtype.F32)["recommended"]["srr_target"]) on the 2^20 analogue,
@@ -69,16 +69,57 @@ def cfg3_grf_f32(side: int = 8192, seed: int = 3) -> np.ndarray:
     return img.astype(np.float32).reshape(-1)
 
 
-def cfg4_modes_f64(side: int = 1024, seed: int = 4, n_modes: int = 64) -> np.ndarray:
+def cfg4_modes_f64(side: int = 1024, seed: int = 4, n_modes: int = 64, device=None):
     """float64 side^3 field: 64 modes A cos(2 pi k.r/side + phi), A ~ N(0,1),
-    k in [-8, 8]^3, phi ~ U(0, 2 pi), plus N(0, sigma=1e-4) (read as sigma)."""
+    k in [-8, 8]^3, phi ~ U(0, 2 pi), plus N(0, sigma=1e-4) (read as sigma).
+
+    Built as one f64 GEMM (cos(a + b) = cos a cos b - sin a sin b with a the
+    x term and b the (y, z) terms), so the full 8 GiB field is generated on
+    the GPU in milliseconds: returns a flat torch f64 tensor on `device`
+    (default cuda:0 when available, else CPU).  Mode parameters are
+    numpy-seeded; the noise comes from a seeded torch generator on the same
+    device, so the field is reproducible per device type."""
+    import torch
+    if device is None:
+        device = "cuda" if torch.cuda.is_available() else "cpu"
+    dev = torch.device(device)
+    rng = np.random.default_rng(seed)
+    A = torch.from_numpy(rng.standard_normal(n_modes)).to(dev)
+    K = torch.from_numpy(rng.integers(-8, 9, size=(n_modes, 3)).astype(np.float64)).to(dev)
+    phi = torch.from_numpy(rng.uniform(0, 2 * np.pi, n_modes)).to(dev)
+    r = torch.arange(side, dtype=torch.float64, device=dev) * (2 * np.pi / side)
+    ax = K[:, 0, None] * r[None, :] + phi[:, None]                     # [m, x]
+    C = torch.cat([torch.cos(ax), -torch.sin(ax)], 0)                 # [2m, x]
+    del ax
+    out = torch.empty(side * side, side, dtype=torch.float64, device=dev)
+    zc = max(1, min(side, (1 << 26) // (side * side) or 1))          # z planes per GEMM chunk
+    for z0 in range(0, side, zc):
+        z1 = min(side, z0 + zc)
+        byz = (K[None, None, :, 1] * r[None, :, None] +
+               K[None, None, :, 2] * r[z0:z1, None, None])            # [z, y, m]
+        B = torch.cat([A * torch.cos(byz), A * torch.sin(byz)], -1)   # [z, y, 2m]
+        out[z0 * side:z1 * side] = B.reshape(-1, 2 * n_modes) @ C
+        del byz, B
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    flat = out.reshape(-1)
+    chunk = 1 << 26
+    for i in range(0, flat.numel(), chunk):
+        seg = flat[i:i + chunk]
+        seg += torch.randn(seg.numel(), dtype=torch.float64, device=dev, generator=g) * 1e-4
+    return flat
+
+
+def cfg4_modes_f64_np(side: int, seed: int = 4, n_modes: int = 64) -> np.ndarray:
+    """numpy form of cfg4_modes_f64 for small sides (the golden fixtures in
+    tests/golden were generated with it): direct cos of the summed phase,
+    numpy N(0, 1e-4) noise."""
     rng = np.random.default_rng(seed)
     A = rng.standard_normal(n_modes)
     K = rng.integers(-8, 9, size=(n_modes, 3))
     phi = rng.uniform(0, 2 * np.pi, n_modes)
     r = np.arange(side, dtype=np.float64) * (2 * np.pi / side)
     out = np.empty((side, side, side), np.float64)
-    # separable: cos(a+b+c+phi) accumulated plane by plane
     for z in range(side):
         plane = np.zeros((side, side), np.float64)
         for m in range(n_modes):

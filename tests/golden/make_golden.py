@@ -201,7 +201,7 @@ def main():
     x1 = W.cfg1_sines_i16(1 << 16)
     x2 = W.cfg2_ar2_f32(1 << 16)
     x3 = W.cfg3_grf_f32(256)
-    x4 = W.cfg4_modes_f64(24)
+    x4 = W.cfg4_modes_f64_np(24)
     x5i = W.cfg5_ar1(1 << 15, "i32")
     x5f = W.cfg5_ar1(1 << 15, "f32")
     whole = [
