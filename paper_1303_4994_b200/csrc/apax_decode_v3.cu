@@ -645,7 +645,7 @@ size_t decode_v3_smem_bytes(int dt, int payload_cap) {
 }
 
 bool decode_v3_supported(int dt, int bs) {
-    return dt >= 0 && dt <= 3 && bs >= 128 && bs <= d3::MAXBS && (bs & (bs - 1)) == 0;
+    return dt >= 0 && dt <= 4 && bs >= 128 && bs <= d3::MAXBS && (bs & (bs - 1)) == 0;
 }
 
 template <int DT, bool FIX>
@@ -655,7 +655,8 @@ static void* d3_kernel(int dt, bool fix) {
         case 0: return d3_fn<0, false>();
         case 1: return fix ? d3_fn<1, true>() : d3_fn<1, false>();
         case 2: return fix ? d3_fn<2, true>() : d3_fn<2, false>();
-        default: return fix ? d3_fn<3, true>() : d3_fn<3, false>();
+        case 3: return fix ? d3_fn<3, true>() : d3_fn<3, false>();
+        default: return fix ? d3_fn<4, true>() : d3_fn<4, false>();
     }
 }
 
@@ -689,7 +690,7 @@ int launch_decode_v3(int dt, const DecParams& P, int grid, size_t smem, cudaStre
     const long long nseg = (P.n_blocks + P.segment_blocks - 1) / P.segment_blocks;
     // full-block segments take the compile-time-geometry kernel; the segment
     // holding a partial last block follows in a generic launch
-    const bool fixable = P.bs == d3::MAXBS && dt >= 1 && dt <= 3;
+    const bool fixable = P.bs == d3::MAXBS && dt >= 1 && dt <= 4;
     long long sfull = fixable ? nseg : 0;
     if (fixable && (P.n % d3::MAXBS) != 0) sfull = nseg - 1;
     if (sfull > 0) {

@@ -341,6 +341,16 @@ __device__ __forceinline__ double deq_of(double qd, double s, double rs) {
     return yi;
 }
 
+// quantize one sample (codec.py:94-132): rint(x * s) as the low word of
+// x*s + 1.5*2^52.  i8/i16/i32/f32 samples have <= 32-bit mantissas, so x*s is
+// exact in f64 and one fma suffices; f64 rounds the product first (the
+// reference's np.rint(x * scale)), then adds.
+template <int DT>
+__device__ __forceinline__ double qround(double xd, double sq) {
+    if (DT == 4) return __dadd_rn(__dmul_rn(xd, sq), kMagic);
+    return __fma_rn(xd, sq, kMagic);
+}
+
 // sum of x^2 over a partial (linear-layout) block, numpy order
 template <int DT>
 __device__ __noinline__ double cold_px(const typename DT_<DT>::T* xs, int n) {
@@ -700,7 +710,27 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
             // full blocks sit in the leaf layout: rows of 8*NL samples, stride RS
             const bool lay = TRL && n == bs;
             const int lgr = FIX ? 8 : 3 + __ffs(NL) - 1;   // log2(8 * NL)
-            if (DT == 3) {
+            if (DT == 4) {
+                // max |x| bit pattern (sign cleared; NaN/inf sort above every
+                // finite value), split into hi / lo words for the warp slots
+                const ulonglong2* x2 = (const ulonglong2*)xs;
+                unsigned long long m = 0;
+                const int n2 = n >> 1;
+                for (int i = tid; i < n2; i += NCT) {
+                    const int p2 = lay ? (((i >> (lgr - 1)) << 7) | (i & ((1 << (lgr - 1)) - 1))) : i;
+                    const ulonglong2 v = x2[p2];
+                    const unsigned long long a0 = v.x & 0x7fffffffffffffffull, a1 = v.y & 0x7fffffffffffffffull;
+                    m = a0 > m ? a0 : m;
+                    m = a1 > m ? a1 : m;
+                }
+                for (int i = (n2 << 1) + tid; i < n; i += NCT) {
+                    const unsigned long long a0 = (unsigned long long)__double_as_longlong((double)xs[i]) &
+                                                  0x7fffffffffffffffull;
+                    m = a0 > m ? a0 : m;
+                }
+                pk = (unsigned)(m >> 32);
+                pn = (unsigned)m;
+            } else if (DT == 3) {
                 const uint4* x4 = (const uint4*)xs;
                 int ms = 0;
                 unsigned mu = 0;
@@ -749,7 +779,12 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
             if (NL >= 4) r += __shfl_xor_sync(0xffffffffu, r, 16);
             pxs = r;
         }
-        if (NEED_PEAK) {
+        if (NEED_PEAK && DT == 4) {
+            // lanes holding the warp's largest hi word compete on the lo word
+            const unsigned hmax = __reduce_max_sync(0xffffffffu, pk);
+            pn = __reduce_max_sync(0xffffffffu, pk == hmax ? pn : 0u);
+            pk = hmax;
+        } else if (NEED_PEAK) {
             pk = (unsigned)__reduce_max_sync(0xffffffffu, (int)pk);
             pn = __reduce_max_sync(0xffffffffu, pn);
         }
@@ -825,13 +860,19 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
             if (tid == 32 && S->store_pending) { bulk_wait_read(); S->store_pending = 0; }
             if (tid == 0) {
                 unsigned pks = 0, pku = 0;
+                unsigned long long pk64 = 0;
                 for (int w = 0; w < NCW; w++) {
                     pks = max(pks, S->pkw[w]);
                     pku = max(pku, S->pnw[w]);
+                    const unsigned long long v = ((unsigned long long)S->pkw[w] << 32) | S->pnw[w];
+                    pk64 = v > pk64 ? v : pk64;
                 }
                 double peak;
                 bool nonfin = false;
-                if (F) {
+                if (DT == 4) {
+                    nonfin = pk64 >= 0x7ff0000000000000ull;
+                    peak = __longlong_as_double((long long)pk64);
+                } else if (F) {
                     // max |x| bit pattern from the signed / unsigned maxima
                     const unsigned pos = ((int)pks >= 0) ? pks : 0u;
                     const unsigned neg = (pku >= 0x80000000u) ? (pku & 0x7fffffffu) : 0u;
@@ -976,7 +1017,7 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
 #pragma unroll
                             for (int i = 0; i < 16; i++) {
                                 const double xd = xd_of<DT>(xp[TRL ? i * RS : 8 * i]);
-                                const double t = __fma_rn(xd, sq, kMagic);
+                                const double t = qround<DT>(xd, sq);
                                 qbuf[qb ^ (4 * ((2 * i) ^ (i >> 2)))] = __double2loint(t);
                                 const double qd = t - kMagic;
                                 const double y = idq ? qd : deq_of<DT>(qd, sd, rs);
@@ -1006,14 +1047,14 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
 #pragma unroll
                         for (int i = 0; i < 16; i++) {
                             const double xd = xd_of<DT>(xp[TRL ? i * RS : 8 * i]);
-                            const double t = __fma_rn(xd, sq, kMagic);
+                            const double t = qround<DT>(xd, sq);
                             qbuf[qb ^ (4 * ((2 * i) ^ (i >> 2)))] = __double2loint(t);
                         }
                     }
                 } else {
                     for (int i = tid; i < np; i += NCT) {
                         int q = 0;
-                        if (i < n) q = __double2loint(__fma_rn(xd_of<DT>(xs[i]), sq, kMagic));
+                        if (i < n) q = __double2loint(qround<DT>(xd_of<DT>(xs[i]), sq));
                         qbuf[qw(i)] = q;
                     }
                 }
@@ -1603,7 +1644,7 @@ int encode_v3_stage_bytes(int dt, int bs) {
 }
 
 bool encode_v3_supported(int dt, int bs) {
-    return dt >= 0 && dt <= 3 && bs >= 128 && bs <= v3::MAXBS && (bs & (bs - 1)) == 0;
+    return dt >= 0 && dt <= 4 && bs >= 128 && bs <= v3::MAXBS && (bs & (bs - 1)) == 0;
 }
 
 template <int DT, bool FIX>
@@ -1616,7 +1657,8 @@ static void* v3_kernel(int dt, bool fix, bool pw) {
         case 0: return v3_fn<0, false>(pw);
         case 1: return fix ? v3_fn<1, true>(pw) : v3_fn<1, false>(pw);
         case 2: return fix ? v3_fn<2, true>(pw) : v3_fn<2, false>(pw);
-        default: return fix ? v3_fn<3, true>(pw) : v3_fn<3, false>(pw);
+        case 3: return fix ? v3_fn<3, true>(pw) : v3_fn<3, false>(pw);
+        default: return fix ? v3_fn<4, true>(pw) : v3_fn<4, false>(pw);
     }
 }
 
@@ -1668,7 +1710,7 @@ int launch_encode_v3(int dt, const EncParams& P, int grid, size_t smem, cudaStre
     // compile-time-geometry kernel; the unit holding a partial last block
     // follows in a generic launch (its look-back reads the first launch's
     // published lengths)
-    const bool fixable = P.bs == v3::MAXBS && dt >= 1 && dt <= 3 && getenv("APAX_V3_NOFIX") == nullptr;
+    const bool fixable = P.bs == v3::MAXBS && dt >= 1 && dt <= 4 && getenv("APAX_V3_NOFIX") == nullptr;
     long long ufull = P.n_units;
     if (fixable && (P.n % v3::MAXBS) != 0) ufull = P.n_units - 1;
     if (!fixable) ufull = 0;
