@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
     __syncthreads();
 
     int kk = 0;   // blocks decoded by this CTA (buffer parity)
+    int jprev = NIB_PER_PASS;   // JEE nibbles of the previous block (first-pass length guess)
     for (long long sg = s_begin + blockIdx.x; sg < s_end; sg += gridDim.x) {
         const long long b0 = sg * P_seg;
         const long long b1 = (b0 + P_seg < P.n_blocks) ? b0 + P_seg : P.n_blocks;
@@ -218,8 +219,13 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                 const int total = 2 * nbj;
                 const int stotal = min(2 * staged, total);
                 int cbase = 0, vbase = 0;
-                for (int pass_base = 0;; pass_base += NIB_PER_PASS) {
+                // The first pass covers only a guess of the JEE length (1.25x the
+                // previous block's + 64 nibbles, whole warps); warps past it skip
+                // the parse.  A stream that runs longer simply takes more passes.
+                const int lim0 = min(NIB_PER_PASS, (jprev + (jprev >> 2) + 64 + 127) & ~127);
+                for (int pass_base = 0, span = lim0;; pass_base += span, span = NIB_PER_PASS) {
                     const int p0 = pass_base + 4 * tid;
+                    const bool wact = 128 * warp < span && pass_base + 128 * warp < stotal + 4;   // warp-uniform
                     auto nb = [&](int k) -> int {
                         if (k >= stotal) return 0;
                         const uint8_t bb = p[k >> 1];
@@ -228,6 +234,16 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                     // nibbles p0-4 .. p0+11 of the JEE stream in one 64-bit window
                     // (zero beyond the staged nibbles)
                     unsigned long long W = 0ULL;
+                    int skip = 0;
+                    bool stv[4] = {false, false, false, false};
+                    int kv[4] = {0, 0, 0, 0}, kab[4] = {0, 0, 0, 0};
+                    bool live = false;
+                    int c_i = 0, f_i = 0, v_i = 0;
+                    auto nw = [&](int k) -> int { return (int)((W >> (4 * (11 - k))) & 15ULL); };   // k in -4..11
+                    constexpr unsigned long long LUT_C = 0x43210cbaba9a98ull;
+                    constexpr unsigned long long LUT_D1 = 0x43210333222111ull;
+                    constexpr unsigned LUT_D2 = 0x24924u;
+                    if (wact) {
                     if (p0 - 4 < stotal) {   // (beyond: no nibbles, and no reads past the buffer)
                         const int byte0 = (int)pay_off + (p0 >> 1) - 2;   // pay_off >= HS >= 4
                         const uint32_t* pw = (const uint32_t*)pay;
@@ -238,10 +254,8 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                         const int rem = stotal - (p0 - 4);
                         if (rem < 16) W = rem <= 0 ? 0ULL : (W & (~0ULL << (4 * (16 - rem))));
                     }
-                    auto nw = [&](int k) -> int { return (int)((W >> (4 * (11 - k))) & 15ULL); };   // k in -4..11
                     // leading positions covered by an escape that started before p0:
                     // two consecutive non-15 nibbles are always followed by a token start
-                    int skip = 0;
                     if (p0 > 0 && p0 < stotal + 4) {
                         const bool f1 = nw(-1) == 15, f2 = nw(-2) == 15, f3 = nw(-3) == 15, f4 = nw(-4) == 15;
                         if (!f1 && !f2) skip = 0;
@@ -267,7 +281,7 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                     const bool st1 = skip == 1 || (st0 && !n0f);
                     const bool st2 = skip == 2 || (st1 && !n1f);
                     const bool st3 = (st2 && !n2f) || (st0 && n0f);
-                    const bool stv[4] = {st0, st1, st2, st3};
+                    stv[0] = st0; stv[1] = st1; stv[2] = st2; stv[3] = st3;
                     // Branch-free token summary (count, escape flag, running value)
                     // of the thread's starts from 16-entry nibble tables packed in
                     // immediates (entropy.py:118-164 token alphabet):
@@ -275,12 +289,8 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                     //   LUT_D1 first exponent's delta + 2;  LUT_D2 (2-bit) second delta + 1
                     // Reserved nibbles, unstaged positions and range errors only raise
                     // an error event (below); their contributions are never used.
-                    constexpr unsigned long long LUT_C = 0x43210cbaba9a98ull;
-                    constexpr unsigned long long LUT_D1 = 0x43210333222111ull;
-                    constexpr unsigned LUT_D2 = 0x24924u;
-                    const bool live = p0 < stotal + 4;   // any of this slice staged
+                    live = 4 * tid < span && p0 < stotal + 4;   // in this pass, any of the slice staged
                     int cnt = 0, flag = 0, val = 0;
-                    int kv[4], kab[4];
 #pragma unroll
                     for (int k = 0; k < 4; k++) {
                         const int v = nw(k);
@@ -297,7 +307,7 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                         flag |= (t && esc) ? 1 : 0;
                     }
                     // warp scan of (cnt, flag, val): A then B = (cA+cB, fA|fB, fB ? vB : vA+vB)
-                    int c_i = cnt, f_i = flag, v_i = val;
+                    c_i = cnt; f_i = flag; v_i = val;
 #pragma unroll
                     for (int d = 1; d < 32; d <<= 1) {
                         const int oc = __shfl_up_sync(0xffffffffu, c_i, d);
@@ -309,6 +319,7 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                             f_i |= of;
                         }
                     }
+                    }   // wact
                     if (lane == 31) { S->sc_cnt[warp] = c_i; S->sc_flag[warp] = f_i; S->sc_val[warp] = v_i; }
                     cbar();
                     // prefix over the previous warps (lanes 0..NW-1) and the previous pass
@@ -356,6 +367,7 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                     // first event (error, or the token that completes G exponents) as
                     // key = position << 1 | is_error
                     int key = 0x7fffffff;
+                    if (wact) {
 #pragma unroll
                     for (int k = 0; k < 4; k++) {
                         const int pos = p0 + k;
@@ -382,6 +394,7 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                         curv = t ? (joint ? e2 : e1) : curv;
                         idx += t ? nexp : 0;
                     }
+                    }   // wact
                     key = __reduce_min_sync(0xffffffffu, key);
                     if (lane == 0) S->ev_min[warp] = key;
                     cbar();
@@ -389,7 +402,7 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                     kmin = __reduce_min_sync(0xffffffffu, kmin);
                     int fallback = 0, fev;
                     if (kmin == 0x7fffffff) {
-                        if (pass_base + NIB_PER_PASS >= stotal) { fallback = 1; fev = -1; }
+                        if (pass_base + span >= stotal) { fallback = 1; fev = -1; }
                         else fev = -2;
                     } else if (kmin & 1) {
                         fallback = 1;
@@ -419,6 +432,7 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                 (void)total;
             }
             const int jee_bytes = (used + 1) >> 1;
+            if (!err) jprev = used;
             // ---- mantissa offsets (entropy.py:209-219): CTA scan of 4*sum(e) ----
             const int g0 = 4 * tid;
             const bool active = FIX ? true : (g0 < G);

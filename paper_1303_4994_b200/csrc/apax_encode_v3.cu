@@ -50,8 +50,19 @@
 #define APAX_V3_MINB 3
 #endif
 
+
 namespace apax {
 namespace v3 {
+#ifdef APAX_V3_TIMES
+// per-CTA timeline (tools/cta_times.py): globaltimer at start, at the end of
+// the last unit's coding, at exit; SM id
+__device__ unsigned long long g_times[8192 * 4];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
 
 constexpr int NCW = 8;             // compute warps
 constexpr int NCT = NCW * 32;      // compute threads
@@ -491,6 +502,8 @@ __device__ __forceinline__ long long unit_prefix(unsigned long long* lookback, l
     const int lane = threadIdx.x & 31;
     long long prefix = 0;
     long long kk = u - 1;
+    unsigned nap = 256;   // exponential back-off: a waiting warp must not steal
+                          // issue slots from the CTAs still coding (one-wave tails)
     for (;;) {
         const long long idx = kk - lane;
         const unsigned long long v = (idx >= 0) ? ld_acquire(&lookback[idx]) : kFlagInc;
@@ -500,7 +513,8 @@ __device__ __forceinline__ long long unit_prefix(unsigned long long* lookback, l
         const int first_inc = inc ? __ffs(inc) - 1 : 32;
         const unsigned need = first_inc >= 31 ? 0xffffffffu : ((2u << first_inc) - 1u);
         if (nrd & need) {
-            __nanosleep(400);
+            __nanosleep(nap);
+            nap = nap < 4096 ? 2 * nap : 4096;
             continue;
         }
         unsigned long long part = (lane <= first_inc) ? (v & kValMask) : 0ULL;
@@ -621,6 +635,14 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
     uint8_t* slot0 = P.slots + (long long)blockIdx.x * (PW ? 2 : 1) * P.slot_bytes;
     uint8_t* slot1 = slot0 + P.slot_bytes;
 
+#ifdef APAX_V3_TIMES
+    if (tid == 0 && blockIdx.x < 8192) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+        g_times[4 * blockIdx.x] = gtimer();
+        g_times[4 * blockIdx.x + 3] = smid;
+    }
+#endif
     if (tid == 0) {
         mbar_init_n(&S->mb_stage[0], NCT);
         mbar_init_n(&S->mb_stage[1], NCT);
@@ -1614,10 +1636,16 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
             for (int k2 = 0; k2 < 8; k2++) h[20 + k2] = (unsigned char)(tb >> (8 * k2));
             P.out[tid] = h[tid];
         }
+#ifdef APAX_V3_TIMES
+        if (last_unit && tid == 0 && blockIdx.x < 8192) g_times[4 * blockIdx.x + 1] = gtimer();
+#endif
         if (last_unit)
             final_place<PW ? NT : NCT>(u, sl, P.n_units, P.n_blocks, P.lookback, P.status, P.block_offsets, P.out,
                                        S, slot);
     }
+#ifdef APAX_V3_TIMES
+    if (tid == 0 && blockIdx.x < 8192) g_times[4 * blockIdx.x + 2] = gtimer();
+#endif
 #ifdef APAX_V3_PROF
     if (tid == 0 && P.trace) {
         const long long c_ = clock64();
@@ -1628,6 +1656,12 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
 }
 
 }  // namespace v3
+
+#ifdef APAX_V3_TIMES
+extern "C" int apax_debug_cta_times(unsigned long long* host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, v3::g_times, (size_t)n * 4 * sizeof(unsigned long long));
+}
+#endif
 
 size_t encode_v3_smem_bytes(int dt, int bs, int stage_bytes) {
     (void)dt; (void)bs;
