@@ -611,6 +611,16 @@ __device__ __noinline__ void final_place(long long u, int sl, long long n_units,
 // PW: a placement warp places finished units while the next ones are coded
 // (more units than resident CTAs).  Without it (one-wave launches: one unit
 // per CTA) the CTA is 256 threads and four fit on an SM.
+constexpr int fix_stage_bytes(int dt) {
+    // encode_v3_stage_bytes(dt, MAXBS): max(MAXBS * width, max block bytes + 32), 128-aligned
+    const int w = dt == 0 ? 1 : (dt == 1 ? 2 : (dt == 4 ? 8 : 4));
+    const int g = MAXBS / 4;
+    const int emax = dt >= 3 ? 34 : (8 * w + 2 < 34 ? 8 * w + 2 : 34);
+    const int mb = (dt >= 3 ? 6 : 4) + (3 * g + 1) / 2 + (4 * emax * g + 7) / 8 + 32;
+    const int xb = MAXBS * w;
+    return ((xb > mb ? xb : mb) + 127) & ~127;
+}
+
 template <int DT, bool FIX, bool PW>
 __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MINB_NP) encode_v3_kernel(EncParams P) {
     using Tr = DT_<DT>;
@@ -627,7 +637,10 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
     const int bs = FIX ? MAXBS : P.bs;
     const int NL = FIX ? 32 : (bs >> 7);        // leaves of a full block
     const bool FQ = (P.mode == 2);
-    const int XB = P.stage_bytes;               // bytes per staging buffer
+    // bytes per staging buffer: a compile-time constant for the bs-4096
+    // instantiation (encode_v3_stage_bytes), so every shared-memory address
+    // folds into an immediate offset instead of being rematerialised
+    const int XB = FIX ? fix_stage_bytes(DT) : P.stage_bytes;
 
     St* S = (St*)smem;
     const int xoff = (int)((sizeof(St) + 127) & ~(size_t)127);
@@ -1740,6 +1753,7 @@ static int launch_v3_range(int dt, bool fix, const EncParams& P, long long u0, l
 }
 
 int launch_encode_v3(int dt, const EncParams& P, int grid, size_t smem, cudaStream_t st) {
+    if (P.bs == v3::MAXBS && P.stage_bytes != v3::fix_stage_bytes(dt)) return APAX_ERR_INTERNAL;
     // bs 4096 (i16/i32/f32): units made only of full blocks take the
     // compile-time-geometry kernel; the unit holding a partial last block
     // follows in a generic launch (its look-back reads the first launch's
