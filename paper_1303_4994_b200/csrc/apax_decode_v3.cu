@@ -474,54 +474,22 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                 cbar();
                 continue;
             }
-            // ---- unpack 16 values ----
-            long long q[SPT];
-            {
-                const uint32_t* w = (const uint32_t*)pay;
-                int bp = 8 * ((int)pay_off + jee_bytes) + (int)bpre;
-                const unsigned wmax4 = epk;   // bytes: widths
-                const unsigned wm = max(max(wmax4 & 0xffu, (wmax4 >> 8) & 0xffu),
-                                        max((wmax4 >> 16) & 0xffu, wmax4 >> 24));
-                if (!__any_sync(0xffffffffu, wm > 16)) {
-                    // every group of the warp fits two 32-bit windows
-#pragma unroll
-                    for (int g = 0; g < 4; g++) {
-                        const int wd = (int)((epk >> (8 * g)) & 0xffu);
-                        const uint32_t c0 = r32(w, bp), c1 = r32(w, bp + 2 * wd);
-                        q[4 * g + 0] = wd ? bfe_s(c0, 32 - wd, wd) : 0;
-                        q[4 * g + 1] = wd ? bfe_s(c0, 32 - 2 * wd, wd) : 0;
-                        q[4 * g + 2] = wd ? bfe_s(c1, 32 - wd, wd) : 0;
-                        q[4 * g + 3] = wd ? bfe_s(c1, 32 - 2 * wd, wd) : 0;
-                        bp += 4 * wd;
-                    }
-                } else {
-#pragma unroll
-                    for (int g = 0; g < 4; g++) {
-                        const int wd = (int)((epk >> (8 * g)) & 0xffu);
-#pragma unroll
-                        for (int k = 0; k < 4; k++) {
-                            const int pb = bp + k * wd;
-                            if (wd == 0) q[4 * g + k] = 0;
-                            else if (wd <= 32) q[4 * g + k] = bfe_s(r32(w, pb), 32 - wd, wd);
-                            else {
-                                const unsigned long long hi = ((unsigned long long)r32(w, pb) << 32) | r32(w, pb + 32);
-                                q[4 * g + k] = (long long)hi >> (64 - wd);
-                            }
-                        }
-                        bp += 4 * wd;
-                    }
-                }
-            }
-            // ---- reconstruct (transform.py:116-129) ----
+            // ---- unpack, reconstruct, dequantize ----
+            const unsigned wm = max(max(epk & 0xffu, (epk >> 8) & 0xffu), max((epk >> 16) & 0xffu, epk >> 24));
+            // warp-uniform: every group width <= 16, so |v| < 2^15 and the
+            // thread sums below are exact in 32 bits
+            const bool narrow = !__any_sync(0xffffffffu, wm > 16);
             const long long p1 = S->p1, p2 = S->p2;
             const unsigned long long h1 = restart ? 0ULL : (unsigned long long)p1;
             const unsigned long long h2 = restart ? 0ULL : (unsigned long long)p2;
-            if (sel >= 1) {
-                // thread sums: s = sum v, t = sum of local partial sums; ranges
-                // compose as (s, t, m): A then B = (sA+sB, tA+tB+mB*sA, mA+mB)
-                unsigned long long s = 0, t = 0;
-#pragma unroll
-                for (int i = 0; i < SPT; i++) { s += (unsigned long long)q[i]; t += s; }
+            const int i0 = SPT * tid;
+            const int j1 = (np - 1) % SPT;            // outgoing history: q[np-1], q[np-2] (padded block)
+            const bool hist_thread = tid == (np - 1) / SPT;
+            // CTA exclusive prefix of the thread aggregates (s = sum v, t = sum of
+            // local partial sums); ranges compose as (s, t, m): A then B =
+            // (sA+sB, tA+tB+mB*sA, mA+mB) (transform.py:116-129 as a scan)
+            auto recon_scan = [&](unsigned long long s, unsigned long long t, unsigned long long& ps,
+                                  unsigned long long& pt) {
                 unsigned long long xs = s, xt = t;
                 unsigned xm = SPT;
 #pragma unroll
@@ -533,95 +501,164 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                 }
                 if (lane == 31) { S->rs_w[warp] = (long long)xs; S->rt_w[warp] = (long long)xt; }
                 cbar();
-                // prefix over the previous warps (each spans 32 x 16 samples)
-                unsigned long long ps, pt;
-                {
-                    unsigned long long ws = (lane < NW) ? (unsigned long long)S->rs_w[lane & (NW - 1)] : 0ULL;
-                    unsigned long long wt = (lane < NW) ? (unsigned long long)S->rt_w[lane & (NW - 1)] : 0ULL;
-                    unsigned wm = 32 * SPT;
+                unsigned long long ws = (lane < NW) ? (unsigned long long)S->rs_w[lane & (NW - 1)] : 0ULL;
+                unsigned long long wt = (lane < NW) ? (unsigned long long)S->rt_w[lane & (NW - 1)] : 0ULL;
+                unsigned wmm = 32 * SPT;
 #pragma unroll
-                    for (int d = 1; d < NW; d <<= 1) {
-                        const unsigned long long os = __shfl_up_sync(0xffffffffu, ws, d);
-                        const unsigned long long ot = __shfl_up_sync(0xffffffffu, wt, d);
-                        const unsigned om = __shfl_up_sync(0xffffffffu, wm, d);
-                        if (lane >= d) { wt = ot + wt + (unsigned long long)wm * os; ws += os; wm += om; }
-                    }
-                    unsigned long long es = __shfl_up_sync(0xffffffffu, ws, 1);
-                    unsigned long long et = __shfl_up_sync(0xffffffffu, wt, 1);
-                    if (lane == 0) { es = 0; et = 0; }
-                    const unsigned long long pws = __shfl_sync(0xffffffffu, es, warp);
-                    const unsigned long long pwt = __shfl_sync(0xffffffffu, et, warp);
-                    // then the lanes before this one inside the warp
-                    unsigned long long ls = __shfl_up_sync(0xffffffffu, xs, 1);
-                    unsigned long long lt = __shfl_up_sync(0xffffffffu, xt, 1);
-                    unsigned lm = __shfl_up_sync(0xffffffffu, xm, 1);
-                    if (lane == 0) { ls = 0; lt = 0; lm = 0; }
-                    ps = pws + ls;
-                    pt = pwt + lt + (unsigned long long)lm * pws;
+                for (int d = 1; d < NW; d <<= 1) {
+                    const unsigned long long os = __shfl_up_sync(0xffffffffu, ws, d);
+                    const unsigned long long ot = __shfl_up_sync(0xffffffffu, wt, d);
+                    const unsigned om = __shfl_up_sync(0xffffffffu, wmm, d);
+                    if (lane >= d) { wt = ot + wt + (unsigned long long)wmm * os; ws += os; wmm += om; }
                 }
-                // history: d1 entering the block = p1 - p2; q entering = p1
-                const int i0 = SPT * tid;
-                if (sel == 1) {
-                    unsigned long long acc = h1 + ps;
-#pragma unroll
-                    for (int i = 0; i < SPT; i++) { acc += (unsigned long long)q[i]; q[i] = (long long)acc; }
+                unsigned long long es = __shfl_up_sync(0xffffffffu, ws, 1);
+                unsigned long long et = __shfl_up_sync(0xffffffffu, wt, 1);
+                if (lane == 0) { es = 0; et = 0; }
+                const unsigned long long pws = __shfl_sync(0xffffffffu, es, warp);
+                const unsigned long long pwt = __shfl_sync(0xffffffffu, et, warp);
+                unsigned long long ls = __shfl_up_sync(0xffffffffu, xs, 1);
+                unsigned long long lt = __shfl_up_sync(0xffffffffu, xt, 1);
+                unsigned lm = __shfl_up_sync(0xffffffffu, xm, 1);
+                if (lane == 0) { ls = 0; lt = 0; lm = 0; }
+                ps = pws + ls;
+                pt = pwt + lt + (unsigned long long)lm * pws;
+            };
+            // dequantize one reconstructed sample (codec.py:135-146): Markstein
+            // quotient against a per-block reciprocal, bit-identical to IEEE
+            // division (profiles/r1_markstein_division_check.txt)
+            double dq_s = 1.0, dq_r = 1.0;
+            if (Tr::F) {
+                dq_s = decode_scale_code(code) * ldexp(1.0, fbe);
+                dq_r = __ddiv_rn(1.0, dq_s);
+            } else {
+                dq_s = decode_scale_code(code);
+                dq_r = __ddiv_rn(1.0, dq_s);
+            }
+            auto deq = [&](double r) -> T {
+                if (Tr::F) {
+                    const double y0 = r * dq_r;
+                    const double ee = __fma_rn(-dq_s, y0, r);
+                    return (T)__fma_rn(ee, dq_r, y0);
                 } else {
-                    unsigned long long d1 = (h1 - h2) + ps;
-                    unsigned long long acc = h1 + (unsigned long long)i0 * (h1 - h2) + pt;
+                    long long yi = (long long)r;
+                    if (dq_s != 1.0) {
+                        const double y0 = r * dq_r;
+                        const double ee = __fma_rn(-dq_s, y0, r);
+                        yi = f2i64(rint(__fma_rn(ee, dq_r, y0)));
+                    }
+                    yi = yi < Tr::LO ? Tr::LO : (yi > Tr::HI ? Tr::HI : yi);
+                    return (T)yi;
+                }
+            };
+            auto i2d = [](int v) -> double { return __hiloint2double(0x43380000, v ^ (int)0x80000000) - kMagicI; };
+            T out[SPT];
+            const uint32_t* w = (const uint32_t*)pay;
+            int bp = 8 * ((int)pay_off + jee_bytes) + (int)bpre;
+            if (narrow) {
+                int v[SPT];
+#pragma unroll
+                for (int g = 0; g < 4; g++) {   // two 32-bit windows per group
+                    const int wd = (int)((epk >> (8 * g)) & 0xffu);
+                    const uint32_t c0 = r32(w, bp), c1 = r32(w, bp + 2 * wd);
+                    v[4 * g + 0] = wd ? bfe_s(c0, 32 - wd, wd) : 0;
+                    v[4 * g + 1] = wd ? bfe_s(c0, 32 - 2 * wd, wd) : 0;
+                    v[4 * g + 2] = wd ? bfe_s(c1, 32 - wd, wd) : 0;
+                    v[4 * g + 3] = wd ? bfe_s(c1, 32 - 2 * wd, wd) : 0;
+                    bp += 4 * wd;
+                }
+                unsigned long long q0 = 0, d0 = 0;   // q and d1 entering this thread (exact, 64-bit)
+                if (sel >= 1) {
+                    int s32 = 0, t32 = 0;
+#pragma unroll
+                    for (int i = 0; i < SPT; i++) { s32 += v[i]; t32 += s32; }
+                    unsigned long long ps, pt;
+                    recon_scan((unsigned long long)(long long)s32, (unsigned long long)(long long)t32, ps, pt);
+                    if (sel == 1) {
+                        q0 = h1 + ps;
+                    } else {
+                        d0 = (h1 - h2) + ps;
+                        q0 = h1 + (unsigned long long)i0 * (h1 - h2) + pt;
+                    }
+                }
+                // the 16 outputs stay inside int32 when |q0| + 16|d0| + 136 * 2^15 < 2^31:
+                // then 32-bit wrap-around arithmetic gives the exact values
+                const long long aq = (long long)q0 < 0 ? -(long long)q0 : (long long)q0;
+                const long long ad = (long long)d0 < 0 ? -(long long)d0 : (long long)d0;
+                const bool fits = sel == 0 || (aq < (1LL << 30) && ad < (1LL << 24));
+                if (fits) {
+                    int qa = (int)q0, da = (int)d0;
 #pragma unroll
                     for (int i = 0; i < SPT; i++) {
-                        d1 += (unsigned long long)q[i];
-                        acc += d1;
-                        q[i] = (long long)acc;
+                        int qv;
+                        if (sel == 0) qv = v[i];
+                        else if (sel == 1) { qa += v[i]; qv = qa; }
+                        else { da += v[i]; qa += da; qv = qa; }
+                        if (hist_thread && i == j1) S->p1 = qv;
+                        if (hist_thread && i == j1 - 1) S->p2 = qv;
+                        out[i] = deq(i2d(qv));
+                    }
+                } else {
+                    unsigned long long qa = q0, da = d0;
+#pragma unroll
+                    for (int i = 0; i < SPT; i++) {
+                        long long qv;
+                        if (sel == 1) { qa += (unsigned long long)(long long)v[i]; qv = (long long)qa; }
+                        else { da += (unsigned long long)(long long)v[i]; qa += da; qv = (long long)qa; }
+                        if (hist_thread && i == j1) S->p1 = qv;
+                        if (hist_thread && i == j1 - 1) S->p2 = qv;
+                        out[i] = deq((double)qv);
                     }
                 }
-            }
-            // outgoing history: q[np-1], q[np-2] (padded block)
-            if (tid == (np - 1) / SPT) {
-                const int j1 = (np - 1) % SPT;
+            } else {
+                long long q[SPT];
+#pragma unroll
+                for (int g = 0; g < 4; g++) {
+                    const int wd = (int)((epk >> (8 * g)) & 0xffu);
+#pragma unroll
+                    for (int k = 0; k < 4; k++) {
+                        const int pb = bp + k * wd;
+                        if (wd == 0) q[4 * g + k] = 0;
+                        else if (wd <= 32) q[4 * g + k] = bfe_s(r32(w, pb), 32 - wd, wd);
+                        else {
+                            const unsigned long long hi = ((unsigned long long)r32(w, pb) << 32) | r32(w, pb + 32);
+                            q[4 * g + k] = (long long)hi >> (64 - wd);
+                        }
+                    }
+                    bp += 4 * wd;
+                }
+                if (sel >= 1) {
+                    unsigned long long s = 0, t = 0;
+#pragma unroll
+                    for (int i = 0; i < SPT; i++) { s += (unsigned long long)q[i]; t += s; }
+                    unsigned long long ps, pt;
+                    recon_scan(s, t, ps, pt);
+                    if (sel == 1) {
+                        unsigned long long acc = h1 + ps;
+#pragma unroll
+                        for (int i = 0; i < SPT; i++) { acc += (unsigned long long)q[i]; q[i] = (long long)acc; }
+                    } else {
+                        unsigned long long d1 = (h1 - h2) + ps;
+                        unsigned long long acc = h1 + (unsigned long long)i0 * (h1 - h2) + pt;
+#pragma unroll
+                        for (int i = 0; i < SPT; i++) {
+                            d1 += (unsigned long long)q[i];
+                            acc += d1;
+                            q[i] = (long long)acc;
+                        }
+                    }
+                }
 #pragma unroll
                 for (int i = 0; i < SPT; i++) {
-                    if (i == j1) S->p1 = q[i];
-                    if (i == j1 - 1) S->p2 = q[i];
+                    if (hist_thread && i == j1) S->p1 = q[i];
+                    if (hist_thread && i == j1 - 1) S->p2 = q[i];
+                    const long long qv = q[i];
+                    out[i] = deq(qv == (long long)(int)qv ? i2d((int)qv) : (double)qv);
                 }
-                if (j1 == 0) S->p2 = 0;   // np is a multiple of 4: never happens
             }
-            // ---- dequantize (codec.py:135-146) into the y buffer ----
+            // ---- y staged in shared memory, one TMA bulk store per block ----
             if (tid == 0 && S->store_pending) { bulk_wait_read(); S->store_pending = 0; }
-            cbar();   // p1/p2 readers are done with the old values; y buffer free
+            cbar();   // the previous block's store has read the y buffer
             if (active) {
-                T out[SPT];
-                if (Tr::F) {
-                    const double s = decode_scale_code(code) * ldexp(1.0, fbe);
-                    const double rs = __ddiv_rn(1.0, s);
-#pragma unroll
-                    for (int i = 0; i < SPT; i++) {
-                        const long long qv = q[i];
-                        double r;
-                        if (qv == (long long)(int)qv)
-                            r = __hiloint2double(0x43380000, (int)qv ^ (int)0x80000000) - kMagicI;
-                        else
-                            r = (double)qv;
-                        const double y0 = r * rs;
-                        const double ee = __fma_rn(-s, y0, r);
-                        out[i] = (T)__fma_rn(ee, rs, y0);
-                    }
-                } else {
-                    const double a = decode_scale_code(code);
-                    const double ra = __ddiv_rn(1.0, a);
-#pragma unroll
-                    for (int i = 0; i < SPT; i++) {
-                        long long yi = q[i];
-                        if (a != 1.0) {
-                            const double r = (double)q[i];
-                            const double y0 = r * ra;
-                            const double ee = __fma_rn(-a, y0, r);
-                            yi = f2i64(rint(__fma_rn(ee, ra, y0)));
-                        }
-                        yi = yi < Tr::LO ? Tr::LO : (yi > Tr::HI ? Tr::HI : yi);
-                        out[i] = (T)yi;
-                    }
-                }
                 constexpr int PER = 16 / (int)sizeof(T);
                 uint4* y4 = (uint4*)(ybuf + SPT * tid);
 #pragma unroll
