@@ -586,17 +586,25 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                 const long long ad = (long long)d0 < 0 ? -(long long)d0 : (long long)d0;
                 const bool fits = sel == 0 || (aq < (1LL << 30) && ad < (1LL << 24));
                 if (fits) {
-                    int qa = (int)q0, da = (int)d0;
+                    // selector-specialised loops (a per-sample select costs as much as the sums)
+                    if (sel == 1) {
+                        int qa = (int)q0;
 #pragma unroll
-                    for (int i = 0; i < SPT; i++) {
-                        int qv;
-                        if (sel == 0) qv = v[i];
-                        else if (sel == 1) { qa += v[i]; qv = qa; }
-                        else { da += v[i]; qa += da; qv = qa; }
-                        if (hist_thread && i == j1) S->p1 = qv;
-                        if (hist_thread && i == j1 - 1) S->p2 = qv;
-                        out[i] = deq(i2d(qv));
+                        for (int i = 0; i < SPT; i++) { qa += v[i]; v[i] = qa; }
+                    } else if (sel == 2) {
+                        int qa = (int)q0, da = (int)d0;
+#pragma unroll
+                        for (int i = 0; i < SPT; i++) { da += v[i]; qa += da; v[i] = qa; }
                     }
+                    if (hist_thread) {
+#pragma unroll
+                        for (int i = 0; i < SPT; i++) {
+                            if (i == j1) S->p1 = v[i];
+                            if (i == j1 - 1) S->p2 = v[i];
+                        }
+                    }
+#pragma unroll
+                    for (int i = 0; i < SPT; i++) out[i] = deq(i2d(v[i]));
                 } else {
                     unsigned long long qa = q0, da = d0;
 #pragma unroll
