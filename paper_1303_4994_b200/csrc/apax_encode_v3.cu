@@ -1035,6 +1035,20 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
             const bool wide = S->wide;
             const int hp1 = (int)S->p1, hp2 = (int)S->p2;
 
+            // quality loop (codec.py:244-252, 179-189).  Full blocks run it on
+            // thread 0 just before B5 (its inputs are the warp partials, its
+            // output feeds the next S1), where warp 0 would otherwise wait
+            // for the slowest phase-D warp; partial blocks read xs here,
+            // before the window zeroing overwrites it.
+            auto fq_update = [&](double px, double pd) {
+                const double pxm = px / (double)n, pdm = pd / (double)n;
+                if (pxm > 0.0) {
+                    const double measured = (pdm == 0.0) ? INFINITY : 10.0 * log10(pxm / pdm);
+                    if (isfinite(measured))
+                        S->att = clamp_att(S->att - clamp_step(0.5 * (measured - P.target)), P.att_lo);
+                }
+                S->a = att_to_a(S->att);
+            };
             // ============ phase B: quantize (+ fixed-quality powers) ============
             {
                 const double sq = S->sq;
@@ -1095,25 +1109,12 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
                 }
                 cbar();  // B3
                 PROF_MARK(2);
-                if (fq_emit && tid == 0) {
-                    // quality loop (codec.py:244-252, 179-189)
-                    double px, pd;
-                    if (regular) {
-                        pd = warp_tree(S->pdw, (NL + 3) / 4);
-                        px = warp_tree(S->pxbw, (NL + 3) / 4);
-                    } else {
-                        px = cold_px<DT>(xs, n);
-                        pd = cold_pd<DT>(xs, qbuf, n, F ? S->s : S->aq, F ? S->rs : S->ra, !F && S->aq == 1.0);
-                    }
-                    const double pxm = px / (double)n, pdm = pd / (double)n;
-                    if (pxm > 0.0) {
-                        const double measured = (pdm == 0.0) ? INFINITY : 10.0 * log10(pxm / pdm);
-                        if (isfinite(measured))
-                            S->att = clamp_att(S->att - clamp_step(0.5 * (measured - P.target)), P.att_lo);
-                    }
-                    S->a = att_to_a(S->att);
+                if (fq_emit && !regular) {
+                    if (tid == 0)
+                        fq_update(cold_px<DT>(xs, n),
+                                  cold_pd<DT>(xs, qbuf, n, F ? S->s : S->aq, F ? S->rs : S->ra, !F && S->aq == 1.0));
+                    cbar();  // thread 0 read xs; the window zeroing follows
                 }
-                if (fq_emit && !regular) cbar();  // thread 0 read xs; the window zeroing follows
             }
 
             // ============ phase C: streams, widths, costs, JEE structure ============
@@ -1426,19 +1427,6 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
                     S->blen = blen;
                     S->tl_next = (int)((wb + blen) & 15);
                     S->gate = gate;
-                    if (P.mode == 1) {
-                        const long long g4 = 4LL * G;
-                        if (S->emitted == 0) {
-                            long long mn = tt0 < tt1 ? tt0 : tt1;
-                            mn = tt2 < mn ? tt2 : mn;
-                            const double bps0 = (double)(4 * mn + g4 + 8LL * HS) / (double)bs;
-                            S->att = clamp_att(S->att - 6.02 * (bps0 - P.target), P.att_lo);
-                        } else {
-                            const double err = (double)(blen * 8) / (double)bs - P.target;
-                            S->att = clamp_att(S->att - clamp_step(0.75 * err), P.att_lo);
-                        }
-                        S->a = att_to_a(S->att);
-                    }
                 }
                 const int bad = S->bad;
                 // ============ phase D: JEE tokens + mantissas into the window ============
@@ -1573,6 +1561,23 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
                         a_done = nb;
                     }
                 }
+            }
+            if (fq_emit && regular && tid == 0)
+                fq_update(warp_tree(S->pxbw, (NL + 3) / 4), warp_tree(S->pdw, (NL + 3) / 4));
+            if (emit && P.mode == 1 && tid == 0) {
+                // rate loop (codec.py:228-243) on this block's exact byte count;
+                // like the quality loop it only feeds the next S1
+                const long long g4 = 4LL * G;
+                if (S->emitted == 0) {
+                    long long mn = tt0 < tt1 ? tt0 : tt1;
+                    mn = tt2 < mn ? tt2 : mn;
+                    const double bps0 = (double)(4 * mn + g4 + 8LL * HS) / (double)bs;
+                    S->att = clamp_att(S->att - 6.02 * (bps0 - P.target), P.att_lo);
+                } else {
+                    const double err = (double)(S->blen * 8) / (double)bs - P.target;
+                    S->att = clamp_att(S->att - clamp_step(0.75 * err), P.att_lo);
+                }
+                S->a = att_to_a(S->att);
             }
             if (emit) fence_proxy_async();  // window writes -> async proxy (bulk store)
             cbar();  // B5
