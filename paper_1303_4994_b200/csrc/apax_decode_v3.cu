@@ -222,7 +222,10 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                 // The first pass covers only a guess of the JEE length (1.25x the
                 // previous block's + 64 nibbles, whole warps); warps past it skip
                 // the parse.  A stream that runs longer simply takes more passes.
-                const int lim0 = min(NIB_PER_PASS, (jprev + (jprev >> 2) + 64 + 127) & ~127);
+#ifndef APAX_D3_JEE_SLACK
+#define APAX_D3_JEE_SLACK 4   // first-pass length: previous JEE length x (1 + 2^-SLACK) + 64 nibbles
+#endif
+                const int lim0 = min(NIB_PER_PASS, (jprev + (jprev >> APAX_D3_JEE_SLACK) + 64 + 127) & ~127);
                 for (int pass_base = 0, span = lim0;; pass_base += span, span = NIB_PER_PASS) {
                     const int p0 = pass_base + 4 * tid;
                     const bool wact = 128 * warp < span && pass_base + 128 * warp < stotal + 4;   // warp-uniform
@@ -378,18 +381,22 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                         const bool joint = !esc && (cd >> 3) != 0;
                         const int e1 = esc ? kab[k] : curv + (int)((LUT_D1 >> (4 * v)) & 15ull) - 2;
                         const int e2 = e1 + (int)((LUT_D2 >> (2 * v)) & 3u) - 1;
-                        bool bad = pos >= stotal || v == 14;
-                        bad |= esc && pos + 2 >= stotal;
-                        bad |= !esc && idx == 0;                     // stream must open with an escape
-                        bad |= (unsigned)e1 > 34u;
-                        bad |= joint && (idx + 1 >= G || (unsigned)e2 > 34u);
+                        // any irregularity (truncation, reserved nibble 14, a stream
+                        // not opening with an escape, an exponent outside [0, 34],
+                        // a joint token past the last group) makes the whole block
+                        // re-run the exact serial parser, which reports the
+                        // reference's first error: one flag is enough (key 1 sorts
+                        // before every completion key), and the exponents written
+                        // here are then rewritten (ebuf has G + 128 bytes)
+                        const bool bad = (pos + (esc ? 2 : 0) >= stotal) | (v == 14) | (!esc & (idx == 0)) |
+                                         ((unsigned)e1 > 34u) | (joint & ((idx + 1 >= G) | ((unsigned)e2 > 34u)));
                         const int nexp = joint ? 2 : 1;
                         const bool done = idx + nexp >= G;
-                        if (t && !bad) {
+                        if (t) {
                             ebuf[idx] = (uint8_t)e1;
                             if (joint) ebuf[idx + 1] = (uint8_t)e2;
                         }
-                        const int kk2 = bad ? ((pos << 1) | 1) : (done ? ((pos + (esc ? 3 : 1)) << 1) : 0x7fffffff);
+                        const int kk2 = bad ? 1 : (done ? ((pos + (esc ? 3 : 1)) << 1) : 0x7fffffff);
                         key = t ? min(key, kk2) : key;
                         curv = t ? (joint ? e2 : e1) : curv;
                         idx += t ? nexp : 0;

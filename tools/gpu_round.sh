@@ -1,10 +1,12 @@
+#!/bin/bash
+# Round measurement: GPU tests, default bench line, per-config lines, launch list, ncu --set full.
+cd "$(dirname "$0")/.."
 set -x
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 tail -3 gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke rc=$?
 timeout 600 python bench.py --steps 20 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc=$?
 cat gpurun_out/bench.json
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke rc=$?
+bash tools/bench_configs.sh
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --profile > gpurun_out/ncu_launch.log 2>&1; echo ncu1 rc=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"encode_v3|decode_v3" -s 6 -c 2 -o gpurun_out/v3full python bench.py --steps 2 --warmup 3 --profile > gpurun_out/ncu_full.log 2>&1; echo ncu2 rc=$?
-ls -la gpurun_out
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"encode_v3|decode_v3" -s 6 -c 2 -o gpurun_out/full python bench.py --steps 2 --warmup 3 --profile > gpurun_out/ncu_full.log 2>&1; echo ncu2 rc=$?

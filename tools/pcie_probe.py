@@ -1,0 +1,55 @@
+"""PCIe probe: pinned H2D, D2H and both directions at once (GB/s), and the
+pipelined e2e round trip of cfg2 at several chunk counts."""
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+from paper_1303_4994_b200 import Dtype, Mode, StreamConfig, wave_segment_blocks  # noqa: E402
+from paper_1303_4994_b200 import workloads as W  # noqa: E402
+from paper_1303_4994_b200.pipeline import HostRoundTrip  # noqa: E402
+
+nb = 256 << 20
+h = torch.empty(nb, dtype=torch.uint8).pin_memory()
+h2 = torch.empty(nb, dtype=torch.uint8).pin_memory()
+d = torch.empty(nb, dtype=torch.uint8, device="cuda")
+d2 = torch.empty(nb, dtype=torch.uint8, device="cuda")
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+for name, fn in (("h2d", lambda: d.copy_(h, non_blocking=True)),
+                 ("d2h", lambda: h.copy_(d, non_blocking=True))):
+    fn(); torch.cuda.synchronize()
+    t = time.perf_counter()
+    for _ in range(5):
+        fn()
+    torch.cuda.synchronize()
+    print(f"{name}: {5 * nb / (time.perf_counter() - t) / 1e9:.1f} GB/s")
+torch.cuda.synchronize()
+t = time.perf_counter()
+for _ in range(5):
+    with torch.cuda.stream(s1):
+        d.copy_(h, non_blocking=True)
+    with torch.cuda.stream(s2):
+        h2.copy_(d2, non_blocking=True)
+torch.cuda.synchronize()
+print(f"both directions: {2 * 5 * nb / (time.perf_counter() - t) / 1e9:.1f} GB/s total")
+x = W.cfg2_ar2_f32()
+n = x.size
+seg = wave_segment_blocks(n, Dtype.F32, Mode.FIXED_QUALITY, 4096)
+cfg = StreamConfig(Dtype.F32, 4096, Mode.FIXED_QUALITY, W.CFG2_TARGET_DB, segment_blocks=seg)
+xh = torch.from_numpy(x).pin_memory()
+yh = torch.empty(n, dtype=torch.float32).pin_memory()
+for chunks in (2, 4, 8, 16, 32):
+    rt = HostRoundTrip(n, cfg, chunks=chunks)
+    blob_h = torch.empty(rt.blob_d.numel(), dtype=torch.uint8).pin_memory()
+    offs_h = torch.empty(rt.n_blocks + 1, dtype=torch.int64).pin_memory()
+    for _ in range(2):
+        rt.run(xh, blob_h, offs_h, yh)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    for _ in range(5):
+        rt.run(xh, blob_h, offs_h, yh)
+    dt = (time.perf_counter() - t) / 5
+    print(f"e2e chunks={chunks}: {dt * 1e3:.2f} ms/step, {n * 4 / dt / 1e9:.1f} GB/s, PCIe {(rt.h2d_bytes + rt.d2h_bytes) / dt / 1e9:.1f} GB/s both ways")
