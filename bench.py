@@ -275,7 +275,7 @@ def main():
                     help="segment policy; auto = warm_self for fixed rate, cold for fixed quality")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-chunks", type=int, default=4, help="pipeline chunks of the e2e round trip")
+    ap.add_argument("--e2e-chunks", type=int, default=8, help="pipeline chunks of the e2e round trip")
     ap.add_argument("--profile", action="store_true",
                     help="short run for ncu: no e2e, no cpu baseline, no clocks")
     args = ap.parse_args()

@@ -56,6 +56,13 @@ int64_t apax_max_encoded_bytes(int64_t n, int dtype, int block_size);
  * the value passed to apax_encode. */
 int64_t apax_encode_wave_segment_blocks(int64_t n, int dtype, int mode, int block_size);
 
+/* Copy n_words (1..32) status words from a device status buffer to PAGE-LOCKED
+ * HOST memory (cudaHostAlloc / torch pin_memory) with stores issued by one
+ * thread block, enqueued on `stream`.  For pipelined host round trips: a
+ * 32-byte copy-engine D2H would queue behind the bulk sample copies of other
+ * chunks.  No reference counterpart (the reference is synchronous). */
+int apax_status_to_host(const uint64_t* status, uint64_t* host_dst, int n_words, void* stream);
+
 /* Device workspace needed by apax_encode for these arguments. */
 int64_t apax_encode_workspace_bytes(int64_t n, int dtype, int mode, int block_size,
                                     int64_t segment_blocks);

@@ -50,6 +50,8 @@ def lib():
     L.apax_decode.restype = I32
     L.apax_encode_wave_segment_blocks.argtypes = [I64, I32, I32, I32]
     L.apax_encode_wave_segment_blocks.restype = I64
+    L.apax_status_to_host.argtypes = [P, P, I32, P]
+    L.apax_status_to_host.restype = I32
     L.apax_decode_segments_workspace_bytes.argtypes = [I64, I32, I32]
     L.apax_decode_segments_workspace_bytes.restype = I64
     L.apax_decode_segments.argtypes = [P, I64, I64, I32, I32, P, I64, P, P, P, I64, P]

@@ -157,6 +157,16 @@ int plan_decode(long long n, int dt, int bs, DecPlan* p) {
 
 }  // namespace
 
+namespace {
+// status words to pinned host memory by plain stores from an SM: a copy-engine
+// D2H of 32 bytes would queue behind the bulk copies of a pipelined round trip
+__global__ void status_to_host_kernel(const unsigned long long* src, unsigned long long* dst, int n) {
+    const int i = threadIdx.x;
+    if (i < n) dst[i] = src[i];
+    __threadfence_system();
+}
+}  // namespace
+
 extern "C" {
 
 const char* apax_version(void) { return "apax-b200 0.1.0 (sm_100a)"; }
@@ -444,6 +454,18 @@ int apax_parse_file_header(const uint8_t* d, int64_t len, int* dt, int* mode, in
     if (*mode == APAX_FIXED_RATE && !(*target > 0)) return APAX_ERR_CFG_FR_TARGET;
     *detail = -1;
     return APAX_OK;
+}
+
+int apax_status_to_host(const uint64_t* status, uint64_t* host_dst, int n_words, void* stream) {
+    if (!status || !host_dst || n_words < 1 || n_words > 32) return APAX_ERR_ARG;
+    void* dptr = nullptr;
+    if (cudaHostGetDevicePointer(&dptr, host_dst, 0) != cudaSuccess || !dptr) {
+        cudaGetLastError();
+        return APAX_ERR_ARG;   // not page-locked host memory
+    }
+    status_to_host_kernel<<<1, 32, 0, (cudaStream_t)stream>>>((const unsigned long long*)status,
+                                                             (unsigned long long*)dptr, n_words);
+    return cudaGetLastError() == cudaSuccess ? APAX_OK : APAX_ERR_CUDA;
 }
 
 }  // extern "C"

@@ -41,8 +41,8 @@ seg = wave_segment_blocks(n, Dtype.F32, Mode.FIXED_QUALITY, 4096)
 cfg = StreamConfig(Dtype.F32, 4096, Mode.FIXED_QUALITY, W.CFG2_TARGET_DB, segment_blocks=seg)
 xh = torch.from_numpy(x).pin_memory()
 yh = torch.empty(n, dtype=torch.float32).pin_memory()
-for chunks in (2, 4, 8, 16, 32):
-    rt = HostRoundTrip(n, cfg, chunks=chunks)
+for chunks, depth in ((4, 3), (8, 3), (8, 4), (16, 3), (16, 4)):
+    rt = HostRoundTrip(n, cfg, chunks=chunks, depth=depth)
     blob_h = torch.empty(rt.blob_d.numel(), dtype=torch.uint8).pin_memory()
     offs_h = torch.empty(rt.n_blocks + 1, dtype=torch.int64).pin_memory()
     for _ in range(2):
@@ -52,4 +52,16 @@ for chunks in (2, 4, 8, 16, 32):
     for _ in range(5):
         rt.run(xh, blob_h, offs_h, yh)
     dt = (time.perf_counter() - t) / 5
-    print(f"e2e chunks={chunks}: {dt * 1e3:.2f} ms/step, {n * 4 / dt / 1e9:.1f} GB/s, PCIe {(rt.h2d_bytes + rt.d2h_bytes) / dt / 1e9:.1f} GB/s both ways")
+    print(f"e2e chunks={chunks} depth={depth}: {dt * 1e3:.2f} ms/step, {n * 4 / dt / 1e9:.1f} GB/s, PCIe {(rt.h2d_bytes + rt.d2h_bytes) / dt / 1e9:.1f} GB/s both ways")
+# timeline of one 4-chunk round trip
+rt = HostRoundTrip(n, cfg, chunks=4, depth=3)
+blob_h = torch.empty(rt.blob_d.numel(), dtype=torch.uint8).pin_memory()
+offs_h = torch.empty(rt.n_blocks + 1, dtype=torch.int64).pin_memory()
+rt.run(xh, blob_h, offs_h, yh)
+t0 = torch.cuda.Event(enable_timing=True)
+t0.record()
+rt.timeline = []
+rt.run(xh, blob_h, offs_h, yh)
+torch.cuda.synchronize()
+for name, a, b in sorted(rt.timeline, key=lambda e: t0.elapsed_time(e[1])):
+    print(f"{name:6s} {t0.elapsed_time(a):8.3f} -> {t0.elapsed_time(b):8.3f} ms ({a.elapsed_time(b):.3f})")
