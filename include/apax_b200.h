@@ -56,6 +56,23 @@ int64_t apax_max_encoded_bytes(int64_t n, int dtype, int block_size);
  * the value passed to apax_encode. */
 int64_t apax_encode_wave_segment_blocks(int64_t n, int dtype, int mode, int block_size);
 
+/* Decode blocks [b0, b1) of a container of n samples (whole-stream or
+ * segmented) given the GLOBAL side-band index `block_offsets` and the
+ * derivative history (q[-1], q[-2] as two's-complement u64) entering block b0
+ * (ignored when b0 is a restart or D0 block; transform.py:31-49).  y receives
+ * samples b0*bs .. min(n, b1*bs); status block indices are relative to b0.
+ * map_out (nullable, 6 device words) receives the range's history map
+ * (m11, m12, m21, m22, c1, c2): the history leaving block b1-1 is
+ * M*(entry) + c, mod 2^64.  Multi-GPU decode of a whole-stream container
+ * (SURVEY.md §8(e)): every rank decodes its block range with entry (0, 0)
+ * and map_out, all-gathers the maps, composes them in rank order and
+ * re-decodes with its exact entry (paper_1303_4994_b200/distributed.py).
+ * Workspace: apax_decode_workspace_bytes(samples of the range, dtype, bs). */
+int apax_decode_range(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, int block_size,
+                      const int64_t* block_offsets, int64_t b0, int64_t b1, uint64_t entry_p1,
+                      uint64_t entry_p2, void* y, uint64_t* map_out, uint64_t* status, void* ws,
+                      int64_t ws_bytes, void* stream);
+
 /* Copy n_words (1..32) status words from a device status buffer to PAGE-LOCKED
  * HOST memory (cudaHostAlloc / torch pin_memory) with stores issued by one
  * thread block, enqueued on `stream`.  For pipelined host round trips: a

@@ -50,6 +50,9 @@ def lib():
     L.apax_decode.restype = I32
     L.apax_encode_wave_segment_blocks.argtypes = [I64, I32, I32, I32]
     L.apax_encode_wave_segment_blocks.restype = I64
+    L.apax_decode_range.argtypes = [P, I64, I64, I32, I32, P, I64, I64, ctypes.c_uint64, ctypes.c_uint64,
+                                    P, P, P, P, I64, P]
+    L.apax_decode_range.restype = I32
     L.apax_status_to_host.argtypes = [P, P, I32, P]
     L.apax_status_to_host.restype = I32
     L.apax_decode_segments_workspace_bytes.argtypes = [I64, I32, I32]
@@ -78,5 +81,5 @@ EXPORTED_SYMBOLS = (
     "apax_decode", "apax_find_blocks", "apax_parse_file_header",
     "apax_decode_segments_workspace_bytes", "apax_decode_segments",
     "apax_encode_wave_segment_blocks", "apax_profile_grid", "apax_profile_sums", "apax_profile_welch",
-    "apax_profile_select",
+    "apax_profile_select", "apax_decode_range", "apax_status_to_host",
 )

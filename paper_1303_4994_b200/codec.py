@@ -244,6 +244,40 @@ def encode_device(x, config: StreamConfig, trace: bool = False) -> EncodedStream
     return res
 
 
+def decode_range(blob, nbytes: int, offsets, count: int, dtype: Dtype, block_size: int, b0: int, b1: int,
+                 entry=(0, 0), want_map: bool = False):
+    """Decode blocks [b0, b1) of a container held in HBM (apax_decode_range):
+    `offsets` is the container's global side-band index (int64 CUDA tensor),
+    `entry` the derivative history entering block b0 as two's-complement u64
+    (q[-1], q[-2]).  Returns (y of the range, history map or None): the map
+    (m11, m12, m21, m22, c1, c2) gives the history leaving block b1-1 as an
+    affine function of `entry` (distributed.py composes them across ranks)."""
+    torch, L = _require_cuda()
+    bs = int(block_size)
+    s0, s1 = b0 * bs, min(count, b1 * bs)
+    m = s1 - s0
+    wsb = int(L.apax_decode_workspace_bytes(m, dtype.wire_code, bs))
+    if wsb < 0:
+        raise InvalidConfig("invalid decode arguments")
+    ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device=blob.device)
+    status = torch.empty(4, dtype=torch.int64, device=blob.device)
+    y = torch.empty(max(m, 1), dtype=torch_dtype(dtype), device=blob.device)
+    mp = torch.zeros(6, dtype=torch.int64, device=blob.device) if want_map else None
+    st = L.apax_decode_range(ctypes.c_void_p(blob.data_ptr()), int(nbytes), int(count), dtype.wire_code, bs,
+                             ctypes.c_void_p(offsets.data_ptr()), int(b0), int(b1),
+                             ctypes.c_uint64(int(entry[0]) & 0xFFFFFFFFFFFFFFFF),
+                             ctypes.c_uint64(int(entry[1]) & 0xFFFFFFFFFFFFFFFF),
+                             ctypes.c_void_p(y.data_ptr()),
+                             ctypes.c_void_p(mp.data_ptr()) if mp is not None else None,
+                             ctypes.c_void_p(status.data_ptr()), ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+                             ctypes.c_void_p(_stream_ptr(None)))
+    raise_status(st)
+    torch.cuda.current_stream().synchronize()
+    _check_status(status.cpu().numpy().view(np.uint64))
+    mv = [int(v) & 0xFFFFFFFFFFFFFFFF for v in mp.cpu().tolist()] if mp is not None else None
+    return y[:m], mv
+
+
 def _decodable_count(count: int, nbytes: int, cfg: StreamConfig) -> int:
     """Samples worth decoding: every block costs >= header + 2 bytes, so a
     count beyond what `nbytes` can hold is guaranteed to fail (truncated)

@@ -338,6 +338,49 @@ int apax_decode(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, int b
     return launch_decode(dtype, P, p.grid, p.smem, s);
 }
 
+int apax_decode_range(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, int block_size,
+                      const int64_t* block_offsets, int64_t b0, int64_t b1, uint64_t entry_p1,
+                      uint64_t entry_p2, void* y, uint64_t* map_out, uint64_t* status, void* ws,
+                      int64_t ws_bytes, void* stream) {
+    // blocks [b0, b1) of a container of n samples, as a container of their own
+    // whose history enters at (entry_p1, entry_p2): the global side-band index
+    // is read from entry b0 on, y receives samples b0*bs .. min(n, b1*bs)
+    if (!block_offsets || b0 < 0 || b1 <= b0 || block_size <= 0) return APAX_ERR_ARG;
+    const long long nb_all = (n + block_size - 1) / block_size;
+    if (b1 > nb_all) return APAX_ERR_ARG;
+    const long long s0 = b0 * (long long)block_size;
+    const long long s1 = (b1 * (long long)block_size < n) ? b1 * (long long)block_size : n;
+    const long long nr = s1 - s0;
+    DecPlan p;
+    int st = plan_decode(nr, dtype, block_size, &p);
+    if (st) return st;
+    if (!blob || !status || !y) return APAX_ERR_ARG;
+    if (ws_bytes < p.ws_total || !ws) return APAX_ERR_WORKSPACE;
+    cudaStream_t s = (cudaStream_t)stream;
+    uint8_t* w = (uint8_t*)ws;
+    if (cudaMemsetAsync(status, 0xFF, 4 * sizeof(uint64_t), s) != cudaSuccess) return APAX_ERR_CUDA;
+    if (cudaMemsetAsync(w, 0, (size_t)p.ws_offsets, s) != cudaSuccess) return APAX_ERR_CUDA;
+    DecParams P;
+    memset(&P, 0, sizeof(P));
+    P.blob = blob;
+    P.nbytes = nbytes;
+    P.offsets = (const long long*)block_offsets + b0;
+    P.y = y;
+    P.n = nr;
+    P.bs = block_size;
+    P.n_blocks = p.n_blocks;
+    P.status = (unsigned long long*)status;
+    P.carry = (unsigned long long*)(w + p.ws_carry);
+    P.ticket = (unsigned int*)(w + p.ws_ticket);
+    P.payload_cap = p.payload_cap;
+    P.entry_p1 = entry_p1;
+    P.entry_p2 = entry_p2;
+    st = p.v2 ? launch_decode_v2(dtype, P, p.grid, p.smem, s) : launch_decode(dtype, P, p.grid, p.smem, s);
+    if (st) return st;
+    if (map_out) return launch_compose_maps(P.carry, p.n_blocks, (unsigned long long*)map_out, s);
+    return APAX_OK;
+}
+
 int64_t apax_encode_wave_segment_blocks(int64_t n, int dtype, int mode, int block_size) {
     // segment length that gives every resident encoder CTA one segment
     // (a one-wave schedule); the container then depends on this value only

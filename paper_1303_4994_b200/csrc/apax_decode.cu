@@ -245,10 +245,14 @@ __global__ void __launch_bounds__(kNT) decode_kernel(DecParams P) {
             if (sel == 0) { M = {0, 0, 0, 0, L1, L2}; }
             else if (sel == 1) { M = {1, 0, 1, 0, L1, L2}; }
             else { M = {unp + 1, (unsigned long long)0 - unp, unp, (unsigned long long)0 - (unp - 1), L1, L2}; }
-            unsigned long long in1 = 0, in2 = 0;
+            // history entering block 0 of the launch (apax_decode_range); restart
+            // and D0 blocks have a constant map.  Every block keeps its map in
+            // cw[1..6] (apax_decode_range composes them).
+            unsigned long long in1 = P.entry_p1, in2 = P.entry_p2;
+            if (sel == 0 || S->restart) { M = {0, 0, 0, 0, M.c1, M.c2}; in1 = 0; in2 = 0; }
+            cw[1] = M.m11; cw[2] = M.m12; cw[3] = M.m21; cw[4] = M.m22; cw[5] = M.c1; cw[6] = M.c2;
             if (sel != 0 && !S->restart && b > 0) {
                 // publish my map, then look back
-                cw[1] = M.m11; cw[2] = M.m12; cw[3] = M.m21; cw[4] = M.m22; cw[5] = M.c1; cw[6] = M.c2;
                 __threadfence();
                 st_release(&cw[0], kFlagAgg);
                 Aff acc = {1, 0, 0, 1, 0, 0};

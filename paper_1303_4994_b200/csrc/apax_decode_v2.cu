@@ -492,10 +492,15 @@ __global__ void __launch_bounds__(NT, APAX_DEC_MINB) decode_v2_kernel(DecParams 
             if (sel == 0) M = {0, 0, 0, 0, L1, L2};
             else if (sel == 1) M = {1, 0, 1, 0, L1, L2};
             else M = {unp + 1, 0ULL - unp, unp, 0ULL - (unp - 1), L1, L2};
-            unsigned long long in1 = 0, in2 = 0;
+            unsigned long long in1 = P.entry_p1, in2 = P.entry_p2;   // history entering block 0
+            // the block's history map (constant for restart / D0 blocks); kept
+            // in cw[1..6] for every block: apax_decode_range composes them
+            if (sel == 0 || S->restart) M = {0, 0, 0, 0, M.c1, M.c2};
+            if (lane == 0) {
+                cw[1] = M.m11; cw[2] = M.m12; cw[3] = M.m21; cw[4] = M.m22; cw[5] = M.c1; cw[6] = M.c2;
+            }
             if (sel != 0 && !S->restart && b > 0) {
                 if (lane == 0) {
-                    cw[1] = M.m11; cw[2] = M.m12; cw[3] = M.m21; cw[4] = M.m22; cw[5] = M.c1; cw[6] = M.c2;
                     __threadfence();
                     st_release(&cw[0], kFlagAgg);
                 }
@@ -517,7 +522,8 @@ __global__ void __launch_bounds__(NT, APAX_DEC_MINB) decode_v2_kernel(DecParams 
                         Ml = {__ldcg(&ck[1]), __ldcg(&ck[2]), __ldcg(&ck[3]), __ldcg(&ck[4]),
                               __ldcg(&ck[5]), __ldcg(&ck[6])};
                     } else if (lane == first_inc) {
-                        Ml = {0, 0, 0, 0, (k >= 0 ? __ldcg(&ck[8]) : 0ULL), (k >= 0 ? __ldcg(&ck[9]) : 0ULL)};
+                        Ml = {0, 0, 0, 0, (k >= 0 ? __ldcg(&ck[8]) : P.entry_p1),
+                              (k >= 0 ? __ldcg(&ck[9]) : P.entry_p2)};
                     }
                     // ordered tree: lane 0 ends with M_0 o M_1 o ... o M_31
 #pragma unroll
@@ -547,6 +553,7 @@ __global__ void __launch_bounds__(NT, APAX_DEC_MINB) decode_v2_kernel(DecParams 
                     base -= 32;
                 }
             }
+            if (sel == 0 || S->restart) { in1 = 0; in2 = 0; }   // history reset / unused
             if (lane == 0) {
                 cw[8] = M.m11 * in1 + M.m12 * in2 + M.c1;
                 cw[9] = M.m21 * in1 + M.m22 * in2 + M.c2;
@@ -646,6 +653,42 @@ int decode_v2_resident_ctas(int dt, size_t smem) {
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, d2::NT, smem) != cudaSuccess || per < 1)
         per = 1;
     return per * (nsm > 0 ? nsm : 148);
+}
+
+// aggregate history map of blocks [0, nb): M_{nb-1} o ... o M_0 from the
+// per-block maps the decode left in the carry records (cw[1..6])
+__global__ void __launch_bounds__(256) compose_maps_kernel(const unsigned long long* carry, long long nb,
+                                                           unsigned long long* out) {
+    using d2::Aff;
+    using d2::aff_compose;
+    __shared__ Aff part[256];
+    const int t = threadIdx.x;
+    const long long per = (nb + 255) / 256;
+    const long long k0 = (long long)t * per, k1 = (k0 + per < nb) ? k0 + per : nb;
+    Aff acc = {1, 0, 0, 1, 0, 0};
+    for (long long k = k0; k < k1; k++) {
+        const unsigned long long* c = carry + 16 * k;
+        const Aff M = {c[1], c[2], c[3], c[4], c[5], c[6]};
+        acc = aff_compose(M, acc);
+    }
+    part[t] = acc;
+    __syncthreads();
+    for (int d = 1; d < 256; d <<= 1) {   // ordered: later ranges after earlier ones
+        Aff r = part[t];
+        if ((t & (2 * d - 1)) == 0 && t + d < 256) r = aff_compose(part[t + d], part[t]);
+        __syncthreads();
+        part[t] = r;
+        __syncthreads();
+    }
+    if (t == 0) {
+        out[0] = part[0].m11; out[1] = part[0].m12; out[2] = part[0].m21;
+        out[3] = part[0].m22; out[4] = part[0].c1; out[5] = part[0].c2;
+    }
+}
+
+int launch_compose_maps(const unsigned long long* carry, long long nb, unsigned long long* out, cudaStream_t st) {
+    compose_maps_kernel<<<1, 256, 0, st>>>(carry, nb, out);
+    return cudaGetLastError() == cudaSuccess ? APAX_OK : APAX_ERR_CUDA;
 }
 
 int launch_decode_v2(int dt, const DecParams& P, int grid, size_t smem, cudaStream_t st) {

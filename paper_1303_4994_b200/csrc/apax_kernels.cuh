@@ -49,6 +49,9 @@ struct DecParams {
     int payload_cap;            // smem bytes reserved for one block payload
     long long segment_blocks;   // d3: every segment_blocks-th block starts a segment
     long long seg_begin, seg_end;
+    // v2 range decode (apax_decode_range): derivative history entering
+    // block 0 of this launch when it is not a restart block (default 0, 0)
+    unsigned long long entry_p1, entry_p2;
 };
 
 size_t encode_smem_bytes(int dt, int bs, int stage_bytes, int x_in_smem);
@@ -75,6 +78,7 @@ size_t decode_v2_smem_bytes(int dt, int bs, int payload_cap);
 bool decode_v2_supported(int bs);
 int decode_v2_resident_ctas(int dt, size_t smem);
 int launch_decode_v2(int dt, const DecParams& P, int grid, size_t smem, cudaStream_t st);
+int launch_compose_maps(const unsigned long long* carry, long long nb, unsigned long long* out, cudaStream_t st);
 int profile_sums(const void* x, const void* y, long long n, int dt, int pass, double mx, double my,
                  double md, double* partials, unsigned long long* counts, int grid, cudaStream_t st);
 size_t profile_welch_smem(int seg);

@@ -10,7 +10,14 @@ stream.  Bodies stay sharded (gathering a multi-GB container would cost
 more than the encode); `global_block_offsets` maps a rank's side-band index
 into the concatenated stream.
 
-Decode: a rank decodes its own body (a container of its segments).
+Decode: a rank decodes its own body (a container of its segments).  A
+whole-stream container (one restart block, no segments) shards by block
+ranges instead: the history entering a range (the last two quantized values
+of the previous block, transform.py:31-49) is an affine function of the
+history entering the previous range, so every rank decodes its range once to
+get that map (apax_decode_range with map_out), the R maps (6 words each) are
+all-gathered and composed in rank order, and every rank re-decodes its range
+from its exact entry history (App. B of SURVEY.md).
 
 Profiler: per-rank sums are all-gathered and added in rank order, so the
 result is deterministic and independent of the collective's reduction tree.
@@ -127,3 +134,66 @@ def sharded_encode(x_local, config, group=None):
     body = bytes(res.blob[FILE_HEADER_SIZE:res.nbytes].cpu().numpy().tobytes())
     offs = global_block_offsets(res.block_offsets.cpu().numpy(), place)
     return body, place, offs
+
+
+# ---------------------------------------------------------------------------
+# whole-stream decode across ranks (SURVEY.md §8(e)): affine history maps
+# ---------------------------------------------------------------------------
+_M64 = (1 << 64) - 1
+
+
+def shard_blocks(n_blocks: int, world: int, rank: int) -> Tuple[int, int]:
+    """[b0, b1) block range of `rank` for a whole-stream container."""
+    return (n_blocks * rank) // world, (n_blocks * (rank + 1)) // world
+
+
+def apply_map(m: Sequence[int], h: Tuple[int, int]) -> Tuple[int, int]:
+    """History leaving a range whose map is m = (m11, m12, m21, m22, c1, c2),
+    given the history h entering it (mod 2^64, two's complement)."""
+    m11, m12, m21, m22, c1, c2 = (int(v) & _M64 for v in m)
+    h1, h2 = h
+    return ((m11 * h1 + m12 * h2 + c1) & _M64, (m21 * h1 + m22 * h2 + c2) & _M64)
+
+
+def range_entries(maps: Sequence[Sequence[int]]) -> list:
+    """Entry history of every range, in rank order: range 0 starts the stream
+    (history (0, 0)), range r+1 enters with range r's map applied to range r's
+    entry."""
+    out = []
+    h = (0, 0)
+    for m in maps:
+        out.append(h)
+        h = apply_map(m, h)
+    return out
+
+
+def whole_stream_entry(my_map: Sequence[int], group=None, device=None) -> Tuple[int, int]:
+    """All-gather of the R range maps (6 x int64 each) and the exclusive
+    composition in rank order: the history entering this rank's range."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    v = torch.tensor([int(x) - (1 << 64) if int(x) >= (1 << 63) else int(x) for x in my_map],
+                     dtype=torch.int64, device=device)
+    out = torch.empty(world * 6, dtype=torch.int64, device=device)
+    dist.all_gather_into_tensor(out, v, group=group)
+    maps = [[int(x) & _M64 for x in row] for row in out.cpu().numpy().reshape(world, 6).tolist()]
+    return range_entries(maps)[dist.get_rank(group)]
+
+
+def sharded_decode_whole_stream(blob, nbytes: int, offsets, group=None):
+    """Decode this rank's block range of a container resident on its GPU
+    (`blob`, uint8 CUDA tensor; `offsets`, the global side-band index, int64
+    CUDA tensor).  Returns (y of the range, (b0, b1))."""
+    import torch.distributed as dist
+    from .codec import decode_range, parse_file_header
+    cfg, count = parse_file_header(bytes(blob[:FILE_HEADER_SIZE].cpu().numpy().tobytes()))
+    nb = (count + cfg.block_size - 1) // cfg.block_size
+    b0, b1 = shard_blocks(nb, dist.get_world_size(group), dist.get_rank(group))
+    if b1 <= b0:
+        import torch
+        return torch.empty(0, device=blob.device), (b0, b1)
+    _, m = decode_range(blob, nbytes, offsets, count, cfg.dtype, cfg.block_size, b0, b1, want_map=True)
+    entry = whole_stream_entry(m, group, blob.device)
+    y, _ = decode_range(blob, nbytes, offsets, count, cfg.dtype, cfg.block_size, b0, b1, entry=entry)
+    return y, (b0, b1)

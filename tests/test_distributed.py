@@ -102,3 +102,40 @@ def test_two_rank_gloo_assembly(tmp_path):
     assert len(res) == len(CASES)
     for r in res:
         assert r == {"same_bytes": True, "same_offsets": True, "total_ok": True, "sum_ok": True}, r
+
+
+def test_range_entries_compose_in_order():
+    rng = np.random.default_rng(3)
+    maps = [[int(v) for v in rng.integers(0, 1 << 63, 6)] for _ in range(5)]
+    ent = D.range_entries(maps)
+    assert ent[0] == (0, 0)
+    h = (0, 0)
+    for r, m in enumerate(maps):
+        assert ent[r] == h
+        m11, m12, m21, m22, c1, c2 = m
+        h = ((m11 * h[0] + m12 * h[1] + c1) % (1 << 64), (m21 * h[0] + m22 * h[1] + c2) % (1 << 64))
+    assert D.shard_blocks(10, 3, 0) == (0, 3) and D.shard_blocks(10, 3, 2) == (6, 10)
+
+
+def _entry_worker(rank, world, port, out_dir):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(11)
+    maps = [[int(v) for v in rng.integers(0, 1 << 64, 6, dtype=np.uint64)] for _ in range(world)]
+    e = D.whole_stream_entry(maps[rank])
+    ok = e == D.range_entries(maps)[rank]
+    with open(os.path.join(out_dir, f"entry{rank}.json"), "w") as f:
+        json.dump({"ok": bool(ok)}, f)
+    dist.destroy_process_group()
+
+
+def test_two_rank_gloo_whole_stream_entries(tmp_path):
+    """The all-gather of the ranks' history maps (u64 words through int64
+    tensors) and their rank-ordered composition."""
+    import torch.multiprocessing as mp
+    port = _free_port()
+    mp.spawn(_entry_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    for r in range(2):
+        assert json.loads((tmp_path / f"entry{r}.json").read_text()) == {"ok": True}
