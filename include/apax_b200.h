@@ -73,6 +73,20 @@ int apax_decode_range(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype,
                       uint64_t entry_p2, void* y, uint64_t* map_out, uint64_t* status, void* ws,
                       int64_t ws_bytes, void* stream);
 
+/* LOSSLESS whole-stream encode of the blocks from first_block on, as a
+ * container of their own whose body (bytes after the 28-byte file header)
+ * equals those blocks' bytes in the one-call whole-stream container
+ * (apax_encode, segment_blocks <= 0): x[0] is global sample first_block*bs
+ * and x[-halo .. 0) must hold the preceding samples, halo >= bs + 2 (bs for
+ * first_block == 1, 0 for first_block == 0): the previous block and the two
+ * samples before it rebuild the first block's codec state (selector costs
+ * and derivative history; reference codec.py:192-255).
+ * The multi-GPU LOSSLESS encode of SURVEY.md §8(e): rank r receives that
+ * halo from rank r-1.  Power-of-two block sizes 128..4096. */
+int apax_encode_lossless_range(const void* x, int64_t halo, int64_t n, int dtype, int block_size,
+                               int64_t first_block, uint8_t* out, int64_t out_cap, int64_t* block_offsets,
+                               uint64_t* status, void* ws, int64_t ws_bytes, void* stream);
+
 /* Copy n_words (1..32) status words from a device status buffer to PAGE-LOCKED
  * HOST memory (cudaHostAlloc / torch pin_memory) with stores issued by one
  * thread block, enqueued on `stream`.  For pipelined host round trips: a

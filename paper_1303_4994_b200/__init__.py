@@ -8,6 +8,7 @@ behind the C ABI in include/apax_b200.h.  `profile` / `ProfileSession`
 (reference profiler.py) run their statistics in csrc/apax_profile.cu.
 """
 from .codec import (Decoder, EncodedStream, Encoder, decode_device, decode_range, decode_stream,
+                    encode_lossless_range,
                     encode_device, encode_stream, max_encoded_bytes, parse_file_header,
                     wave_segment_blocks)
 from .dtypes import BlockHeader, Dtype, Mode, StreamConfig, decode_scale_code, encode_scale_code
@@ -16,7 +17,7 @@ from .profiler import ProfileSession, profile
 
 __all__ = [
     "Dtype", "Mode", "StreamConfig", "BlockHeader", "encode_stream", "decode_stream",
-    "parse_file_header", "encode_device", "decode_device", "decode_range", "Encoder", "Decoder",
+    "parse_file_header", "encode_device", "decode_device", "decode_range", "encode_lossless_range", "Encoder", "Decoder",
     "EncodedStream", "max_encoded_bytes", "wave_segment_blocks", "profile", "ProfileSession", "encode_scale_code", "decode_scale_code", "errors",
 ]
 

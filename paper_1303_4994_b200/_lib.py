@@ -53,6 +53,8 @@ def lib():
     L.apax_decode_range.argtypes = [P, I64, I64, I32, I32, P, I64, I64, ctypes.c_uint64, ctypes.c_uint64,
                                     P, P, P, P, I64, P]
     L.apax_decode_range.restype = I32
+    L.apax_encode_lossless_range.argtypes = [P, I64, I64, I32, I32, I64, P, I64, P, P, P, I64, P]
+    L.apax_encode_lossless_range.restype = I32
     L.apax_status_to_host.argtypes = [P, P, I32, P]
     L.apax_status_to_host.restype = I32
     L.apax_decode_segments_workspace_bytes.argtypes = [I64, I32, I32]
@@ -82,4 +84,5 @@ EXPORTED_SYMBOLS = (
     "apax_decode_segments_workspace_bytes", "apax_decode_segments",
     "apax_encode_wave_segment_blocks", "apax_profile_grid", "apax_profile_sums", "apax_profile_welch",
     "apax_profile_select", "apax_decode_range", "apax_status_to_host",
+    "apax_encode_lossless_range",
 )

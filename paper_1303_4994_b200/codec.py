@@ -244,6 +244,44 @@ def encode_device(x, config: StreamConfig, trace: bool = False) -> EncodedStream
     return res
 
 
+def encode_lossless_range(x_ext, halo: int, first_block: int, dtype: Dtype, block_size: int) -> EncodedStream:
+    """LOSSLESS whole-stream encode of the blocks from `first_block` on
+    (apax_encode_lossless_range).  `x_ext` (CUDA tensor of the dtype) holds
+    the `halo` samples before global sample first_block * block_size
+    followed by the range's samples.  The result is a container of its own;
+    its body (after the 28-byte header) is those blocks' bytes in the
+    one-call whole-stream container, and its side-band index is relative to
+    its own header."""
+    torch, L = _require_cuda()
+    x_ext = x_ext.reshape(-1).contiguous()
+    if x_ext.dtype != torch_dtype(dtype):
+        raise InvalidConfig("input dtype differs from the config dtype")
+    n = int(x_ext.numel()) - int(halo)
+    bs = int(block_size)
+    cfg = StreamConfig(dtype, bs, Mode.LOSSLESS)
+    cfg.validate()
+    cap = int(L.apax_max_encoded_bytes(n, dtype.wire_code, bs))
+    wsb = int(L.apax_encode_workspace_bytes(n, dtype.wire_code, 0, bs, 0))
+    if cap < 0 or wsb < 0:
+        raise InvalidConfig("invalid encode arguments")
+    dev = x_ext.device
+    out = torch.empty(cap + 64, dtype=torch.uint8, device=dev)
+    ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device=dev)
+    status = torch.empty(4, dtype=torch.int64, device=dev)
+    nb = (n + bs - 1) // bs
+    offs = torch.empty(nb + 1, dtype=torch.int64, device=dev)
+    xp = x_ext.data_ptr() + int(halo) * x_ext.element_size()
+    st = L.apax_encode_lossless_range(ctypes.c_void_p(xp), int(halo), n, dtype.wire_code, bs, int(first_block),
+                                      ctypes.c_void_p(out.data_ptr()), cap, ctypes.c_void_p(offs.data_ptr()),
+                                      ctypes.c_void_p(status.data_ptr()), ctypes.c_void_p(ws.data_ptr()),
+                                      ws.numel(), ctypes.c_void_p(_stream_ptr(None)))
+    raise_status(st)
+    torch.cuda.current_stream().synchronize()
+    s = status.cpu().numpy().view(np.uint64)
+    _check_status(s)
+    return EncodedStream(out, int(s[2]), offs, cfg, n)
+
+
 def decode_range(blob, nbytes: int, offsets, count: int, dtype: Dtype, block_size: int, b0: int, b1: int,
                  entry=(0, 0), want_map: bool = False):
     """Decode blocks [b0, b1) of a container held in HBM (apax_decode_range):

@@ -268,6 +268,56 @@ int apax_encode(const void* x, int64_t n, int dtype, int mode, double target, in
     return launch_encode(dtype, P, p.grid, p.smem, s);
 }
 
+int apax_encode_lossless_range(const void* x, int64_t halo, int64_t n, int dtype, int block_size,
+                               int64_t first_block, uint8_t* out, int64_t out_cap, int64_t* block_offsets,
+                               uint64_t* status, void* ws, int64_t ws_bytes, void* stream) {
+    // blocks first_block .. of a whole-stream LOSSLESS container, as their own
+    // container (its body concatenates with the neighbouring ranges' bodies
+    // into the one-GPU container): x[0] is sample first_block * bs, and the
+    // (bs + 2)-sample halo x[-bs-2 .. 0) rebuilds the first block's state
+    // (App. C E2)
+    if (first_block < 0) return APAX_ERR_ARG;
+    const long long need = first_block == 0 ? 0 : (first_block == 1 ? block_size : block_size + 2);
+    if (halo < need) return APAX_ERR_ARG;
+    EncPlan p;
+    int st = plan_encode(n, dtype, APAX_LOSSLESS, block_size, 0, &p);
+    if (st) return st;
+    if (dtype >= APAX_F32) return APAX_ERR_CFG_LOSSLESS_FLOAT;
+    if (!p.v3) return APAX_ERR_ARG;        // power-of-two block sizes 128..4096
+    if (!x || !out || !status || (p.ws_total > 0 && !ws)) return APAX_ERR_ARG;
+    if (out_cap < apax_max_encoded_bytes(n, dtype, block_size)) return APAX_ERR_CAPACITY;
+    if (ws_bytes < p.ws_total) return APAX_ERR_WORKSPACE;
+    cudaStream_t s = (cudaStream_t)stream;
+    uint8_t* w = (uint8_t*)ws;
+    if (cudaMemsetAsync(status, 0xFF, 4 * sizeof(uint64_t), s) != cudaSuccess) return APAX_ERR_CUDA;
+    if (cudaMemsetAsync(w, 0, (size_t)p.ws_slots, s) != cudaSuccess) return APAX_ERR_CUDA;
+    EncParams P;
+    memset(&P, 0, sizeof(P));
+    P.x = x;
+    P.n = n;
+    P.mode = APAX_LOSSLESS;
+    P.bs = block_size;
+    P.n_blocks = p.n_blocks;
+    P.unit_blocks = p.unit_blocks;
+    P.n_units = p.n_units;
+    P.halo = 1;
+    P.gblock0 = first_block;
+    P.out = out;
+    P.out_cap = out_cap;
+    P.block_offsets = (long long*)block_offsets;
+    P.status = (unsigned long long*)status;
+    P.lookback = (unsigned long long*)(w + p.ws_lookback);
+    P.ticket = (unsigned int*)(w + p.ws_ticket);
+    P.slots = w + p.ws_slots;
+    P.slot_bytes = p.slot_bytes;
+    P.stage_bytes = p.stage_bytes;
+    P.x_in_smem = p.x_in_smem;
+    P.att_lo = 20.0 * log10(ldexp(1.0, -31));
+    P.pow10_t20 = 1.0;
+    P.sqrt12 = sqrt(12.0);
+    return launch_encode_v3(dtype, P, p.grid, p.smem, s);
+}
+
 int64_t apax_decode_workspace_bytes(int64_t n, int dtype, int block_size) {
     DecPlan p;
     if (plan_decode(n, dtype, block_size, &p)) return -1;

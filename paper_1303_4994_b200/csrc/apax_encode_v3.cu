@@ -688,7 +688,9 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
 #endif
     auto xbuf = [&](int k) -> T* { return (T*)(smem + xoff + (k ? XB : 0)); };
     // staging state of the two buffers, in scalars (no local memory)
-    long long bb0 = -1, bb1 = -1;       // block held by buffer 0 / 1
+    // block held by buffer 0 / 1 (kNone: empty; block -1 is a range encode's halo)
+    constexpr long long kNone = -(1LL << 62);
+    long long bb0 = kNone, bb1 = kNone;
     uint32_t wst = 3u;                  // bit k: buffer k already waited on
     uint32_t phs = 0u;                  // bit k: mbarrier phase parity of buffer k
     auto bufblk_get = [&](int k) -> long long { return k ? bb1 : bb0; };
@@ -828,9 +830,9 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
 
     auto first_block = [&](long long uu) -> long long {
         const long long bb = uu * P.unit_blocks;
-        return (P.halo && bb > 0) ? bb - 1 : bb;
+        return (P.halo && bb + P.gblock0 > 0) ? bb - 1 : bb;
     };
-    long long a_done = -1;
+    long long a_done = kNone;
     int kunit = 0;
 
     for (long long u = P.unit_begin + blockIdx.x; u < P.unit_end; u += gridDim.x, kunit++) {
@@ -838,7 +840,7 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
         uint8_t* slot = sl ? slot1 : slot0;
         const long long b0 = u * P.unit_blocks;
         const long long b1 = (b0 + P.unit_blocks < P.n_blocks) ? b0 + P.unit_blocks : P.n_blocks;
-        const bool halo = P.halo && b0 > 0;
+        const bool halo = P.halo && b0 + P.gblock0 > 0;
         const bool warm = !P.halo && P.policy == 1 && P.mode == 1;
         const int npre = halo ? 1 : (warm ? 2 : 0);
         const long long npass = npre + (b1 - b0);
@@ -851,7 +853,7 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
             S->att = 0.0; S->p1 = 0; S->p2 = 0; S->has_pc = 0; S->initialized = 0;
             S->emitted = 0; S->win_base = 0; S->tail_len = 0; S->unit_len = 0; S->blen = 0; S->tl_next = 0;
             S->tail[0] = S->tail[1] = S->tail[2] = S->tail[3] = 0u;
-            if (P.halo && b0 > 1) {  // history entering block b0-1 (App. C E2)
+            if (P.halo && b0 + P.gblock0 > 1) {  // history entering block b0-1 (App. C E2)
                 const T* xh = (const T*)P.x + (b0 - 1) * (long long)bs;
                 S->p1 = (long long)xh[-1];
                 S->p2 = (long long)xh[-2];
@@ -866,7 +868,7 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
                 if (k < 0) {
                     if (tid == 32 && S->store_pending) { bulk_wait_read(); S->store_pending = 0; }
                     cbar();
-                    k = (bb0 == -1) ? 0 : ((bb1 == -1) ? 1 : 0);
+                    k = (bb0 == kNone) ? 0 : ((bb1 == kNone) ? 1 : 0);
                     stage(bf, k);
                 }
                 wait_buf(k);
@@ -1010,16 +1012,16 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
 
             // stage the next distinct block into the other buffer
             {
-                long long nb = -1;
+                long long nb = kNone;
                 for (long long kk = kp + 1; kk < npass; kk++) {
                     const long long bb = pass_block(kk);
                     if (bb != b) { nb = bb; break; }
                 }
-                if (nb < 0 && u + gridDim.x < P.unit_end) {
+                if (nb == kNone && u + gridDim.x < P.unit_end) {
                     const long long bb = first_block(u + gridDim.x);
                     if (bb != b) nb = bb;
                 }
-                if (nb >= 0 && bufblk_get(cur ^ 1) != nb) {
+                if (nb != kNone && bufblk_get(cur ^ 1) != nb) {
                     stage(nb, cur ^ 1);
                     if (tid == 0) {
                         const long long pb = nb + 1;   // warm L2 one block further ahead
@@ -1316,7 +1318,7 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
                 const int nz = zlen >> 4;
                 for (int i = tid; i < nz; i += NCT) w4[i] = make_uint4(0u, 0u, 0u, 0u);
                 if (tid == 0) w4[0] = make_uint4(S->tail[0], S->tail[1], S->tail[2], S->tail[3]);
-                bufblk_set(cur, -1);
+                bufblk_set(cur, kNone);
             }
             cbar();  // B4
             PROF_MARK(3);
@@ -1548,12 +1550,12 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
             PROF_MARK(4);
             // ============ phase A of the next pass block (overlaps this block's tail) ============
             {
-                long long nb = -1;
+                long long nb = kNone;
                 bool nfirst = false;
                 if (kp + 1 < npass) nb = pass_block(kp + 1);
                 else if (u + gridDim.x < P.unit_end) { nb = first_block(u + gridDim.x); nfirst = true; }
-                a_done = -1;
-                if (nb >= 0) {
+                a_done = kNone;
+                if (nb != kNone) {
                     const int k = (bb0 == nb) ? 0 : ((bb1 == nb) ? 1 : -1);
                     if (k >= 0) {
                         wait_buf(k);

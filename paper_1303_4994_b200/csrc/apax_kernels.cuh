@@ -33,6 +33,8 @@ struct EncParams {
     double pow10_t20;             // 10**(T/20), glibc (codec.py:167)
     double sqrt12;                // math.sqrt(12)
     double* trace;                // nullable, 10 doubles per block
+    long long gblock0;            // v3 lossless range encode: global index of block 0
+                                  // (x[-bs-2 .. 0) holds the halo when > 0)
 };
 
 struct DecParams {

@@ -19,6 +19,12 @@ get that map (apax_decode_range with map_out), the R maps (6 words each) are
 all-gathered and composed in rank order, and every rank re-decodes its range
 from its exact entry history (App. B of SURVEY.md).
 
+Whole-stream LOSSLESS encode: blocks depend on their predecessor only
+through the previous block's costs and the last two samples, so ranks own
+contiguous block ranges and each receives the (bs + 2)-sample halo before
+its range from rank r-1 (one all-gather of R tails); the bodies then
+concatenate into the one-GPU whole-stream container.
+
 Profiler: per-rank sums are all-gathered and added in rank order, so the
 result is deterministic and independent of the collective's reduction tree.
 
@@ -197,3 +203,42 @@ def sharded_decode_whole_stream(blob, nbytes: int, offsets, group=None):
     entry = whole_stream_entry(m, group, blob.device)
     y, _ = decode_range(blob, nbytes, offsets, count, cfg.dtype, cfg.block_size, b0, b1, entry=entry)
     return y, (b0, b1)
+
+
+
+# ---------------------------------------------------------------------------
+# whole-stream LOSSLESS encode across ranks: halo exchange
+# ---------------------------------------------------------------------------
+def lossless_halo(x_local, block_size: int, group=None):
+    """The (bs + 2) samples before this rank's range, from rank r-1: one
+    all-gather of every rank's tail (equal lengths; a rank whose range is
+    shorter pads on the left).  Rank 0 receives an empty halo."""
+    import torch
+    import torch.distributed as dist
+    h = block_size + 2
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    tail = x_local[-h:] if x_local.numel() >= h else x_local
+    pad = torch.zeros(h, dtype=x_local.dtype, device=x_local.device)
+    pad[h - tail.numel():] = tail
+    out = torch.empty(world * h, dtype=x_local.dtype, device=x_local.device)
+    dist.all_gather_into_tensor(out, pad, group=group)
+    if rank == 0:
+        return x_local[:0]
+    return out[(rank - 1) * h: rank * h]
+
+
+def sharded_encode_lossless_whole_stream(x_local, first_block: int, dtype, block_size: int, group=None):
+    """Encode this rank's block range of a whole-stream LOSSLESS container:
+    halo exchange, range encode on this rank's GPU, body placement.  Returns
+    (body bytes, ShardPlacement, global block offsets).  Every rank's range
+    must start on a block boundary (shard_blocks)."""
+    import torch
+    from .codec import encode_lossless_range
+    halo = lossless_halo(x_local, block_size, group)
+    x_ext = torch.cat([halo, x_local]) if halo.numel() else x_local
+    res = encode_lossless_range(x_ext, halo.numel(), first_block, dtype, block_size)
+    body_len = res.nbytes - FILE_HEADER_SIZE
+    place = place_bodies(body_len, group, x_local.device)
+    body = bytes(res.blob[FILE_HEADER_SIZE:res.nbytes].cpu().numpy().tobytes())
+    offs = global_block_offsets(res.block_offsets.cpu().numpy(), place)
+    return body, place, offs

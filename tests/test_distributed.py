@@ -139,3 +139,31 @@ def test_two_rank_gloo_whole_stream_entries(tmp_path):
     mp.spawn(_entry_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
     for r in range(2):
         assert json.loads((tmp_path / f"entry{r}.json").read_text()) == {"ok": True}
+
+
+def _halo_worker(rank, world, port, out_dir):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    bs, nb = 64, 11
+    x = torch.arange(bs * nb - 5, dtype=torch.int32) * 7 - 300
+    b0, b1 = D.shard_blocks(nb, world, rank)
+    s0, s1 = b0 * bs, min(x.numel(), b1 * bs)
+    halo = D.lossless_halo(x[s0:s1], bs)
+    want = x[max(0, s0 - bs - 2):s0]
+    ok = torch.equal(halo, want) if rank > 0 else halo.numel() == 0
+    with open(os.path.join(out_dir, f"halo{rank}.json"), "w") as f:
+        json.dump({"ok": bool(ok)}, f)
+    dist.destroy_process_group()
+
+
+def test_three_rank_gloo_lossless_halo(tmp_path):
+    """Rank r's halo for a whole-stream LOSSLESS encode is the (bs + 2)
+    samples before its block range (the all-gather of rank tails)."""
+    import torch.multiprocessing as mp
+    port = _free_port()
+    mp.spawn(_halo_worker, args=(3, port, str(tmp_path)), nprocs=3, join=True)
+    for r in range(3):
+        assert json.loads((tmp_path / f"halo{r}.json").read_text()) == {"ok": True}
