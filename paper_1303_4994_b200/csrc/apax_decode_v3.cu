@@ -9,21 +9,27 @@
 // derivative history (transform.py:31-49) stays in shared memory and no
 // cross-block carry protocol is needed; segments are spread over the CTAs.
 //
-// Per block (256 threads, 16 samples per thread):
-//   * the block (header + payload) arrives by one TMA bulk copy issued while
-//     the previous block was decoded;
-//   * JEE (entropy.py:118-164): every thread parses the tokens that start in
-//     its 4-nibble slice (two consecutive non-15 nibbles always precede a
-//     token start), then one CTA scan of (exponent count, escape reset,
-//     running value) places every exponent; an irregular stream re-runs the
-//     exact serial parser (apax_jee.cuh) for the reference's status code;
+// Blocks go in batches of JB = 8:
+//   * JEE (entropy.py:118-164): warp w parses block w of the batch straight
+//     from global memory, 4 nibbles per lane and 128 per step (two
+//     consecutive non-15 nibbles always precede a token start, so each lane
+//     finds its token starts from a 16-nibble window; one warp scan of
+//     (count, escape reset, running value) places the exponents); no CTA
+//     barrier inside, and any irregularity re-runs the exact parser
+//     (apax_jee.cuh) for the reference's status code;
+//   * then the CTA decodes the batch's blocks in order (256 threads, 16
+//     samples per thread), each block (header + payload) arriving by one TMA
+//     bulk copy issued while the previous block was decoded:
 //   * mantissa bit offsets: a CTA scan of 4*sum(e) over the thread's 4
 //     groups; 32-bit funnel windows + signed bit-field extracts unpack them
 //     (entropy.py:249-277);
-//   * D1/D2 (transform.py:116-129) in 64-bit: one CTA scan of (sum, sum of
-//     partial sums) per block, then d1 += v; q += d1 per sample;
+//   * D1/D2 (transform.py:116-129): one CTA scan of (sum, sum of partial
+//     sums) in 64-bit gives each thread its entry values; narrow blocks then
+//     run the per-sample sums in 32-bit wrap-around arithmetic (exact: the
+//     entry values bound every output inside int32);
 //   * dequantize (codec.py:135-146) with the Markstein quotient, y staged in
-//     shared memory, one TMA bulk store per block.
+//     the block's own (now dead) payload buffer (f64: its own buffer), one
+//     TMA bulk store per block.
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -43,6 +49,8 @@ constexpr int NW = NT / 32;
 constexpr int SPT = 16;
 constexpr int MAXBS = 4096;
 constexpr int NIB_PER_PASS = 4 * NT;
+constexpr int JB = 8;                                  // blocks per JEE batch (one warp each)
+constexpr int EBS = MAXBS / 4 + 128;                   // exponent bytes per batch slot
 constexpr double kMagicI = 6755401588539392.0;   // 1.5 * 2^52 + 2^31
 
 struct __align__(16) St {
@@ -61,6 +69,7 @@ struct __align__(16) St {
     unsigned bits_w[NW];
     long long rs_w[NW], rt_w[NW];
     int store_pending;
+    int jst[JB], jused[JB];   // JEE batch: status (0 ok) and nibbles used per slot
 };
 
 using namespace apax::tma;
@@ -89,6 +98,158 @@ __device__ __forceinline__ uint32_t r32(const uint32_t* w, int bp) {
     return __funnelshift_l(bswap32(w[k + 1]), bswap32(w[k]), (unsigned)(bp & 31));
 }
 
+
+// ---------------------------------------------------------------------------
+// JEE decode of one block by one warp (entropy.py:118-164), reading the
+// nibble stream straight from global memory (read-only path): 128 nibbles
+// per step, 4 per lane.  Two consecutive non-15 nibbles always precede a
+// token start, so every lane finds the token starts in its slice from a
+// 16-nibble window; one warp scan of (exponent count, escape reset, running
+// value) places the exponents.  Returns 0 with e[0..G) and *used (nibbles
+// consumed), or -1 on ANY irregularity (reserved nibble, range, truncation,
+// missing opening escape, joint token past the last group): the caller then
+// runs the exact parser (apax_jee.cuh), which reports the reference's first
+// error.  e must hold G + 128 bytes (tokens are written before validation).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int warp_jee_fast(const uint8_t* p, const uint8_t* pend, int total, int G,
+                                             uint8_t* e, int& used) {
+    const int lane = threadIdx.x & 31;
+    constexpr unsigned long long LUT_C = 0x43210cbaba9a98ull;    // bit 3 joint, bits 0-2 delta sum + 2
+    constexpr unsigned long long LUT_D1 = 0x43210333222111ull;   // first exponent's delta + 2
+    constexpr unsigned LUT_D2 = 0x24924u;                        // (2-bit) second delta + 1
+    int cbase = 0, vbase = 0;
+    for (int base = 0; base < total + 4; base += 128) {
+        const int p0 = base + 4 * lane;
+        // nibbles p0-4 .. p0+11 (zero beyond `total`); bytes before p are the
+        // block header (>= 4 bytes), so p0 = 0 reads inside the container
+        unsigned long long W = 0ULL;
+        if (p0 - 4 < total) {
+            const uint8_t* bp = p + (p0 >> 1) - 2;
+            const uintptr_t a = (uintptr_t)bp;
+            const uint32_t* wp = (const uint32_t*)(a & ~(uintptr_t)3);
+            const unsigned sh = (unsigned)(a & 3) * 8u;
+            uint32_t w0, w1, w2;
+            if ((const uint8_t*)(wp + 3) <= pend) {
+                w0 = bswap32(__ldg(wp)); w1 = bswap32(__ldg(wp + 1)); w2 = bswap32(__ldg(wp + 2));
+            } else {   // the last words of the container: bytewise, zero past the end
+                uint32_t w[3];
+                for (int k = 0; k < 3; k++) {
+                    uint32_t v = 0;
+                    for (int c = 0; c < 4; c++) {
+                        const uint8_t* q = (const uint8_t*)(wp + k) + c;
+                        v = (v << 8) | (q < pend ? (uint32_t)*q : 0u);
+                    }
+                    w[k] = v;
+                }
+                w0 = w[0]; w1 = w[1]; w2 = w[2];
+            }
+            W = ((unsigned long long)__funnelshift_l(w1, w0, sh) << 32) | __funnelshift_l(w2, w1, sh);
+            const int rem = total - (p0 - 4);
+            if (rem < 16) W = rem <= 0 ? 0ULL : (W & (~0ULL << (4 * (16 - rem))));
+        }
+        auto nw = [&](int k) -> int { return (int)((W >> (4 * (11 - k))) & 15ULL); };   // k in -4..11
+        // leading positions covered by an escape that started before p0
+        int skip = 0;
+        if (p0 > 0 && p0 < total + 4) {
+            const bool f1 = nw(-1) == 15, f2 = nw(-2) == 15, f3 = nw(-3) == 15, f4 = nw(-4) == 15;
+            if (!f1 && !f2) skip = 0;
+            else if (!f2 && !f3) skip = f1 ? 2 : 0;
+            else if (!f3 && !f4) skip = f2 ? 1 : (f1 ? 2 : 0);
+            else {
+                // long escape run: walk back to a definite start (rare)
+                auto nb = [&](int k) -> int {
+                    if (k >= total) return 0;
+                    const uint8_t b = p[k >> 1];
+                    return (k & 1) ? (b & 15) : (b >> 4);
+                };
+                int q = p0;
+                while (q > 0 && !(nb(q - 1) != 15 && (q < 2 || nb(q - 2) != 15))) q--;
+                int pos = q;
+                while (pos < p0) pos += (nb(pos) == 15) ? 3 : 1;
+                skip = pos - p0;
+            }
+        }
+        const bool n0f = nw(0) == 15, n1f = nw(1) == 15, n2f = nw(2) == 15;
+        const bool st0 = skip == 0;
+        const bool st1 = skip == 1 || (st0 && !n0f);
+        const bool st2 = skip == 2 || (st1 && !n1f);
+        const bool st3 = (st2 && !n2f) || (st0 && n0f);
+        const bool stv[4] = {st0, st1, st2, st3};
+        const bool live = p0 < total + 4;
+        int cnt = 0, flag = 0, val = 0;
+        int kv[4], kab[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int v = nw(k);
+            const int ab = (int)((W >> (4 * (9 - k))) & 0xffULL);   // nibbles k+1, k+2
+            kv[k] = v;
+            kab[k] = ab;
+            const int cd = (int)((LUT_C >> (4 * v)) & 15ull);
+            const bool esc = v == 15;
+            const int c = esc ? 1 : (cd >> 3) + 1;
+            const int dv = (cd & 7) - 2;
+            const bool t = stv[k] && live;
+            cnt += t ? c : 0;
+            val = t ? (esc ? ab : val + dv) : val;
+            flag |= (t && esc) ? 1 : 0;
+        }
+        // warp scan of (cnt, flag, val): A then B = (cA+cB, fA|fB, fB ? vB : vA+vB)
+        int c_i = cnt, f_i = flag, v_i = val;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int oc = __shfl_up_sync(0xffffffffu, c_i, d);
+            const int of = __shfl_up_sync(0xffffffffu, f_i, d);
+            const int ov = __shfl_up_sync(0xffffffffu, v_i, d);
+            if (lane >= d) {
+                c_i += oc;
+                if (!f_i) v_i += ov;
+                f_i |= of;
+            }
+        }
+        int ec = __shfl_up_sync(0xffffffffu, c_i, 1), ef = __shfl_up_sync(0xffffffffu, f_i, 1),
+            evv = __shfl_up_sync(0xffffffffu, v_i, 1);
+        if (lane == 0) { ec = 0; ef = 0; evv = 0; }
+        int idx = cbase + ec;
+        int curv = ef ? evv : vbase + evv;
+        int key = 0x7fffffff;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int pos = p0 + k;
+            const int v = kv[k];
+            const bool t = stv[k] && live && idx < G;   // tokens after the G-th exponent are not read
+            const bool esc = v == 15;
+            const int cd = (int)((LUT_C >> (4 * v)) & 15ull);
+            const bool joint = !esc && (cd >> 3) != 0;
+            const int e1 = esc ? kab[k] : curv + (int)((LUT_D1 >> (4 * v)) & 15ull) - 2;
+            const int e2 = e1 + (int)((LUT_D2 >> (2 * v)) & 3u) - 1;
+            const bool bad = (pos + (esc ? 2 : 0) >= total) | (v == 14) | (!esc & (idx == 0)) |
+                             ((unsigned)e1 > 34u) | (joint & ((idx + 1 >= G) | ((unsigned)e2 > 34u)));
+            const int nexp = joint ? 2 : 1;
+            const bool done = idx + nexp >= G;
+            if (t) {
+                e[idx] = (uint8_t)e1;
+                if (joint) e[idx + 1] = (uint8_t)e2;
+            }
+            const int kk2 = bad ? 1 : (done ? ((pos + (esc ? 3 : 1)) << 1) : 0x7fffffff);
+            key = t ? min(key, kk2) : key;
+            curv = t ? (joint ? e2 : e1) : curv;
+            idx += t ? nexp : 0;
+        }
+        key = __reduce_min_sync(0xffffffffu, key);
+        if (key != 0x7fffffff) {
+            if (key & 1) return -1;
+            used = key >> 1;
+            return 0;
+        }
+        // the next step continues the scan
+        const int tc = __shfl_sync(0xffffffffu, c_i, 31), tf = __shfl_sync(0xffffffffu, f_i, 31),
+                  tv = __shfl_sync(0xffffffffu, v_i, 31);
+        cbase += tc;
+        vbase = tf ? tv : vbase + tv;
+    }
+    return -1;
+}
+
 template <int DT, bool FIX>
 __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P) {
     using Tr = DT_<DT>;
@@ -100,10 +261,13 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
 
     St* S = (St*)smem;
     size_t off = (sizeof(St) + 127) & ~(size_t)127;
-    uint8_t* ebuf = smem + off;                           // group exponents
-    off += ((size_t)MAXBS / 4 + 128 + 127) & ~(size_t)127;
-    T* ybuf = (T*)(smem + off);                           // decoded block
-    off += ((size_t)MAXBS * sizeof(T) + 127) & ~(size_t)127;
+    uint8_t* ebufs = smem + off;                          // group exponents, JB slots
+    off += (size_t)JB * (((size_t)EBS + 127) & ~(size_t)127);
+    // decoded block: f64 has its own buffer; narrower types reuse the block's
+    // payload buffer, dead once every thread holds its unpacked values
+    constexpr bool YOWN = (DT == 4);
+    T* ybuf_own = (T*)(smem + off);
+    if (YOWN) off += ((size_t)MAXBS * sizeof(T) + 127) & ~(size_t)127;
     const int bufsz = (P.payload_cap + 64 + 127) & ~127;
     uint8_t* pbuf0 = smem + off;
     uint8_t* pbuf1 = smem + off + bufsz;
@@ -164,12 +328,40 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
     __syncthreads();
 
     int kk = 0;   // blocks decoded by this CTA (buffer parity)
-    int jprev = NIB_PER_PASS;   // JEE nibbles of the previous block (first-pass length guess)
     for (long long sg = s_begin + blockIdx.x; sg < s_end; sg += gridDim.x) {
         const long long b0 = sg * P_seg;
         const long long b1 = (b0 + P_seg < P.n_blocks) ? b0 + P_seg : P.n_blocks;
         if (tid == 0) { S->p1 = 0; S->p2 = 0; }
-        for (long long b = b0; b < b1; b++, kk++) {
+        for (long long bb = b0; bb < b1; bb += JB) {
+        const int nbat = (int)((b1 - bb) < JB ? (b1 - bb) : JB);
+        // ---- JEE of the batch (entropy.py:118-164): warp w parses block bb + w
+        // from global memory, no CTA barrier inside; the CTA phases below use it
+        if (warp < nbat) {
+            const long long bj = bb + warp;
+            const long long sj = bj * (long long)bs;
+            const int nj = FIX ? MAXBS : (int)((P.n - sj) < bs ? (P.n - sj) : bs);
+            const int Gj = FIX ? MAXBS / 4 : (nj + 3) >> 2;
+            const long long o0 = P.offsets[bj];
+            int st = 0, u = 0;
+            if (o0 >= 0 && P.nbytes - o0 >= HS) {
+                const long long ps = o0 + HS;
+                const long long avl = P.nbytes - ps;
+                const int maxj = (3 * Gj + 2) / 2;
+                const int nbj = (int)(avl < maxj ? avl : maxj);
+                uint8_t* ej = ebufs + (size_t)warp * (((size_t)EBS + 127) & ~(size_t)127);
+                st = warp_jee_fast(P.blob + ps, P.blob + P.nbytes, 2 * nbj, Gj, ej, u);
+                if (st < 0) {   // exact serial semantics and status code (apax_jee.cuh)
+                    long long u2 = 0, esum = 0;
+                    st = warp_jee_decode(P.blob + ps, 2LL * nbj, Gj, ej, u2, esum);
+                    u = (int)u2;
+                }
+            }
+            if (lane == 0) { S->jst[warp] = st; S->jused[warp] = u; }
+        }
+        cbar();
+        for (int kb = 0; kb < nbat; kb++, kk++) {
+            const long long b = bb + kb;
+            uint8_t* ebuf = ebufs + (size_t)kb * (((size_t)EBS + 127) & ~(size_t)127);
             const int cur = kk & 1;
             uint8_t* pay = cur ? pbuf1 : pbuf0;
             const long long start = b * (long long)bs;
@@ -181,6 +373,8 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                 long long nb = -1;
                 if (b + 1 < b1) nb = b + 1;
                 else if (sg + gridDim.x < s_end) nb = (sg + gridDim.x) * P_seg;
+                // the other buffer may still be read by the previous block's y store
+                if (!YOWN && S->store_pending) { bulk_wait_read(); S->store_pending = 0; }
                 if (nb >= 0) issue(nb, cur ^ 1);
             }
             const bool was_tma = S->ld_tma[cur] != 0;
@@ -210,236 +404,13 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                 fbe = Tr::F ? (int)(int8_t)h[4] : 0;
                 if (sel == 3) err = APAX_ERR_SELECTOR;
             }
-            // ---- JEE: parallel token parse ----
+            // ---- JEE exponents: parsed by the batch's warp (above) ----
             int used = 0;
             if (!err) {
-                const uint8_t* p = pay + pay_off;
-                const int maxj = (3 * G + 2) / 2;
-                const int nbj = avail < maxj ? avail : maxj;
-                const int total = 2 * nbj;
-                const int stotal = min(2 * staged, total);
-                int cbase = 0, vbase = 0;
-                // The first pass covers only a guess of the JEE length (1.25x the
-                // previous block's + 64 nibbles, whole warps); warps past it skip
-                // the parse.  A stream that runs longer simply takes more passes.
-#ifndef APAX_D3_JEE_SLACK
-#define APAX_D3_JEE_SLACK 4   // first-pass length: previous JEE length x (1 + 2^-SLACK) + 64 nibbles
-#endif
-                const int lim0 = min(NIB_PER_PASS, (jprev + (jprev >> APAX_D3_JEE_SLACK) + 64 + 127) & ~127);
-                for (int pass_base = 0, span = lim0;; pass_base += span, span = NIB_PER_PASS) {
-                    const int p0 = pass_base + 4 * tid;
-                    const bool wact = 128 * warp < span && pass_base + 128 * warp < stotal + 4;   // warp-uniform
-                    auto nb = [&](int k) -> int {
-                        if (k >= stotal) return 0;
-                        const uint8_t bb = p[k >> 1];
-                        return (k & 1) ? (bb & 15) : (bb >> 4);
-                    };
-                    // nibbles p0-4 .. p0+11 of the JEE stream in one 64-bit window
-                    // (zero beyond the staged nibbles)
-                    unsigned long long W = 0ULL;
-                    int skip = 0;
-                    bool stv[4] = {false, false, false, false};
-                    int kv[4] = {0, 0, 0, 0}, kab[4] = {0, 0, 0, 0};
-                    bool live = false;
-                    int c_i = 0, f_i = 0, v_i = 0;
-                    auto nw = [&](int k) -> int { return (int)((W >> (4 * (11 - k))) & 15ULL); };   // k in -4..11
-                    constexpr unsigned long long LUT_C = 0x43210cbaba9a98ull;
-                    constexpr unsigned long long LUT_D1 = 0x43210333222111ull;
-                    constexpr unsigned LUT_D2 = 0x24924u;
-                    if (wact) {
-                    if (p0 - 4 < stotal) {   // (beyond: no nibbles, and no reads past the buffer)
-                        const int byte0 = (int)pay_off + (p0 >> 1) - 2;   // pay_off >= HS >= 4
-                        const uint32_t* pw = (const uint32_t*)pay;
-                        const int wi = byte0 >> 2;
-                        const unsigned sh = (unsigned)(byte0 & 3) * 8u;
-                        const uint32_t w0 = bswap32(pw[wi]), w1 = bswap32(pw[wi + 1]), w2 = bswap32(pw[wi + 2]);
-                        W = ((unsigned long long)__funnelshift_l(w1, w0, sh) << 32) | __funnelshift_l(w2, w1, sh);
-                        const int rem = stotal - (p0 - 4);
-                        if (rem < 16) W = rem <= 0 ? 0ULL : (W & (~0ULL << (4 * (16 - rem))));
-                    }
-                    // leading positions covered by an escape that started before p0:
-                    // two consecutive non-15 nibbles are always followed by a token start
-                    if (p0 > 0 && p0 < stotal + 4) {
-                        const bool f1 = nw(-1) == 15, f2 = nw(-2) == 15, f3 = nw(-3) == 15, f4 = nw(-4) == 15;
-                        if (!f1 && !f2) skip = 0;
-                        else if (!f2 && !f3) skip = f1 ? 2 : 0;
-                        else if (!f3 && !f4) skip = f2 ? 1 : (f1 ? 2 : 0);
-                        else {
-                            // long escape run: walk back to a definite start (rare)
-                            auto nb = [&](int k) -> int {
-                                if (k >= stotal) return 0;
-                                const uint8_t bb = p[k >> 1];
-                                return (k & 1) ? (bb & 15) : (bb >> 4);
-                            };
-                            int q = p0;
-                            while (q > 0 && !(nb(q - 1) != 15 && (q < 2 || nb(q - 2) != 15))) q--;
-                            int pos = q;
-                            while (pos < p0) pos += (nb(pos) == 15) ? 3 : 1;
-                            skip = pos - p0;
-                        }
-                    }
-                    // token starts among this thread's 4 positions
-                    const bool n0f = nw(0) == 15, n1f = nw(1) == 15, n2f = nw(2) == 15;
-                    const bool st0 = skip == 0;
-                    const bool st1 = skip == 1 || (st0 && !n0f);
-                    const bool st2 = skip == 2 || (st1 && !n1f);
-                    const bool st3 = (st2 && !n2f) || (st0 && n0f);
-                    stv[0] = st0; stv[1] = st1; stv[2] = st2; stv[3] = st3;
-                    // Branch-free token summary (count, escape flag, running value)
-                    // of the thread's starts from 16-entry nibble tables packed in
-                    // immediates (entropy.py:118-164 token alphabet):
-                    //   LUT_C  bit 3 = joint token (two exponents), bits 0-2 = delta sum + 2
-                    //   LUT_D1 first exponent's delta + 2;  LUT_D2 (2-bit) second delta + 1
-                    // Reserved nibbles, unstaged positions and range errors only raise
-                    // an error event (below); their contributions are never used.
-                    live = 4 * tid < span && p0 < stotal + 4;   // in this pass, any of the slice staged
-                    int cnt = 0, flag = 0, val = 0;
-#pragma unroll
-                    for (int k = 0; k < 4; k++) {
-                        const int v = nw(k);
-                        const int ab = (int)((W >> (4 * (9 - k))) & 0xffULL);   // nibbles k+1, k+2
-                        kv[k] = v;
-                        kab[k] = ab;
-                        const int cd = (int)((LUT_C >> (4 * v)) & 15ull);
-                        const bool esc = v == 15;
-                        const int c = esc ? 1 : (cd >> 3) + 1;
-                        const int dv = (cd & 7) - 2;
-                        const bool t = stv[k] && live;
-                        cnt += t ? c : 0;
-                        val = t ? (esc ? ab : val + dv) : val;
-                        flag |= (t && esc) ? 1 : 0;
-                    }
-                    // warp scan of (cnt, flag, val): A then B = (cA+cB, fA|fB, fB ? vB : vA+vB)
-                    c_i = cnt; f_i = flag; v_i = val;
-#pragma unroll
-                    for (int d = 1; d < 32; d <<= 1) {
-                        const int oc = __shfl_up_sync(0xffffffffu, c_i, d);
-                        const int of = __shfl_up_sync(0xffffffffu, f_i, d);
-                        const int ov = __shfl_up_sync(0xffffffffu, v_i, d);
-                        if (lane >= d) {
-                            c_i += oc;
-                            if (!f_i) v_i += ov;
-                            f_i |= of;
-                        }
-                    }
-                    }   // wact
-                    if (lane == 31) { S->sc_cnt[warp] = c_i; S->sc_flag[warp] = f_i; S->sc_val[warp] = v_i; }
-                    cbar();
-                    // prefix over the previous warps (lanes 0..NW-1) and the previous pass
-                    int pc, pf, pv;
-                    {
-                        const int w = lane & (NW - 1);
-                        int wc = (lane < NW) ? S->sc_cnt[w] : 0, wf = (lane < NW) ? S->sc_flag[w] : 0;
-                        int wv = (lane < NW) ? S->sc_val[w] : 0;
-#pragma unroll
-                        for (int d = 1; d < NW; d <<= 1) {
-                            const int oc = __shfl_up_sync(0xffffffffu, wc, d);
-                            const int of = __shfl_up_sync(0xffffffffu, wf, d);
-                            const int ov = __shfl_up_sync(0xffffffffu, wv, d);
-                            if (lane >= d) {
-                                wc += oc;
-                                if (!wf) wv += ov;
-                                wf |= of;
-                            }
-                        }
-                        // exclusive for warp `warp`
-                        int ec = __shfl_up_sync(0xffffffffu, wc, 1), ef = __shfl_up_sync(0xffffffffu, wf, 1);
-                        int evv = __shfl_up_sync(0xffffffffu, wv, 1);
-                        if (lane == 0) { ec = 0; ef = 0; evv = 0; }
-                        pc = __shfl_sync(0xffffffffu, ec, warp);
-                        pf = __shfl_sync(0xffffffffu, ef, warp);
-                        pv = __shfl_sync(0xffffffffu, evv, warp);
-                        // pass totals for the next pass
-                        const int tc = __shfl_sync(0xffffffffu, wc, NW - 1);
-                        const int tf = __shfl_sync(0xffffffffu, wf, NW - 1);
-                        const int tv = __shfl_sync(0xffffffffu, wv, NW - 1);
-                        const int nbase_c = cbase + tc;
-                        const int nbase_v = tf ? tv : vbase + tv;
-                        pc += cbase;
-                        pv = pf ? pv : vbase + pv;
-                        cbase = nbase_c;
-                        vbase = nbase_v;
-                    }
-                    // this thread's exclusive prefix inside its warp
-                    int ec = __shfl_up_sync(0xffffffffu, c_i, 1), ef = __shfl_up_sync(0xffffffffu, f_i, 1),
-                        evv = __shfl_up_sync(0xffffffffu, v_i, 1);
-                    if (lane == 0) { ec = 0; ef = 0; evv = 0; }
-                    int idx = pc + ec;
-                    int curv = ef ? evv : pv + evv;
-                    // evaluate the thread's tokens in order: exponents into ebuf, and the
-                    // first event (error, or the token that completes G exponents) as
-                    // key = position << 1 | is_error
-                    int key = 0x7fffffff;
-                    if (wact) {
-#pragma unroll
-                    for (int k = 0; k < 4; k++) {
-                        const int pos = p0 + k;
-                        const int v = kv[k];
-                        const bool t = stv[k] && live && idx < G;   // tokens after the G-th exponent are not read
-                        const bool esc = v == 15;
-                        const int cd = (int)((LUT_C >> (4 * v)) & 15ull);
-                        const bool joint = !esc && (cd >> 3) != 0;
-                        const int e1 = esc ? kab[k] : curv + (int)((LUT_D1 >> (4 * v)) & 15ull) - 2;
-                        const int e2 = e1 + (int)((LUT_D2 >> (2 * v)) & 3u) - 1;
-                        // any irregularity (truncation, reserved nibble 14, a stream
-                        // not opening with an escape, an exponent outside [0, 34],
-                        // a joint token past the last group) makes the whole block
-                        // re-run the exact serial parser, which reports the
-                        // reference's first error: one flag is enough (key 1 sorts
-                        // before every completion key), and the exponents written
-                        // here are then rewritten (ebuf has G + 128 bytes)
-                        const bool bad = (pos + (esc ? 2 : 0) >= stotal) | (v == 14) | (!esc & (idx == 0)) |
-                                         ((unsigned)e1 > 34u) | (joint & ((idx + 1 >= G) | ((unsigned)e2 > 34u)));
-                        const int nexp = joint ? 2 : 1;
-                        const bool done = idx + nexp >= G;
-                        if (t) {
-                            ebuf[idx] = (uint8_t)e1;
-                            if (joint) ebuf[idx + 1] = (uint8_t)e2;
-                        }
-                        const int kk2 = bad ? 1 : (done ? ((pos + (esc ? 3 : 1)) << 1) : 0x7fffffff);
-                        key = t ? min(key, kk2) : key;
-                        curv = t ? (joint ? e2 : e1) : curv;
-                        idx += t ? nexp : 0;
-                    }
-                    }   // wact
-                    key = __reduce_min_sync(0xffffffffu, key);
-                    if (lane == 0) S->ev_min[warp] = key;
-                    cbar();
-                    int kmin = (lane < NW) ? S->ev_min[lane & (NW - 1)] : 0x7fffffff;
-                    kmin = __reduce_min_sync(0xffffffffu, kmin);
-                    int fallback = 0, fev;
-                    if (kmin == 0x7fffffff) {
-                        if (pass_base + span >= stotal) { fallback = 1; fev = -1; }
-                        else fev = -2;
-                    } else if (kmin & 1) {
-                        fallback = 1;
-                        fev = kmin >> 1;
-                    } else {
-                        fev = kmin >> 1;
-                        used = kmin >> 1;
-                    }
-                    if (fev != -2) {
-                        if (fallback) {
-                            // exact serial parse (reference semantics and status code)
-                            cbar();
-                            if (warp == 0) {
-                                long long u2 = 0, esum = 0;
-                                const int st = warp_jee_decode(P.blob + boff + HS, 2LL * nbj, G, ebuf, u2, esum);
-                                if (lane == 0) { S->err = st; S->used = (int)u2; }
-                            }
-                            cbar();
-                            err = S->err;
-                            used = S->used;
-                            cbar();
-                        }
-                        break;
-                    }
-                    cbar();   // the per-warp words are rewritten by the next pass
-                }
-                (void)total;
+                err = S->jst[kb];
+                used = S->jused[kb];
             }
             const int jee_bytes = (used + 1) >> 1;
-            if (!err) jprev = used;
             // ---- mantissa offsets (entropy.py:209-219): CTA scan of 4*sum(e) ----
             const int g0 = 4 * tid;
             const bool active = FIX ? true : (g0 < G);
@@ -671,8 +642,9 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                 }
             }
             // ---- y staged in shared memory, one TMA bulk store per block ----
-            if (tid == 0 && S->store_pending) { bulk_wait_read(); S->store_pending = 0; }
-            cbar();   // the previous block's store has read the y buffer
+            T* ybuf = YOWN ? ybuf_own : (T*)pay;
+            if (YOWN && tid == 0 && S->store_pending) { bulk_wait_read(); S->store_pending = 0; }
+            cbar();   // the y buffer is free: the previous store has read it (f64) / the payload is unpacked
             if (active) {
                 constexpr int PER = 16 / (int)sizeof(T);
                 uint4* y4 = (uint4*)(ybuf + SPT * tid);
@@ -697,7 +669,8 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                     for (int i = 0; i < bytes; i++) ((uint8_t*)y)[i] = ((const uint8_t*)ybuf)[i];
                 }
             }
-        }
+        }   // blocks of the batch
+        }   // batches
     }
     if (tid == 0 && S->store_pending) bulk_wait_all();
 }
@@ -706,7 +679,7 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
 
 size_t decode_v3_smem_bytes(int dt, int payload_cap) {
     auto al = [](size_t v) { return (v + 127) & ~(size_t)127; };
-    return al(sizeof(d3::St)) + al((size_t)d3::MAXBS / 4 + 128) + al((size_t)d3::MAXBS * dt_width(dt)) +
+    return al(sizeof(d3::St)) + (size_t)d3::JB * al((size_t)d3::EBS) + (dt == 4 ? al((size_t)d3::MAXBS * 8) : 0) +
            2 * (size_t)((payload_cap + 64 + 127) & ~127);
 }
 
