@@ -70,6 +70,7 @@ struct __align__(16) St {
     long long rs_w[NW], rt_w[NW];
     int store_pending;
     int jst[JB], jused[JB];   // JEE batch: status (0 ok) and nibbles used per slot
+    unsigned wbits[JB][8];    // mantissa bits up to the end of each decode warp's 128 groups
 };
 
 using namespace apax::tma;
@@ -355,6 +356,29 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                     st = warp_jee_decode(P.blob + ps, 2LL * nbj, Gj, ej, u2, esum);
                     u = (int)u2;
                 }
+                if (st == 0) {
+                    // mantissa bits (entropy.py:209-219) per decode warp (128 groups
+                    // = 4 lanes of 32 here): the decode phase then needs only a warp scan
+                    unsigned sb = 0;
+#pragma unroll
+                    for (int k = 0; k < 32; k += 4) {
+                        const int g = 32 * lane + k;
+                        uint32_t ew;
+                        if (FIX || g + 4 <= Gj) ew = *(const uint32_t*)(ej + g);
+                        else {
+                            ew = 0;
+                            for (int c = 0; c < 4; c++) ew |= (g + c < Gj ? (uint32_t)ej[g + c] : 0u) << (8 * c);
+                        }
+                        sb += (unsigned)__dp4a(ew, 0x01010101u, 0u);
+                    }
+                    sb *= 4u;
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const unsigned o = __shfl_up_sync(0xffffffffu, sb, d);
+                        if (lane >= d) sb += o;
+                    }
+                    if ((lane & 3) == 3) S->wbits[warp][lane >> 2] = sb;
+                }
             }
             if (lane == 0) { S->jst[warp] = st; S->jused[warp] = u; }
         }
@@ -427,21 +451,9 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                 const unsigned o = __shfl_up_sync(0xffffffffu, xb, d);
                 if (lane >= d) xb += o;
             }
-            if (lane == 31) S->bits_w[warp] = xb;
-            cbar();
-            unsigned bpre, btot;
-            {
-                unsigned wb = (lane < NW) ? S->bits_w[lane & (NW - 1)] : 0u;
-#pragma unroll
-                for (int d = 1; d < NW; d <<= 1) {
-                    const unsigned o = __shfl_up_sync(0xffffffffu, wb, d);
-                    if (lane >= d) wb += o;
-                }
-                btot = __shfl_sync(0xffffffffu, wb, NW - 1);
-                const unsigned ex = __shfl_up_sync(0xffffffffu, wb, 1);
-                bpre = __shfl_sync(0xffffffffu, lane == 0 ? 0u : ex, warp);
-                bpre = (warp == 0 ? 0u : bpre) + (xb - lbits);
-            }
+            // the warps' bases come from the JEE warp (S->wbits): no CTA scan
+            const unsigned btot = err ? 0u : S->wbits[kb][NW - 1];
+            const unsigned bpre = (err || warp == 0 ? 0u : S->wbits[kb][warp - 1]) + (xb - lbits);
             if (!err) {
                 const long long mant_bytes = ((long long)btot + 7) / 8;
                 if (avail < jee_bytes + mant_bytes) err = APAX_ERR_MANTISSA_TRUNCATED;
@@ -644,7 +656,9 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
             // ---- y staged in shared memory, one TMA bulk store per block ----
             T* ybuf = YOWN ? ybuf_own : (T*)pay;
             if (YOWN && tid == 0 && S->store_pending) { bulk_wait_read(); S->store_pending = 0; }
-            cbar();   // the y buffer is free: the previous store has read it (f64) / the payload is unpacked
+            // the y buffer is free: the previous store has read it (f64); the payload
+            // is unpacked by every thread (D1/D2: the reconstruct scan's barrier did it)
+            if (YOWN || sel == 0) cbar();
             if (active) {
                 constexpr int PER = 16 / (int)sizeof(T);
                 uint4* y4 = (uint4*)(ybuf + SPT * tid);
