@@ -17,7 +17,8 @@ from paper_1303_4994_b200 import workloads as W  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--log2-bytes", default="20,22,24,26,28,30")
+    ap.add_argument("--log2-bytes", default="20,22,24,26,28,30,32,34")
+    ap.add_argument("--big-rates", default="2,4,10", help="rates at >= 4 GiB (generated on the GPU)")
     ap.add_argument("--rates", default="2,3,4,6,8,10")
     ap.add_argument("--dtypes", default="i32,f32")
     ap.add_argument("--steps", type=int, default=10)
@@ -29,8 +30,9 @@ def main():
         dt = Dtype.I32 if dts == "i32" else Dtype.F32
         for lb in [int(v) for v in a.log2_bytes.split(",")]:
             n = 1 << (lb - 2)
-            x = torch.from_numpy(W.cfg5_ar1(n, dts)).to(dev)
-            for r in [float(v) for v in a.rates.split(",")]:
+            big = lb >= 32
+            x = (W.cfg5_ar1_device(n, dts, device=dev) if big else torch.from_numpy(W.cfg5_ar1(n, dts)).to(dev))
+            for r in [float(v) for v in (a.big_rates if big else a.rates).split(",")]:
                 seg = wave_segment_blocks(n, dt, Mode.FIXED_RATE, 4096)
                 cfg = StreamConfig(dt, 4096, Mode.FIXED_RATE, 32.0 / r, segment_blocks=seg,
                                    segment_policy="warm_self")
@@ -53,6 +55,7 @@ def main():
                 td = sum(e[2].elapsed_time(e[3]) for e in ev[3:]) / a.steps
                 ib = n * 4
                 print(json.dumps({"workload": "cfg5", "dtype": dts, "bytes": ib, "rate": r,
+                                  "generator": "cfg5_ar1_device" if big else "cfg5_ar1",
                                   "segment_blocks": seg, "segment_policy": "warm_self", "container_bytes": nb, "ratio": ib / nb,
                                   "encode_ms": te, "decode_ms": td,
                                   "encode_gbs": ib / te / 1e6, "decode_gbs": ib / td / 1e6,
