@@ -53,6 +53,11 @@
 
 namespace apax {
 namespace v3 {
+#ifdef APAX_V3_PROF2
+// S1 anatomy (tools/prof_s1.py): cycles of thread 0's S1 chain, of thread
+// 32's wait for the previous window store, and of thread 0's wait at B2
+__device__ unsigned long long g_prof2[4];
+#endif
 #ifdef APAX_V3_TIMES
 // per-CTA timeline (tools/cta_times.py): globaltimer at start, at the end of
 // the last unit's coding, at exit; SM id
@@ -894,7 +899,14 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
             // ============ S1 (thread 0): gain, code, scale ============
             // the previous block's bulk store must have read its window
             // before B2 (this block stages into that buffer after B2)
+#ifdef APAX_V3_PROF2
+            long long p2_t0 = clock64();
+#endif
             if (tid == 32 && S->store_pending) { bulk_wait_read(); S->store_pending = 0; }
+#ifdef APAX_V3_PROF2
+            if (tid == 32) atomicAdd(&g_prof2[1], (unsigned long long)(clock64() - p2_t0));
+            p2_t0 = clock64();
+#endif
             if (tid == 0) {
                 unsigned pks = 0, pku = 0;
                 unsigned long long pk64 = 0;
@@ -1007,7 +1019,14 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
                 if (!pbl || zg > XB) zg = XB;
                 S->zlen = (int)zg;
             }
+#ifdef APAX_V3_PROF2
+            if (tid == 0) atomicAdd(&g_prof2[0], (unsigned long long)(clock64() - p2_t0));
+            p2_t0 = clock64();
+#endif
             cbar();  // B2
+#ifdef APAX_V3_PROF2
+            if (tid == 0) { atomicAdd(&g_prof2[2], (unsigned long long)(clock64() - p2_t0)); atomicAdd(&g_prof2[3], 1ull); }
+#endif
             PROF_MARK(1);
 
             // stage the next distinct block into the other buffer
@@ -1677,6 +1696,11 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
 
 }  // namespace v3
 
+#ifdef APAX_V3_PROF2
+extern "C" int apax_debug_prof2(unsigned long long* host) {
+    return (int)cudaMemcpyFromSymbol(host, v3::g_prof2, 4 * sizeof(unsigned long long));
+}
+#endif
 #ifdef APAX_V3_TIMES
 extern "C" int apax_debug_cta_times(unsigned long long* host, int n) {
     return (int)cudaMemcpyFromSymbol(host, v3::g_times, (size_t)n * 4 * sizeof(unsigned long long));
