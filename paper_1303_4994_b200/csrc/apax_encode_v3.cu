@@ -847,11 +847,16 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
         const long long b1 = (b0 + P.unit_blocks < P.n_blocks) ? b0 + P.unit_blocks : P.n_blocks;
         const bool halo = P.halo && b0 + P.gblock0 > 0;
         const bool warm = !P.halo && P.policy == 1 && P.mode == 1;
-        const int npre = halo ? 1 : (warm ? 2 : 0);
+        // warm_self (App. C E8): one cost-only pass of the segment's first block
+        // at gain 1 gives the FR init jump; the first block's selector is then
+        // its own cost argmin (the reference preset: prev_costs = the block's
+        // own costs at the jumped gain), decided in resolve -- the costs of
+        // the gain-1 pass only seed the speculation
+        const int npre = halo ? 1 : (warm ? 1 : 0);
         const long long npass = npre + (b1 - b0);
         auto pass_block = [&](long long k) -> long long {
             if (halo) return k == 0 ? b0 - 1 : b0 + k - 1;
-            if (warm) return k < 2 ? b0 : b0 + k - 2;
+            if (warm) return k < 1 ? b0 : b0 + k - 1;
             return b0 + k;
         };
         if (tid == 0) {
@@ -885,7 +890,7 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
 
         for (long long kp = 0; kp < npass; kp++) {
             const long long b = pass_block(kp);
-            const int kind = halo ? (kp == 0 ? 1 : 0) : (warm ? (kp == 0 ? 2 : (kp == 1 ? 3 : 0)) : 0);
+            const int kind = halo ? (kp == 0 ? 1 : 0) : (warm ? (kp == 0 ? 2 : 0) : 0);
             const int n = block_n(b);
             const int G = FIX ? MAXBS / 4 : (n + 3) >> 2;
             const int np = FIX ? MAXBS : 4 * G;
@@ -1360,7 +1365,12 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
             // exact monitor only when the sign-flip bound cannot rule out the
             // 1/3 gate (transform.py:67-83,107-113)
             const int gate = (3LL * flt > 2LL * (np - 1)) ? cold_monitor(qbuf, S, np) : 0;
-            const int sel = gate ? 0 : sel_spec;
+            int sel_pre = sel_spec;
+            if (warm && emit && S->emitted == 0) {   // warm_self: the block's own costs
+                sel_pre = tt1 < tt0 ? 1 : 0;
+                if (tt2 < (sel_pre ? tt1 : tt0)) sel_pre = 2;
+            }
+            const int sel = gate ? 0 : sel_pre;
             if (emit && sel != sel_spec) {
                 cbar();   // everyone read the per-warp JEE words
                 jee_prep(sel);
@@ -1385,6 +1395,8 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
                         const double att0 = clamp_att(0.0 - 6.02 * (bps0 - P.target), P.att_lo);
                         S->att = att0;
                         S->a = att_to_a(att0);
+                        S->has_pc = 1;   // speculation only (resolve takes the own-cost argmin)
+                        S->pc[0] = 4 * tt0 + g4; S->pc[1] = 4 * tt1 + g4; S->pc[2] = 4 * tt2 + g4;
                     } else {
                         S->has_pc = 1;
                         S->pc[0] = 4 * tt0 + g4; S->pc[1] = 4 * tt1 + g4; S->pc[2] = 4 * tt2 + g4;
@@ -1448,6 +1460,7 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
                     S->blen = blen;
                     S->tl_next = (int)((wb + blen) & 15);
                     S->gate = gate;
+                    S->sel_spec = sel_pre;   // the block's pre-gate selector (trace)
                 }
                 const int bad = S->bad;
                 // ============ phase D: JEE tokens + mantissas into the window ============
