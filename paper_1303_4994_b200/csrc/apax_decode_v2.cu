@@ -250,158 +250,24 @@ __global__ void __launch_bounds__(NT, APAX_DEC_MINB) decode_v2_kernel(DecParams 
             }
         }
         __syncthreads();
-        // ---- parallel JEE parse ----
-        if (S->err == 0) {
-            const uint8_t* p = pay + S->pay_off;
+        // ---- JEE (entropy.py:118-164): one warp parses the block from global
+        // memory (apax_jee.cuh); any irregularity re-runs the exact parser
+        if (S->err == 0 && warp == 0) {
             const long long maxj = (3LL * G + 2) / 2;
             const long long nbj = S->avail < maxj ? S->avail : maxj;
-            const int total = (int)(2 * nbj);                         // nibbles the reference sees
-            const int stotal = (int)min(2 * S->staged, (long long)total);  // nibbles staged
-            int done = 0;
-            for (int pass_base = 0; !done; pass_base += NIB_PER_PASS) {
-                const int p0 = pass_base + 4 * tid;
-                auto nb = [&](int k) -> int { return k < stotal ? nib_at(p, k) : 0; };
-                // entry skip: nearest definite start at or before p0
-                int skip = 0;
-                if (p0 > 0) {
-                    int q = p0;
-                    while (q > 0 && !(nb(q - 1) != 15 && (q < 2 || nb(q - 2) != 15))) q--;
-                    int pos = q;
-                    while (pos < p0) pos += (nb(pos) == 15) ? 3 : 1;
-                    skip = pos - p0;
-                }
-                // tokens starting in [p0, p0+4)
-                int cnt = 0, flag = 0, val = 0;
-                int tk_pos[4], tk_kind[4], tk_a[4], tk_b[4], ntok = 0;
-                for (int pos = p0 + skip; pos < p0 + 4 && ntok < 4;) {
-                    const int v = nb(pos);
-                    int kind, len = 1;
-                    if (pos >= stotal) kind = 5;               // out of staged data
-                    else if (v == 14) kind = 4;                // reserved
-                    else if (v == 15) {
-                        kind = 1; len = 3;
-                        if (pos + 2 >= stotal) kind = 5;
-                        else {
-                            const int a = (nb(pos + 1) << 4) | nb(pos + 2);
-                            tk_a[ntok] = a;
-                            flag = 1; val = a; cnt += 1;
-                        }
-                    } else if (v >= 9) {
-                        kind = 3; tk_a[ntok] = v - 11; val += v - 11; cnt += 1;
-                    } else {
-                        kind = 2; tk_a[ntok] = v / 3 - 1; tk_b[ntok] = v % 3 - 1;
-                        val += (v / 3 - 1) + (v % 3 - 1); cnt += 2;
-                    }
-                    tk_pos[ntok] = pos;
-                    tk_kind[ntok] = kind;
-                    ntok++;
-                    pos += len;
-                    if (kind >= 4) break;                      // irregular: stop here
-                }
-                // CTA scan of (cnt, flag, val): A then B = (cA+cB, fA|fB, fB ? vB : vA+vB)
-                int c_i = cnt, f_i = flag, v_i = val;
-#pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const int oc = __shfl_up_sync(0xffffffffu, c_i, d);
-                    const int of = __shfl_up_sync(0xffffffffu, f_i, d);
-                    const int ov = __shfl_up_sync(0xffffffffu, v_i, d);
-                    if (lane >= d) {
-                        c_i += oc;
-                        if (!f_i) v_i += ov;
-                        f_i |= of;
-                    }
-                }
-                if (lane == 31) { S->sc_cnt[warp] = c_i; S->sc_flag[warp] = f_i; S->sc_val[warp] = v_i; }
-                __syncthreads();
-                if (tid == 0) {
-                    int ac = S->cnt_base, af = 0, av = S->val_base;
-                    for (int w = 0; w < NW; w++) {
-                        S->pre_cnt[w] = ac; S->pre_flag[w] = af; S->pre_val[w] = av;
-                        ac += S->sc_cnt[w];
-                        if (S->sc_flag[w]) { av = S->sc_val[w]; af = 1; } else av += S->sc_val[w];
-                    }
-                    S->cnt_base = ac;
-                    S->val_base = av;
-                }
-                __syncthreads();
-                // exclusive prefix for this thread
-                int ec = __shfl_up_sync(0xffffffffu, c_i, 1), ef = __shfl_up_sync(0xffffffffu, f_i, 1),
-                    evv = __shfl_up_sync(0xffffffffu, v_i, 1);
-                if (lane == 0) { ec = 0; ef = 0; evv = 0; }
-                int idx = S->pre_cnt[warp] + ec;
-                int cur = ef ? evv : S->pre_val[warp] + evv;
-                // evaluate tokens in order; first event = error or completion
-                int ev_pos = 0x7fffffff, ev_done = 0;
-                for (int k2 = 0; k2 < ntok; k2++) {
-                    if (idx >= G) break;
-                    const int kind = tk_kind[k2], pos = tk_pos[k2];
-                    int err = 0, adv = 0;
-                    if (kind >= 4) err = 1;
-                    else if (kind == 1) {
-                        if (tk_a[k2] > 34) err = 1;
-                        else { cur = tk_a[k2]; e[idx] = (uint8_t)cur; adv = 1; }
-                    } else if (idx == 0) err = 1;
-                    else if (kind == 3) {
-                        cur += tk_a[k2];
-                        if (cur < 0 || cur > 34) err = 1;
-                        else { e[idx] = (uint8_t)cur; adv = 1; }
-                    } else {
-                        cur += tk_a[k2];
-                        if (cur < 0 || cur > 34 || idx + 1 >= G) err = 1;
-                        else {
-                            e[idx] = (uint8_t)cur;
-                            cur += tk_b[k2];
-                            if (cur < 0 || cur > 34) err = 1;
-                            else { e[idx + 1] = (uint8_t)cur; adv = 2; }
-                        }
-                    }
-                    if (err) { ev_pos = pos; ev_done = 0; break; }
-                    idx += adv;
-                    if (idx >= G) { ev_pos = pos + (kind == 1 ? 3 : 1); ev_done = 1; break; }
-                }
-                // CTA min over events (done events store end position; both
-                // orderings agree because tokens do not overlap)
-                int m = ev_pos;
-                int key = (ev_pos == 0x7fffffff) ? 0x7fffffff : ((ev_pos << 1) | (ev_done ? 0 : 1));
-                key = __reduce_min_sync(0xffffffffu, key);
-                if (lane == 0) S->ev_min[warp] = key;
-                (void)m;
-                __syncthreads();
-                if (tid == 0) {
-                    int kmin = 0x7fffffff;
-                    for (int w = 0; w < NW; w++) kmin = min(kmin, S->ev_min[w]);
-                    if (kmin == 0x7fffffff) {
-                        // no event in this pass: continue, unless the data ran out
-                        if (pass_base + NIB_PER_PASS >= stotal) { S->fallback = 1; S->first_event = -1; }
-                        else S->first_event = -2;
-                    } else if (kmin & 1) {
-                        S->fallback = 1;  // an error: let the exact parser report it
-                        S->first_event = kmin >> 1;
-                    } else {
-                        S->first_event = kmin >> 1;
-                        S->used = kmin >> 1;
-                    }
-                }
-                __syncthreads();
-                done = S->first_event != -2;
+            int u = 0;
+            int st = warp_jee_fast(P.blob + boff + HS, P.blob + P.nbytes, (int)(2 * nbj), G, e, u);
+            if (st < 0) {
+                long long u2 = 0, esum = 0;
+                st = warp_jee_decode(P.blob + boff + HS, 2 * nbj, G, e, u2, esum);
+                u = (int)u2;
             }
-            (void)total;
+            if (lane == 0) {
+                if (st) S->err = st;
+                else S->used = u;
+            }
         }
         __syncthreads();
-        if (S->err == 0 && S->fallback) {
-            // exact serial parse (reference semantics, incl. the error code)
-            if (tid < 32) {
-                const long long maxj = (3LL * G + 2) / 2;
-                const long long nbj = S->avail < maxj ? S->avail : maxj;
-                long long used = 0, esum = 0;
-                const int st = warp_jee_decode(P.blob + boff + HS, 2 * nbj, G, e, used, esum);
-                if (tid == 0) {
-                    if (st) S->err = st;
-                    else { S->used = used; S->fallback = 0; }
-                }
-            }
-            __syncthreads();
-        }
         if (tid == 0 && S->err == 0) {
             S->jee_bytes = (S->used + 1) >> 1;
         }

@@ -4,6 +4,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "apax_device.cuh"
+
 namespace apax {
 
 // read one nibble k of the payload (first nibble in the high half)
@@ -148,6 +150,157 @@ static __device__ __noinline__ int warp_jee_decode(const uint8_t* p, long long t
             return 1;
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// JEE decode of one block by one warp (entropy.py:118-164), reading the
+// nibble stream straight from global memory (read-only path): 128 nibbles
+// per step, 4 per lane.  Two consecutive non-15 nibbles always precede a
+// token start, so every lane finds the token starts in its slice from a
+// 16-nibble window; one warp scan of (exponent count, escape reset, running
+// value) places the exponents.  Returns 0 with e[0..G) and *used (nibbles
+// consumed), or -1 on ANY irregularity (reserved nibble, range, truncation,
+// missing opening escape, joint token past the last group): the caller then
+// runs the exact parser (apax_jee.cuh), which reports the reference's first
+// error.  e must hold G + 128 bytes (tokens are written before validation).
+// ---------------------------------------------------------------------------
+static __device__ __forceinline__ int warp_jee_fast(const uint8_t* p, const uint8_t* pend, int total, int G,
+                                             uint8_t* e, int& used) {
+    const int lane = threadIdx.x & 31;
+    constexpr unsigned long long LUT_C = 0x43210cbaba9a98ull;    // bit 3 joint, bits 0-2 delta sum + 2
+    constexpr unsigned long long LUT_D1 = 0x43210333222111ull;   // first exponent's delta + 2
+    constexpr unsigned LUT_D2 = 0x24924u;                        // (2-bit) second delta + 1
+    int cbase = 0, vbase = 0;
+    for (int base = 0; base < total + 4; base += 128) {
+        const int p0 = base + 4 * lane;
+        // nibbles p0-4 .. p0+11 (zero beyond `total`); bytes before p are the
+        // block header (>= 4 bytes), so p0 = 0 reads inside the container
+        unsigned long long W = 0ULL;
+        if (p0 - 4 < total) {
+            const uint8_t* bp = p + (p0 >> 1) - 2;
+            const uintptr_t a = (uintptr_t)bp;
+            const uint32_t* wp = (const uint32_t*)(a & ~(uintptr_t)3);
+            const unsigned sh = (unsigned)(a & 3) * 8u;
+            uint32_t w0, w1, w2;
+            if ((const uint8_t*)(wp + 3) <= pend) {
+                w0 = bswap32(__ldg(wp)); w1 = bswap32(__ldg(wp + 1)); w2 = bswap32(__ldg(wp + 2));
+            } else {   // the last words of the container: bytewise, zero past the end
+                uint32_t w[3];
+                for (int k = 0; k < 3; k++) {
+                    uint32_t v = 0;
+                    for (int c = 0; c < 4; c++) {
+                        const uint8_t* q = (const uint8_t*)(wp + k) + c;
+                        v = (v << 8) | (q < pend ? (uint32_t)*q : 0u);
+                    }
+                    w[k] = v;
+                }
+                w0 = w[0]; w1 = w[1]; w2 = w[2];
+            }
+            W = ((unsigned long long)__funnelshift_l(w1, w0, sh) << 32) | __funnelshift_l(w2, w1, sh);
+            const int rem = total - (p0 - 4);
+            if (rem < 16) W = rem <= 0 ? 0ULL : (W & (~0ULL << (4 * (16 - rem))));
+        }
+        auto nw = [&](int k) -> int { return (int)((W >> (4 * (11 - k))) & 15ULL); };   // k in -4..11
+        // leading positions covered by an escape that started before p0
+        int skip = 0;
+        if (p0 > 0 && p0 < total + 4) {
+            const bool f1 = nw(-1) == 15, f2 = nw(-2) == 15, f3 = nw(-3) == 15, f4 = nw(-4) == 15;
+            if (!f1 && !f2) skip = 0;
+            else if (!f2 && !f3) skip = f1 ? 2 : 0;
+            else if (!f3 && !f4) skip = f2 ? 1 : (f1 ? 2 : 0);
+            else {
+                // long escape run: walk back to a definite start (rare)
+                auto nb = [&](int k) -> int {
+                    if (k >= total) return 0;
+                    const uint8_t b = p[k >> 1];
+                    return (k & 1) ? (b & 15) : (b >> 4);
+                };
+                int q = p0;
+                while (q > 0 && !(nb(q - 1) != 15 && (q < 2 || nb(q - 2) != 15))) q--;
+                int pos = q;
+                while (pos < p0) pos += (nb(pos) == 15) ? 3 : 1;
+                skip = pos - p0;
+            }
+        }
+        const bool n0f = nw(0) == 15, n1f = nw(1) == 15, n2f = nw(2) == 15;
+        const bool st0 = skip == 0;
+        const bool st1 = skip == 1 || (st0 && !n0f);
+        const bool st2 = skip == 2 || (st1 && !n1f);
+        const bool st3 = (st2 && !n2f) || (st0 && n0f);
+        const bool stv[4] = {st0, st1, st2, st3};
+        const bool live = p0 < total + 4;
+        int cnt = 0, flag = 0, val = 0;
+        int kv[4], kab[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int v = nw(k);
+            const int ab = (int)((W >> (4 * (9 - k))) & 0xffULL);   // nibbles k+1, k+2
+            kv[k] = v;
+            kab[k] = ab;
+            const int cd = (int)((LUT_C >> (4 * v)) & 15ull);
+            const bool esc = v == 15;
+            const int c = esc ? 1 : (cd >> 3) + 1;
+            const int dv = (cd & 7) - 2;
+            const bool t = stv[k] && live;
+            cnt += t ? c : 0;
+            val = t ? (esc ? ab : val + dv) : val;
+            flag |= (t && esc) ? 1 : 0;
+        }
+        // warp scan of (cnt, flag, val): A then B = (cA+cB, fA|fB, fB ? vB : vA+vB)
+        int c_i = cnt, f_i = flag, v_i = val;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int oc = __shfl_up_sync(0xffffffffu, c_i, d);
+            const int of = __shfl_up_sync(0xffffffffu, f_i, d);
+            const int ov = __shfl_up_sync(0xffffffffu, v_i, d);
+            if (lane >= d) {
+                c_i += oc;
+                if (!f_i) v_i += ov;
+                f_i |= of;
+            }
+        }
+        int ec = __shfl_up_sync(0xffffffffu, c_i, 1), ef = __shfl_up_sync(0xffffffffu, f_i, 1),
+            evv = __shfl_up_sync(0xffffffffu, v_i, 1);
+        if (lane == 0) { ec = 0; ef = 0; evv = 0; }
+        int idx = cbase + ec;
+        int curv = ef ? evv : vbase + evv;
+        int key = 0x7fffffff;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int pos = p0 + k;
+            const int v = kv[k];
+            const bool t = stv[k] && live && idx < G;   // tokens after the G-th exponent are not read
+            const bool esc = v == 15;
+            const int cd = (int)((LUT_C >> (4 * v)) & 15ull);
+            const bool joint = !esc && (cd >> 3) != 0;
+            const int e1 = esc ? kab[k] : curv + (int)((LUT_D1 >> (4 * v)) & 15ull) - 2;
+            const int e2 = e1 + (int)((LUT_D2 >> (2 * v)) & 3u) - 1;
+            const bool bad = (pos + (esc ? 2 : 0) >= total) | (v == 14) | (!esc & (idx == 0)) |
+                             ((unsigned)e1 > 34u) | (joint & ((idx + 1 >= G) | ((unsigned)e2 > 34u)));
+            const int nexp = joint ? 2 : 1;
+            const bool done = idx + nexp >= G;
+            if (t) {
+                e[idx] = (uint8_t)e1;
+                if (joint) e[idx + 1] = (uint8_t)e2;
+            }
+            const int kk2 = bad ? 1 : (done ? ((pos + (esc ? 3 : 1)) << 1) : 0x7fffffff);
+            key = t ? min(key, kk2) : key;
+            curv = t ? (joint ? e2 : e1) : curv;
+            idx += t ? nexp : 0;
+        }
+        key = __reduce_min_sync(0xffffffffu, key);
+        if (key != 0x7fffffff) {
+            if (key & 1) return -1;
+            used = key >> 1;
+            return 0;
+        }
+        // the next step continues the scan
+        const int tc = __shfl_sync(0xffffffffu, c_i, 31), tf = __shfl_sync(0xffffffffu, f_i, 31),
+                  tv = __shfl_sync(0xffffffffu, v_i, 31);
+        cbase += tc;
+        vbase = tf ? tv : vbase + tv;
+    }
+    return -1;
 }
 
 
