@@ -389,7 +389,9 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                     return (T)yi;
                 }
             };
-            auto i2d = [](int v) -> double { return __hiloint2double(0x43380000, v ^ (int)0x80000000) - kMagicI; };
+            // I2F.F64 on the conversion pipe: the magic-number form cost an ALU
+            // op per sample on the decoder's busiest pipe
+            auto i2d = [](int v) -> double { return (double)v; };
             T out[SPT];
             const uint32_t* w = (const uint32_t*)pay;
             int bp = 8 * ((int)pay_off + jee_bytes) + (int)bpre;
