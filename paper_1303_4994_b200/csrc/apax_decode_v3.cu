@@ -69,7 +69,7 @@ struct __align__(16) St {
     unsigned bits_w[NW];
     long long rs_w[NW], rt_w[NW];
     int store_pending;
-    int jst[JB], jused[JB];   // JEE batch: status (0 ok) and nibbles used per slot
+    int4 jinfo[JB];           // JEE batch per slot: packed header, JEE status (0 ok), nibbles used
     unsigned wbits[JB][8];    // mantissa bits up to the end of each decode warp's 128 groups
 };
 
@@ -90,6 +90,16 @@ __device__ __forceinline__ void bulk_wait_all() {
 __device__ __forceinline__ int bfe_s(uint32_t v, int pos, int len) {
     int r;
     asm("bfe.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(v), "r"(pos), "r"(len));
+    return r;
+}
+__device__ __forceinline__ int sar32(int v, uint32_t n) {
+    int r;
+    asm("shr.s32 %0, %1, %2;" : "=r"(r) : "r"(v), "r"(n));
+    return r;
+}
+__device__ __forceinline__ uint32_t shl32(uint32_t v, uint32_t n) {
+    uint32_t r;
+    asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(v), "r"(n));
     return r;
 }
 // 32 bits of the MSB-first stream starting at bit position bp (word array
@@ -192,8 +202,15 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
             const int nj = FIX ? MAXBS : (int)((P.n - sj) < bs ? (P.n - sj) : bs);
             const int Gj = FIX ? MAXBS / 4 : (nj + 3) >> 2;
             const long long o0 = P.offsets[bj];
-            int st = 0, u = 0;
+            int st = 0, u = 0, hdr = 0;
             if (o0 >= 0 && P.nbytes - o0 >= HS) {
+                // block header (dtypes.py:156-180) packed for the decode phase:
+                // selector | restart << 2 | code << 8 | fbe << 24
+                if (lane == 0) {
+                    const uint8_t* h = P.blob + o0;
+                    hdr = (int)(h[0] & 7) | ((int)h[1] << 8) | ((int)h[2] << 16) |
+                          (Tr::F ? ((int)h[4] << 24) : 0);
+                }
                 const long long ps = o0 + HS;
                 const long long avl = P.nbytes - ps;
                 const int maxj = (3 * Gj + 2) / 2;
@@ -229,7 +246,7 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                     if ((lane & 3) == 3) S->wbits[warp][lane >> 2] = sb;
                 }
             }
-            if (lane == 0) { S->jst[warp] = st; S->jused[warp] = u; }
+            if (lane == 0) S->jinfo[warp] = make_int4(hdr, st, u, 0);
         }
         cbar();
         for (int kb = 0; kb < nbat; kb++, kk++) {
@@ -266,23 +283,14 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                 cbar();
             }
             // ---- block header (dtypes.py:156-180), read by every thread ----
+            // (header and JEE results: from the batch's warp, one 16-byte read)
             int err = S->ld_err[cur];
-            int sel = 0, restart = 0, code = 0, fbe = 0;
             const int pay_off = S->ld_payoff[cur], avail = S->ld_avail[cur], staged = S->ld_staged[cur];
-            if (!err) {
-                const uint8_t* h = pay + S->ld_hoff[cur];
-                sel = h[0] & 3;
-                restart = (h[0] >> 2) & 1;
-                code = h[1] | (h[2] << 8);
-                fbe = Tr::F ? (int)(int8_t)h[4] : 0;
-                if (sel == 3) err = APAX_ERR_SELECTOR;
-            }
-            // ---- JEE exponents: parsed by the batch's warp (above) ----
-            int used = 0;
-            if (!err) {
-                err = S->jst[kb];
-                used = S->jused[kb];
-            }
+            const int4 ji = S->jinfo[kb];
+            const int sel = ji.x & 3, restart = (ji.x >> 2) & 1, code = (ji.x >> 8) & 0xFFFF;
+            const int fbe = Tr::F ? (ji.x >> 24) : 0;     // int8 (arithmetic shift)
+            if (!err) err = (sel == 3) ? APAX_ERR_SELECTOR : ji.y;
+            const int used = ji.z;
             const int jee_bytes = (used + 1) >> 1;
             // ---- mantissa offsets (entropy.py:209-219): CTA scan of 4*sum(e) ----
             const int g0 = 4 * tid;
@@ -400,11 +408,14 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
 #pragma unroll
                 for (int g = 0; g < 4; g++) {   // two 32-bit windows per group
                     const int wd = (int)((epk >> (8 * g)) & 0xffu);
-                    const uint32_t c0 = r32(w, bp), c1 = r32(w, bp + 2 * wd);
-                    v[4 * g + 0] = wd ? bfe_s(c0, 32 - wd, wd) : 0;
-                    v[4 * g + 1] = wd ? bfe_s(c0, 32 - 2 * wd, wd) : 0;
-                    v[4 * g + 2] = wd ? bfe_s(c1, 32 - wd, wd) : 0;
-                    v[4 * g + 3] = wd ? bfe_s(c1, 32 - 2 * wd, wd) : 0;
+                    // sign-extending shifts (PTX: shifts >= 32 saturate); a zero
+                    // width zeroes the windows instead of selecting every value
+                    const uint32_t c0 = wd ? r32(w, bp) : 0u, c1 = wd ? r32(w, bp + 2 * wd) : 0u;
+                    const uint32_t rs = 32u - (uint32_t)wd;
+                    v[4 * g + 0] = sar32((int)c0, rs);
+                    v[4 * g + 1] = sar32((int)shl32(c0, (uint32_t)wd), rs);
+                    v[4 * g + 2] = sar32((int)c1, rs);
+                    v[4 * g + 3] = sar32((int)shl32(c1, (uint32_t)wd), rs);
                     bp += 4 * wd;
                 }
                 unsigned long long q0 = 0, d0 = 0;   // q and d1 entering this thread (exact, 64-bit)
