@@ -242,3 +242,51 @@ def sharded_encode_lossless_whole_stream(x_local, first_block: int, dtype, block
     body = bytes(res.blob[FILE_HEADER_SIZE:res.nbytes].cpu().numpy().tobytes())
     offs = global_block_offsets(res.block_offsets.cpu().numpy(), place)
     return body, place, offs
+
+
+# ---------------------------------------------------------------------------
+# profiler statistics across ranks: global sums and
+# S2R order statistics of a sharded (x, y)
+# ---------------------------------------------------------------------------
+def sharded_window_stats(x_local, y_local, dtype, group=None) -> dict:
+    """Window statistics of (x, y, d = x - y) split over ranks (CUDA tensors
+    of `dtype`, any shard sizes): the moments, uncentred pearson_r and SRR
+    from rank-ordered merges of every rank's GPU sums (profiler.py:40-48,
+    127-159), the std from a second pass about the global means, and the
+    2-sigma S2R margin plus the zero counts from a radix multi-select whose
+    per-pass digit histograms are all-reduced (profiler.py:105-124)."""
+    import math
+
+    import torch
+    import torch.distributed as dist
+    from .profiler import TWO_SIGMA_COVERAGE, _key_to_ratio, _s2r_of_ratios, _select_ratio_keys, _Sums
+    # collectives on the GPU with NCCL; through host tensors with gloo
+    dev = x_local.device if dist.get_backend(group) == "nccl" else None
+    s = _Sums(x_local, y_local, dtype)
+    tot = merge_sums([s.sx, s.sy, s.sd, s.sxx, s.syy, s.sdd, s.sxy, float(s.n), float(s.zero_x),
+                      float(s.zero_d)], group, dev)
+    sx, sy, sd, sxx, syy, sdd, sxy = (float(v) for v in tot[:7])
+    n, zero_x, zero_d = int(tot[7]), int(tot[8]), int(tot[9])
+    c = _Sums(x_local, y_local, dtype, centred=True, means=(sx / n, sy / n, sd / n))
+    cen = merge_sums([c.cxx or 0.0, c.cyy or 0.0, c.cdd or 0.0], group, dev)
+
+    def reduce_hist(h):
+        if dev is None:
+            hc = h.cpu()
+            dist.all_reduce(hc, op=dist.ReduceOp.SUM, group=group)
+            h.copy_(hc)
+        else:
+            dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+
+    k = math.ceil(TWO_SIGMA_COVERAGE * n)
+    rank = n - k
+    keys = _select_ratio_keys(x_local, y_local, dtype, [rank], True, reduce_hist=reduce_hist)
+    margin = float(_s2r_of_ratios([_key_to_ratio(keys[rank])])[0])
+    rms_x, rms_d = math.sqrt(sxx / n), math.sqrt(sdd / n)
+    return {
+        "n": n, "mean_x": sx / n, "mean_y": sy / n, "mean_d": sd / n,
+        "std_x": math.sqrt(cen[0] / n), "std_y": math.sqrt(cen[1] / n), "std_d": math.sqrt(cen[2] / n),
+        "pearson_r": sxy / math.sqrt(sxx * syy),
+        "srr_db": (20.0 * math.log10(rms_x / rms_d)) if rms_d > 0 else math.inf,
+        "two_sigma_s2r_margin_db": margin, "zero_x": zero_x, "zero_d": zero_d,
+    }

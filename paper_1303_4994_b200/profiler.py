@@ -77,7 +77,7 @@ def _ptr(t):
 class _Sums:
     """pass-0 and pass-1 sums of (x, y, d = x - y) on the device."""
 
-    def __init__(self, xd, yd, dtype: Dtype, centred: bool = False):
+    def __init__(self, xd, yd, dtype: Dtype, centred: bool = False, means=None):
         torch, L = _require_cuda()
         n = int(xd.numel())
         grid = int(L.apax_profile_grid())
@@ -93,7 +93,8 @@ class _Sums:
         self.zero_d = int(c[1])     # d == 0
         self.cxx = self.cyy = self.cdd = None
         if centred and n:
-            mx, my, md = self.sx / n, self.sy / n, self.sd / n
+            # about the local means, or the global ones of a sharded array
+            mx, my, md = means if means is not None else (self.sx / n, self.sy / n, self.sd / n)
             raise_status(L.apax_profile_sums(_ptr(xd), _ptr(yd), n, dtype.wire_code, 1, mx, my, md,
                                              _ptr(part), _ptr(cnt), ctypes.c_void_p(_stream_ptr(None))))
             s2 = part.cpu().numpy().reshape(grid, 8).sum(axis=0)
@@ -207,9 +208,13 @@ def fft_s2r_margin(x_spec: SpectrumStats, d_spec: SpectrumStats) -> float:
 # ---------------------------------------------------------------------------
 # S2R distribution: exact order statistics by radix multi-select
 # ---------------------------------------------------------------------------
-def _select_ratio_keys(xd, yd, dtype: Dtype, ranks: Sequence[int], y_is_output: bool) -> Dict[int, int]:
+def _select_ratio_keys(xd, yd, dtype: Dtype, ranks: Sequence[int], y_is_output: bool,
+                       reduce_hist=None) -> Dict[int, int]:
     """Ascending-rank order statistics (as uint64 bit patterns) of the
-    ratio keys |x| / |d| over all n samples (16 passes of 4-bit digits)."""
+    ratio keys |x| / |d| over all n samples (16 passes of 4-bit digits).
+    `reduce_hist` (multi-GPU) sums each pass's digit histograms over the
+    ranks in place, so every rank picks the same digits and the ranks are
+    global (distributed.sharded_window_stats)."""
     torch, L = _require_cuda()
     n = int(xd.numel())
     targets = sorted(set(int(r) for r in ranks))
@@ -222,6 +227,8 @@ def _select_ratio_keys(xd, yd, dtype: Dtype, ranks: Sequence[int], y_is_output: 
         raise_status(L.apax_profile_select(_ptr(xd), _ptr(yd), n, dtype.wire_code, p, _ptr(pre), len(uniq),
                                            _ptr(hist), 1 if y_is_output else 0,
                                            ctypes.c_void_p(_stream_ptr(None))))
+        if reduce_hist is not None:
+            reduce_hist(hist)
         h = hist.cpu().numpy().reshape(len(uniq), 16)
         slot = {v: i for i, v in enumerate(uniq)}
         for r in targets:

@@ -1,0 +1,70 @@
+"""Profiler statistics of an array split over ranks
+(distributed.sharded_window_stats): two processes (gloo; both on cuda:0 of
+this one-GPU pool, which is fine for correctness: no kernel waits on another
+rank) each hold half of (x, y = the GPU decode of x); the merged moments,
+pearson r and SRR must match the one-process statistics of the whole array
+to 1e-12 (the sums are added in a different order), and the 2-sigma S2R
+margin -- an exact order statistic via all-reduced radix histograms --
+must match exactly."""
+import json
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _data():
+    from paper_1303_4994_b200 import Dtype, Mode, StreamConfig, decode_device, encode_device
+    from paper_1303_4994_b200 import workloads as W
+    x = W.cfg2_ar2_f32((1 << 18) + 12345)
+    xd = torch.from_numpy(x).cuda()
+    res = encode_device(xd, StreamConfig(Dtype.F32, 4096, Mode.FIXED_QUALITY, 45.0))
+    y = decode_device(res.blob, res.nbytes, res.block_offsets)
+    return xd, y
+
+
+def _worker(rank, world, port, out_dir):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1303_4994_b200 import Dtype
+    from paper_1303_4994_b200 import distributed as D
+    xd, y = _data()
+    n = xd.numel()
+    a, b = (n * rank) // world, (n * (rank + 1)) // world
+    st = D.sharded_window_stats(xd[a:b].contiguous(), y[a:b].contiguous(), Dtype.F32)
+    with open(os.path.join(out_dir, f"s{rank}.json"), "w") as f:
+        json.dump(st, f)
+    dist.destroy_process_group()
+
+
+def test_two_rank_window_stats_match_whole_array(tmp_path):
+    import torch.multiprocessing as mp
+    from paper_1303_4994_b200 import Dtype
+    from paper_1303_4994_b200.profiler import S2RDistribution, _Sums
+    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    r0 = json.loads((tmp_path / "s0.json").read_text())
+    r1 = json.loads((tmp_path / "s1.json").read_text())
+    assert r0 == r1
+    xd, y = _data()
+    s = _Sums(xd, y, Dtype.F32, centred=True)
+    n = s.n
+    whole = {"mean_x": s.sx / n, "mean_y": s.sy / n, "mean_d": s.sd / n,
+             "std_x": (s.cxx / n) ** 0.5, "std_y": (s.cyy / n) ** 0.5, "std_d": (s.cdd / n) ** 0.5,
+             "pearson_r": s.pearson(), "srr_db": 10.0 * np.log10(s.sxx / s.sdd)}
+    assert r0["n"] == n and r0["zero_x"] == s.zero_x and r0["zero_d"] == s.zero_d
+    for k, v in whole.items():
+        assert abs(r0[k] - v) <= 1e-12 * max(1.0, abs(v)), (k, r0[k], v)
+    assert r0["two_sigma_s2r_margin_db"] == S2RDistribution(xd, y, Dtype.F32, True).two_sigma_margin_db
