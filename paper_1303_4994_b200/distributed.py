@@ -290,3 +290,48 @@ def sharded_window_stats(x_local, y_local, dtype, group=None) -> dict:
         "srr_db": (20.0 * math.log10(rms_x / rms_d)) if rms_d > 0 else math.inf,
         "two_sigma_s2r_margin_db": margin, "zero_x": zero_x, "zero_d": zero_d,
     }
+
+
+def sharded_welch(x_local, y_local, dtype, which: int = 0, seg: int = 4096, group=None):
+    """Welch power spectrum (profiler.py:61-74: Hann frames of `seg`, hop
+    seg/2) of x (which 0), y (1) or d = x - y (2) split over ranks.  Every
+    rank's shard must start on a hop boundary of the global array (all but
+    the last rank hold a multiple of seg/2 samples); rank r borrows the first
+    seg/2 samples of rank r+1 for the frames that straddle the boundary, so
+    the union of the ranks' frames is exactly the one-array frame set.  The
+    per-rank frame sums (seg/2 + 1 bins) and frame counts are all-gathered
+    and added in rank order.  Returns the power spectrum (numpy f64)."""
+    import torch
+    import torch.distributed as dist
+    from .profiler import _welch_frame_sums, _welch_scale
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    hop = seg // 2
+    n_local = int(x_local.numel())
+    if rank < world - 1 and n_local % hop:
+        raise ValueError("sharded_welch: every shard but the last must hold a multiple of seg/2 samples")
+    # heads (hop samples of x and y) of every rank, through host tensors
+    def _head(t):
+        h = torch.zeros(hop, dtype=torch.float64)
+        k = min(hop, n_local)
+        h[:k] = t[:k].double().cpu()
+        return h
+    hx = _head(x_local)
+    hy = _head(y_local) if y_local is not None else torch.zeros(hop, dtype=torch.float64)
+    gx = torch.empty(world * hop, dtype=torch.float64)
+    gy = torch.empty(world * hop, dtype=torch.float64)
+    dist.all_gather_into_tensor(gx, hx, group=group)
+    dist.all_gather_into_tensor(gy, hy, group=group)
+    xe, ye = x_local.double(), (y_local.double() if y_local is not None else None)
+    if rank < world - 1:
+        xe = torch.cat([xe, gx[(rank + 1) * hop:(rank + 2) * hop].to(xe.device)])
+        if ye is not None:
+            ye = torch.cat([ye, gy[(rank + 1) * hop:(rank + 2) * hop].to(ye.device)])
+    ne = int(xe.numel())
+    from .dtypes import Dtype
+    if ne >= seg:
+        tot, nf = _welch_frame_sums(xe.contiguous(), ye.contiguous() if ye is not None else None, Dtype.F64,
+                                    which, ne, seg)
+    else:
+        tot, nf = np.zeros(hop + 1), 0
+    parts = merge_sums(list(tot) + [float(nf)], group, None)
+    return _welch_scale(parts[:-1], int(parts[-1]), seg)

@@ -154,7 +154,9 @@ def _welch_tables(seg: int, device):
     return t
 
 
-def _welch_power(xd, yd, dtype: Dtype, which: int, n: int, seg: int) -> np.ndarray:
+def _welch_frame_sums(xd, yd, dtype: Dtype, which: int, n: int, seg: int):
+    """Sum over the Hann-windowed frames (hop seg/2) of |rfft|^2 and the
+    frame count (scipy.signal.welch before its scaling and mean)."""
     torch, L = _require_cuda()
     grid = int(L.apax_profile_grid())
     nb = seg // 2 + 1
@@ -162,13 +164,20 @@ def _welch_power(xd, yd, dtype: Dtype, which: int, n: int, seg: int) -> np.ndarr
     tab = _welch_tables(seg, xd.device)
     raise_status(L.apax_profile_welch(_ptr(xd), _ptr(yd) if yd is not None else None, n, dtype.wire_code, which,
                                       seg, _ptr(tab), _ptr(part), ctypes.c_void_p(_stream_ptr(None))))
-    tot = part.cpu().numpy().reshape(grid, nb).sum(axis=0)
-    nframes = (n - seg) // (seg // 2) + 1
+    return part.cpu().numpy().reshape(grid, nb).sum(axis=0), (n - seg) // (seg // 2) + 1
+
+
+def _welch_scale(tot: np.ndarray, nframes: int, seg: int) -> np.ndarray:
     win = hann_periodic(seg)
     scale = 1.0 / win.sum() ** 2
     pxx = tot * scale
     pxx[1:-1] *= 2.0               # one-sided, even nfft: DC and Nyquist not doubled
     return pxx / nframes
+
+
+def _welch_power(xd, yd, dtype: Dtype, which: int, n: int, seg: int) -> np.ndarray:
+    tot, nframes = _welch_frame_sums(xd, yd, dtype, which, n, seg)
+    return _welch_scale(tot, nframes, seg)
 
 
 def _stats_from_power(pxx: np.ndarray) -> SpectrumStats:

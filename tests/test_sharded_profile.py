@@ -45,6 +45,11 @@ def _worker(rank, world, port, out_dir):
     n = xd.numel()
     a, b = (n * rank) // world, (n * (rank + 1)) // world
     st = D.sharded_window_stats(xd[a:b].contiguous(), y[a:b].contiguous(), Dtype.F32)
+    # Welch spectra: shards on hop (2048) boundaries
+    hop = 2048
+    cut = ((n // world) // hop) * hop
+    a2, b2 = (0, cut) if rank == 0 else (cut, n)
+    st["welch"] = [D.sharded_welch(xd[a2:b2], y[a2:b2], Dtype.F32, which=w).tolist() for w in (0, 1, 2)]
     with open(os.path.join(out_dir, f"s{rank}.json"), "w") as f:
         json.dump(st, f)
     dist.destroy_process_group()
@@ -68,3 +73,8 @@ def test_two_rank_window_stats_match_whole_array(tmp_path):
     for k, v in whole.items():
         assert abs(r0[k] - v) <= 1e-12 * max(1.0, abs(v)), (k, r0[k], v)
     assert r0["two_sigma_s2r_margin_db"] == S2RDistribution(xd, y, Dtype.F32, True).two_sigma_margin_db
+    from paper_1303_4994_b200.profiler import _welch_power
+    for w in (0, 1, 2):
+        ref = _welch_power(xd.double(), y.double(), Dtype.F64, w, n, 4096)
+        got = np.array(r0["welch"][w])
+        assert np.allclose(got, ref, rtol=1e-12, atol=0.0), w
