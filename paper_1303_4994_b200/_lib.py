@@ -50,13 +50,17 @@ def lib():
     L.apax_decode.restype = I32
     L.apax_encode_wave_segment_blocks.argtypes = [I64, I32, I32, I32]
     L.apax_encode_wave_segment_blocks.restype = I64
-    L.apax_decode_range.argtypes = [P, I64, I64, I32, I32, P, I64, I64, ctypes.c_uint64, ctypes.c_uint64,
-                                    P, P, P, P, I64, P]
-    L.apax_decode_range.restype = I32
-    L.apax_encode_lossless_range.argtypes = [P, I64, I64, I32, I32, I64, P, I64, P, P, P, I64, P]
-    L.apax_encode_lossless_range.restype = I32
-    L.apax_status_to_host.argtypes = [P, P, I32, P]
-    L.apax_status_to_host.restype = I32
+    # (bound only when present: APAX_LIB_PATH may point at an older tuning build)
+    if hasattr(L, "apax_decode_range"):
+        L.apax_decode_range.argtypes = [P, I64, I64, I32, I32, P, I64, I64, ctypes.c_uint64, ctypes.c_uint64,
+                                        P, P, P, P, I64, P]
+        L.apax_decode_range.restype = I32
+    if hasattr(L, "apax_encode_lossless_range"):
+        L.apax_encode_lossless_range.argtypes = [P, I64, I64, I32, I32, I64, P, I64, P, P, P, I64, P]
+        L.apax_encode_lossless_range.restype = I32
+    if hasattr(L, "apax_status_to_host"):
+        L.apax_status_to_host.argtypes = [P, P, I32, P]
+        L.apax_status_to_host.restype = I32
     L.apax_decode_segments_workspace_bytes.argtypes = [I64, I32, I32]
     L.apax_decode_segments_workspace_bytes.restype = I64
     L.apax_decode_segments.argtypes = [P, I64, I64, I32, I32, P, I64, P, P, P, I64, P]

@@ -404,7 +404,9 @@ __device__ __noinline__ int cold_monitor(const int* qbuf, St* S, int np) {
     const int t0 = SPT * ct;
     int ch = 0, fs = 0, lsg = 0;
     if (t0 < np) {
-        for (int k2 = 0; k2 < SPT; k2++) {
+        // only the padded block's np samples: past np the q buffer holds the
+        // previous pass's values (a partial last block of 1..12 groups)
+        for (int k2 = 0; k2 < SPT && t0 + k2 < np; k2++) {
             const int v = qbuf[qw(t0 + k2)];
             const int sg = (v > 0) - (v < 0);
             if (sg) {

@@ -209,3 +209,19 @@ def test_bench_size_cfg1_lossless_round_trip():
     assert res.to_bytes() == ref
     y = decode_device(res.blob, res.nbytes, res.block_offsets).cpu().numpy()
     assert np.array_equal(y, x)
+
+
+@pytest.mark.parametrize("n", [4096 * 3 + 3, 4096 + 1, 4096 * 3 + 4, 4096 * 2 + 29, 4096 * 5 + 100])
+@pytest.mark.parametrize("dt,mode,target", [(Dtype.I16, Mode.LOSSLESS, 0.0), (Dtype.I32, Mode.LOSSLESS, 0.0),
+                                            (Dtype.F32, Mode.FIXED_RATE, 8.0), (Dtype.I16, Mode.FIXED_QUALITY, 40.0)])
+def test_short_partial_last_block(n, dt, mode, target):
+    """A last block of a few groups (np not a multiple of a thread's 16
+    samples): the exact centre-frequency monitor must look at the padded
+    block only (a regression: stale q-buffer values past np fired the 1/3
+    gate and forced D0 on cfg1's 3-sample tail)."""
+    x = W.cfg1_sines_i16(n).astype(dt.np_dtype)
+    res = encode_device(torch.from_numpy(x).cuda(), StreamConfig(dt, 4096, mode, target))
+    ref, offs, _ = O.encode(x, dt.wire_code, mode.value, target, 4096)
+    assert res.to_bytes() == ref
+    assert np.array_equal(res.block_offsets.cpu().numpy(), offs)
+    assert np.array_equal(decode_device(res.blob, res.nbytes).cpu().numpy(), O.decode(ref))
