@@ -225,3 +225,44 @@ def test_short_partial_last_block(n, dt, mode, target):
     assert res.to_bytes() == ref
     assert np.array_equal(res.block_offsets.cpu().numpy(), offs)
     assert np.array_equal(decode_device(res.blob, res.nbytes).cpu().numpy(), O.decode(ref))
+
+
+def _oscillating_case(rng, dt, n):
+    """High-frequency sinusoid mixtures (centre frequency near the 1/3 gate
+    of transform.py:107-113) plus noise and a random level."""
+    t = np.arange(n, dtype=np.float64)
+    f = rng.uniform(0.05, 0.5, 3)
+    x = sum(rng.uniform(0.3, 1.0) * np.sin(2 * np.pi * fi * t + rng.uniform(0, 6.3)) for fi in f)
+    x = x + rng.normal(0, rng.uniform(0.0, 0.5), n) + rng.uniform(-0.5, 0.5)
+    if dt.is_float:
+        return (x * 10.0 ** rng.uniform(-3, 5)).astype(dt.np_dtype)
+    info = np.iinfo(dt.np_dtype)
+    return np.clip(np.rint(x * 0.3 * info.max), info.min, info.max).astype(dt.np_dtype)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_short_tails_vs_oracle(seed):
+    """Random dtype / mode / block size / segments over oscillating data
+    whose last block is a short tail (1..70 samples): the monitor gate, the
+    partial-block paths and the d3 / v2 decoders, all against the oracle."""
+    rng = np.random.default_rng(7000 + seed)
+    for _ in range(8):
+        dt = [Dtype.I8, Dtype.I16, Dtype.I32, Dtype.F32, Dtype.F64][rng.integers(0, 5)]
+        modes = [Mode.FIXED_RATE, Mode.FIXED_QUALITY] + ([] if dt.is_float else [Mode.LOSSLESS])
+        mode = modes[rng.integers(0, len(modes))]
+        bs = int(rng.choice([128, 256, 1000, 2048, 4096, 5000]))
+        n = bs * int(rng.integers(1, 9)) + int(rng.integers(1, 71))
+        target = float(rng.uniform(1, 12)) if mode is Mode.FIXED_RATE else float(rng.uniform(10, 100))
+        seg = int(rng.choice([0, 0, 1, 2, 3]))
+        pol = "warm_self" if (mode is Mode.FIXED_RATE and rng.integers(0, 2)) else "cold"
+        x = _oscillating_case(rng, dt, n)
+        cfg = StreamConfig(dt, bs, mode, target, segment_blocks=seg or None, segment_policy=pol)
+        ref, offs, _ = O.encode(x, dt.wire_code, mode.value, target, bs, segment_blocks=seg,
+                                policy=1 if pol == "warm_self" else 0)
+        res = encode_device(torch.from_numpy(x).cuda(), cfg)
+        assert res.to_bytes() == ref, (dt, mode, bs, target, seg, pol, n)
+        yo = O.decode(ref)
+        assert np.array_equal(decode_device(res.blob, res.nbytes).cpu().numpy(), yo), (dt, mode, bs, seg)
+        if seg:
+            y3 = decode_device(res.blob, res.nbytes, res.block_offsets, segment_blocks=seg).cpu().numpy()
+            assert np.array_equal(y3, yo), (dt, mode, bs, seg, "d3")
