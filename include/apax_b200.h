@@ -87,6 +87,15 @@ int apax_encode_lossless_range(const void* x, int64_t halo, int64_t n, int dtype
                                int64_t first_block, uint8_t* out, int64_t out_cap, int64_t* block_offsets,
                                uint64_t* status, void* ws, int64_t ws_bytes, void* stream);
 
+/* Segment length of a container from its block index (device pointers):
+ * writes P to *segment_blocks_out when block b carries the restart flag
+ * (header byte 0, bit 2) exactly for b % P == 0, else 0 (a
+ * whole-stream container, or any other pattern).  Lets an index-less decode
+ * of a segmented container (offsets from apax_find_blocks) take
+ * apax_decode_segments.  One CTA; enqueued on `stream`. */
+int apax_detect_segments(const uint8_t* blob, int64_t nbytes, const int64_t* block_offsets, int64_t n_blocks,
+                         uint64_t* segment_blocks_out, void* stream);
+
 /* Copy n_words (1..32) status words from a device status buffer to PAGE-LOCKED
  * HOST memory (cudaHostAlloc / torch pin_memory) with stores issued by one
  * thread block, enqueued on `stream`.  For pipelined host round trips: a

@@ -58,6 +58,9 @@ def lib():
     if hasattr(L, "apax_encode_lossless_range"):
         L.apax_encode_lossless_range.argtypes = [P, I64, I64, I32, I32, I64, P, I64, P, P, P, I64, P]
         L.apax_encode_lossless_range.restype = I32
+    if hasattr(L, "apax_detect_segments"):
+        L.apax_detect_segments.argtypes = [P, I64, P, I64, P, P]
+        L.apax_detect_segments.restype = I32
     if hasattr(L, "apax_status_to_host"):
         L.apax_status_to_host.argtypes = [P, P, I32, P]
         L.apax_status_to_host.restype = I32
@@ -88,5 +91,5 @@ EXPORTED_SYMBOLS = (
     "apax_decode_segments_workspace_bytes", "apax_decode_segments",
     "apax_encode_wave_segment_blocks", "apax_profile_grid", "apax_profile_sums", "apax_profile_welch",
     "apax_profile_select", "apax_decode_range", "apax_status_to_host",
-    "apax_encode_lossless_range",
+    "apax_encode_lossless_range", "apax_detect_segments",
 )

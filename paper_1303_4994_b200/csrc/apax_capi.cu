@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <mutex>
 #include <cuda_runtime.h>
 
 #include "../../include/apax_b200.h"
@@ -158,6 +159,34 @@ int plan_decode(long long n, int dt, int bs, DecPlan* p) {
 }  // namespace
 
 namespace {
+// segment structure of a container from its block index: the restart flags
+// (header byte 0, bit 2) must sit exactly on the multiples of the first
+// restart block's index P > 0; out[0] = P, or 0 when the pattern does not
+// hold (or no block but the first restarts)
+__global__ void detect_segments_kernel(const uint8_t* blob, long long nbytes, const long long* offs,
+                                       long long nb, unsigned long long* out) {
+    __shared__ unsigned long long first;
+    __shared__ int broken;
+    if (threadIdx.x == 0) { first = ~0ULL; broken = 0; }
+    __syncthreads();
+    for (long long b = 1 + threadIdx.x; b < nb; b += blockDim.x) {
+        const long long o = offs[b];
+        if (o < 0 || o >= nbytes) { broken = 1; continue; }
+        if ((blob[o] >> 2) & 1) atomicMin(&first, (unsigned long long)b);
+    }
+    __syncthreads();
+    const unsigned long long P = first;
+    if (P != ~0ULL) {
+        for (long long b = 1 + threadIdx.x; b < nb; b += blockDim.x) {
+            const long long o = offs[b];
+            const int r = (o >= 0 && o < nbytes) ? ((blob[o] >> 2) & 1) : 0;
+            if (r != ((unsigned long long)b % P == 0 ? 1 : 0)) broken = 1;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) out[0] = (P == ~0ULL || broken) ? 0ULL : P;
+}
+
 // status words to pinned host memory by plain stores from an SM: a copy-engine
 // D2H of 32 bytes would queue behind the bulk copies of a pipelined round trip
 __global__ void status_to_host_kernel(const unsigned long long* src, unsigned long long* dst, int n) {
@@ -337,7 +366,19 @@ int apax_find_blocks(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, 
     if (nb < 2 || !env_int("APAX_K5", 1))
         return launch_walk(blob, nbytes, n, block_size, dtype, nb, (long long*)offsets,
                            (unsigned long long*)status, s);
-    // K5 scratch from the stream-ordered pool (this entry point takes no workspace)
+    // K5 scratch from the stream-ordered pool (this entry point takes no
+    // workspace); the pool keeps its memory across calls instead of
+    // returning it at every synchronisation (re-mapping cost ms per call)
+    static std::once_flag pool_once;
+    std::call_once(pool_once, [] {
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            unsigned long long keep = ~0ULL;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        cudaGetLastError();
+    });
     void* ws = nullptr;
     if (cudaMallocAsync(&ws, find_blocks_k5_ws_bytes(nb), s) != cudaSuccess) return APAX_ERR_CUDA;
     int st = launch_find_blocks_k5(blob, nbytes, n, block_size, dtype, nb, (long long*)offsets,
@@ -547,6 +588,14 @@ int apax_parse_file_header(const uint8_t* d, int64_t len, int* dt, int* mode, in
     if (*mode == APAX_FIXED_RATE && !(*target > 0)) return APAX_ERR_CFG_FR_TARGET;
     *detail = -1;
     return APAX_OK;
+}
+
+int apax_detect_segments(const uint8_t* blob, int64_t nbytes, const int64_t* block_offsets, int64_t n_blocks,
+                         uint64_t* segment_blocks_out, void* stream) {
+    if (!blob || !block_offsets || !segment_blocks_out || n_blocks < 1) return APAX_ERR_ARG;
+    detect_segments_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(blob, nbytes, (const long long*)block_offsets,
+                                                                 n_blocks, (unsigned long long*)segment_blocks_out);
+    return cudaGetLastError() == cudaSuccess ? APAX_OK : APAX_ERR_CUDA;
 }
 
 int apax_status_to_host(const uint64_t* status, uint64_t* host_dst, int n_words, void* stream) {
