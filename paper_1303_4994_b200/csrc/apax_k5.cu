@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(NT) parse_kernel(const uint8_t* blob, long lon
     const long long nc = (long long)W.hdr->ncand;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int G = bs >> 2;
-    uint8_t* e = smem_k5 + warp * ((G + 15) & ~15);
+    uint8_t* e = smem_k5 + warp * ((G + 16 + 15) & ~15);   // the fast parser may write e[G]
     const int hs = hdr_size(dt);
     const long long maxj = (3LL * G + 2) / 2;
     const long long nwarps = (long long)gridDim.x * NW;
@@ -219,7 +219,27 @@ __global__ void __launch_bounds__(NT) parse_kernel(const uint8_t* blob, long lon
         if (avail >= 0) {
             const long long nbj = avail < maxj ? avail : maxj;
             long long used = 0, esum = 0;
-            const int st = warp_jee_decode(blob + pos + hs, 2 * nbj, G, e, used, esum);
+            // fast parse (128 nibbles per step); any irregularity -- which
+            // most false candidates hit within a few tokens -- takes the
+            // exact parser, which decides the candidate
+            int u = 0;
+            int st = warp_jee_fast(blob + pos + hs, blob + nbytes, (int)(2 * nbj), G, e, u);
+            if (st == 0) {
+                used = u;
+                unsigned sb = 0;
+                for (int g = 4 * lane; g < G; g += 128) {
+                    uint32_t ew;
+                    if (g + 4 <= G) ew = *(const uint32_t*)(e + g);
+                    else {
+                        ew = 0;
+                        for (int c = 0; c < 4; c++) ew |= (g + c < G ? (uint32_t)e[g + c] : 0u) << (8 * c);
+                    }
+                    sb += (unsigned)__dp4a(ew, 0x01010101u, 0u);
+                }
+                esum = __reduce_add_sync(0xffffffffu, sb);
+            } else {
+                st = warp_jee_decode(blob + pos + hs, 2 * nbj, G, e, used, esum);
+            }
             const long long sz = (used + 1) / 2 + (4 * esum + 7) / 8;
             if (!st && avail >= sz) nxt = pos + hs + sz;
         }
@@ -328,7 +348,7 @@ int launch_find_blocks_k5(const uint8_t* blob, long long nbytes, long long n, in
     count_kernel<<<ncb, NT, 0, st>>>(blob, nbytes, hs, ncb, W.ccount);
     scan_kernel<<<1, 1024, 0, st>>>(W.ccount, ncb, W.cbase, &W.hdr->ncand, W.cap, &W.hdr->fail);
     emit_kernel<<<ncb, NT, 0, st>>>(blob, nbytes, hs, ncb, W);
-    const size_t psmem = (size_t)NW * (((bs >> 2) + 15) & ~15);
+    const size_t psmem = (size_t)NW * (((bs >> 2) + 16 + 15) & ~15);
     if (cudaFuncSetAttribute(parse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem) != cudaSuccess)
         return APAX_ERR_CUDA;
     long long pgrid = (W.cap + NW - 1) / NW;
