@@ -425,6 +425,14 @@ int apax_decode(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, int b
     P.carry = (unsigned long long*)(w + p.ws_carry);
     P.ticket = (unsigned int*)(w + p.ws_ticket);
     P.payload_cap = p.payload_cap;
+    if (decode_v3_supported(dtype, block_size) && env_int("APAX_DEC_VER", 0) != 2) {
+        // any container through the segment-serial decoder: one-wave pseudo-
+        // segments, pass 1 for their history maps, pass 2 with the composed
+        // entries (the carry region holds maps + entries)
+        const size_t sm3 = decode_v3_smem_bytes(dtype, p.payload_cap);
+        const int g3 = decode_v3_resident_ctas(dtype, sm3);
+        return launch_decode_v3_two_pass(dtype, P, g3, sm3, P.carry, s);
+    }
     if (p.v2) return launch_decode_v2(dtype, P, p.grid, p.smem, s);
     return launch_decode(dtype, P, p.grid, p.smem, s);
 }

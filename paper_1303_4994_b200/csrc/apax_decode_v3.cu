@@ -110,7 +110,10 @@ __device__ __forceinline__ uint32_t r32(const uint32_t* w, int bp) {
 }
 
 
-template <int DT, bool FIX>
+// TP: 0 a segmented container; 1 pass 1 of a two-pass decode (segment
+// history maps, no samples); 2 pass 2 (segments start from composed entries).
+// A template parameter so the segmented hot path carries none of it.
+template <int DT, bool FIX, int TP>
 __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P) {
     using Tr = DT_<DT>;
     using T = typename Tr::T;
@@ -191,7 +194,15 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
     for (long long sg = s_begin + blockIdx.x; sg < s_end; sg += gridDim.x) {
         const long long b0 = sg * P_seg;
         const long long b1 = (b0 + P_seg < P.n_blocks) ? b0 + P_seg : P.n_blocks;
-        if (tid == 0) { S->p1 = 0; S->p2 = 0; }
+        // history entering the segment: (0, 0) at a restart (a segmented
+        // container), or the composed entry of pass 2 of a two-pass decode
+        if (tid == 0) {
+            S->p1 = TP == 2 ? (long long)P.seg_entry[2 * sg] : 0;
+            S->p2 = TP == 2 ? (long long)P.seg_entry[2 * sg + 1] : 0;
+        }
+        // pass 1: the segment's history map, A composed block by block (c is
+        // the history leaving the segment from a (0, 0) entry)
+        unsigned long long A11 = 1, A12 = 0, A21 = 0, A22 = 1;
         for (long long bb = b0; bb < b1; bb += JB) {
         const int nbat = (int)((b1 - bb) < JB ? (b1 - bb) : JB);
         // ---- JEE of the batch (entropy.py:118-164): warp w parses block bb + w
@@ -401,6 +412,7 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
             // op per sample on the decoder's busiest pipe
             auto i2d = [](int v) -> double { return (double)v; };
             T out[SPT];
+            constexpr bool want_y = TP != 1;   // pass 1 of a two-pass decode needs the history only
             const uint32_t* w = (const uint32_t*)pay;
             int bp = 8 * ((int)pay_off + jee_bytes) + (int)bpre;
             if (narrow) {
@@ -456,7 +468,8 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                         }
                     }
 #pragma unroll
-                    for (int i = 0; i < SPT; i++) out[i] = deq(i2d(v[i]));
+                    if (want_y)
+                        for (int i = 0; i < SPT; i++) out[i] = deq(i2d(v[i]));
                 } else {
                     unsigned long long qa = q0, da = d0;
 #pragma unroll
@@ -466,7 +479,7 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                         else { da += (unsigned long long)(long long)v[i]; qa += da; qv = (long long)qa; }
                         if (hist_thread && i == j1) S->p1 = qv;
                         if (hist_thread && i == j1 - 1) S->p2 = qv;
-                        out[i] = deq((double)qv);
+                        if (want_y) out[i] = deq((double)qv);
                     }
                 }
             } else {
@@ -512,16 +525,28 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                     if (hist_thread && i == j1) S->p1 = q[i];
                     if (hist_thread && i == j1 - 1) S->p2 = q[i];
                     const long long qv = q[i];
-                    out[i] = deq(qv == (long long)(int)qv ? i2d((int)qv) : (double)qv);
+                    if (want_y) out[i] = deq(qv == (long long)(int)qv ? i2d((int)qv) : (double)qv);
                 }
             }
             // ---- y staged in shared memory, one TMA bulk store per block ----
+            if (TP == 1 && tid == 0) {
+                // the block's history map (transform.py:116-129): D0 and
+                // restart blocks forget the entry; D1 adds it; D2 adds a line
+                unsigned long long b11, b12, b21, b22;
+                const unsigned long long unp = (unsigned long long)np;
+                if (sel == 0 || restart) { b11 = b12 = b21 = b22 = 0; }
+                else if (sel == 1) { b11 = 1; b12 = 0; b21 = 1; b22 = 0; }
+                else { b11 = unp + 1; b12 = 0ULL - unp; b21 = unp; b22 = 0ULL - (unp - 1); }
+                const unsigned long long n11 = b11 * A11 + b12 * A21, n12 = b11 * A12 + b12 * A22;
+                const unsigned long long n21 = b21 * A11 + b22 * A21, n22 = b21 * A12 + b22 * A22;
+                A11 = n11; A12 = n12; A21 = n21; A22 = n22;
+            }
             T* ybuf = YOWN ? ybuf_own : (T*)pay;
             if (YOWN && tid == 0 && S->store_pending) { bulk_wait_read(); S->store_pending = 0; }
             // the y buffer is free: the previous store has read it (f64); the payload
             // is unpacked by every thread (D1/D2: the reconstruct scan's barrier did it)
             if (YOWN || sel == 0) cbar();
-            if (active) {
+            if (active && want_y) {
                 constexpr int PER = 16 / (int)sizeof(T);
                 uint4* y4 = (uint4*)(ybuf + SPT * tid);
 #pragma unroll
@@ -533,7 +558,7 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
             }
             fence_proxy_async();
             cbar();
-            if (tid == 0) {
+            if (tid == 0 && want_y) {
                 T* y = (T*)P.y + start;
                 const int bytes = n * (int)sizeof(T);
                 const int full = bytes & ~15;
@@ -547,6 +572,11 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
             }
         }   // blocks of the batch
         }   // batches
+        if (TP == 1 && tid == 0) {   // S->p1/p2 are final: the last block's barriers ordered them
+            unsigned long long* m = P.seg_map + 6 * sg;
+            m[0] = A11; m[1] = A12; m[2] = A21; m[3] = A22;
+            m[4] = (unsigned long long)S->p1; m[5] = (unsigned long long)S->p2;
+        }
     }
     if (tid == 0 && S->store_pending) bulk_wait_all();
 }
@@ -564,14 +594,17 @@ bool decode_v3_supported(int dt, int bs) {
 }
 
 template <int DT, bool FIX>
-static void* d3_fn() { return (void*)d3::decode_v3_kernel<DT, FIX>; }
-static void* d3_kernel(int dt, bool fix) {
+static void* d3_fn(int tp) {
+    return tp == 1 ? (void*)d3::decode_v3_kernel<DT, FIX, 1>
+                   : (tp == 2 ? (void*)d3::decode_v3_kernel<DT, FIX, 2> : (void*)d3::decode_v3_kernel<DT, FIX, 0>);
+}
+static void* d3_kernel(int dt, bool fix, int tp = 0) {
     switch (dt) {
-        case 0: return d3_fn<0, false>();
-        case 1: return fix ? d3_fn<1, true>() : d3_fn<1, false>();
-        case 2: return fix ? d3_fn<2, true>() : d3_fn<2, false>();
-        case 3: return fix ? d3_fn<3, true>() : d3_fn<3, false>();
-        default: return fix ? d3_fn<4, true>() : d3_fn<4, false>();
+        case 0: return d3_fn<0, false>(tp);
+        case 1: return fix ? d3_fn<1, true>(tp) : d3_fn<1, false>(tp);
+        case 2: return fix ? d3_fn<2, true>(tp) : d3_fn<2, false>(tp);
+        case 3: return fix ? d3_fn<3, true>(tp) : d3_fn<3, false>(tp);
+        default: return fix ? d3_fn<4, true>(tp) : d3_fn<4, false>(tp);
     }
 }
 
@@ -587,8 +620,8 @@ int decode_v3_resident_ctas(int dt, size_t smem) {
 }
 
 static int launch_d3_range(int dt, bool fix, const DecParams& P, long long s0, long long s1, int grid,
-                           size_t smem, cudaStream_t st) {
-    const void* fn = d3_kernel(dt, fix);
+                           size_t smem, cudaStream_t st, int tp) {
+    const void* fn = d3_kernel(dt, fix, tp);
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return APAX_ERR_CUDA;
     DecParams p = P;
@@ -601,7 +634,50 @@ static int launch_d3_range(int dt, bool fix, const DecParams& P, long long s0, l
     return APAX_OK;
 }
 
+// entries of a two-pass decode: e_0 = (0, 0), e_{k+1} = F_k(e_k) (one thread;
+// a few hundred segments)
+__global__ void compose_entries_kernel(const unsigned long long* maps, long long nseg, unsigned long long* entries) {
+    unsigned long long h1 = 0, h2 = 0;
+    for (long long k = 0; k < nseg; k++) {
+        entries[2 * k] = h1;
+        entries[2 * k + 1] = h2;
+        const unsigned long long* m = maps + 6 * k;
+        const unsigned long long o1 = m[0] * h1 + m[1] * h2 + m[4];
+        const unsigned long long o2 = m[2] * h1 + m[3] * h2 + m[5];
+        h1 = o1;
+        h2 = o2;
+    }
+}
+
+static int launch_decode_v3_tp(int dt, const DecParams& P, int grid, size_t smem, cudaStream_t st, int tp);
+
+// any container through d3: pseudo-segments of P blocks (one wave), pass 1
+// for their history maps, a sequential composition, pass 2 with the entries
+int launch_decode_v3_two_pass(int dt, DecParams P, int grid, size_t smem, unsigned long long* scratch,
+                              cudaStream_t st) {
+    const long long seg = (P.n_blocks + grid - 1) / grid;
+    const long long nseg = (P.n_blocks + seg - 1) / seg;
+    unsigned long long* maps = scratch;
+    unsigned long long* entries = scratch + 6 * nseg;
+    P.segment_blocks = seg;
+    P.seg_map = maps;
+    P.seg_entry = nullptr;
+    P.no_store = 1;
+    int r = launch_decode_v3_tp(dt, P, grid, smem, st, 1);
+    if (r) return r;
+    compose_entries_kernel<<<1, 1, 0, st>>>(maps, nseg, entries);
+    if (cudaGetLastError() != cudaSuccess) return APAX_ERR_CUDA;
+    P.seg_map = nullptr;
+    P.seg_entry = entries;
+    P.no_store = 0;
+    return launch_decode_v3_tp(dt, P, grid, smem, st, 2);
+}
+
 int launch_decode_v3(int dt, const DecParams& P, int grid, size_t smem, cudaStream_t st) {
+    return launch_decode_v3_tp(dt, P, grid, smem, st, 0);
+}
+
+static int launch_decode_v3_tp(int dt, const DecParams& P, int grid, size_t smem, cudaStream_t st, int tp) {
     const long long nseg = (P.n_blocks + P.segment_blocks - 1) / P.segment_blocks;
     // full-block segments take the compile-time-geometry kernel; the segment
     // holding a partial last block follows in a generic launch
@@ -609,10 +685,10 @@ int launch_decode_v3(int dt, const DecParams& P, int grid, size_t smem, cudaStre
     long long sfull = fixable ? nseg : 0;
     if (fixable && (P.n % d3::MAXBS) != 0) sfull = nseg - 1;
     if (sfull > 0) {
-        const int r = launch_d3_range(dt, true, P, 0, sfull, grid, smem, st);
+        const int r = launch_d3_range(dt, true, P, 0, sfull, grid, smem, st, tp);
         if (r) return r;
     }
-    if (sfull < nseg) return launch_d3_range(dt, false, P, sfull, nseg, grid, smem, st);
+    if (sfull < nseg) return launch_d3_range(dt, false, P, sfull, nseg, grid, smem, st, tp);
     return APAX_OK;
 }
 

@@ -54,6 +54,12 @@ struct DecParams {
     // v2 range decode (apax_decode_range): derivative history entering
     // block 0 of this launch when it is not a restart block (default 0, 0)
     unsigned long long entry_p1, entry_p2;
+    // d3 two-pass decode of any container (apax_decode): pass 1 writes each
+    // segment's history map (A11, A12, A21, A22, c1, c2) to seg_map and skips
+    // the samples (no_store); pass 2 starts segment k from seg_entry[2k..2k+1]
+    unsigned long long* seg_map;
+    const unsigned long long* seg_entry;
+    int no_store;
 };
 
 size_t encode_smem_bytes(int dt, int bs, int stage_bytes, int x_in_smem);
@@ -76,6 +82,8 @@ size_t decode_v3_smem_bytes(int dt, int payload_cap);
 bool decode_v3_supported(int dt, int bs);
 int decode_v3_resident_ctas(int dt, size_t smem);
 int launch_decode_v3(int dt, const DecParams& P, int grid, size_t smem, cudaStream_t st);
+int launch_decode_v3_two_pass(int dt, DecParams P, int grid, size_t smem, unsigned long long* scratch,
+                              cudaStream_t st);
 size_t decode_v2_smem_bytes(int dt, int bs, int payload_cap);
 bool decode_v2_supported(int bs);
 int decode_v2_resident_ctas(int dt, size_t smem);
