@@ -48,10 +48,8 @@ constexpr int NT = 256;
 constexpr int NW = NT / 32;
 constexpr int SPT = 16;
 constexpr int MAXBS = 4096;
-constexpr int NIB_PER_PASS = 4 * NT;
 constexpr int JB = 8;                                  // blocks per JEE batch (one warp each)
 constexpr int EBS = MAXBS / 4 + 128;                   // exponent bytes per batch slot
-constexpr double kMagicI = 6755401588539392.0;   // 1.5 * 2^52 + 2^31
 
 struct __align__(16) St {
     // block descriptor (thread 0 at issue time) for the two payload buffers
@@ -214,6 +212,7 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
             const int Gj = FIX ? MAXBS / 4 : (nj + 3) >> 2;
             const long long o0 = P.offsets[bj];
             int st = 0, u = 0, hdr = 0;
+            unsigned wmax = 64;
             if (o0 >= 0 && P.nbytes - o0 >= HS) {
                 // block header (dtypes.py:156-180) packed for the decode phase:
                 // selector | restart << 2 | code << 8 | fbe << 24
@@ -236,7 +235,7 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                 if (st == 0) {
                     // mantissa bits (entropy.py:209-219) per decode warp (128 groups
                     // = 4 lanes of 32 here): the decode phase then needs only a warp scan
-                    unsigned sb = 0;
+                    unsigned sb = 0, em = 0;
 #pragma unroll
                     for (int k = 0; k < 32; k += 4) {
                         const int g = 32 * lane + k;
@@ -247,8 +246,13 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                             for (int c = 0; c < 4; c++) ew |= (g + c < Gj ? (uint32_t)ej[g + c] : 0u) << (8 * c);
                         }
                         sb += (unsigned)__dp4a(ew, 0x01010101u, 0u);
+                        em = __vmaxu4(em, ew);
                     }
                     sb *= 4u;
+                    // the block's widest group: <= 16 lets the reconstruct scan
+                    // carry the value sums in 32 bits (CTA-uniform choice)
+                    em = max(max(em & 0xffu, (em >> 8) & 0xffu), max((em >> 16) & 0xffu, em >> 24));
+                    wmax = __reduce_max_sync(0xffffffffu, em);
 #pragma unroll
                     for (int d = 1; d < 32; d <<= 1) {
                         const unsigned o = __shfl_up_sync(0xffffffffu, sb, d);
@@ -257,7 +261,7 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                     if ((lane & 3) == 3) S->wbits[warp][lane >> 2] = sb;
                 }
             }
-            if (lane == 0) S->jinfo[warp] = make_int4(hdr, st, u, 0);
+            if (lane == 0) S->jinfo[warp] = make_int4(hdr, st, u, (int)wmax);
         }
         cbar();
         for (int kb = 0; kb < nbat; kb++, kk++) {
@@ -302,6 +306,7 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
             const int fbe = Tr::F ? (ji.x >> 24) : 0;     // int8 (arithmetic shift)
             if (!err) err = (sel == 3) ? APAX_ERR_SELECTOR : ji.y;
             const int used = ji.z;
+            const bool bnarrow = ji.w <= 16;
             const int jee_bytes = (used + 1) >> 1;
             // ---- mantissa offsets (entropy.py:209-219): CTA scan of 4*sum(e) ----
             const int g0 = 4 * tid;
@@ -346,40 +351,41 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
             // CTA exclusive prefix of the thread aggregates (s = sum v, t = sum of
             // local partial sums); ranges compose as (s, t, m): A then B =
             // (sA+sB, tA+tB+mB*sA, mA+mB) (transform.py:116-129 as a scan)
-            auto recon_scan = [&](unsigned long long s, unsigned long long t, unsigned long long& ps,
-                                  unsigned long long& pt) {
-                unsigned long long xs = s, xt = t;
-                unsigned xm = SPT;
+            // The count m of a range is implied by the lanes it covers (the B side of
+            // step d spans d lanes / warps), so only s and t travel.  VS is the
+            // type of s: 32 bits when the block's widest group is <= 16 (|CTA sum|
+            // < 4096 * 2^15), else 64.
+            auto recon_scan = [&](auto s, unsigned long long t, unsigned long long& ps, unsigned long long& pt) {
+                using VS = decltype(s);
+                auto wide = [](VS v) -> unsigned long long { return (unsigned long long)(long long)v; };
+                VS xs = s;
+                unsigned long long xt = t;
 #pragma unroll
                 for (int d = 1; d < 32; d <<= 1) {
-                    const unsigned long long os = __shfl_up_sync(0xffffffffu, xs, d);
+                    const VS os = __shfl_up_sync(0xffffffffu, xs, d);
                     const unsigned long long ot = __shfl_up_sync(0xffffffffu, xt, d);
-                    const unsigned om = __shfl_up_sync(0xffffffffu, xm, d);
-                    if (lane >= d) { xt = ot + xt + (unsigned long long)xm * os; xs += os; xm += om; }
+                    if (lane >= d) { xt = ot + xt + (unsigned long long)(d * SPT) * wide(os); xs += os; }
                 }
                 if (lane == 31) { S->rs_w[warp] = (long long)xs; S->rt_w[warp] = (long long)xt; }
                 cbar();
-                unsigned long long ws = (lane < NW) ? (unsigned long long)S->rs_w[lane & (NW - 1)] : 0ULL;
+                VS ws = (lane < NW) ? (VS)S->rs_w[lane & (NW - 1)] : (VS)0;
                 unsigned long long wt = (lane < NW) ? (unsigned long long)S->rt_w[lane & (NW - 1)] : 0ULL;
-                unsigned wmm = 32 * SPT;
 #pragma unroll
                 for (int d = 1; d < NW; d <<= 1) {
-                    const unsigned long long os = __shfl_up_sync(0xffffffffu, ws, d);
+                    const VS os = __shfl_up_sync(0xffffffffu, ws, d);
                     const unsigned long long ot = __shfl_up_sync(0xffffffffu, wt, d);
-                    const unsigned om = __shfl_up_sync(0xffffffffu, wmm, d);
-                    if (lane >= d) { wt = ot + wt + (unsigned long long)wmm * os; ws += os; wmm += om; }
+                    if (lane >= d) { wt = ot + wt + (unsigned long long)(d * 32 * SPT) * wide(os); ws += os; }
                 }
-                unsigned long long es = __shfl_up_sync(0xffffffffu, ws, 1);
+                VS es = __shfl_up_sync(0xffffffffu, ws, 1);
                 unsigned long long et = __shfl_up_sync(0xffffffffu, wt, 1);
                 if (lane == 0) { es = 0; et = 0; }
-                const unsigned long long pws = __shfl_sync(0xffffffffu, es, warp);
+                const VS pws = __shfl_sync(0xffffffffu, es, warp);
                 const unsigned long long pwt = __shfl_sync(0xffffffffu, et, warp);
-                unsigned long long ls = __shfl_up_sync(0xffffffffu, xs, 1);
+                VS ls = __shfl_up_sync(0xffffffffu, xs, 1);
                 unsigned long long lt = __shfl_up_sync(0xffffffffu, xt, 1);
-                unsigned lm = __shfl_up_sync(0xffffffffu, xm, 1);
-                if (lane == 0) { ls = 0; lt = 0; lm = 0; }
-                ps = pws + ls;
-                pt = pwt + lt + (unsigned long long)lm * pws;
+                if (lane == 0) { ls = 0; lt = 0; }
+                ps = wide(pws) + wide(ls);
+                pt = pwt + lt + (unsigned long long)(lane * SPT) * wide(pws);
             };
             // dequantize one reconstructed sample (codec.py:135-146): Markstein
             // quotient against a per-block reciprocal, bit-identical to IEEE
@@ -436,7 +442,8 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
 #pragma unroll
                     for (int i = 0; i < SPT; i++) { s32 += v[i]; t32 += s32; }
                     unsigned long long ps, pt;
-                    recon_scan((unsigned long long)(long long)s32, (unsigned long long)(long long)t32, ps, pt);
+                    if (bnarrow) recon_scan(s32, (unsigned long long)(long long)t32, ps, pt);
+                    else recon_scan((long long)s32, (unsigned long long)(long long)t32, ps, pt);
                     if (sel == 1) {
                         q0 = h1 + ps;
                     } else {
@@ -467,9 +474,10 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                             if (i == j1 - 1) S->p2 = v[i];
                         }
                     }
+                    if (want_y) {
 #pragma unroll
-                    if (want_y)
                         for (int i = 0; i < SPT; i++) out[i] = deq(i2d(v[i]));
+                    }
                 } else {
                     unsigned long long qa = q0, da = d0;
 #pragma unroll
@@ -504,7 +512,7 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
 #pragma unroll
                     for (int i = 0; i < SPT; i++) { s += (unsigned long long)q[i]; t += s; }
                     unsigned long long ps, pt;
-                    recon_scan(s, t, ps, pt);
+                    recon_scan((long long)s, t, ps, pt);
                     if (sel == 1) {
                         unsigned long long acc = h1 + ps;
 #pragma unroll

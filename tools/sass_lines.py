@@ -31,9 +31,9 @@ def main():
             continue
         if not inside:
             continue
-        m = re.search(r'line (\d+)', ln) if "//##" in ln else None
+        m = re.search(r'File "([^"]*)", line (\d+)', ln) if "//##" in ln else None
         if m:
-            line = int(m.group(1))
+            line = (m.group(1).split("/")[-1], int(m.group(2)))
             continue
         m = re.search(r'/\*([0-9a-f]{4,})\*/', ln)
         if m and line is not None:
@@ -41,14 +41,14 @@ def main():
     agg = defaultdict(lambda: [0, 0])
     tot = totw = 0
     for a, ni, nw, src in prof:
-        l = off2line.get(a - base, -1)
+        l = off2line.get(a - base, ('?', -1))
         agg[l][0] += ni
         agg[l][1] += nw
         tot += ni
         totw += nw
     print("total inst", tot, "stall samples", totw)
     for l, (ni, nw) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
-        print(f"L{l:5d} inst {ni / tot * 100:5.1f}%  stall {nw / totw * 100:5.1f}%")
+        print(f"{str(l):40s} inst {ni / tot * 100:5.1f}%  stall {nw / totw * 100:5.1f}%")
 
 
 if __name__ == "__main__":
