@@ -276,6 +276,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=8, help="pipeline chunks of the e2e round trip")
+    ap.add_argument("--e2e-taper", type=int, default=1,
+                    help="> 1: geometric ramp of chunk sizes at both ends, capped at this weight")
     ap.add_argument("--profile", action="store_true",
                     help="short run for ncu: no e2e, no cpu baseline, no clocks")
     args = ap.parse_args()
@@ -393,7 +395,7 @@ def main():
     e2e = None
     if not args.no_e2e and not args.profile and x_host is not None:
         from paper_1303_4994_b200.pipeline import HostRoundTrip
-        rt = HostRoundTrip(n, cfg, chunks=args.e2e_chunks, device=dev)
+        rt = HostRoundTrip(n, cfg, chunks=args.e2e_chunks, device=dev, taper=args.e2e_taper)
         xh = torch.from_numpy(x_host).pin_memory()
         blob_h = torch.empty(rt.blob_d.numel(), dtype=torch.uint8).pin_memory()
         offs_h = torch.empty(enc.n_blocks + 1, dtype=torch.int64).pin_memory()
@@ -436,7 +438,7 @@ def main():
                "ms_per_step": e2e_s * 1e3,
                "path": f"C-ABI apax_encode/apax_decode_segments with pinned host buffers, container + "
                        f"side-band block index round-tripped through the host, pipelined over "
-                       f"{len(rt.ranges)} chunks of whole segments (copy-in/compute/copy-out streams)",
+                       f"{len(rt.ranges)} chunks of whole segments (taper {args.e2e_taper}; copy-in/compute/copy-out streams)",
                "bit_exact_vs_device_path": ok_e2e,
                "indexless_decode": {"value": world * in_bytes / il_s / 1e9, "unit": UNIT,
                                     "ms_per_step": il_s * 1e3,

@@ -38,14 +38,27 @@ from .dtypes import StreamConfig
 from .errors import InvalidConfig
 
 
+def chunk_weights(k: int, taper: int = 1) -> List[int]:
+    """Relative chunk sizes: all equal for taper <= 1, else min(2^i,
+    2^(k-1-i), taper) (a geometric ramp up and down, capped)."""
+    if taper <= 1:
+        return [1] * k
+    return [min(1 << min(i, 30), 1 << min(k - 1 - i, 30), int(taper)) for i in range(k)]
+
+
 class HostRoundTrip:
     """Reusable pipelined host encode+decode plan for (n, config).
 
     `config.segment_blocks` must be set (chunks are whole segments).
     `chunks` is the number of pipeline chunks (rounded to segment
-    boundaries)."""
+    boundaries).  `taper` > 1 shrinks the first and last chunks
+    geometrically (weights 1, 2, 4, ... up to `taper`, mirrored): the
+    pipeline fill (the first upload before any download can start) and
+    drain (the last decode and download after the uploads end) then cost
+    a small chunk each instead of a full one."""
 
-    def __init__(self, n: int, config: StreamConfig, chunks: int = 8, device=None, depth: int = 3):
+    def __init__(self, n: int, config: StreamConfig, chunks: int = 8, device=None, depth: int = 3,
+                 taper: int = 1):
         import torch
         if not config.segment_blocks:
             raise InvalidConfig("HostRoundTrip needs a segmented StreamConfig")
@@ -56,7 +69,9 @@ class HostRoundTrip:
         seg_samples = bs * P
         n_seg = (self.n + seg_samples - 1) // seg_samples
         k = max(1, min(int(chunks), n_seg))
-        bounds = [min(self.n, ((n_seg * i) // k) * seg_samples) for i in range(k + 1)]
+        wts = chunk_weights(k, taper)
+        cw = np.concatenate([[0], np.cumsum(wts)])
+        bounds = [min(self.n, int((n_seg * int(c)) // int(cw[-1])) * seg_samples) for c in cw]
         self.ranges = [(a, b) for a, b in zip(bounds, bounds[1:]) if b > a]
         self.depth = max(2, min(depth, len(self.ranges)))
         # one encoder / decoder per in-flight slot (buffers reused round-robin)

@@ -35,14 +35,30 @@ for _ in range(5):
         h2.copy_(d2, non_blocking=True)
 torch.cuda.synchronize()
 print(f"both directions: {2 * 5 * nb / (time.perf_counter() - t) / 1e9:.1f} GB/s total")
+# chunk-sized copies (8.3 MB, a cfg2 container chunk) at aligned and odd offsets
+ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+m = 8_300_000
+for off in (0, 28, 64, 4096 + 12):
+    for name, fn in (("h2d", lambda: d[off:off + m].copy_(h[off:off + m], non_blocking=True)),
+                     ("d2h", lambda: h[off:off + m].copy_(d[off:off + m], non_blocking=True)),
+                     ("d2h-skew", lambda: h[off:off + m].copy_(d[28:28 + m], non_blocking=True))):
+        fn()
+        ev[0].record()
+        for _ in range(10):
+            fn()
+        ev[1].record()
+        torch.cuda.synchronize()
+        print(f"{name} 8.3 MB at offset {off}: {10 * m / ev[0].elapsed_time(ev[1]) / 1e6:.1f} GB/s")
 x = W.cfg2_ar2_f32()
 n = x.size
 seg = wave_segment_blocks(n, Dtype.F32, Mode.FIXED_QUALITY, 4096)
 cfg = StreamConfig(Dtype.F32, 4096, Mode.FIXED_QUALITY, W.CFG2_TARGET_DB, segment_blocks=seg)
 xh = torch.from_numpy(x).pin_memory()
 yh = torch.empty(n, dtype=torch.float32).pin_memory()
-for chunks, depth in ((4, 3), (8, 3), (8, 4), (16, 3), (16, 4)):
-    rt = HostRoundTrip(n, cfg, chunks=chunks, depth=depth)
+# PROBE_CFGS="chunks,depth,taper ..."; PROBE_TL="chunks,depth,taper" for the timeline
+cfgs = [tuple(int(v) for v in c.split(",")) for c in os.environ.get("PROBE_CFGS", "4,3,1 8,3,1 8,4,1 16,3,1 16,4,1").split()]
+for chunks, depth, taper in cfgs:
+    rt = HostRoundTrip(n, cfg, chunks=chunks, depth=depth, taper=taper)
     blob_h = torch.empty(rt.blob_d.numel(), dtype=torch.uint8).pin_memory()
     offs_h = torch.empty(rt.n_blocks + 1, dtype=torch.int64).pin_memory()
     for _ in range(2):
@@ -52,9 +68,10 @@ for chunks, depth in ((4, 3), (8, 3), (8, 4), (16, 3), (16, 4)):
     for _ in range(5):
         rt.run(xh, blob_h, offs_h, yh)
     dt = (time.perf_counter() - t) / 5
-    print(f"e2e chunks={chunks} depth={depth}: {dt * 1e3:.2f} ms/step, {n * 4 / dt / 1e9:.1f} GB/s, PCIe {(rt.h2d_bytes + rt.d2h_bytes) / dt / 1e9:.1f} GB/s both ways")
-# timeline of one 4-chunk round trip
-rt = HostRoundTrip(n, cfg, chunks=4, depth=3)
+    print(f"e2e chunks={chunks} depth={depth} taper={taper}: {dt * 1e3:.2f} ms/step, {n * 4 / dt / 1e9:.1f} GB/s, PCIe {(rt.h2d_bytes + rt.d2h_bytes) / dt / 1e9:.1f} GB/s both ways")
+# timeline of one round trip
+tc, td, tt = (int(v) for v in os.environ.get("PROBE_TL", "4,3,1").split(","))
+rt = HostRoundTrip(n, cfg, chunks=tc, depth=td, taper=tt)
 blob_h = torch.empty(rt.blob_d.numel(), dtype=torch.uint8).pin_memory()
 offs_h = torch.empty(rt.n_blocks + 1, dtype=torch.int64).pin_memory()
 rt.run(xh, blob_h, offs_h, yh)
