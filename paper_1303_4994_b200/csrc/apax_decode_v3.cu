@@ -69,6 +69,7 @@ struct __align__(16) St {
     int store_pending;
     int4 jinfo[JB];           // JEE batch per slot: packed header, JEE status (0 ok), nibbles used
     unsigned wbits[JB][8];    // mantissa bits up to the end of each decode warp's 128 groups
+    unsigned short tpre[JB][NT];   // each thread's mantissa bit offset inside its decode warp
 };
 
 using namespace apax::tma;
@@ -235,7 +236,7 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                 if (st == 0) {
                     // mantissa bits (entropy.py:209-219) per decode warp (128 groups
                     // = 4 lanes of 32 here): the decode phase then needs only a warp scan
-                    unsigned sb = 0, em = 0;
+                    unsigned sb = 0, em = 0, wb[8];
 #pragma unroll
                     for (int k = 0; k < 32; k += 4) {
                         const int g = 32 * lane + k;
@@ -245,10 +246,11 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                             ew = 0;
                             for (int c = 0; c < 4; c++) ew |= (g + c < Gj ? (uint32_t)ej[g + c] : 0u) << (8 * c);
                         }
-                        sb += (unsigned)__dp4a(ew, 0x01010101u, 0u);
+                        wb[k >> 2] = 4u * (unsigned)__dp4a(ew, 0x01010101u, 0u);
+                        sb += wb[k >> 2];
                         em = __vmaxu4(em, ew);
                     }
-                    sb *= 4u;
+                    const unsigned own = sb;
                     // the block's widest group: <= 16 lets the reconstruct scan
                     // carry the value sums in 32 bits (CTA-uniform choice)
                     em = max(max(em & 0xffu, (em >> 8) & 0xffu), max((em >> 16) & 0xffu, em >> 24));
@@ -259,6 +261,12 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                         if (lane >= d) sb += o;
                     }
                     if ((lane & 3) == 3) S->wbits[warp][lane >> 2] = sb;
+                    // per decode thread (8 per lane: 4 groups each), relative to its
+                    // decode warp (4 lanes here; < 128 * 4 * 34 bits): no scan there
+                    const unsigned sx = sb - own;
+                    unsigned run = sx - __shfl_sync(0xffffffffu, sx, lane & ~3);
+#pragma unroll
+                    for (int i = 0; i < 8; i++) { S->tpre[warp][8 * lane + i] = (unsigned short)run; run += wb[i]; }
                 }
             }
             if (lane == 0) S->jinfo[warp] = make_int4(hdr, st, u, (int)wmax);
@@ -317,16 +325,9 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                 else
                     for (int g = 0; g < 4; g++) epk |= (g0 + g < G ? (uint32_t)ebuf[g0 + g] : 0u) << (8 * g);
             }
-            const unsigned lbits = 4u * ((epk & 0xffu) + ((epk >> 8) & 0xffu) + ((epk >> 16) & 0xffu) + (epk >> 24));
-            unsigned xb = lbits;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const unsigned o = __shfl_up_sync(0xffffffffu, xb, d);
-                if (lane >= d) xb += o;
-            }
-            // the warps' bases come from the JEE warp (S->wbits): no CTA scan
+            // bit offsets from the JEE warp (S->wbits, S->tpre): no scan here
             const unsigned btot = err ? 0u : S->wbits[kb][NW - 1];
-            const unsigned bpre = (err || warp == 0 ? 0u : S->wbits[kb][warp - 1]) + (xb - lbits);
+            const unsigned bpre = err ? 0u : (warp == 0 ? 0u : S->wbits[kb][warp - 1]) + (unsigned)S->tpre[kb][tid];
             if (!err) {
                 const long long mant_bytes = ((long long)btot + 7) / 8;
                 if (avail < jee_bytes + mant_bytes) err = APAX_ERR_MANTISSA_TRUNCATED;
