@@ -246,22 +246,19 @@ static __device__ __forceinline__ int warp_jee_fast(const uint8_t* p, const uint
             val = t ? (esc ? ab : val + dv) : val;
             flag |= (t && esc) ? 1 : 0;
         }
-        // warp scan of (cnt, flag, val): A then B = (cA+cB, fA|fB, fB ? vB : vA+vB)
-        int c_i = cnt, f_i = flag, v_i = val;
+        // warp scan of (cnt, flag, val): A then B = (cA+cB, fA|fB, fB ? vB : vA+vB),
+        // packed in one word (cnt bits 0-14, flag bit 15, val bits 16-31 signed:
+        // |cnt| <= 256, -256 <= val <= 509 over a warp), so a step is one shuffle
+        auto pk = [](int c, int f, int v) -> unsigned { return (unsigned)c | ((unsigned)f << 15) | ((unsigned)v << 16); };
+        unsigned X = pk(cnt, flag, val);
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
-            const int oc = __shfl_up_sync(0xffffffffu, c_i, d);
-            const int of = __shfl_up_sync(0xffffffffu, f_i, d);
-            const int ov = __shfl_up_sync(0xffffffffu, v_i, d);
-            if (lane >= d) {
-                c_i += oc;
-                if (!f_i) v_i += ov;
-                f_i |= of;
-            }
+            const unsigned O = __shfl_up_sync(0xffffffffu, X, d);
+            if (lane >= d) X += (X & 0x8000u) ? (O & 0x7fffu) : O;
         }
-        int ec = __shfl_up_sync(0xffffffffu, c_i, 1), ef = __shfl_up_sync(0xffffffffu, f_i, 1),
-            evv = __shfl_up_sync(0xffffffffu, v_i, 1);
-        if (lane == 0) { ec = 0; ef = 0; evv = 0; }
+        unsigned EX = __shfl_up_sync(0xffffffffu, X, 1);
+        if (lane == 0) EX = 0;
+        const int ec = (int)(EX & 0x7fffu), ef = (int)((EX >> 15) & 1u), evv = (int)EX >> 16;
         int idx = cbase + ec;
         int curv = ef ? evv : vbase + evv;
         int key = 0x7fffffff;
@@ -295,8 +292,8 @@ static __device__ __forceinline__ int warp_jee_fast(const uint8_t* p, const uint
             return 0;
         }
         // the next step continues the scan
-        const int tc = __shfl_sync(0xffffffffu, c_i, 31), tf = __shfl_sync(0xffffffffu, f_i, 31),
-                  tv = __shfl_sync(0xffffffffu, v_i, 31);
+        const unsigned TX = __shfl_sync(0xffffffffu, X, 31);
+        const int tc = (int)(TX & 0x7fffu), tf = (int)((TX >> 15) & 1u), tv = (int)TX >> 16;
         cbase += tc;
         vbase = tf ? tv : vbase + tv;
     }
