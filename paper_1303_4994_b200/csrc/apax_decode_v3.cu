@@ -30,6 +30,7 @@
 //   * dequantize (codec.py:135-146) with the Markstein quotient, y staged in
 //     the block's own (now dead) payload buffer (f64: its own buffer), one
 //     TMA bulk store per block.
+#include <type_traits>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -356,7 +357,10 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
             // step d spans d lanes / warps), so only s and t travel.  VS is the
             // type of s: 32 bits when the block's widest group is <= 16 (|CTA sum|
             // < 4096 * 2^15), else 64.
-            auto recon_scan = [&](auto s, unsigned long long t, unsigned long long& ps, unsigned long long& pt) {
+            // WT (compile time): carry t (D2); D1 needs the value prefix only.
+            auto recon_scan = [&](auto s, unsigned long long t, unsigned long long& ps, unsigned long long& pt,
+                                  auto wt_tag) {
+                constexpr bool wt = decltype(wt_tag)::value;
                 using VS = decltype(s);
                 auto wide = [](VS v) -> unsigned long long { return (unsigned long long)(long long)v; };
                 VS xs = s;
@@ -364,26 +368,32 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
 #pragma unroll
                 for (int d = 1; d < 32; d <<= 1) {
                     const VS os = __shfl_up_sync(0xffffffffu, xs, d);
-                    const unsigned long long ot = __shfl_up_sync(0xffffffffu, xt, d);
-                    if (lane >= d) { xt = ot + xt + (unsigned long long)(d * SPT) * wide(os); xs += os; }
+                    if constexpr (wt) {
+                        const unsigned long long ot = __shfl_up_sync(0xffffffffu, xt, d);
+                        if (lane >= d) xt = ot + xt + (unsigned long long)(d * SPT) * wide(os);
+                    }
+                    if (lane >= d) xs += os;
                 }
                 if (lane == 31) { S->rs_w[warp] = (long long)xs; S->rt_w[warp] = (long long)xt; }
                 cbar();
                 VS ws = (lane < NW) ? (VS)S->rs_w[lane & (NW - 1)] : (VS)0;
-                unsigned long long wt = (lane < NW) ? (unsigned long long)S->rt_w[lane & (NW - 1)] : 0ULL;
+                unsigned long long wtt = (wt && lane < NW) ? (unsigned long long)S->rt_w[lane & (NW - 1)] : 0ULL;
 #pragma unroll
                 for (int d = 1; d < NW; d <<= 1) {
                     const VS os = __shfl_up_sync(0xffffffffu, ws, d);
-                    const unsigned long long ot = __shfl_up_sync(0xffffffffu, wt, d);
-                    if (lane >= d) { wt = ot + wt + (unsigned long long)(d * 32 * SPT) * wide(os); ws += os; }
+                    if constexpr (wt) {
+                        const unsigned long long ot = __shfl_up_sync(0xffffffffu, wtt, d);
+                        if (lane >= d) wtt = ot + wtt + (unsigned long long)(d * 32 * SPT) * wide(os);
+                    }
+                    if (lane >= d) ws += os;
                 }
                 VS es = __shfl_up_sync(0xffffffffu, ws, 1);
-                unsigned long long et = __shfl_up_sync(0xffffffffu, wt, 1);
+                unsigned long long et = wt ? __shfl_up_sync(0xffffffffu, wtt, 1) : 0ULL;
                 if (lane == 0) { es = 0; et = 0; }
                 const VS pws = __shfl_sync(0xffffffffu, es, warp);
-                const unsigned long long pwt = __shfl_sync(0xffffffffu, et, warp);
+                const unsigned long long pwt = wt ? __shfl_sync(0xffffffffu, et, warp) : 0ULL;
                 VS ls = __shfl_up_sync(0xffffffffu, xs, 1);
-                unsigned long long lt = __shfl_up_sync(0xffffffffu, xt, 1);
+                unsigned long long lt = wt ? __shfl_up_sync(0xffffffffu, xt, 1) : 0ULL;
                 if (lane == 0) { ls = 0; lt = 0; }
                 ps = wide(pws) + wide(ls);
                 pt = pwt + lt + (unsigned long long)(lane * SPT) * wide(pws);
@@ -443,8 +453,14 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
 #pragma unroll
                     for (int i = 0; i < SPT; i++) { s32 += v[i]; t32 += s32; }
                     unsigned long long ps, pt;
-                    if (bnarrow) recon_scan(s32, (unsigned long long)(long long)t32, ps, pt);
-                    else recon_scan((long long)s32, (unsigned long long)(long long)t32, ps, pt);
+                    const unsigned long long t64 = (unsigned long long)(long long)t32;
+                    if (sel == 1) {
+                        if (bnarrow) recon_scan(s32, t64, ps, pt, std::false_type{});
+                        else recon_scan((long long)s32, t64, ps, pt, std::false_type{});
+                    } else {
+                        if (bnarrow) recon_scan(s32, t64, ps, pt, std::true_type{});
+                        else recon_scan((long long)s32, t64, ps, pt, std::true_type{});
+                    }
                     if (sel == 1) {
                         q0 = h1 + ps;
                     } else {
@@ -513,7 +529,8 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
 #pragma unroll
                     for (int i = 0; i < SPT; i++) { s += (unsigned long long)q[i]; t += s; }
                     unsigned long long ps, pt;
-                    recon_scan((long long)s, t, ps, pt);
+                    if (sel == 1) recon_scan((long long)s, t, ps, pt, std::false_type{});
+                    else recon_scan((long long)s, t, ps, pt, std::true_type{});
                     if (sel == 1) {
                         unsigned long long acc = h1 + ps;
 #pragma unroll
