@@ -1252,7 +1252,7 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
             uint32_t esel = 0;                  // packed widths of the selected stream
             int eprev = 0, enext = 0;
             unsigned jscan = 0, jown = 0;       // packed nibble scan (inclusive) and own value
-            int mbi = 0, mbo = 0;               // mantissa bits: inclusive scan, own
+            int mbo = 0;                        // mantissa bits of this thread
             unsigned nonA = 0, kbits = 0;
             auto jee_prep = [&](int sl2) {
                 const uint32_t es = sl2 == 0 ? epk0 : (sl2 == 1 ? epk1 : epk2);
@@ -1299,26 +1299,27 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
                 kbits = __ballot_sync(0xffffffffu, co0 != 0);     // the carry-out when Pb != 0xF
                 const unsigned below = nonA & ((1u << lane) - 1u);
                 unsigned v;
+                // one packed word per lane: nibbles under carry-in 0 (bits 0-8) and 1
+                // (bits 9-17), exponent sum = mantissa bits / 4 (bits 18-31); a warp
+                // holds <= 32 * 12 nibbles and <= 32 * 4 * 65 exponent units
                 if (below) {
                     const int cin = (kbits >> (31 - __clz((int)below))) & 1u;
-                    v = (unsigned)(cin ? n1 : n0) * 0x10001u;
+                    v = (unsigned)(cin ? n1 : n0) * 0x201u;
                 } else {
-                    v = (unsigned)n0 | ((unsigned)n1 << 16);
+                    v = (unsigned)n0 | ((unsigned)n1 << 9);
                 }
+                v |= (unsigned)(mbo >> 2) << 18;
                 jown = v;
                 unsigned x = v;
-                int mb = mbo;
 #pragma unroll
                 for (int d = 1; d < 32; d <<= 1) {
                     const unsigned o = __shfl_up_sync(0xffffffffu, x, d);
-                    const int om = __shfl_up_sync(0xffffffffu, mb, d);
-                    if (lane >= d) { x += o; mb += om; }
+                    if (lane >= d) x += o;
                 }
                 jscan = x;
-                mbi = mb;
                 if (lane == 31) {
-                    S->jw[warp] = x;
-                    S->mbw[warp] = mb;
+                    S->jw[warp] = (x & 0x1ffu) | (((x >> 9) & 0x1ffu) << 16);
+                    S->mbw[warp] = 4 * (int)(x >> 18);
                     const int top = nonA ? 31 - __clz((int)nonA) : 0;
                     S->jc[warp] = (nonA ? 1 : 0) | (nonA ? (int)(((kbits >> top) & 1u) << 1) : 0);
                 }
@@ -1454,8 +1455,8 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
                 const unsigned below = nonA & ((1u << lane) - 1u);
                 const int cin_t = below ? (int)((kbits >> (31 - __clz((int)below))) & 1u) : cin_w;
                 const unsigned jx = jscan - jown;
-                const int nib_off = nib_pre + (int)(cin_w ? (jx >> 16) : (jx & 0xffffu));
-                const int mb_off = mb_pre + (mbi - mbo);
+                const int nib_off = nib_pre + (int)(cin_w ? ((jx >> 9) & 0x1ffu) : (jx & 0x1ffu));
+                const int mb_off = mb_pre + 4 * (int)(jx >> 18);
                 if (emt > (unsigned)kMaxExponent && tid == 0 && !S->bad) S->bad = APAX_ERR_INTERNAL;
                 // FR loop needs this block's exact byte count (codec.py:228-243)
                 if (tid == 0) {
