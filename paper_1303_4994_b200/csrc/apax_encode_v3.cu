@@ -1415,31 +1415,33 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
                     const int jcv = S->jc[w];
                     const int mbv = S->mbw[w];
                     // transfer f_w(c) = has ? k : c, composed left to right
-                    int h = (lane < NCW) ? (jcv & 1) : 0;
-                    int kk = (jcv >> 1) & 1;
+                    // (has, k) in bits 0, 1 of one word
+                    int hk = (lane < NCW) ? (jcv & 3) : 0;
 #pragma unroll
                     for (int d = 1; d < NCW; d <<= 1) {
-                        const int oh = __shfl_up_sync(0xffffffffu, h, d);
-                        const int ok = __shfl_up_sync(0xffffffffu, kk, d);
-                        if (lane >= d && !h) { h = oh; kk = ok; }
+                        const int o = __shfl_up_sync(0xffffffffu, hk, d);
+                        if (lane >= d && !(hk & 1)) hk = o;
                     }
-                    const int ph2 = __shfl_up_sync(0xffffffffu, h, 1);
-                    const int pk2 = __shfl_up_sync(0xffffffffu, kk, 1);
-                    const int cin = (lane == 0) ? 0 : (ph2 ? pk2 : 0);
+                    const int phk = __shfl_up_sync(0xffffffffu, hk, 1);
+                    const int cin = (lane == 0) ? 0 : ((phk & 1) ? (phk >> 1) & 1 : 0);
                     const int nw_ = (lane < NCW) ? (int)(cin ? (jwv >> 16) : (jwv & 0xffffu)) : 0;
                     const int mw_ = (lane < NCW) ? mbv : 0;
-                    int ns = nw_, ms = mw_;
+                    // nibbles (bits 0-13, <= 8 * 384) and exponent units = mantissa
+                    // bits / 4 (bits 14-31, <= 8 * 8320) in one word
+                    const unsigned own = (unsigned)nw_ | ((unsigned)(mw_ >> 2) << 14);
+                    unsigned nm = own;
 #pragma unroll
                     for (int d = 1; d < NCW; d <<= 1) {
-                        const int o1 = __shfl_up_sync(0xffffffffu, ns, d);
-                        const int o2 = __shfl_up_sync(0xffffffffu, ms, d);
-                        if (lane >= d) { ns += o1; ms += o2; }
+                        const unsigned o = __shfl_up_sync(0xffffffffu, nm, d);
+                        if (lane >= d) nm += o;
                     }
-                    nib_total = __shfl_sync(0xffffffffu, ns, NCW - 1);
-                    mb_total = __shfl_sync(0xffffffffu, ms, NCW - 1);
+                    const unsigned tot = __shfl_sync(0xffffffffu, nm, NCW - 1);
+                    nib_total = (int)(tot & 0x3fffu);
+                    mb_total = 4 * (int)(tot >> 14);
+                    const unsigned pre = __shfl_sync(0xffffffffu, nm - own, warp);
                     cin_w = __shfl_sync(0xffffffffu, cin, warp);
-                    nib_pre = __shfl_sync(0xffffffffu, ns - nw_, warp);
-                    mb_pre = __shfl_sync(0xffffffffu, ms - mw_, warp);
+                    nib_pre = (int)(pre & 0x3fffu);
+                    mb_pre = 4 * (int)(pre >> 14);
                 }
                 const int jee_bytes = (nib_total + 1) >> 1;
                 const long long blen = HS + jee_bytes + ((long long)mb_total + 7) / 8;
