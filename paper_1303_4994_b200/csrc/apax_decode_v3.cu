@@ -70,7 +70,8 @@ struct __align__(16) St {
     int store_pending;
     int4 jinfo[JB];           // JEE batch per slot: packed header, JEE status (0 ok), nibbles used
     unsigned wbits[JB][8];    // mantissa bits up to the end of each decode warp's 128 groups
-    unsigned short tpre[JB][NT];   // each thread's mantissa bit offset inside its decode warp
+    unsigned short tpre[JB][NT];
+    double2 dq[JB];           // dequantize scale and its reciprocal per slot   // each thread's mantissa bit offset inside its decode warp
 };
 
 using namespace apax::tma;
@@ -270,7 +271,14 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                     for (int i = 0; i < 8; i++) { S->tpre[warp][8 * lane + i] = (unsigned short)run; run += wb[i]; }
                 }
             }
-            if (lane == 0) S->jinfo[warp] = make_int4(hdr, st, u, (int)wmax);
+            if (lane == 0) {
+                S->jinfo[warp] = make_int4(hdr, st, u, (int)wmax);
+                // codec.py:135-146 scale (floats: times 2^fbe) and the reciprocal
+                // the Markstein quotient uses; once per block, not per thread
+                const int code = (hdr >> 8) & 0xFFFF;
+                const double ds = Tr::F ? decode_scale_code(code) * ldexp(1.0, hdr >> 24) : decode_scale_code(code);
+                S->dq[warp] = make_double2(ds, __ddiv_rn(1.0, ds));
+            }
         }
         cbar();
         for (int kb = 0; kb < nbat; kb++, kk++) {
@@ -311,8 +319,7 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
             int err = S->ld_err[cur];
             const int pay_off = S->ld_payoff[cur], avail = S->ld_avail[cur], staged = S->ld_staged[cur];
             const int4 ji = S->jinfo[kb];
-            const int sel = ji.x & 3, restart = (ji.x >> 2) & 1, code = (ji.x >> 8) & 0xFFFF;
-            const int fbe = Tr::F ? (ji.x >> 24) : 0;     // int8 (arithmetic shift)
+            const int sel = ji.x & 3, restart = (ji.x >> 2) & 1;   // scale code, fbe: S->dq
             if (!err) err = (sel == 3) ? APAX_ERR_SELECTOR : ji.y;
             const int used = ji.z;
             const bool bnarrow = ji.w <= 16;
@@ -358,19 +365,23 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
             // type of s: 32 bits when the block's widest group is <= 16 (|CTA sum|
             // < 4096 * 2^15), else 64.
             // WT (compile time): carry t (D2); D1 needs the value prefix only.
-            auto recon_scan = [&](auto s, unsigned long long t, unsigned long long& ps, unsigned long long& pt,
+            // VT: the type of the warp-level t (32 bits when the block's widest
+            // group is <= 14: a warp's weighted sum is < 512 * 513 / 2 * 2^13 < 2^31).
+            auto recon_scan = [&](auto s, auto t, unsigned long long& ps, unsigned long long& pt,
                                   auto wt_tag) {
                 constexpr bool wt = decltype(wt_tag)::value;
                 using VS = decltype(s);
+                using VT = decltype(t);
                 auto wide = [](VS v) -> unsigned long long { return (unsigned long long)(long long)v; };
+                auto widet = [](VT v) -> unsigned long long { return (unsigned long long)(long long)v; };
                 VS xs = s;
-                unsigned long long xt = t;
+                VT xt = t;
 #pragma unroll
                 for (int d = 1; d < 32; d <<= 1) {
                     const VS os = __shfl_up_sync(0xffffffffu, xs, d);
                     if constexpr (wt) {
-                        const unsigned long long ot = __shfl_up_sync(0xffffffffu, xt, d);
-                        if (lane >= d) xt = ot + xt + (unsigned long long)(d * SPT) * wide(os);
+                        const VT ot = __shfl_up_sync(0xffffffffu, xt, d);
+                        if (lane >= d) xt = ot + xt + (VT)(d * SPT) * (VT)os;
                     }
                     if (lane >= d) xs += os;
                 }
@@ -393,7 +404,7 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                 const VS pws = __shfl_sync(0xffffffffu, es, warp);
                 const unsigned long long pwt = wt ? __shfl_sync(0xffffffffu, et, warp) : 0ULL;
                 VS ls = __shfl_up_sync(0xffffffffu, xs, 1);
-                unsigned long long lt = wt ? __shfl_up_sync(0xffffffffu, xt, 1) : 0ULL;
+                unsigned long long lt = wt ? widet(__shfl_up_sync(0xffffffffu, xt, 1)) : 0ULL;
                 if (lane == 0) { ls = 0; lt = 0; }
                 ps = wide(pws) + wide(ls);
                 pt = pwt + lt + (unsigned long long)(lane * SPT) * wide(pws);
@@ -401,14 +412,8 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
             // dequantize one reconstructed sample (codec.py:135-146): Markstein
             // quotient against a per-block reciprocal, bit-identical to IEEE
             // division (profiles/r1_markstein_division_check.txt)
-            double dq_s = 1.0, dq_r = 1.0;
-            if (Tr::F) {
-                dq_s = decode_scale_code(code) * ldexp(1.0, fbe);
-                dq_r = __ddiv_rn(1.0, dq_s);
-            } else {
-                dq_s = decode_scale_code(code);
-                dq_r = __ddiv_rn(1.0, dq_s);
-            }
+            const double2 dqv = S->dq[kb];
+            const double dq_s = dqv.x, dq_r = dqv.y;
             auto deq = [&](double r) -> T {
                 if (Tr::F) {
                     const double y0 = r * dq_r;
@@ -455,10 +460,11 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                     unsigned long long ps, pt;
                     const unsigned long long t64 = (unsigned long long)(long long)t32;
                     if (sel == 1) {
-                        if (bnarrow) recon_scan(s32, t64, ps, pt, std::false_type{});
+                        if (bnarrow) recon_scan(s32, t32, ps, pt, std::false_type{});
                         else recon_scan((long long)s32, t64, ps, pt, std::false_type{});
                     } else {
-                        if (bnarrow) recon_scan(s32, t64, ps, pt, std::true_type{});
+                        if (ji.w <= 14) recon_scan(s32, t32, ps, pt, std::true_type{});
+                        else if (bnarrow) recon_scan(s32, t64, ps, pt, std::true_type{});
                         else recon_scan((long long)s32, t64, ps, pt, std::true_type{});
                     }
                     if (sel == 1) {
