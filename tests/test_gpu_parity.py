@@ -266,3 +266,28 @@ def test_random_short_tails_vs_oracle(seed):
         if seg:
             y3 = decode_device(res.blob, res.nbytes, res.block_offsets, segment_blocks=seg).cpu().numpy()
             assert np.array_equal(y3, yo), (dt, mode, bs, seg, "d3")
+
+
+@pytest.mark.parametrize("k", [10, 11, 12, 13, 14, 15])
+def test_segment_decoder_width_boundaries(k):
+    """The segment decoder's reconstruct scan switches arithmetic on the
+    block's widest group (<= 14: 32-bit warp-level partial sums; <= 16:
+    32-bit value sums; wider: 64-bit).  A 2^30 sine (D2 residual ~2^10) plus
+    uniform noise of +-2^k gives D2 widths around k + 3, i.e. both sides of
+    each switch: the LOSSLESS round trip is exact, the whole-stream and
+    segmented decodes agree, and the container is the oracle's."""
+    rng = np.random.default_rng(5000 + k)
+    n = 4096 * 24 + 777
+    i = np.arange(n)
+    x = (np.round((2 ** 30) * np.sin(i * 2.0 ** -10)) +
+         rng.integers(-(2 ** k), 2 ** k, n)).astype(np.int32)
+    for seg in (4, None):
+        cfg = StreamConfig(Dtype.I32, 4096, Mode.LOSSLESS, 0.0, segment_blocks=seg)
+        res = encode_device(torch.from_numpy(x).cuda(), cfg)
+        blob = res.to_bytes()
+        assert blob == O.encode(x, Dtype.I32.wire_code, Mode.LOSSLESS.value, 0.0, 4096,
+                                segment_blocks=seg or 0)[0]
+        y = decode_device(res.blob, res.nbytes, res.block_offsets, segment_blocks=seg).cpu().numpy()
+        assert np.array_equal(y, x), (k, seg)
+        y2 = decode_device(res.blob, res.nbytes).cpu().numpy()
+        assert np.array_equal(y2, x), (k, seg)
