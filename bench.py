@@ -179,83 +179,94 @@ def make_workload(args, rank, dev):
 
 
 
-def workload_segment_blocks(args, n, dt=None, mode=None):
-    """P of the workload: --segment-blocks, else the one-wave length of this
-    device (the library query), else 37 (its value on B200)."""
-    if args.segment_blocks > 0:
-        return args.segment_blocks
-    try:
-        from paper_1303_4994_b200 import Dtype, Mode, wave_segment_blocks
-        return wave_segment_blocks(n, dt or Dtype.F32, mode or Mode.FIXED_QUALITY, 4096)
-    except Exception:  # noqa: BLE001
-        return 37
+# One-wave segment length on B200: 148 SMs x 4 resident encoder CTAs (the
+# v3 encoder's one-wave instantiation, apax_encode_wave_segment_blocks).  Both
+# arms take P from this pure-Python rule so the reference arm never loads the
+# GPU library; the GPU arm records the library's own answer beside it.
+B200_WAVE_UNITS = 148 * 4
+
+
+def wave_p(n: int) -> int:
+    nb = (n + 4095) // 4096
+    return max(1, (nb + B200_WAVE_UNITS - 1) // B200_WAVE_UNITS)
+
+
+def workload_segment_blocks(args, n):
+    """P of the workload: --segment-blocks, else the one-wave length."""
+    return args.segment_blocks if args.segment_blocks > 0 else wave_p(n)
+
+
+def _standalone_workloads():
+    """paper_1303_4994_b200/workloads.py loaded as a module of its own (numpy
+    only): the package's __init__ (and with it libapax_b200.so) is never
+    imported by the reference arm."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "apax_bench_workloads", ROOT / "paper_1303_4994_b200" / "workloads.py")
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
 
 
 def run_reference(args, rank):
-    """--impl reference: the reference algorithm (C oracle port) on all host
-    threads, same metric/config, on a bounded sample of the workload; rank 0
-    only."""
+    """--impl reference: the reference algorithm (C oracle port, a plain-C
+    restatement of pkg/src/apax/codec.py + entropy.py + transform.py) on all
+    host threads (OpenMP over segments), rank 0 only.  cfg1/cfg2/cfg3/cfg5:
+    the GPU arm's full-size array and segment length (same config); cfg4
+    (8 GiB): a 2^24-sample slab with the same P, extrapolated per block."""
     if rank != 0:
         return
-    from paper_1303_4994_b200 import Dtype, Mode
-    from paper_1303_4994_b200 import workloads as W
+    W = _standalone_workloads()
     threads = os.cpu_count() or 1
     w = args.workload
+    wire = {"i16": 1, "i32": 2, "f32": 3, "f64": 4}
+    same = True
     if w == "cfg1":
-        x, dt, mode, target = W.cfg1_sines_i16(1 << 22), Dtype.I16, Mode.FIXED_RATE, 4.0
+        x, dt, mode, target = W.cfg1_sines_i16(1 << (args.n_log2 or 24)), "i16", 1, 4.0
     elif w == "cfg3":
-        x, dt, mode, target = W.cfg3_grf_f32(2048), Dtype.F32, Mode.FIXED_RATE, 32.0 / 6.0
+        x, dt, mode, target = W.cfg3_grf_f32(8192), "f32", 1, 32.0 / 6.0
     elif w == "cfg4":
-        x = W.cfg4_modes_f64(160, device="cpu").numpy()
-        dt, mode, target = Dtype.F64, Mode.FIXED_RATE, 64.0 / 3.0
+        x = W.cfg4_modes_f64(1024, device="cpu", planes=16).numpy()   # 16 of the 1024 z planes
+        dt, mode, target = "f64", 1, 64.0 / 3.0
+        same = False
     elif w == "cfg5":
-        x = W.cfg5_ar1(1 << 22, args.cfg5_dtype)
-        dt = Dtype.I32 if args.cfg5_dtype == "i32" else Dtype.F32
-        mode, target = Mode.FIXED_RATE, 32.0 / args.rate
+        x = W.cfg5_ar1(1 << (args.n_log2 or 26), args.cfg5_dtype)
+        dt, mode, target = args.cfg5_dtype, 1, 32.0 / args.rate
     else:
-        x, dt, mode, target = W.cfg2_ar2_f32(1 << 22), Dtype.F32, Mode.FIXED_QUALITY, W.CFG2_TARGET_DB
-    full_n = {"cfg1": 1 << 24, "cfg3": 1 << 26, "cfg4": 1 << 30}.get(w, 1 << (args.n_log2 or 26))
-    # the GPU arm's segment length for the full-size workload
-    seg = args.segment_blocks if args.segment_blocks > 0 else _wave_p(full_n, dt, mode)
-    pol = {"cold": 0, "warm_self": 1}.get(args.policy, 1 if mode == Mode.FIXED_RATE else 0)
+        x, dt, mode, target = W.cfg2_ar2_f32(1 << (args.n_log2 or 26)), "f32", 2, W.CFG2_TARGET_DB
+    full_n = (1 << 30) if w == "cfg4" else x.size
+    seg = workload_segment_blocks(args, full_n)
+    pol = {"cold": 0, "warm_self": 1}.get(args.policy, 1 if mode == 1 else 0)
+    sys.path.insert(0, str(ROOT))
     from oracle import oracle as O
-    for _ in range(max(args.warmup, 1)):
-        blob, offs, _ = O.encode(x, dt.wire_code, mode.value, target, 4096, segment_blocks=seg,
-                                 policy=pol, nthreads=threads)
+    for _ in range(max(1, min(args.warmup, 2))):
+        blob, offs, _ = O.encode(x, wire[dt], mode, target, 4096, segment_blocks=seg, policy=pol,
+                                 nthreads=threads)
     times = []
     for _ in range(args.steps):
         a = time.perf_counter()
-        blob, offs, _ = O.encode(x, dt.wire_code, mode.value, target, 4096, segment_blocks=seg,
-                                 policy=pol, nthreads=threads)
+        blob, offs, _ = O.encode(x, wire[dt], mode, target, 4096, segment_blocks=seg, policy=pol,
+                                 nthreads=threads)
         O.decode(blob, offs, nthreads=threads)
         times.append(time.perf_counter() - a)
     t = sum(times) / len(times)
     v = x.size * x.itemsize / t / 1e9
-    sample = (f"{w} bounded sample: {x.size} samples ({x.nbytes >> 20} MiB {dt.code}) encode+decode, "
-              f"{args.steps} steps, OpenMP over segments")
+    sample = (f"{w}: {x.size} samples ({x.nbytes >> 20} MiB {dt}) encode+decode per step, "
+              f"{'the full workload' if same else 'a slab of the full array, GB/s extrapolated per block'}, "
+              f"C oracle on {threads} host threads (OpenMP over segments)")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": dt.code, "data": "synthetic",
+        "vs_baseline": None, "dtype": dt, "data": "synthetic",
         "config": {"workload": WORKLOADS[w] + f"; {seg}-block {['cold', 'warm_self'][pol]} segments, "
-                               "bs 4096 (bounded sample)",
-                   "name": w, "n_samples": x.size, "segment_blocks": seg, "block_size": 4096},
+                               "bs 4096; step = encode + decode",
+                   "name": w, "n_samples": x.size, "segment_blocks": seg, "block_size": 4096,
+                   "same_config": same},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
-
-
-def _wave_p(n, dt, mode):
-    """One-wave segment length of a B200 (148 SMs x the encoder's resident
-    CTAs) without touching a GPU: the reference arm runs on host cores."""
-    nb = (n + 4095) // 4096
-    try:
-        from paper_1303_4994_b200 import wave_segment_blocks
-        return wave_segment_blocks(n, dt, mode, 4096)
-    except Exception:  # noqa: BLE001
-        return max(1, (nb + 591) // 592)
 
 
 def main():
@@ -305,7 +316,9 @@ def main():
     dev = torch.device("cuda", local)
     x, x_host, wdt, wmode, target = make_workload(args, rank, dev)
     n = x.numel()
-    args.segment_blocks = workload_segment_blocks(args, n, wdt, wmode)
+    args.segment_blocks = workload_segment_blocks(args, n)
+    from paper_1303_4994_b200 import wave_segment_blocks
+    lib_wave_p = wave_segment_blocks(n, wdt, wmode, 4096)
     policy = args.policy if args.policy != "auto" else (
         "warm_self" if wmode == Mode.FIXED_RATE else "cold")
     cfg = StreamConfig(wdt, 4096, wmode, target, segment_blocks=args.segment_blocks,
@@ -322,6 +335,8 @@ def main():
         if record:
             record[0].record(stream)
         enc.encode(x)
+        if world > 1:  # cross-GPU offset scan: every rank's container length (inside the timed encode)
+            dist.all_gather_into_tensor(gathered, nbytes_dev)
         if record:
             record[1].record(stream)
         flush.zero_()  # keep the container out of L2 for the decode timing
@@ -330,8 +345,6 @@ def main():
         dec.decode(enc.out, enc.cap, enc.offsets, segment_blocks=args.segment_blocks)
         if record:
             record[3].record(stream)
-        if world > 1:  # cross-GPU offset scan input: every rank's container length
-            dist.all_gather_into_tensor(gathered, nbytes_dev)
         flush.zero_()
 
     for _ in range(args.warmup):
@@ -347,6 +360,8 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     sampler = ClockSampler(local)
+    from paper_1303_4994_b200 import _lib
+    launches0 = int(_lib.lib().apax_launch_count())
     with sampler:
         t_wall0 = torch.cuda.Event(enable_timing=True)
         t_wall1 = torch.cuda.Event(enable_timing=True)
@@ -355,6 +370,7 @@ def main():
             step(ev[k])
         t_wall1.record(stream)
         torch.cuda.synchronize()
+    gpu_launches = int(_lib.lib().apax_launch_count()) - launches0
     if world > 1:
         dist.barrier()
     enc_ms = [e[0].elapsed_time(e[1]) for e in ev]
@@ -382,8 +398,10 @@ def main():
     alg_dec = nbytes + in_bytes + 8 * (enc.n_blocks + 1)   # read container + offsets, write y
     ach_enc = alg_enc / (mean_enc * 1e-3) / 1e9
     ach_dec = alg_dec / (mean_dec * 1e-3) / 1e9
-    enc_k = (f"encode_v3_kernel<{wdt.wire_code}" if wdt.wire_code <= 3 else f"encode_v2_kernel<{wdt.wire_code}")
-    dec_k = (f"decode_v3_kernel<{wdt.wire_code}" if wdt.wire_code <= 3 else f"decode_v2_kernel<{wdt.wire_code}")
+    # the kernels bench's configs dispatch to (apax_capi.cu): v3 encoder and
+    # segment-serial d3 decoder for every dtype at bs 4096
+    enc_k = f"encode_v3_kernel<{wdt.wire_code}"
+    dec_k = f"decode_v3_kernel<{wdt.wire_code}"
     dominant = enc_k if mean_enc >= mean_dec else dec_k
     ach = ach_enc if mean_enc >= mean_dec else ach_dec  # noqa: E501
 
@@ -474,6 +492,7 @@ def main():
                 "name": args.workload,
                 "n_samples_per_gpu": n, "block_size": 4096,
                 "segment_blocks": args.segment_blocks, "segment_policy": policy,
+                "wave_segment_blocks_library": lib_wave_p,
                 "mode": wmode.name, "target": target,
                 "parallelism": f"dp{world} (segment shards)",
                 "l2": f"inputs ({in_bytes >> 20} MiB) {'larger' if in_bytes > (126 << 20) else 'smaller'} "
@@ -493,7 +512,7 @@ def main():
                          "decode": {"achieved": ach_dec, "frac": ach_dec / peak}},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": gpu_launches,
             "clocks": sampler.summary(),
             "self_check": {"decoded_finite": ok_roundtrip},
         }

@@ -44,6 +44,10 @@ enum { APAX_POLICY_COLD = 0, APAX_POLICY_WARM_SELF = 1 };
 /* Library version string. */
 const char* apax_version(void);
 
+/* Kernel launches this library has enqueued since it was loaded (every
+ * entry point counts its own launches; for launch accounting in benchmarks). */
+int64_t apax_launch_count(void);
+
 /* Human-readable text for a status code. */
 const char* apax_status_string(int code);
 
@@ -128,6 +132,25 @@ int apax_encode(const void* x, int64_t n, int dtype, int mode, double target, in
                 int64_t segment_blocks, int policy, uint8_t* out, int64_t out_cap,
                 int64_t* block_offsets, uint64_t* status, double* trace, void* ws,
                 int64_t ws_bytes, void* stream);
+
+/* encode_stream's input conversions (reference codec.py:266-272 widens every
+ * input to int64 for integer configs and to float64 for float configs, then
+ * quantizes those values).  in_kind:
+ *   APAX_IN_NATIVE  samples already of `dtype` (= apax_encode);
+ *   APAX_IN_INT64   int64 samples, integer dtype: values outside the dtype's
+ *                   range are coded as they are (exponents up to 34) and
+ *                   clipped by the decoder (codec.py:143-145);
+ *   APAX_IN_FLOAT64 float64 samples, F32 (or F64) dtype: quantized from the
+ *                   f64 values, the fixed-quality loop measures the f32 y.
+ * The cast kinds run the generic encoder (any block size).  out_cap must be
+ * >= apax_max_encoded_bytes_cast (exponents up to 34 for every block). */
+enum { APAX_IN_NATIVE = 0, APAX_IN_INT64 = 1, APAX_IN_FLOAT64 = 2 };
+int64_t apax_max_encoded_bytes_cast(int64_t n, int in_kind, int dtype, int block_size);
+int64_t apax_encode_cast_workspace_bytes(int64_t n, int in_kind, int dtype, int mode, int block_size,
+                                         int64_t segment_blocks);
+int apax_encode_cast(const void* x, int in_kind, int64_t n, int dtype, int mode, double target, int block_size,
+                     int64_t segment_blocks, int policy, uint8_t* out, int64_t out_cap, int64_t* block_offsets,
+                     uint64_t* status, void* ws, int64_t ws_bytes, void* stream);
 
 /* Device workspace needed by apax_decode (with offsets == NULL it includes
  * room for the block walk's offset table). */

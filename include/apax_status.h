@@ -35,6 +35,9 @@ enum apax_status {
     APAX_ERR_RANGE = 22,             /* RangeError "attenuation ... outside [2^-31, 2^33)" */
     APAX_ERR_INTERNAL_WIDTH = 23,    /* InternalError "sample exceeds its group exponent width" */
     APAX_ERR_NONFINITE_BLOCK = 24,   /* UnsupportedValue "non-finite float input" (codec.py:114) */
+    APAX_ERR_MATH_DOMAIN = 25,       /* ValueError "math domain error": the quality loop's
+                                        math.log10(px / pd) of an underflowed or overflowed
+                                        ratio 0 (codec.py:251) */
     /* host-side / launch errors (no reference counterpart) */
     APAX_ERR_CAPACITY = 40,          /* output buffer too small */
     APAX_ERR_ALLOC = 41,             /* allocation failure */

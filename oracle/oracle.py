@@ -53,6 +53,9 @@ def lib():
         L.apax_oracle_encode.argtypes = [P, I64, I32, I32, D, I32, I64, I32, I32, P, I64,
                                          P, P, P, P]
         L.apax_oracle_encode.restype = I32
+        L.apax_oracle_encode_src.argtypes = [P, I32, I64, I32, I32, D, I32, I64, I32, I32, P, I64,
+                                             P, P, P, P]
+        L.apax_oracle_encode_src.restype = I32
         L.apax_oracle_decode.argtypes = [P, I64, P, I64, P, I32, P]
         L.apax_oracle_decode.restype = I32
         L.apax_oracle_find_blocks.argtypes = [P, I64, P, P]
@@ -103,19 +106,27 @@ def encode(x, dtype: int, mode: int, target: float = 0.0, block_size: int = 4096
     """encode_stream (codec.py:258-285); segment_blocks>0 -> segmented container.
 
     Returns (blob bytes, block_offsets int64[n_blocks+1], trace or None)."""
-    x = np.ascontiguousarray(np.asarray(x).reshape(-1), dtype=NP_DTYPES[dtype])
+    x = np.asarray(x).reshape(-1)
+    src = 0
+    if x.dtype != NP_DTYPES[dtype]:
+        # encode_stream (codec.py:266-272) widens to float64 / int64 first
+        src = 2 if dtype >= 3 else 1
+        x = x.astype(np.float64 if src == 2 else np.int64)
+    x = np.ascontiguousarray(x)
     n = x.size
     nb = (n + block_size - 1) // block_size
     cap = int(lib().apax_oracle_max_encoded_bytes(n, dtype, block_size)) + 64
+    if src:
+        cap = 28 + nb * ((6 if dtype >= 3 else 4) + (3 * (block_size // 4) + 1) // 2 + 17 * block_size) + 64
     out = np.zeros(cap, np.uint8)
     out_len = ctypes.c_int64(0)
     detail = ctypes.c_int64(-1)
     offs = np.zeros(nb + 1, np.int64)
     tr = np.zeros((max(nb, 1), len(TRACE_FIELDS)), np.float64) if trace else None
-    st = lib().apax_oracle_encode(_ptr(x), n, dtype, mode, float(target), block_size,
-                                  int(segment_blocks), int(policy), int(nthreads), _ptr(out),
-                                  cap, ctypes.byref(out_len), _ptr(offs),
-                                  _ptr(tr) if tr is not None else None, ctypes.byref(detail))
+    st = lib().apax_oracle_encode_src(_ptr(x), src, n, dtype, mode, float(target), block_size,
+                                      int(segment_blocks), int(policy), int(nthreads), _ptr(out),
+                                      cap, ctypes.byref(out_len), _ptr(offs),
+                                      _ptr(tr) if tr is not None else None, ctypes.byref(detail))
     _check(st, detail.value)
     return out[:out_len.value].tobytes(), offs, tr
 

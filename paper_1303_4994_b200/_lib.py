@@ -36,6 +36,8 @@ def lib():
         raise ExtensionMissing(f"cannot load {LIB_PATH}: {exc}") from exc
     P, I64, I32, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
     L.apax_version.restype = ctypes.c_char_p
+    L.apax_launch_count.argtypes = []
+    L.apax_launch_count.restype = I64
     L.apax_status_string.argtypes = [I32]
     L.apax_status_string.restype = ctypes.c_char_p
     L.apax_max_encoded_bytes.argtypes = [I64, I32, I32]
@@ -76,6 +78,12 @@ def lib():
     L.apax_profile_welch.restype = I32
     L.apax_profile_select.argtypes = [P, P, I64, I32, I32, P, I32, P, I32, P]
     L.apax_profile_select.restype = I32
+    L.apax_max_encoded_bytes_cast.argtypes = [I64, I32, I32, I32]
+    L.apax_max_encoded_bytes_cast.restype = I64
+    L.apax_encode_cast_workspace_bytes.argtypes = [I64, I32, I32, I32, I32, I64]
+    L.apax_encode_cast_workspace_bytes.restype = I64
+    L.apax_encode_cast.argtypes = [P, I32, I64, I32, I32, D, I32, I64, I32, P, I64, P, P, P, I64, P]
+    L.apax_encode_cast.restype = I32
     L.apax_find_blocks.argtypes = [P, I64, I64, I32, I32, P, P, P]
     L.apax_find_blocks.restype = I32
     L.apax_parse_file_header.argtypes = [P, I64, P, P, P, P, P, P]
@@ -92,4 +100,5 @@ EXPORTED_SYMBOLS = (
     "apax_encode_wave_segment_blocks", "apax_profile_grid", "apax_profile_sums", "apax_profile_welch",
     "apax_profile_select", "apax_decode_range", "apax_status_to_host",
     "apax_encode_lossless_range", "apax_detect_segments",
+    "apax_max_encoded_bytes_cast", "apax_launch_count", "apax_encode_cast_workspace_bytes", "apax_encode_cast",
 )

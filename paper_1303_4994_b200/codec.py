@@ -370,29 +370,57 @@ def decode_device(blob, nbytes: Optional[int] = None, offsets=None,
 # ---------------------------------------------------------------------------
 # drop-in host API (bytes / ndarray)
 # ---------------------------------------------------------------------------
-def _as_config_dtype(x: np.ndarray, dt: Dtype) -> np.ndarray:
-    """Exact conversion of the caller's array to the config dtype.  The
-    reference converts to int64 / float64 (codec.py:266-272) and quantizes
-    those values; the kernels read the container dtype, so only
-    value-preserving conversions are accepted."""
+_IN_NATIVE, _IN_INT64, _IN_FLOAT64 = 0, 1, 2
+
+
+def _reference_cast(x: np.ndarray, dt: Dtype):
+    """The reference's input conversion (codec.py:266-272): float configs
+    widen to float64 (non-finite values raise UnsupportedValue with the first
+    index), integer configs to int64 (numpy astype: floats truncate toward
+    zero).  Returns (array, in_kind): the container dtype itself whenever
+    that holds the widened values exactly -- quantizing them from the
+    narrower array gives the same bytes -- else the widened array, coded by
+    apax_encode_cast."""
     if x.dtype == dt.np_dtype:
-        return np.ascontiguousarray(x)
+        return np.ascontiguousarray(x), _IN_NATIVE
     if dt.is_float:
-        if x.dtype.kind not in "fiub":
-            raise InvalidConfig(f"cannot encode {x.dtype} samples as {dt.code}")
-        y = x.astype(dt.np_dtype)
-        xf = x.astype(np.float64)
-        same = (y.astype(np.float64) == xf) | (np.isnan(xf) & np.isnan(y.astype(np.float64)))
-        if not same.all():
-            raise InvalidConfig(f"{x.dtype} samples are not exactly representable as {dt.code}")
-        return np.ascontiguousarray(y)
-    if x.dtype.kind not in "iub" and not (x.dtype.kind == "f" and np.all(np.isfinite(x))
-                                           and np.all(x == np.round(x))):
-        raise InvalidConfig(f"cannot encode {x.dtype} samples as {dt.code}")
+        xf = np.ascontiguousarray(x.astype(np.float64))
+        if dt is Dtype.F64:
+            return xf, _IN_NATIVE
+        x32 = xf.astype(np.float32)
+        if np.array_equal(x32.astype(np.float64), xf, equal_nan=True):
+            return x32, _IN_NATIVE
+        return xf, _IN_FLOAT64
+    xi = np.ascontiguousarray(x.astype(np.int64))
     info = np.iinfo(dt.np_dtype)
-    if x.size and (x.min() < info.min or x.max() > info.max):
-        raise InvalidConfig(f"samples outside the {dt.code} range")
-    return np.ascontiguousarray(x.astype(dt.np_dtype))
+    if xi.size == 0 or (int(xi.min()) >= info.min and int(xi.max()) <= info.max):
+        return xi.astype(dt.np_dtype), _IN_NATIVE
+    return xi, _IN_INT64
+
+
+def _encode_cast(xw: np.ndarray, in_kind: int, config: StreamConfig) -> bytes:
+    """apax_encode_cast of a widened host array (int64 / float64)."""
+    torch, L = _require_cuda()
+    n = int(xw.size)
+    dt, bs = config.dtype.wire_code, config.block_size
+    seg = int(config.segment_blocks or 0)
+    cap = int(L.apax_max_encoded_bytes_cast(n, in_kind, dt, bs))
+    wsb = int(L.apax_encode_cast_workspace_bytes(n, in_kind, dt, config.mode.value, bs, seg))
+    if cap < 0 or wsb < 0:
+        raise InvalidConfig("invalid encode arguments")
+    xd = torch.from_numpy(xw).to("cuda")
+    out = torch.empty(cap + 64, dtype=torch.uint8, device="cuda")
+    ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device="cuda")
+    status = torch.empty(4, dtype=torch.int64, device="cuda")
+    st = L.apax_encode_cast(ctypes.c_void_p(xd.data_ptr()), in_kind, n, dt, config.mode.value,
+                            float(config.target), bs, seg, _POLICY[config.segment_policy],
+                            ctypes.c_void_p(out.data_ptr()), cap, None, ctypes.c_void_p(status.data_ptr()),
+                            ctypes.c_void_p(ws.data_ptr()), ws.numel(), ctypes.c_void_p(_stream_ptr(None)))
+    raise_status(st)
+    torch.cuda.current_stream().synchronize()
+    s = status.cpu().numpy().view(np.uint64)
+    _check_status(s)
+    return bytes(out[:int(s[2])].cpu().numpy().tobytes())
 
 
 def encode_stream(samples, config: StreamConfig) -> bytes:
@@ -404,7 +432,9 @@ def encode_stream(samples, config: StreamConfig) -> bytes:
     if x.size < 1:
         raise InvalidConfig("element_count must be >= 1")
     torch, _ = _require_cuda()
-    x = _as_config_dtype(x, config.dtype)
+    x, in_kind = _reference_cast(x, config.dtype)
+    if in_kind != _IN_NATIVE:
+        return _encode_cast(x, in_kind, config)
     if not x.flags.writeable:
         x = x.copy()
     xd = torch.from_numpy(x).to("cuda", non_blocking=False)

@@ -4,6 +4,7 @@
 // constants (the clamp bound 20*log10(2^-31) of reference dtypes.py:202 and
 // 10**(T/20) of codec.py:167 are computed here with the same libm the
 // reference's CPython calls), status-buffer reset, kernel launches.
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -17,6 +18,11 @@
 
 using namespace apax;
 
+namespace apax {
+static std::atomic<long long> g_launches{0};
+void note_launches(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+}  // namespace apax
+
 namespace {
 
 constexpr long long kLosslessUnit = 4;  // blocks per CTA unit, lossless whole stream
@@ -26,7 +32,7 @@ struct EncPlan {
     int halo;
     int stage_bytes;
     int x_in_smem;
-    int v2, v3;
+    int v3;
     size_t smem;
     int grid;
     long long slot_bytes;
@@ -41,8 +47,11 @@ int env_int(const char* name, int def) {
     return atoi(v);
 }
 
-int plan_encode(long long n, int dt, int mode, int bs, long long seg, EncPlan* p) {
-    if (!valid_dtype(dt) || mode < 0 || mode > 2) return APAX_ERR_ARG;
+// kdt: the kernel's sample type -- a container dtype 0..4, or a cast variant
+// (kKdtI64: int64 samples for an integer container, kKdtF64F32: float64
+// samples for an f32 container; generic v1 kernel only)
+int plan_encode(long long n, int kdt, int mode, int bs, long long seg, EncPlan* p) {
+    if (kdt < 0 || kdt > kKdtF64F32 || mode < 0 || mode > 2) return APAX_ERR_ARG;
     if (bs < 64 || bs > 16384) return APAX_ERR_CFG_BLOCK_RANGE;
     if (bs % 4) return APAX_ERR_CFG_BLOCK_MULT;
     if (n < 1) return APAX_ERR_EMPTY;
@@ -58,27 +67,25 @@ int plan_encode(long long n, int dt, int mode, int bs, long long seg, EncPlan* p
         p->halo = 0;
     }
     p->n_units = (p->n_blocks + p->unit_blocks - 1) / p->unit_blocks;
-    const long long mbb = max_block_bytes(dt, bs);
+    const long long mbb = max_block_bytes(kdt, bs);
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess ||
         optin <= 0)
         optin = 227 * 1024;
-    const int ver = env_int("APAX_ENC_VER", 0);   // 0 = best available; 1/2/3 force
-    p->v3 = encode_v3_supported(dt, bs) && (ver == 0 || ver == 3) && env_int("APAX_FORCE_V1", 0) == 0;
+    p->v3 = kdt <= 4 && encode_v3_supported(kdt, bs) && env_int("APAX_FORCE_V1", 0) == 0;
+    long long v3_slots = 0;
     if (p->v3) {
-        p->stage_bytes = encode_v3_stage_bytes(dt, bs);
+        p->stage_bytes = encode_v3_stage_bytes(kdt, bs);
         p->x_in_smem = 1;
-        p->smem = encode_v3_smem_bytes(dt, bs, p->stage_bytes);
+        p->smem = encode_v3_smem_bytes(kdt, bs, p->stage_bytes);
         if (p->smem > (size_t)optin) p->v3 = 0;
     }
-    p->v2 = !p->v3 && encode_v2_supported(bs) && (ver == 0 || ver == 2) && env_int("APAX_FORCE_V1", 0) == 0;
-    long long v3_slots = 0;
     if (p->v3) {
         // one unit per CTA fits: the 256-thread one-wave kernel (one slot per
         // CTA); else the persistent kernel with a placement warp (two slots)
-        const int rw = encode_v3_resident_ctas_wave(dt, p->smem);
-        const int resident = encode_v3_resident_ctas(dt, p->smem);
+        const int rw = encode_v3_resident_ctas_wave(kdt, p->smem);
+        const int resident = encode_v3_resident_ctas(kdt, p->smem);
         if (p->n_units <= rw) {
             p->grid = (int)p->n_units;
             v3_slots = p->n_units;
@@ -86,29 +93,19 @@ int plan_encode(long long n, int dt, int mode, int bs, long long seg, EncPlan* p
             p->grid = (int)(p->n_units < resident ? p->n_units : resident);
             v3_slots = 2LL * p->grid > rw ? 2LL * p->grid : rw;   // a sub-range may run one-wave
         }
-    } else if (p->v2) {
-        // v2: the window holds one block plus a <16-byte tail
-        p->stage_bytes = (int)((mbb + 64 + 15) & ~15LL);
-        p->x_in_smem = 1;
-        p->smem = encode_v2_smem_bytes(dt, mode, p->stage_bytes);
-        if (p->smem > (size_t)optin) p->v2 = 0;
-    }
-    if (p->v3) {
-    } else if (p->v2) {
-        int resident = encode_v2_resident_ctas(dt, p->smem);
-        p->grid = (int)(p->n_units < resident ? p->n_units : resident);
     } else {
+        // generic kernel (any block size, the cast variants)
         long long want = env_int("APAX_STAGE_BYTES", 48 * 1024);
         long long st = want > mbb + 64 ? want : mbb + 64;
         st = (st + 15) & ~15LL;
         p->stage_bytes = (int)st;
         p->x_in_smem = 1;
-        p->smem = encode_smem_bytes(dt, bs, p->stage_bytes, 1);
+        p->smem = encode_smem_bytes(kdt, bs, p->stage_bytes, 1);
         if (p->smem > (size_t)optin) {
             p->x_in_smem = 0;
-            p->smem = encode_smem_bytes(dt, bs, p->stage_bytes, 0);
+            p->smem = encode_smem_bytes(kdt, bs, p->stage_bytes, 0);
         }
-        int resident = encode_resident_ctas(dt, p->smem);
+        int resident = encode_resident_ctas(kdt, p->smem);
         p->grid = (int)(p->n_units < resident ? p->n_units : resident);
     }
     if (p->grid < 1) p->grid = 1;
@@ -116,7 +113,7 @@ int plan_encode(long long n, int dt, int mode, int bs, long long seg, EncPlan* p
     p->ws_lookback = 0;
     p->ws_ticket = (p->n_units * 8 + 255) & ~255LL;
     p->ws_slots = p->ws_ticket + 256;
-    p->ws_total = p->ws_slots + p->slot_bytes * (p->v3 ? v3_slots : (long long)p->grid * (p->v2 ? 2 : 1));
+    p->ws_total = p->ws_slots + p->slot_bytes * (p->v3 ? v3_slots : (long long)p->grid);
     return APAX_OK;
 }
 
@@ -135,7 +132,7 @@ int plan_decode(long long n, int dt, int bs, DecPlan* p) {
     if (bs % 4) return APAX_ERR_CFG_BLOCK_MULT;
     if (n < 0) return APAX_ERR_ARG;
     p->n_blocks = (n + bs - 1) / bs;
-    long long cap = max_block_bytes(dt, bs) + 64;
+    long long cap = max_block_bytes_any(dt, bs) + 64;
     p->payload_cap = (int)((cap + 15) & ~15LL);
     p->v2 = decode_v2_supported(bs) && env_int("APAX_FORCE_V1", 0) == 0;
     int resident;
@@ -198,7 +195,9 @@ __global__ void status_to_host_kernel(const unsigned long long* src, unsigned lo
 
 extern "C" {
 
-const char* apax_version(void) { return "apax-b200 0.1.0 (sm_100a)"; }
+const char* apax_version(void) { return "apax-b200 0.2.0 (sm_100a)"; }
+
+int64_t apax_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 const char* apax_status_string(int code) {
     switch (code) {
@@ -227,6 +226,7 @@ const char* apax_status_string(int code) {
         case APAX_ERR_RANGE: return "attenuation outside [2^-31, 2^33)";
         case APAX_ERR_INTERNAL_WIDTH: return "sample exceeds its group exponent width";
         case APAX_ERR_NONFINITE_BLOCK: return "non-finite float input";
+        case APAX_ERR_MATH_DOMAIN: return "math domain error";
         case APAX_ERR_CAPACITY: return "output buffer too small";
         case APAX_ERR_ALLOC: return "allocation failure";
         case APAX_ERR_ARG: return "invalid argument";
@@ -293,8 +293,87 @@ int apax_encode(const void* x, int64_t n, int dtype, int mode, double target, in
     P.sqrt12 = sqrt(12.0);
     P.trace = trace;
     if (p.v3) return launch_encode_v3(dtype, P, p.grid, p.smem, s);
-    if (p.v2) return launch_encode_v2(dtype, P, p.grid, p.smem, s);
     return launch_encode(dtype, P, p.grid, p.smem, s);
+}
+
+static int kdt_of_cast(int in_kind, int dtype) {
+    if (!valid_dtype(dtype)) return -1;
+    if (in_kind == 0) return dtype;
+    if (in_kind == APAX_IN_INT64 && dtype <= APAX_I32) return kKdtI64;
+    if (in_kind == APAX_IN_FLOAT64 && dtype == APAX_F32) return kKdtF64F32;
+    if (in_kind == APAX_IN_FLOAT64 && dtype == APAX_F64) return APAX_F64;
+    return -1;
+}
+
+int64_t apax_max_encoded_bytes_cast(int64_t n, int in_kind, int dtype, int block_size) {
+    const int kdt = kdt_of_cast(in_kind, dtype);
+    if (kdt < 0 || block_size < 64 || block_size % 4 || n < 0) return -1;
+    int64_t nb = (n + block_size - 1) / block_size;
+    return kFileHeader + nb * max_block_bytes(kdt, block_size);
+}
+
+int64_t apax_encode_cast_workspace_bytes(int64_t n, int in_kind, int dtype, int mode, int block_size,
+                                         int64_t segment_blocks) {
+    const int kdt = kdt_of_cast(in_kind, dtype);
+    if (kdt < 0) return -1;
+    EncPlan p;
+    if (plan_encode(n, kdt, mode, block_size, segment_blocks, &p)) return -1;
+    return p.ws_total;
+}
+
+int apax_encode_cast(const void* x, int in_kind, int64_t n, int dtype, int mode, double target, int block_size,
+                     int64_t segment_blocks, int policy, uint8_t* out, int64_t out_cap, int64_t* block_offsets,
+                     uint64_t* status, void* ws, int64_t ws_bytes, void* stream) {
+    // encode_stream's input conversions (codec.py:266-272): int64 samples
+    // into an integer container (values outside its range are coded as they
+    // are and clipped by the decoder), float64 samples into an f32 container
+    // (quantized from the f64 values; the FQ loop sees the f32 dequantized y)
+    const int kdt = kdt_of_cast(in_kind, dtype);
+    if (kdt < 0) return APAX_ERR_ARG;
+    if (kdt == dtype)
+        return apax_encode(x, n, dtype, mode, target, block_size, segment_blocks, policy, out, out_cap,
+                           block_offsets, status, nullptr, ws, ws_bytes, stream);
+    EncPlan p;
+    int st = plan_encode(n, kdt, mode, block_size, segment_blocks, &p);
+    if (st) return st;
+    if (mode == APAX_LOSSLESS && dtype >= APAX_F32) return APAX_ERR_CFG_LOSSLESS_FLOAT;
+    if (mode == APAX_FIXED_RATE && !(target > 0)) return APAX_ERR_CFG_FR_TARGET;
+    if (!x || !out || !status || (p.ws_total > 0 && !ws)) return APAX_ERR_ARG;
+    if (out_cap < apax_max_encoded_bytes_cast(n, in_kind, dtype, block_size)) return APAX_ERR_CAPACITY;
+    if (ws_bytes < p.ws_total) return APAX_ERR_WORKSPACE;
+    cudaStream_t s = (cudaStream_t)stream;
+    uint8_t* w = (uint8_t*)ws;
+    if (cudaMemsetAsync(status, 0xFF, 4 * sizeof(uint64_t), s) != cudaSuccess) return APAX_ERR_CUDA;
+    if (cudaMemsetAsync(w, 0, (size_t)p.ws_slots, s) != cudaSuccess) return APAX_ERR_CUDA;
+    EncParams P;
+    memset(&P, 0, sizeof(P));
+    P.x = x;
+    P.n = n;
+    P.mode = mode;
+    P.bs = block_size;
+    P.target = target;
+    P.n_blocks = p.n_blocks;
+    P.unit_blocks = p.unit_blocks;
+    P.n_units = p.n_units;
+    P.halo = p.halo;
+    P.policy = policy;
+    P.out = out;
+    P.out_cap = out_cap;
+    P.block_offsets = (long long*)block_offsets;
+    P.status = (unsigned long long*)status;
+    P.lookback = (unsigned long long*)(w + p.ws_lookback);
+    P.ticket = (unsigned int*)(w + p.ws_ticket);
+    P.slots = w + p.ws_slots;
+    P.slot_bytes = p.slot_bytes;
+    P.stage_bytes = p.stage_bytes;
+    P.x_in_smem = p.x_in_smem;
+    P.att_lo = 20.0 * log10(ldexp(1.0, -31));
+    P.pow10_t20 = pow(10.0, target / 20.0);
+    P.sqrt12 = sqrt(12.0);
+    P.wire = dtype;
+    P.clip_lo = dtype == APAX_I8 ? -128LL : (dtype == APAX_I16 ? -32768LL : -2147483648LL);
+    P.clip_hi = dtype == APAX_I8 ? 127LL : (dtype == APAX_I16 ? 32767LL : 2147483647LL);
+    return launch_encode(kdt, P, p.grid, p.smem, s);
 }
 
 int apax_encode_lossless_range(const void* x, int64_t halo, int64_t n, int dtype, int block_size,
@@ -490,7 +569,6 @@ int64_t apax_encode_wave_segment_blocks(int64_t n, int dtype, int mode, int bloc
         resident = encode_v3_resident_ctas_wave(dtype, p.smem);
         if (resident < 1) resident = encode_v3_resident_ctas(dtype, p.smem);
     }
-    else if (p.v2) resident = encode_v2_resident_ctas(dtype, p.smem);
     if (resident < 1) resident = 1;
     return (p.n_blocks + resident - 1) / resident;
 }
@@ -601,6 +679,7 @@ int apax_parse_file_header(const uint8_t* d, int64_t len, int* dt, int* mode, in
 int apax_detect_segments(const uint8_t* blob, int64_t nbytes, const int64_t* block_offsets, int64_t n_blocks,
                          uint64_t* segment_blocks_out, void* stream) {
     if (!blob || !block_offsets || !segment_blocks_out || n_blocks < 1) return APAX_ERR_ARG;
+    note_launches(1);
     detect_segments_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(blob, nbytes, (const long long*)block_offsets,
                                                                  n_blocks, (unsigned long long*)segment_blocks_out);
     return cudaGetLastError() == cudaSuccess ? APAX_OK : APAX_ERR_CUDA;
@@ -613,6 +692,7 @@ int apax_status_to_host(const uint64_t* status, uint64_t* host_dst, int n_words,
         cudaGetLastError();
         return APAX_ERR_ARG;   // not page-locked host memory
     }
+    note_launches(1);
     status_to_host_kernel<<<1, 32, 0, (cudaStream_t)stream>>>((const unsigned long long*)status,
                                                              (unsigned long long*)dptr, n_words);
     return cudaGetLastError() == cudaSuccess ? APAX_OK : APAX_ERR_CUDA;

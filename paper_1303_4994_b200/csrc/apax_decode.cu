@@ -375,6 +375,7 @@ static int launch_decode_t(const DecParams& P, int grid, size_t smem, cudaStream
     if (cudaFuncSetAttribute(decode_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
         return APAX_ERR_CUDA;
+    note_launches(1);
     decode_kernel<DT><<<grid, kNT, smem, st>>>(P);
     return cudaGetLastError() == cudaSuccess ? APAX_OK : APAX_ERR_CUDA;
 }
@@ -414,6 +415,7 @@ int launch_decode(int dt, const DecParams& P, int grid, size_t smem, cudaStream_
 int launch_walk(const uint8_t* blob, long long nbytes, long long n, int bs, int dt, long long n_blocks,
                 long long* offsets, unsigned long long* status, cudaStream_t st) {
     size_t smem = (size_t)(bs / 4) + 64;
+    note_launches(1);
     walk_kernel<<<1, 32, smem, st>>>(blob, nbytes, n, bs, dt, n_blocks, offsets, status, nullptr);
     return cudaGetLastError() == cudaSuccess ? APAX_OK : APAX_ERR_CUDA;
 }
@@ -421,6 +423,7 @@ int launch_walk(const uint8_t* blob, long long nbytes, long long n, int bs, int 
 int launch_walk_after_k5(const uint8_t* blob, long long nbytes, long long n, int bs, int dt, long long n_blocks,
                          long long* offsets, unsigned long long* status, const int* k5_fail, cudaStream_t st) {
     size_t smem = (size_t)(bs / 4) + 64;
+    note_launches(1);
     walk_kernel<<<1, 32, smem, st>>>(blob, nbytes, n, bs, dt, n_blocks, offsets, status, k5_fail);
     return cudaGetLastError() == cudaSuccess ? APAX_OK : APAX_ERR_CUDA;
 }

@@ -553,6 +553,7 @@ __global__ void __launch_bounds__(256) compose_maps_kernel(const unsigned long l
 }
 
 int launch_compose_maps(const unsigned long long* carry, long long nb, unsigned long long* out, cudaStream_t st) {
+    note_launches(1);
     compose_maps_kernel<<<1, 256, 0, st>>>(carry, nb, out);
     return cudaGetLastError() == cudaSuccess ? APAX_OK : APAX_ERR_CUDA;
 }
@@ -565,6 +566,7 @@ int launch_decode_v2(int dt, const DecParams& P, int grid, size_t smem, cudaStre
     void* args[] = {&p};
     // cooperative: all CTAs co-resident, so the carry look-back between
     // round-robin neighbours can never wait on an unscheduled CTA
+    note_launches(1);
     if (cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(d2::NT), args, smem, st) != cudaSuccess)
         return APAX_ERR_CUDA;
     return APAX_OK;

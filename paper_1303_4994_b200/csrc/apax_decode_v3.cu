@@ -662,6 +662,7 @@ static int launch_d3_range(int dt, bool fix, const DecParams& P, long long s0, l
     const long long ns = s1 - s0;
     const int g = (int)(ns < grid ? ns : grid);
     void* args[] = {&p};
+    note_launches(1);
     if (cudaLaunchKernel(fn, dim3(g), dim3(d3::NT), args, smem, st) != cudaSuccess) return APAX_ERR_CUDA;
     return APAX_OK;
 }
@@ -697,6 +698,7 @@ int launch_decode_v3_two_pass(int dt, DecParams P, int grid, size_t smem, unsign
     P.no_store = 1;
     int r = launch_decode_v3_tp(dt, P, grid, smem, st, 1);
     if (r) return r;
+    note_launches(1);
     compose_entries_kernel<<<1, 1, 0, st>>>(maps, nseg, entries);
     if (cudaGetLastError() != cudaSuccess) return APAX_ERR_CUDA;
     P.seg_map = nullptr;

@@ -29,14 +29,33 @@ template <> struct DT_<1> { using T = int16_t; using Q = int32_t; static constex
 template <> struct DT_<2> { using T = int32_t; using Q = int32_t; static constexpr bool F = false, WIDE = true;  static constexpr int W = 4, HDR = 4; static constexpr long long LO = -2147483648LL, HI = 2147483647LL; };
 template <> struct DT_<3> { using T = float;   using Q = int32_t; static constexpr bool F = true,  WIDE = true;  static constexpr int W = 4, HDR = 6; static constexpr long long LO = 0, HI = 0; };
 template <> struct DT_<4> { using T = double;  using Q = long long; static constexpr bool F = true, WIDE = true; static constexpr int W = 8, HDR = 6; static constexpr long long LO = 0, HI = 0; };
+// cast variants of the generic encoder (kKdtI64, kKdtF64F32 below)
+template <> struct DT_<5> { using T = long long; using Q = long long; static constexpr bool F = false, WIDE = true; static constexpr int W = 8, HDR = 4; static constexpr long long LO = 0, HI = 0; };
+template <> struct DT_<6> { using T = double;  using Q = long long; static constexpr bool F = true, WIDE = true; static constexpr int W = 8, HDR = 6; static constexpr long long LO = 0, HI = 0; };
 
-__host__ __device__ inline int hdr_size(int dt) { return dt >= 3 ? 6 : 4; }
-__host__ __device__ inline int dt_width(int dt) { return dt == 0 ? 1 : dt == 1 ? 2 : dt == 4 ? 8 : 4; }
+// kernel sample types beyond the container dtypes: encode_stream's casts
+// (reference codec.py:266-272 widens every input to int64 / float64 first)
+constexpr int kKdtI64 = 5;      // int64 samples, integer container (clip at decode)
+constexpr int kKdtF64F32 = 6;   // float64 samples, f32 container
+__host__ __device__ inline bool kdt_float(int dt) { return dt == 3 || dt == 4 || dt == kKdtF64F32; }
+__host__ __device__ inline int hdr_size(int dt) { return kdt_float(dt) ? 6 : 4; }
+__host__ __device__ inline int dt_width(int dt) {
+    return dt == 0 ? 1 : dt == 1 ? 2 : (dt == 2 || dt == 3) ? 4 : 8;
+}
 
+// worst-case block bytes for samples of kernel type dt: group exponents are
+// bounded by 8w+2 for native integer samples, 34 otherwise
 __host__ __device__ inline long long max_block_bytes(int dt, int bs) {
     long long g = bs / 4;
-    long long emax = dt >= 3 ? 34 : (8LL * dt_width(dt) + 2 < 34 ? 8LL * dt_width(dt) + 2 : 34);
+    long long emax = (kdt_float(dt) || dt == kKdtI64) ? 34
+                   : (8LL * dt_width(dt) + 2 < 34 ? 8LL * dt_width(dt) + 2 : 34);
     return hdr_size(dt) + (3 * g + 1) / 2 + (4 * emax * g + 7) / 8;
+}
+// worst case of any valid container block (a decoder must take every block
+// the reference's decoder takes, exponents up to 34 whatever the dtype)
+__host__ __device__ inline long long max_block_bytes_any(int dt, int bs) {
+    long long g = bs / 4;
+    return hdr_size(dt) + (3 * g + 1) / 2 + (4 * 34 * g + 7) / 8;
 }
 
 // ---------------------------------------------------------------------------

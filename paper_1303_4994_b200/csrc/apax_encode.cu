@@ -512,11 +512,12 @@ __global__ void __launch_bounds__(kNT) encode_kernel(EncParams P) {
                         double yv;
                         if (Tr::F) {
                             double y = __ddiv_rn((double)(long long)qv, deq_s);
-                            yv = (DT == 3) ? (double)__double2float_rn(y) : y;
+                            yv = (DT == 3 || DT == 6) ? (double)__double2float_rn(y) : y;
                         } else {
                             long long yi = (deq_a == 1.0) ? (long long)qv
                                                           : f2i64(rint(__ddiv_rn((double)(long long)qv, deq_a)));
-                            yi = yi < Tr::LO ? Tr::LO : (yi > Tr::HI ? Tr::HI : yi);
+                            const long long lo = DT == 5 ? P.clip_lo : Tr::LO, hi = DT == 5 ? P.clip_hi : Tr::HI;
+                            yi = yi < lo ? lo : (yi > hi ? hi : yi);
                             yv = (double)yi;
                         }
                         double d = xv - yv;
@@ -881,6 +882,8 @@ __global__ void __launch_bounds__(kNT) encode_kernel(EncParams P) {
                     }
                 } else if (P.mode == 2) {
                     double px = S->px / (double)n, pd = S->pd / (double)n;
+                    // math.log10 of a ratio that underflowed (or of px / inf) raises
+                    if (px > 0.0 && pd != 0.0 && px / pd == 0.0) report_error(P.status, b, APAX_ERR_MATH_DOMAIN);
                     if (px > 0.0) {
                         double measured = (pd == 0.0) ? INFINITY : 10.0 * log10(px / pd);
                         if (isfinite(measured)) {
@@ -928,7 +931,7 @@ __global__ void __launch_bounds__(kNT) encode_kernel(EncParams P) {
                 // file header "<4sBBBBIQd" (codec.py:277-279)
                 unsigned char h[kFileHeader];
                 h[0] = 'A'; h[1] = 'P'; h[2] = 'A'; h[3] = 'X';
-                h[4] = 1; h[5] = (unsigned char)DT; h[6] = (unsigned char)P.mode; h[7] = 0;
+                h[4] = 1; h[5] = (unsigned char)(DT >= 5 ? P.wire : DT); h[6] = (unsigned char)P.mode; h[7] = 0;
                 unsigned bsz = (unsigned)bs;
                 for (int k = 0; k < 4; k++) h[8 + k] = (unsigned char)(bsz >> (8 * k));
                 unsigned long long cnt = (unsigned long long)P.n;
@@ -951,7 +954,7 @@ __global__ void __launch_bounds__(kNT) encode_kernel(EncParams P) {
 size_t encode_smem_bytes(int dt, int bs, int stage_bytes, int x_in_smem) {
     auto al = [](size_t v) { return (v + 15) & ~(size_t)15; };
     size_t w = (size_t)dt_width(dt);
-    size_t qw = dt == 4 ? 8 : 4;
+    size_t qw = dt_width(dt) == 8 ? 8 : 4;
     return al(sizeof(EncState)) + al(sizeof(LeafList)) + (x_in_smem ? al((size_t)bs * w) : 0) +
            al((size_t)(bs + 4) * qw) + al((size_t)3 * (bs / 4) + 16) + (size_t)stage_bytes + 16;
 }
@@ -961,28 +964,33 @@ static int launch_encode_t(const EncParams& P, int grid, size_t smem, cudaStream
     cudaError_t e = cudaFuncSetAttribute(encode_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return APAX_ERR_CUDA;
+    note_launches(1);
     encode_kernel<DT><<<grid, kNT, smem, st>>>(P);
     return cudaGetLastError() == cudaSuccess ? APAX_OK : APAX_ERR_CUDA;
+}
+
+template <int DT>
+static int resident_t(size_t smem) {
+    int per = 0;
+    cudaFuncSetAttribute(encode_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, encode_kernel<DT>, kNT, smem) != cudaSuccess) per = 1;
+    return per;
 }
 
 int encode_resident_ctas(int dt, size_t smem) {
     int dev = 0, nsm = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaError_t e = cudaSuccess;
     switch (dt) {
-        case 0: cudaFuncSetAttribute(encode_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, encode_kernel<0>, kNT, smem); break;
-        case 1: cudaFuncSetAttribute(encode_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, encode_kernel<1>, kNT, smem); break;
-        case 2: cudaFuncSetAttribute(encode_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, encode_kernel<2>, kNT, smem); break;
-        case 3: cudaFuncSetAttribute(encode_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, encode_kernel<3>, kNT, smem); break;
-        default: cudaFuncSetAttribute(encode_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, encode_kernel<4>, kNT, smem); break;
+        case 0: per = resident_t<0>(smem); break;
+        case 1: per = resident_t<1>(smem); break;
+        case 2: per = resident_t<2>(smem); break;
+        case 3: per = resident_t<3>(smem); break;
+        case 4: per = resident_t<4>(smem); break;
+        case 5: per = resident_t<5>(smem); break;
+        default: per = resident_t<6>(smem); break;
     }
-    if (e != cudaSuccess || per < 1) per = 1;
+    if (per < 1) per = 1;
     return per * (nsm > 0 ? nsm : 148);
 }
 
@@ -993,6 +1001,8 @@ int launch_encode(int dt, const EncParams& P, int grid, size_t smem, cudaStream_
         case 2: return launch_encode_t<2>(P, grid, smem, st);
         case 3: return launch_encode_t<3>(P, grid, smem, st);
         case 4: return launch_encode_t<4>(P, grid, smem, st);
+        case kKdtI64: return launch_encode_t<kKdtI64>(P, grid, smem, st);
+        case kKdtF64F32: return launch_encode_t<kKdtF64F32>(P, grid, smem, st);
     }
     return APAX_ERR_ARG;
 }

@@ -1070,6 +1070,8 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
             // before the window zeroing overwrites it.
             auto fq_update = [&](double px, double pd) {
                 const double pxm = px / (double)n, pdm = pd / (double)n;
+                // math.log10 of a ratio that underflowed (or of px / inf) raises
+                if (pxm > 0.0 && pdm != 0.0 && pxm / pdm == 0.0 && !S->bad) S->bad = APAX_ERR_MATH_DOMAIN;
                 if (pxm > 0.0) {
                     const double measured = (pdm == 0.0) ? INFINITY : 10.0 * log10(pxm / pdm);
                     if (isfinite(measured))
@@ -1796,6 +1798,7 @@ static int launch_v3_range(int dt, bool fix, const EncParams& P, long long u0, l
     p.unit_end = u1;
     const int g = pw ? (int)(nu < grid ? nu : grid) : (int)nu;
     void* args[] = {&p};
+    note_launches(1);
     if (cudaLaunchCooperativeKernel(fn, dim3(g), dim3(pw ? v3::NT : v3::NCT), args, smem, st) != cudaSuccess)
         return APAX_ERR_CUDA;
     return APAX_OK;

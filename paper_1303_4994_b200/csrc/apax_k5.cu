@@ -345,27 +345,37 @@ int launch_find_blocks_k5(const uint8_t* blob, long long nbytes, long long n, in
     long long span = nbytes - hs - kFileHeader;
     int ncb = (int)((span + 32767) / 32768);
     ncb = ncb < 1 ? 1 : (ncb > CMAX ? CMAX : ncb);
+    note_launches(1);
     count_kernel<<<ncb, NT, 0, st>>>(blob, nbytes, hs, ncb, W.ccount);
+    note_launches(1);
     scan_kernel<<<1, 1024, 0, st>>>(W.ccount, ncb, W.cbase, &W.hdr->ncand, W.cap, &W.hdr->fail);
+    note_launches(1);
     emit_kernel<<<ncb, NT, 0, st>>>(blob, nbytes, hs, ncb, W);
     const size_t psmem = (size_t)NW * (((bs >> 2) + 16 + 15) & ~15);
     if (cudaFuncSetAttribute(parse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem) != cudaSuccess)
         return APAX_ERR_CUDA;
     long long pgrid = (W.cap + NW - 1) / NW;
     if (pgrid > (long long)nsm * 8) pgrid = (long long)nsm * 8;
+    note_launches(1);
     parse_kernel<<<(int)pgrid, NT, psmem, st>>>(blob, nbytes, bs, dt, W);
     long long mgrid = (W.cap + NT - 1) / NT;
     if (mgrid > (long long)nsm * 8) mgrid = (long long)nsm * 8;
+    note_launches(1);
     mark_kernel<<<(int)mgrid, NT, 0, st>>>(nullptr, W.keep0, W);
+    note_launches(1);
     mark_kernel<<<(int)mgrid, NT, 0, st>>>(W.keep0, W.keep1, W);
     // survivors in order: chunks over the candidate index (<= cap)
     int nck = (int)((W.cap + 4095) / 4096);
     nck = nck < 1 ? 1 : (nck > CMAX ? CMAX : nck);
+    note_launches(1);
     kcount_kernel<<<nck, NT, 0, st>>>(W.keep1, nck, W);
+    note_launches(1);
     scan_kernel<<<1, 1024, 0, st>>>(W.ccount, nck, W.cbase, &W.hdr->nkept, (long long)1 << 62, &W.hdr->fail);
+    note_launches(1);
     kemit_kernel<<<nck, NT, 0, st>>>(W.keep1, nck, n_blocks, offsets, W);
     long long vgrid = (n_blocks + NT - 1) / NT;
     if (vgrid > (long long)nsm * 8) vgrid = (long long)nsm * 8;
+    note_launches(1);
     verify_kernel<<<(int)vgrid, NT, 0, st>>>(n_blocks, offsets, W);
     if (cudaGetLastError() != cudaSuccess) return APAX_ERR_CUDA;
     // last block (true group count) or, on any anomaly, the full serial walk

@@ -35,6 +35,10 @@ struct EncParams {
     double* trace;                // nullable, 10 doubles per block
     long long gblock0;            // v3 lossless range encode: global index of block 0
                                   // (x[-bs-2 .. 0) holds the halo when > 0)
+    // cast variants (generic kernel, kdt 5 / 6): the container's wire code and,
+    // for integer containers, the dequantizer's clip range (codec.py:143-145)
+    int wire;
+    long long clip_lo, clip_hi;
 };
 
 struct DecParams {
@@ -62,15 +66,14 @@ struct DecParams {
     int no_store;
 };
 
+// kernel launches enqueued by the library (apax_launch_count)
+void note_launches(int k);
+
 size_t encode_smem_bytes(int dt, int bs, int stage_bytes, int x_in_smem);
 int encode_resident_ctas(int dt, size_t smem);
 int launch_encode(int dt, const EncParams& P, int grid, size_t smem, cudaStream_t st);
 size_t decode_smem_bytes(int dt, int bs, int payload_cap);
 int decode_resident_ctas(int dt, size_t smem);
-size_t encode_v2_smem_bytes(int dt, int mode, int window_bytes);
-bool encode_v2_supported(int bs);
-int encode_v2_resident_ctas(int dt, size_t smem);
-int launch_encode_v2(int dt, const EncParams& P, int grid, size_t smem, cudaStream_t st);
 size_t encode_v3_smem_bytes(int dt, int bs, int stage_bytes);
 int encode_v3_stage_bytes(int dt, int bs);
 bool encode_v3_supported(int dt, int bs);

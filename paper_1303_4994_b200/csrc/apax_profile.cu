@@ -191,11 +191,11 @@ __global__ void __launch_bounds__(NT) select_kernel(const void* x, const void* y
 int profile_sums(const void* x, const void* y, long long n, int dt, int pass, double mx, double my,
                  double md, double* partials, unsigned long long* counts, int grid, cudaStream_t st) {
     switch (dt) {
-        case 0: prof::sums_kernel<0><<<grid, prof::NT, 0, st>>>(x, y, n, pass, mx, my, md, partials, counts); break;
-        case 1: prof::sums_kernel<1><<<grid, prof::NT, 0, st>>>(x, y, n, pass, mx, my, md, partials, counts); break;
-        case 2: prof::sums_kernel<2><<<grid, prof::NT, 0, st>>>(x, y, n, pass, mx, my, md, partials, counts); break;
-        case 3: prof::sums_kernel<3><<<grid, prof::NT, 0, st>>>(x, y, n, pass, mx, my, md, partials, counts); break;
-        default: prof::sums_kernel<4><<<grid, prof::NT, 0, st>>>(x, y, n, pass, mx, my, md, partials, counts); break;
+        case 0: note_launches(1); prof::sums_kernel<0><<<grid, prof::NT, 0, st>>>(x, y, n, pass, mx, my, md, partials, counts); break;
+        case 1: note_launches(1); prof::sums_kernel<1><<<grid, prof::NT, 0, st>>>(x, y, n, pass, mx, my, md, partials, counts); break;
+        case 2: note_launches(1); prof::sums_kernel<2><<<grid, prof::NT, 0, st>>>(x, y, n, pass, mx, my, md, partials, counts); break;
+        case 3: note_launches(1); prof::sums_kernel<3><<<grid, prof::NT, 0, st>>>(x, y, n, pass, mx, my, md, partials, counts); break;
+        default: note_launches(1); prof::sums_kernel<4><<<grid, prof::NT, 0, st>>>(x, y, n, pass, mx, my, md, partials, counts); break;
     }
     return cudaGetLastError() == cudaSuccess ? APAX_OK : APAX_ERR_CUDA;
 }
@@ -210,6 +210,7 @@ int profile_welch(const void* x, const void* y, long long n, int dt, int which, 
     auto go = [&](auto kfn) -> int {
         if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
             return APAX_ERR_CUDA;
+        note_launches(1);
         kfn<<<grid, prof::NT, smem, st>>>(x, y, n, which, seg, lg, nframes, tw, partials);
         return cudaGetLastError() == cudaSuccess ? APAX_OK : APAX_ERR_CUDA;
     };
@@ -229,6 +230,7 @@ int profile_select(const void* x, const void* y, long long n, int dt, int pass,
     auto go = [&](auto kfn) -> int {
         if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
             return APAX_ERR_CUDA;
+        note_launches(1);
         kfn<<<grid, prof::NT, smem, st>>>(x, y, n, pass, prefixes, npre, hist, ydiff);
         return cudaGetLastError() == cudaSuccess ? APAX_OK : APAX_ERR_CUDA;
     };

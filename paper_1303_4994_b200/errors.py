@@ -102,6 +102,7 @@ _STATUS = {
     22: (RangeError, "attenuation outside [2^-31, 2^33)"),                     # dtypes.py:112
     23: (InternalError, "sample exceeds its group exponent width"),            # entropy.py:234
     24: (UnsupportedValue, "non-finite float input"),                          # codec.py:114
+    25: (ValueError, "math domain error"),                                     # codec.py:251 log10(0)
     40: (ValueError, "output buffer too small"),
     41: (MemoryError, "allocation failure"),
     42: (ValueError, "invalid argument"),

@@ -464,15 +464,16 @@ def recommend_operating_point(curve: RateCorrelationCurve,
     target = lo.srr_target + (threshold - lo.r) / (hi.r - lo.r) * (hi.srr_target - lo.srr_target)
     if reencode is None:
         return hi
+    # reference :240-246: the point of the 8th bisection step is never
+    # checked; the loop falls through to re-encoding the upper bracket
+    upper = hi.srr_target
     point = reencode(target)
-    steps = 0
-    while point.r < threshold and steps < 8:
-        target = 0.5 * (target + hi.srr_target)
+    for _ in range(8):
+        if point.r >= threshold:
+            return point
+        target = 0.5 * (target + upper)
         point = reencode(target)
-        steps += 1
-    if point.r >= threshold:
-        return point
-    return reencode(hi.srr_target)
+    return reencode(upper)
 
 
 class ProfileSession:

@@ -69,7 +69,7 @@ def cfg3_grf_f32(side: int = 8192, seed: int = 3) -> np.ndarray:
     return img.astype(np.float32).reshape(-1)
 
 
-def cfg4_modes_f64(side: int = 1024, seed: int = 4, n_modes: int = 64, device=None):
+def cfg4_modes_f64(side: int = 1024, seed: int = 4, n_modes: int = 64, device=None, planes=None):
     """float64 side^3 field: 64 modes A cos(2 pi k.r/side + phi), A ~ N(0,1),
     k in [-8, 8]^3, phi ~ U(0, 2 pi), plus N(0, sigma=1e-4) (read as sigma).
 
@@ -78,7 +78,8 @@ def cfg4_modes_f64(side: int = 1024, seed: int = 4, n_modes: int = 64, device=No
     the GPU in milliseconds: returns a flat torch f64 tensor on `device`
     (default cuda:0 when available, else CPU).  Mode parameters are
     numpy-seeded; the noise comes from a seeded torch generator on the same
-    device, so the field is reproducible per device type."""
+    device, so the field is reproducible per device type.  `planes` limits
+    the field to its first z planes (a slab; the CPU reference arm)."""
     import torch
     if device is None:
         device = "cuda" if torch.cuda.is_available() else "cpu"
@@ -91,10 +92,11 @@ def cfg4_modes_f64(side: int = 1024, seed: int = 4, n_modes: int = 64, device=No
     ax = K[:, 0, None] * r[None, :] + phi[:, None]                     # [m, x]
     C = torch.cat([torch.cos(ax), -torch.sin(ax)], 0)                 # [2m, x]
     del ax
-    out = torch.empty(side * side, side, dtype=torch.float64, device=dev)
-    zc = max(1, min(side, (1 << 26) // (side * side) or 1))          # z planes per GEMM chunk
-    for z0 in range(0, side, zc):
-        z1 = min(side, z0 + zc)
+    nz = side if planes is None else int(planes)
+    out = torch.empty(nz * side, side, dtype=torch.float64, device=dev)
+    zc = max(1, min(nz, (1 << 26) // (side * side) or 1))            # z planes per GEMM chunk
+    for z0 in range(0, nz, zc):
+        z1 = min(nz, z0 + zc)
         byz = (K[None, None, :, 1] * r[None, :, None] +
                K[None, None, :, 2] * r[z0:z1, None, None])            # [z, y, m]
         B = torch.cat([A * torch.cos(byz), A * torch.sin(byz)], -1)   # [z, y, 2m]

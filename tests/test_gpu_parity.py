@@ -291,3 +291,62 @@ def test_segment_decoder_width_boundaries(k):
         assert np.array_equal(y, x), (k, seg)
         y2 = decode_device(res.blob, res.nbytes).cpu().numpy()
         assert np.array_equal(y2, x), (k, seg)
+
+
+# ---------------------------------------------------------------------------
+# encode_stream's input conversions (reference codec.py:266-272): inputs of
+# other dtypes, coded by the container dtype path when it holds the widened
+# values exactly, else by apax_encode_cast (generic kernel on int64 / f64)
+# ---------------------------------------------------------------------------
+def _cast_cases():
+    return [m["name"] for m in json.loads((GOLDEN / "cast_manifest.json").read_text())]
+
+
+@pytest.mark.parametrize("name", _cast_cases())
+def test_cast_container_vs_reference(name):
+    c = load_container(GOLDEN / "containers" / f"{name}.npz")
+    m = c["meta"]
+    cfg = StreamConfig(DT[m["dtype"]], m["block_size"], Mode(m["mode"]), float.fromhex(m["target_hex"]))
+    got = encode_stream(c["x"], cfg)
+    assert got == c["blob"], name
+    y = decode_stream(c["blob"])
+    assert y.dtype == c["y"].dtype and np.array_equal(y, c["y"])
+
+
+def test_cast_errors_vs_reference():
+    for case in json.loads((GOLDEN / "cast_errors.json").read_text()):
+        x = np.frombuffer(bytes.fromhex(case["x_hex"]), np.dtype(case["x_dtype"]))
+        cfg = StreamConfig(DT[case["dtype"]], case["block_size"], Mode(case["mode"]), case["target"])
+        if case["exc"] is None:
+            assert encode_stream(x, cfg).hex() == case["blob_hex"], case["name"]
+            continue
+        with pytest.raises(Exception) as ei:
+            encode_stream(x, cfg)
+        assert type(ei.value).__name__ == case["exc"], case["name"]
+        assert str(ei.value) == case["msg"], case["name"]
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_cast_random_vs_oracle(seed):
+    """f64 samples into f32 containers and int64 samples into narrower
+    integer containers, every mode, random block sizes, against the oracle's
+    restatement of the reference's widening."""
+    rng = np.random.default_rng(3000 + seed)
+    for _ in range(6):
+        n = int(rng.integers(1, 30000))
+        bs = int(rng.choice([64, 100, 512, 1000, 4096]))
+        if rng.integers(0, 2):
+            dt = Dtype.F32
+            x = np.cumsum(rng.standard_normal(n)) * 10.0 ** rng.uniform(-3, 5)
+            mode = Mode(int(rng.integers(1, 3)))
+        else:
+            dt = DT[str(rng.choice(["i8", "i16", "i32"]))]
+            info = np.iinfo(dt.np_dtype)
+            x = (np.cumsum(rng.standard_normal(n)) * float(info.max) * rng.uniform(0.01, 0.3)).astype(np.int64)
+            mode = Mode(int(rng.integers(0, 3)))
+        T = {Mode.LOSSLESS: 0.0, Mode.FIXED_RATE: float(rng.uniform(2, 12)),
+             Mode.FIXED_QUALITY: float(rng.uniform(20, 90))}[mode]
+        cfg = StreamConfig(dt, bs, mode, T)
+        ref = O.encode(x, dt.wire_code, mode.value, T, bs)[0]
+        assert encode_stream(x, cfg) == ref, (n, bs, dt, mode, T)
+        assert np.array_equal(decode_stream(ref), O.decode(ref))

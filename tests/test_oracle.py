@@ -175,3 +175,61 @@ def test_segment_independence_property(rng):
     assert np.array_equal(O.decode(whole), x)
     seg0, _, _ = O.encode(x[:5 * 1024], 1, 0, 0.0, 1024)
     assert blob[28:int(offs[5])] == seg0[28:]
+
+
+# ---------------------------------------------------------------------------
+# encode_stream's input conversions (reference codec.py:266-272), pinned by
+# containers the live reference produced from inputs of other dtypes
+# (tests/golden/make_cast_golden.py)
+# ---------------------------------------------------------------------------
+def _cast_cases():
+    return [m["name"] for m in json.loads((GOLDEN / "cast_manifest.json").read_text())]
+
+
+_ORACLE_EXC = {"InternalError": 10, "UnsupportedValue": 9, "ValueError": 25}
+
+
+@pytest.mark.parametrize("name", _cast_cases())
+def test_oracle_cast_container_parity(name):
+    c = load_container(GOLDEN / "containers" / f"{name}.npz")
+    m = c["meta"]
+    blob, offs, _ = O.encode(c["x"], O.DTYPE_CODES[m["dtype"]], m["mode"], float.fromhex(m["target_hex"]),
+                             m["block_size"])
+    assert blob == c["blob"], name
+    assert np.array_equal(offs, c["offsets"])
+    y = O.decode(c["blob"])
+    assert y.dtype == c["y"].dtype and np.array_equal(y, c["y"])
+
+
+def test_oracle_cast_errors():
+    for case in json.loads((GOLDEN / "cast_errors.json").read_text()):
+        x = np.frombuffer(bytes.fromhex(case["x_hex"]), np.dtype(case["x_dtype"]))
+        args = (x, O.DTYPE_CODES[case["dtype"]], case["mode"], case["target"], case["block_size"])
+        if case["exc"] is None:
+            assert O.encode(*args)[0].hex() == case["blob_hex"], case["name"]
+            continue
+        with pytest.raises(O.OracleError) as ei:
+            O.encode(*args)
+        assert ei.value.code == _ORACLE_EXC[case["exc"]], case["name"]
+
+
+def test_reference_cast_routing():
+    """The product widens exactly like the reference and codes the widened
+    values in the container dtype whenever that holds them exactly."""
+    from paper_1303_4994_b200.codec import _IN_FLOAT64, _IN_INT64, _IN_NATIVE, _reference_cast
+    from paper_1303_4994_b200.dtypes import Dtype
+    for m in json.loads((GOLDEN / "cast_manifest.json").read_text()):
+        c = load_container(GOLDEN / "containers" / f"{m['name']}.npz")
+        dt = {"i8": Dtype.I8, "i16": Dtype.I16, "i32": Dtype.I32, "f32": Dtype.F32, "f64": Dtype.F64}[m["dtype"]]
+        x = c["x"]
+        xw, kind = _reference_cast(x, dt)
+        wide = x.astype(np.float64 if dt.is_float else np.int64)
+        if kind == _IN_NATIVE:
+            assert xw.dtype == dt.np_dtype
+            assert np.array_equal(xw.astype(wide.dtype), wide)
+        else:
+            assert kind == (_IN_FLOAT64 if dt.is_float else _IN_INT64)
+            assert xw.dtype == wide.dtype and np.array_equal(xw, wide)
+    x = np.array([1.5, -2.7, 3e9])
+    xw, kind = _reference_cast(x, Dtype.I32)
+    assert kind == _IN_INT64 and xw.tolist() == [1, -2, 3000000000]

@@ -86,6 +86,33 @@ def test_recommend_interpolation_and_bisection():
         assert b == 0.5 * (a + 50.0)
 
 
+@pytest.mark.parametrize("clear_at", list(range(0, 11)))
+def test_recommend_bisection_call_sequence(clear_at):
+    """Reference profiler.py:240-246: re-encode the interpolated target, up to
+    8 bisection steps toward the upper bracket, and the point of the 8th step
+    is never checked -- the loop falls through to reencode(upper).  The stub
+    first clears the threshold on call number `clear_at` (0 = the
+    interpolated point, 8 = the 8th bisection, 9+ = never)."""
+    pts = (P.OperatingPoint(40.0, 6.0, 0.9999), P.OperatingPoint(50.0, 5.0, 0.999995))
+    curve = P.RateCorrelationCurve(pts)
+    calls = []
+
+    def reencode(t):
+        calls.append(t)
+        ok = len(calls) - 1 >= clear_at or t == 50.0
+        return P.OperatingPoint(t, 7.0 - len(calls) * 0.1, 0.999999 if ok else 0.99998)
+    rec = P.recommend_operating_point(curve, reencode)
+    if clear_at <= 7:
+        assert len(calls) == clear_at + 1 and rec.srr_target == calls[-1]
+    else:
+        # the 8th bisection point (call 9) may clear the threshold: ignored
+        assert len(calls) == 10 and calls[-1] == 50.0 and rec.srr_target == 50.0
+    frac = (P.FIVE_NINES - pts[0].r) / (pts[1].r - pts[0].r)
+    assert calls[0] == 40.0 + frac * 10.0
+    for a, b in zip(calls[:9], calls[1:9]):
+        assert b == 0.5 * (a + 50.0)
+
+
 def test_recommend_non_monotone():
     above, below = 0.999995, 0.9999
     # no (below, above) neighbours: the first point at/above the threshold wins
