@@ -150,7 +150,7 @@ WORKLOADS = {
 }
 
 
-def make_workload(args, rank, dev):
+def make_workload(args, rank, dev, world=1):
     """(x on the device, x on the host or None, StreamConfig, short name)."""
     import torch
     from paper_1303_4994_b200 import Dtype, Mode, StreamConfig
@@ -166,8 +166,19 @@ def make_workload(args, rank, dev):
         xh = W.cfg3_grf_f32(8192, seed=3 + rank)
         dt, mode, target = Dtype.F32, Mode.FIXED_RATE, 32.0 / 6.0
     elif w == "cfg4":
-        xd = W.cfg4_modes_f64(1024, seed=4 + rank, device=dev)
         dt, mode, target = Dtype.F64, Mode.FIXED_RATE, 64.0 / 3.0
+        if args.shard_global:
+            # this rank's contiguous segment range of ONE seeded 1024^3 field
+            # (only its own z planes are generated)
+            from paper_1303_4994_b200.distributed import shard_samples
+            n_all, plane = 1 << 30, 1 << 20
+            P = workload_segment_blocks(args, n_all, "f64")
+            s0, s1 = shard_samples(n_all, 4096, P, world, rank)
+            za, zb = s0 // plane, (s1 + plane - 1) // plane
+            xd = W.cfg4_modes_f64(1024, seed=4, device=dev, z0=za, planes=zb - za)
+            xd = xd[s0 - za * plane:s1 - za * plane].contiguous()
+            return xd, None, dt, mode, target
+        xd = W.cfg4_modes_f64(1024, seed=4 + rank, device=dev)
         return xd, None, dt, mode, target
     elif w == "cfg5":
         xh = W.cfg5_ar1(1 << (args.n_log2 or 26), args.cfg5_dtype, seed=5 + rank)
@@ -183,17 +194,25 @@ def make_workload(args, rank, dev):
 # v3 encoder's one-wave instantiation, apax_encode_wave_segment_blocks).  Both
 # arms take P from this pure-Python rule so the reference arm never loads the
 # GPU library; the GPU arm records the library's own answer beside it.
-B200_WAVE_UNITS = 148 * 4
+B200_SMS = 148
+WAVE_CTAS_PER_SM = {"i8": 4, "i16": 4, "i32": 4, "f32": 4, "f64": 2}
 
 
-def wave_p(n: int) -> int:
+def wave_p(n: int, dt: str = "f32") -> int:
     nb = (n + 4095) // 4096
-    return max(1, (nb + B200_WAVE_UNITS - 1) // B200_WAVE_UNITS)
+    units = B200_SMS * WAVE_CTAS_PER_SM[dt]
+    return max(1, (nb + units - 1) // units)
 
 
-def workload_segment_blocks(args, n):
-    """P of the workload: --segment-blocks, else the one-wave length."""
-    return args.segment_blocks if args.segment_blocks > 0 else wave_p(n)
+def workload_segment_blocks(args, n, dt: str = "f32"):
+    """P of the workload: --segment-blocks, else the one-wave length (for
+    --shard-global: of one eighth of the array, so the container is the same
+    at every GPU count)."""
+    if args.segment_blocks > 0:
+        return args.segment_blocks
+    if getattr(args, "shard_global", False):
+        return wave_p(n // 8, dt)
+    return wave_p(n, dt)
 
 
 def _standalone_workloads():
@@ -235,7 +254,7 @@ def run_reference(args, rank):
     else:
         x, dt, mode, target = W.cfg2_ar2_f32(1 << (args.n_log2 or 26)), "f32", 2, W.CFG2_TARGET_DB
     full_n = (1 << 30) if w == "cfg4" else x.size
-    seg = workload_segment_blocks(args, full_n)
+    seg = workload_segment_blocks(args, full_n, dt)
     pol = {"cold": 0, "warm_self": 1}.get(args.policy, 1 if mode == 1 else 0)
     sys.path.insert(0, str(ROOT))
     from oracle import oracle as O
@@ -284,6 +303,9 @@ def main():
     ap.add_argument("--rate", type=float, default=4.0, help="cfg5 compression ratio r (bps = 32/r)")
     ap.add_argument("--policy", default="auto", choices=["auto", "cold", "warm_self"],
                     help="segment policy; auto = warm_self for fixed rate, cold for fixed quality")
+    ap.add_argument("--shard-global", action="store_true",
+                    help="cfg4: ranks hold contiguous segment ranges of ONE 1024^3 field (strong scaling); "
+                         "the global profiler statistics are timed beside the codec step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=8, help="pipeline chunks of the e2e round trip")
@@ -314,9 +336,9 @@ def main():
     from paper_1303_4994_b200 import workloads as W
 
     dev = torch.device("cuda", local)
-    x, x_host, wdt, wmode, target = make_workload(args, rank, dev)
+    x, x_host, wdt, wmode, target = make_workload(args, rank, dev, world)
     n = x.numel()
-    args.segment_blocks = workload_segment_blocks(args, n)
+    args.segment_blocks = workload_segment_blocks(args, (1 << 30) if args.shard_global else n, wdt.code)
     from paper_1303_4994_b200 import wave_segment_blocks
     lib_wave_p = wave_segment_blocks(n, wdt, wmode, 4096)
     policy = args.policy if args.policy != "auto" else (
@@ -390,9 +412,12 @@ def main():
         total_container = nbytes
 
     in_bytes = n * width
-    value = world * in_bytes / (mean_step * 1e-3) / 1e9
-    enc_gbs = in_bytes / (mean_enc * 1e-3) / 1e9
-    dec_gbs = in_bytes / (mean_dec * 1e-3) / 1e9
+    # whole-job input bytes: every rank's shard of one array (--shard-global)
+    # or world independent arrays (weak scaling)
+    job_bytes = (1 << 30) * width if args.shard_global else world * in_bytes
+    value = job_bytes / (mean_step * 1e-3) / 1e9
+    enc_gbs = job_bytes / world / (mean_enc * 1e-3) / 1e9
+    dec_gbs = job_bytes / world / (mean_dec * 1e-3) / 1e9
     peak, peak_kind = _peaks()
     alg_enc = in_bytes + nbytes + 8 * (enc.n_blocks + 1)   # read x, write container + offsets
     alg_dec = nbytes + in_bytes + 8 * (enc.n_blocks + 1)   # read container + offsets, write y
@@ -464,6 +489,38 @@ def main():
                                             "discovery, segment detection, decode, D2H samples",
                                     "bit_exact_vs_device_path": ok_il}}
 
+    # ---- --shard-global: the global profiler statistics of the one array ----
+    prof = None
+    if args.shard_global:
+        from paper_1303_4994_b200 import distributed as D
+        y_loc = dec.y[:n]
+        grp = None
+        if world == 1:   # a one-rank process group so the same collectives run
+            import socket
+            if not dist.is_initialized():
+                with socket.socket() as so:
+                    so.bind(("127.0.0.1", 0))
+                    port = so.getsockname()[1]
+                dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                                        device_id=dev)
+        D.sharded_window_stats(x, y_loc, wdt, grp)   # warm-up (tables, allocator)
+        torch.cuda.synchronize()
+        dist.barrier()
+        a = time.perf_counter()
+        wst = D.sharded_window_stats(x, y_loc, wdt, grp)
+        wx = D.sharded_welch(x, y_loc, wdt, 0, 4096, grp)
+        wd = D.sharded_welch(x, y_loc, wdt, 2, 4096, grp)
+        torch.cuda.synchronize()
+        t_prof = torch.tensor([time.perf_counter() - a], dtype=torch.float64, device=dev)
+        dist.all_reduce(t_prof, op=dist.ReduceOp.MAX)
+        prof = {"ms": float(t_prof.item()) * 1e3,
+                "what": "global window statistics (rank-ordered merged sums, two-pass std, exact S2R margin by "
+                        "all-reduced radix histograms) + Welch spectra of x and d over all ranks (NCCL)",
+                "pearson_r": wst["pearson_r"], "srr_db": wst["srr_db"],
+                "two_sigma_s2r_margin_db": wst["two_sigma_s2r_margin_db"],
+                "welch_x_peak_db": float(10 * np.log10(wx.max() + 1e-30)),
+                "welch_d_peak_db": float(10 * np.log10(wd.max() + 1e-30))}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
         threads = os.cpu_count() or 1
@@ -481,8 +538,8 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": wdt.code, "data": "synthetic",
+            "higher_is_better": True, "scaling": "strong" if args.shard_global else "weak",
+            "vs_baseline": None, "dtype": wdt.code, "data": "synthetic",
             "config": {
                 "workload": WORKLOADS[args.workload] +
                             (f" ({args.cfg5_dtype}, r={args.rate:g}, 2^{(n).bit_length() - 1} samples)"
@@ -494,13 +551,14 @@ def main():
                 "segment_blocks": args.segment_blocks, "segment_policy": policy,
                 "wave_segment_blocks_library": lib_wave_p,
                 "mode": wmode.name, "target": target,
-                "parallelism": f"dp{world} (segment shards)",
+                "parallelism": (f"dp{world} (contiguous segment ranges of one array)" if args.shard_global
+                                else f"dp{world} (segment shards)"),
                 "l2": f"inputs ({in_bytes >> 20} MiB) {'larger' if in_bytes > (126 << 20) else 'smaller'} "
                       "than L2; L2 flushed (256 MiB write) between encode and decode and after decode",
             },
             "encode_gbs": enc_gbs * world, "decode_gbs": dec_gbs * world,
             "encode_ms": mean_enc, "decode_ms": mean_dec,
-            "container_bytes": total_container, "ratio": world * in_bytes / total_container,
+            "container_bytes": total_container, "ratio": job_bytes / total_container,
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                          "frac": ach / peak,
                          "traffic": (_ncu_traffic(dominant) or {}).get("bytes"),
@@ -512,6 +570,7 @@ def main():
                          "decode": {"achieved": ach_dec, "frac": ach_dec / peak}},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "profile_stats": prof,
             "gpu_launches": gpu_launches,
             "clocks": sampler.summary(),
             "self_check": {"decoded_finite": ok_roundtrip},

@@ -33,10 +33,11 @@ struct EncPlan {
     int stage_bytes;
     int x_in_smem;
     int v3;
+    int split;             // chain (v3 META) + block-parallel packer (v4)
     size_t smem;
     int grid;
     long long slot_bytes;
-    long long ws_lookback, ws_ticket, ws_slots, ws_total;
+    long long ws_lookback, ws_ticket, ws_slots, ws_v4, ws_total;
 };
 
 bool valid_dtype(int dt) { return dt >= 0 && dt <= 4; }
@@ -114,6 +115,15 @@ int plan_encode(long long n, int kdt, int mode, int bs, long long seg, EncPlan* 
     p->ws_ticket = (p->n_units * 8 + 255) & ~255LL;
     p->ws_slots = p->ws_ticket + 256;
     p->ws_total = p->ws_slots + p->slot_bytes * (p->v3 ? v3_slots : (long long)p->grid);
+    // split encoder (bs 4096, i16/i32/f32/f64): per-block quantizer records,
+    // published costs, look-back words, one ticket counter
+    // (segmented fixed-rate / fixed-quality containers stay on the fused v3
+    // kernel: one CTA per segment is faster there, tools/time_encode.py)
+    const int sp = env_int("APAX_ENC_SPLIT", -1);
+    p->split = p->v3 && encode_v4_supported(kdt, bs) &&
+               (sp == 1 || (sp < 0 && (seg <= 0 || mode == APAX_LOSSLESS)));
+    p->ws_v4 = (p->ws_total + 255) & ~255LL;
+    if (p->split) p->ws_total = p->ws_v4 + p->n_blocks * (16 + 8 + 8) + 256;
     return APAX_OK;
 }
 
@@ -292,6 +302,25 @@ int apax_encode(const void* x, int64_t n, int dtype, int mode, double target, in
     P.pow10_t20 = pow(10.0, target / 20.0);
     P.sqrt12 = sqrt(12.0);
     P.trace = trace;
+    if (p.split && (((uintptr_t)x) & 15) == 0) {
+        // the chain writes each block's quantizer record; the packer codes
+        // every block on its own at its final offset (apax_encode_v4.cu)
+        uint8_t* v4 = w + p.ws_v4;
+        BlockMeta* meta = (BlockMeta*)v4;
+        unsigned long long* costs = (unsigned long long*)(v4 + p.n_blocks * 16);
+        unsigned long long* lb = costs + p.n_blocks;
+        unsigned long long* ticket = lb + p.n_blocks;
+        if (cudaMemsetAsync(costs, 0, (size_t)p.n_blocks * 16 + 8, s) != cudaSuccess) return APAX_ERR_CUDA;
+        if (mode != APAX_LOSSLESS) {
+            P.meta = meta;
+            int r = launch_encode_v3_chain(dtype, P, p.smem, s);
+            if (r) return r;
+        }
+        EncParams Q = P;
+        Q.unit_blocks = segment_blocks > 0 ? p.unit_blocks : p.n_blocks;   // restart every unit_blocks
+        Q.ticket = (unsigned int*)ticket;
+        return launch_encode_v4(dtype, Q, mode != APAX_LOSSLESS ? meta : nullptr, costs, lb, s);
+    }
     if (p.v3) return launch_encode_v3(dtype, P, p.grid, p.smem, s);
     return launch_encode(dtype, P, p.grid, p.smem, s);
 }

@@ -628,7 +628,11 @@ constexpr int fix_stage_bytes(int dt) {
     return ((xb > mb ? xb : mb) + 127) & ~127;
 }
 
-template <int DT, bool FIX, bool PW>
+// META: the chain of the split encoder (apax_encode_v4.cu): only what the
+// gain recurrence needs runs (fixed quality: quantize + powers; fixed rate:
+// + widths, JEE counts, exact byte count), no output; each block's quantizer
+// record goes to P.meta
+template <int DT, bool FIX, bool PW, bool META = false>
 __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MINB_NP) encode_v3_kernel(EncParams P) {
     using Tr = DT_<DT>;
     using T = typename Tr::T;
@@ -1009,7 +1013,10 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
                 S->ra = (!F && aq != 1.0) ? __ddiv_rn(1.0, aq) : 1.0;
                 S->sq = F ? (zero ? 0.0 : s) : aq;      // quantizer multiplier
                 S->qpk = qpk;
-                S->wide = (qpk >= (1LL << 29)) ? 1 : 0;
+                // 32-bit phase C/D is exact while every |q| <= 2^30 (floats:
+                // the headroom guarantees it) and every |d1| < 2^30 (checked
+                // per warp in phase C)
+                S->wide = (qpk > (1LL << 30)) ? 1 : 0;
                 S->bad = bad;
                 int sel = 0;
                 if (S->has_pc) {
@@ -1147,6 +1154,11 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
                 }
             }
 
+            long long tt0 = 0, tt1 = 0, tt2 = 0;
+            if (META && FQ) {
+                // the quality loop needs no stream work: the buffer is free
+                if (emit) bufblk_set(cur, kNone);
+            } else {
             // ============ phase C: streams, widths, costs, JEE structure ============
             const int sel_spec = S->sel_spec;
             const int t0 = SPT * tid;
@@ -1159,42 +1171,59 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
             int flips = 0;
             unsigned emax = 0;
             int hq1 = hp1, hq2 = hp2;                  // q[t0-1], q[t0-2]
-            if (active) {
+            bool ww = wide;                            // this warp: 64-bit arithmetic
+            {
                 int q[SPT];
-#pragma unroll
-                for (int m = 0; m < 4; m++) {
-                    const int4 v = qb4[qpb ^ m];
-                    q[4 * m] = v.x; q[4 * m + 1] = v.y; q[4 * m + 2] = v.z; q[4 * m + 3] = v.w;
-                }
-                if (tid > 0) {
-                    const int2 h = *(const int2*)&qbuf[(swz(4 * tid - 1) << 2) + 2];
-                    hq2 = h.x; hq1 = h.y;
-                }
                 const int ng = FIX ? 4 : min(4, G - p0);   // valid groups of this thread (>= 1)
-                if (!wide) {
-                    int m1 = hq1, dprev = hq1 - hq2;
-                    unsigned sgn = (unsigned)hq1 >> 31;   // sign bits, oldest first
+                if (active) {
 #pragma unroll
-                    for (int g = 0; g < 4; g++) {
-                        unsigned o0 = 0, o1 = 0, o2 = 0;
-#pragma unroll
-                        for (int kk = 0; kk < 4; kk++) {
-                            const int v0 = q[4 * g + kk];
-                            const int v1 = v0 - m1;
-                            const int v2 = v1 - dprev;
-                            o0 |= wb32(v0); o1 |= wb32(v1); o2 |= wb32(v2);
-                            sgn = __funnelshift_l((unsigned)v0, sgn, 1);
-                            m1 = v0; dprev = v1;
-                        }
-                        if (g < ng) {
-                            epk0 |= (uint32_t)bitlen32(o0) << (8 * g);
-                            epk1 |= (uint32_t)bitlen32(o1) << (8 * g);
-                            epk2 |= (uint32_t)bitlen32(o2) << (8 * g);
-                        }
+                    for (int m = 0; m < 4; m++) {
+                        const int4 v = qb4[qpb ^ m];
+                        q[4 * m] = v.x; q[4 * m + 1] = v.y; q[4 * m + 2] = v.z; q[4 * m + 3] = v.w;
                     }
-                    // sign-bit flips between neighbours (17 bits: q[t0-1] .. q[t0+15])
-                    flips = __popc((sgn ^ (sgn >> 1)) & 0xffffu);
-                } else {
+                    if (tid > 0) {
+                        const int2 h = *(const int2*)&qbuf[(swz(4 * tid - 1) << 2) + 2];
+                        hq2 = h.x; hq1 = h.y;
+                    }
+                }
+                if (!wide) {
+                    if (active) {
+                        int m1 = hq1, dprev = hq1 - hq2;
+                        unsigned sgn = (unsigned)hq1 >> 31;   // sign bits, oldest first
+#pragma unroll
+                        for (int g = 0; g < 4; g++) {
+                            unsigned o0 = 0, o1 = 0, o2 = 0;
+#pragma unroll
+                            for (int kk = 0; kk < 4; kk++) {
+                                const int v0 = q[4 * g + kk];
+                                const int v1 = v0 - m1;
+                                const int v2 = v1 - dprev;
+                                o0 |= wb32(v0); o1 |= wb32(v1); o2 |= wb32(v2);
+                                sgn = __funnelshift_l((unsigned)v0, sgn, 1);
+                                m1 = v0; dprev = v1;
+                            }
+                            if (g < ng) {
+                                epk0 |= (uint32_t)bitlen32(o0) << (8 * g);
+                                epk1 |= (uint32_t)bitlen32(o1) << (8 * g);
+                                epk2 |= (uint32_t)bitlen32(o2) << (8 * g);
+                            }
+                        }
+                        // sign-bit flips between neighbours (17 bits: q[t0-1] .. q[t0+15])
+                        flips = __popc((sgn ^ (sgn >> 1)) & 0xffffu);
+                    }
+                    // exact only when every |d1| < 2^30 (a D1 width of 32 flags it,
+                    // wrapped values included) and, for thread 0, the history
+                    // entering the block is inside the same bounds
+                    bool bad = active && (epk1 & 0x20202020u) != 0;
+                    if (tid == 0) {
+                        const long long d = (long long)hq1 - (long long)hq2;
+                        bad = bad || d < -(1LL << 30) || d >= (1LL << 30) || hq1 < -(1 << 30) || hq1 > (1 << 30) ||
+                              hq2 < -(1 << 30) || hq2 > (1 << 30);
+                    }
+                    ww = __any_sync(0xffffffffu, bad);
+                    if (ww) { epk0 = epk1 = epk2 = 0u; flips = 0; }
+                }
+                if (active && ww) {
                     long long m1 = hq1, dprev = (long long)hq1 - (long long)hq2;
 #pragma unroll
                     for (int g = 0; g < 4; g++) {
@@ -1218,23 +1247,11 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
                         }
                     }
                 }
-                if (t0 == 0) flips -= (int)((unsigned)(q[0] ^ hq1) >> 31);  // no predecessor in the block
+                if (active && t0 == 0) flips -= (int)((unsigned)(q[0] ^ hq1) >> 31);  // no predecessor in the block
             }
             // byte sums of the packed widths
             auto bsum = [](uint32_t e) -> int { return (int)__dp4a(e, 0x01010101u, 0u); };
             // width of the group starting at sample i0 of stream sl2 (boundary lanes only)
-            auto edge_w32 = [&](int sl2, int4 a, int m1, int m2) -> int {
-                const int v[4] = {a.x, a.y, a.z, a.w};
-                int dp = m1 - m2;
-                unsigned o = 0;
-#pragma unroll
-                for (int kk = 0; kk < 4; kk++) {
-                    const int v1 = v[kk] - m1, v2 = v1 - dp;
-                    o |= wb32(sl2 == 0 ? v[kk] : (sl2 == 1 ? v1 : v2));
-                    m1 = v[kk]; dp = v1;
-                }
-                return bitlen32(o);
-            };
             auto edge_w = [&](int sl2, int4 a, long long m1, long long m2) -> int {
                 const long long v[4] = {a.x, a.y, a.z, a.w};
                 long long dp = m1 - m2;
@@ -1270,7 +1287,7 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
                     // the two samples before that group: chunk 4t-2 (lane 0) or
                     // this thread's own last chunk (lane 31: q14, q15)
                     const int2 h = *(const int2*)&qbuf[(swz(ed0 ? 4 * tid - 2 : 4 * tid + 3) << 2) + 2];
-                    const int ew = wide ? edge_w(sl2, a, h.y, h.x) : edge_w32(sl2, a, h.y, h.x);
+                    const int ew = edge_w(sl2, a, h.y, h.x);   // the neighbour warp may be 64-bit
                     if (ed0) eprev = ew;
                     else enext = ew;
                 }
@@ -1342,7 +1359,8 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
             // zero the window (this block's staging buffer is dead now):
             // chunk 0 carries the previous block's tail
             const int zlen = S->zlen;
-            if (emit) {
+            if (META && emit) bufblk_set(cur, kNone);
+            if (!META && emit) {
                 uint4* w4 = (uint4*)xs;
                 const int nz = zlen >> 4;
                 for (int i = tid; i < nz; i += NCT) w4[i] = make_uint4(0u, 0u, 0u, 0u);
@@ -1353,7 +1371,6 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
             PROF_MARK(3);
 
             // ============ resolve: totals, selector, offsets ============
-            long long tt0, tt1, tt2;
             int flt;
             unsigned emt;
             {
@@ -1449,7 +1466,7 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
                 const long long blen = HS + jee_bytes + ((long long)mb_total + 7) / 8;
                 const int wb = S->tail_len;
                 // window zero fix-up when the guess was short (rare)
-                if (wb + blen + 16 > zlen) {
+                if (!META && wb + blen + 16 > zlen) {
                     uint4* w4 = (uint4*)xs;
                     const int nz = (int)((wb + blen + 16 + 15) >> 4);
                     for (int i = (zlen >> 4) + tid; i < nz; i += NCT) w4[i] = make_uint4(0u, 0u, 0u, 0u);
@@ -1472,7 +1489,7 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
                 const int bad = S->bad;
                 // ============ phase D: JEE tokens + mantissas into the window ============
                 uint32_t* win = (uint32_t*)xs;
-                if (active && !bad) {
+                if (!META && active && !bad) {
                     // JEE tokens of this thread's positions, gathered into <= 48 bits
                     {
                         uint32_t co;
@@ -1511,7 +1528,7 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
                     }
                     int pos = 8 * (wb + HS + jee_bytes) + mb_off;
                     const int ng = FIX ? 4 : min(4, G - p0);
-                    if (!wide) {
+                    if (!ww) {
                         auto emit_groups = [&](auto SELC) {
                             constexpr int SL = decltype(SELC)::value;
                             int m1 = hq1, dprev = hq1 - hq2;
@@ -1571,7 +1588,7 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
                         }
                     }
                 }
-                if (tid == 0) {
+                if (!META && tid == 0) {
                     // block header (dtypes.py:156-165)
                     const int restart = (S->emitted == 0);
                     const int code = S->code;
@@ -1586,6 +1603,7 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
                 }
             }
 
+            }   // stream work (skipped by the fixed-quality chain)
             PROF_MARK(4);
             // ============ phase A of the next pass block (overlaps this block's tail) ============
             {
@@ -1620,7 +1638,7 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
                 }
                 S->a = att_to_a(S->att);
             }
-            if (emit) fence_proxy_async();  // window writes -> async proxy (bulk store)
+            if (emit && !META) fence_proxy_async();  // window writes -> async proxy (bulk store)
             cbar();  // B5
             PROF_MARK(5);
 
@@ -1628,7 +1646,7 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
             // Thread 32 owns the window bytes: bulk store, tail, offsets,
             // win_base / tail_len, and the store's read wait before the next
             // barrier; thread 0 goes straight on to the next block's S1.
-            if (emit && tid == 32) {
+            if (!META && emit && tid == 32) {
                 const int wb = S->tail_len;
                 const long long blen = S->blen;
                 const uint32_t* win = (const uint32_t*)xs;
@@ -1649,7 +1667,15 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
             if (emit && tid == 0) {
                 const long long blen = S->blen;
                 const int sel = S->gate ? 0 : S->sel_spec;
-                if (P.trace) {
+                if (META) {
+                    BlockMeta m;
+                    m.sq = S->sq; m.code = S->code; m.fbe = (short)S->fbe; m.wide = (short)S->wide;
+                    P.meta[b] = m;
+                    if (P.trace) {   // the packer adds selector, costs, bytes, restart
+                        double* tr = P.trace + 10 * b;
+                        tr[0] = S->att; tr[1] = S->a; tr[2] = S->code; tr[3] = S->fbe;
+                    }
+                } else if (P.trace) {
                     double* tr = P.trace + 10 * b;
                     tr[0] = S->att; tr[1] = S->a; tr[2] = S->code; tr[3] = S->fbe; tr[4] = sel;
                     tr[5] = (double)(4 * tt0 + 4LL * G); tr[6] = (double)(4 * tt1 + 4LL * G);
@@ -1669,6 +1695,10 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
 
         PROF_MARK(6);
         // ---------------- unit end: last tail, publish, hand to the placement warp ----------------
+        if (META) {
+            cbar();
+            continue;
+        }
         if (tid == 32) {
             if (S->store_pending) { bulk_wait_all(); S->store_pending = 0; }
             if (S->tail_len > 0) {
@@ -1801,6 +1831,47 @@ static int launch_v3_range(int dt, bool fix, const EncParams& P, long long u0, l
     note_launches(1);
     if (cudaLaunchCooperativeKernel(fn, dim3(g), dim3(pw ? v3::NT : v3::NCT), args, smem, st) != cudaSuccess)
         return APAX_ERR_CUDA;
+    return APAX_OK;
+}
+
+template <int DT, bool FIX>
+static void* v3_chain_fn() { return (void*)v3::encode_v3_kernel<DT, FIX, false, true>; }
+
+static void* v3_chain_kernel(int dt, bool fix) {
+    switch (dt) {
+        case 1: return fix ? v3_chain_fn<1, true>() : v3_chain_fn<1, false>();
+        case 2: return fix ? v3_chain_fn<2, true>() : v3_chain_fn<2, false>();
+        case 3: return fix ? v3_chain_fn<3, true>() : v3_chain_fn<3, false>();
+        default: return fix ? v3_chain_fn<4, true>() : v3_chain_fn<4, false>();
+    }
+}
+
+// the split encoder's chain over every unit: quantizer records only
+int launch_encode_v3_chain(int dt, const EncParams& P, size_t smem, cudaStream_t st) {
+    if (dt < 1 || dt > 4 || P.bs != v3::MAXBS || P.stage_bytes != v3::fix_stage_bytes(dt) || !P.meta)
+        return APAX_ERR_INTERNAL;
+    long long ufull = P.n_units;
+    if ((P.n % v3::MAXBS) != 0) ufull = P.n_units - 1;
+    for (int part = 0; part < 2; part++) {
+        const long long u0 = part ? ufull : 0, u1 = part ? P.n_units : ufull;
+        if (u1 <= u0) continue;
+        const void* fn = v3_chain_kernel(dt, part == 0);
+        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return APAX_ERR_CUDA;
+        int dev = 0, nsm = 0, per = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, v3::NCT, smem) != cudaSuccess || per < 1) per = 1;
+        const long long res = (long long)per * (nsm > 0 ? nsm : 148);
+        EncParams p = P;
+        p.unit_begin = u0;
+        p.unit_end = u1;
+        const long long g = (u1 - u0) < res ? (u1 - u0) : res;
+        note_launches(1);
+        void* args[] = {&p};
+        if (cudaLaunchKernel(fn, dim3((unsigned)g), dim3(v3::NCT), args, smem, st) != cudaSuccess)
+            return APAX_ERR_CUDA;
+    }
     return APAX_OK;
 }
 

@@ -7,6 +7,15 @@
 
 namespace apax {
 
+// per-block quantizer record of the split encoder: the chain writes it, the
+// packer (apax_encode_v4.cu) re-quantizes the block with it
+struct __align__(16) BlockMeta {
+    double sq;       // quantizer multiplier (codec.py:94-132: a_q for ints, the float scale S)
+    int code;        // 16-bit scale code
+    short fbe;       // float block exponent
+    short wide;      // max |q| > 2^30: 64-bit differences
+};
+
 struct EncParams {
     const void* x;
     long long n;
@@ -39,6 +48,7 @@ struct EncParams {
     // for integer containers, the dequantizer's clip range (codec.py:143-145)
     int wire;
     long long clip_lo, clip_hi;
+    BlockMeta* meta;              // split encoder: the chain's per-block records (v3 META)
 };
 
 struct DecParams {
@@ -80,6 +90,14 @@ bool encode_v3_supported(int dt, int bs);
 int encode_v3_resident_ctas(int dt, size_t smem);
 int encode_v3_resident_ctas_wave(int dt, size_t smem);
 int launch_encode_v3(int dt, const EncParams& P, int grid, size_t smem, cudaStream_t st);
+// split encoder: the chain (v3 with META: quantizer records, no output) and
+// the block-parallel packer (apax_encode_v4.cu)
+int launch_encode_v3_chain(int dt, const EncParams& P, size_t smem, cudaStream_t st);
+size_t encode_v4_smem_bytes(int dt);
+bool encode_v4_supported(int dt, int bs);
+int encode_v4_resident_ctas(int dt);
+int launch_encode_v4(int dt, const EncParams& P, const BlockMeta* meta, unsigned long long* costs,
+                     unsigned long long* lb, cudaStream_t st);
 int launch_decode(int dt, const DecParams& P, int grid, size_t smem, cudaStream_t st);
 size_t decode_v3_smem_bytes(int dt, int payload_cap);
 bool decode_v3_supported(int dt, int bs);

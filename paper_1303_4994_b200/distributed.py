@@ -296,42 +296,88 @@ def sharded_welch(x_local, y_local, dtype, which: int = 0, seg: int = 4096, grou
     """Welch power spectrum (profiler.py:61-74: Hann frames of `seg`, hop
     seg/2) of x (which 0), y (1) or d = x - y (2) split over ranks.  Every
     rank's shard must start on a hop boundary of the global array (all but
-    the last rank hold a multiple of seg/2 samples); rank r borrows the first
-    seg/2 samples of rank r+1 for the frames that straddle the boundary, so
-    the union of the ranks' frames is exactly the one-array frame set.  The
-    per-rank frame sums (seg/2 + 1 bins) and frame counts are all-gathered
-    and added in rank order.  Returns the power spectrum (numpy f64)."""
+    the last rank hold a multiple of seg/2 samples, at least seg/2).  A rank
+    sums the frames inside its shard straight from its own array; the one
+    frame that straddles its end is built from its last seg/2 samples and the
+    first seg/2 of rank r+1 (an all-gather of every rank's head), so the
+    union of the ranks' frames is exactly the one-array frame set.  Frame
+    sums (seg/2 + 1 bins) and frame counts are all-gathered and added in
+    rank order.  Collectives run on the GPU under NCCL, through host tensors
+    under gloo.  Returns the power spectrum (numpy f64)."""
     import torch
     import torch.distributed as dist
+    from .dtypes import Dtype
     from .profiler import _welch_frame_sums, _welch_scale
     world, rank = dist.get_world_size(group), dist.get_rank(group)
+    dev = x_local.device if dist.get_backend(group) == "nccl" else None
     hop = seg // 2
     n_local = int(x_local.numel())
-    if rank < world - 1 and n_local % hop:
-        raise ValueError("sharded_welch: every shard but the last must hold a multiple of seg/2 samples")
-    # heads (hop samples of x and y) of every rank, through host tensors
+    if rank < world - 1 and (n_local % hop or n_local < hop):
+        raise ValueError("sharded_welch: every shard but the last must hold a non-zero multiple of seg/2 samples")
+    cdev = dev if dev is not None else torch.device("cpu")
+
     def _head(t):
-        h = torch.zeros(hop, dtype=torch.float64)
+        h = torch.zeros(hop, dtype=torch.float64, device=cdev)
         k = min(hop, n_local)
-        h[:k] = t[:k].double().cpu()
+        if t is not None and k:
+            h[:k] = t[:k].to(device=cdev, dtype=torch.float64)
         return h
-    hx = _head(x_local)
-    hy = _head(y_local) if y_local is not None else torch.zeros(hop, dtype=torch.float64)
-    gx = torch.empty(world * hop, dtype=torch.float64)
-    gy = torch.empty(world * hop, dtype=torch.float64)
+    hx, hy = _head(x_local), _head(y_local)
+    gx = torch.empty(world * hop, dtype=torch.float64, device=cdev)
+    gy = torch.empty(world * hop, dtype=torch.float64, device=cdev)
     dist.all_gather_into_tensor(gx, hx, group=group)
     dist.all_gather_into_tensor(gy, hy, group=group)
-    xe, ye = x_local.double(), (y_local.double() if y_local is not None else None)
-    if rank < world - 1:
-        xe = torch.cat([xe, gx[(rank + 1) * hop:(rank + 2) * hop].to(xe.device)])
-        if ye is not None:
-            ye = torch.cat([ye, gy[(rank + 1) * hop:(rank + 2) * hop].to(ye.device)])
-    ne = int(xe.numel())
-    from .dtypes import Dtype
-    if ne >= seg:
-        tot, nf = _welch_frame_sums(xe.contiguous(), ye.contiguous() if ye is not None else None, Dtype.F64,
-                                    which, ne, seg)
-    else:
-        tot, nf = np.zeros(hop + 1), 0
-    parts = merge_sums(list(tot) + [float(nf)], group, None)
+    nb = hop + 1
+    tot, nf = np.zeros(nb), 0
+    if n_local >= seg:   # frames inside the shard, read in the shard's own dtype
+        t, k = _welch_frame_sums(x_local, y_local, dtype, which, n_local, seg)
+        tot, nf = tot + t, nf + k
+    if rank < world - 1:  # the frame across the boundary with rank r + 1
+        xs = x_local.device
+        bx = torch.cat([x_local[n_local - hop:].double(), gx[(rank + 1) * hop:(rank + 2) * hop].to(xs)])
+        by = (torch.cat([y_local[n_local - hop:].double(), gy[(rank + 1) * hop:(rank + 2) * hop].to(xs)])
+              if y_local is not None else None)
+        t, k = _welch_frame_sums(bx.contiguous(), by.contiguous() if by is not None else None, Dtype.F64,
+                                 which, seg, seg)
+        tot, nf = tot + t, nf + k
+    parts = merge_sums(list(tot) + [float(nf)], group, dev)
     return _welch_scale(parts[:-1], int(parts[-1]), seg)
+
+
+# ---------------------------------------------------------------------------
+# one array sharded by segment ranges (BASELINE cfg4): codec + global
+# profiler statistics
+# ---------------------------------------------------------------------------
+def sharded_round_trip(x_local, config, group=None, stats: bool = True, welch_seg: int = 4096) -> dict:
+    """This rank's contiguous segment range of ONE array (x_local, CUDA
+    tensor of the config dtype, starting on a segment boundary): encode the
+    range on this GPU, place its body in the concatenated container (the
+    all-gather of body lengths + exclusive scan), decode the body, and --
+    with `stats` -- the global profiler statistics of (x, y = decode) over
+    all ranks: moments, pearson r, SRR and the exact S2R margin
+    (sharded_window_stats) and the Welch spectra of x and d
+    (sharded_welch).  Returns a dict with the placement, this rank's body
+    length, decoded range and the statistics."""
+    from .codec import Decoder, Encoder
+    if not config.segment_blocks:
+        raise ValueError("sharded_round_trip needs a segmented StreamConfig")
+    n_local = int(x_local.numel())
+    enc = Encoder(n_local, config, device=x_local.device)
+    enc.encode(x_local)
+    nbytes = enc.finish()
+    place = place_bodies(nbytes - FILE_HEADER_SIZE, group, x_local.device
+                         if _backend(group) == "nccl" else None)
+    dec = Decoder(n_local, config.dtype, config.block_size, device=x_local.device)
+    dec.decode(enc.out, nbytes, enc.offsets, segment_blocks=config.segment_blocks)
+    y = dec.finish()
+    out = {"placement": place, "body_len": nbytes - FILE_HEADER_SIZE, "y": y, "encoder": enc}
+    if stats:
+        out["window"] = sharded_window_stats(x_local, y, config.dtype, group)
+        out["welch_x"] = sharded_welch(x_local, y, config.dtype, 0, welch_seg, group)
+        out["welch_d"] = sharded_welch(x_local, y, config.dtype, 2, welch_seg, group)
+    return out
+
+
+def _backend(group=None) -> str:
+    import torch.distributed as dist
+    return dist.get_backend(group)

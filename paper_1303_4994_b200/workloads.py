@@ -69,7 +69,8 @@ def cfg3_grf_f32(side: int = 8192, seed: int = 3) -> np.ndarray:
     return img.astype(np.float32).reshape(-1)
 
 
-def cfg4_modes_f64(side: int = 1024, seed: int = 4, n_modes: int = 64, device=None, planes=None):
+def cfg4_modes_f64(side: int = 1024, seed: int = 4, n_modes: int = 64, device=None, planes=None,
+                   z0: int = 0):
     """float64 side^3 field: 64 modes A cos(2 pi k.r/side + phi), A ~ N(0,1),
     k in [-8, 8]^3, phi ~ U(0, 2 pi), plus N(0, sigma=1e-4) (read as sigma).
 
@@ -77,9 +78,11 @@ def cfg4_modes_f64(side: int = 1024, seed: int = 4, n_modes: int = 64, device=No
     x term and b the (y, z) terms), so the full 8 GiB field is generated on
     the GPU in milliseconds: returns a flat torch f64 tensor on `device`
     (default cuda:0 when available, else CPU).  Mode parameters are
-    numpy-seeded; the noise comes from a seeded torch generator on the same
-    device, so the field is reproducible per device type.  `planes` limits
-    the field to its first z planes (a slab; the CPU reference arm)."""
+    numpy-seeded; the noise comes in chunks of 2^26 samples, chunk c from a
+    torch generator seeded (seed, c) on the same device, so the field is
+    reproducible per device type and any slab can be generated on its own:
+    `z0` / `planes` give the z planes [z0, z0 + planes) of the one field (a
+    rank's shard of a sharded array, the CPU reference arm's sample)."""
     import torch
     if device is None:
         device = "cuda" if torch.cuda.is_available() else "cpu"
@@ -92,23 +95,27 @@ def cfg4_modes_f64(side: int = 1024, seed: int = 4, n_modes: int = 64, device=No
     ax = K[:, 0, None] * r[None, :] + phi[:, None]                     # [m, x]
     C = torch.cat([torch.cos(ax), -torch.sin(ax)], 0)                 # [2m, x]
     del ax
-    nz = side if planes is None else int(planes)
+    z0 = int(z0)
+    nz = (side - z0) if planes is None else min(int(planes), side - z0)
     out = torch.empty(nz * side, side, dtype=torch.float64, device=dev)
     zc = max(1, min(nz, (1 << 26) // (side * side) or 1))            # z planes per GEMM chunk
-    for z0 in range(0, nz, zc):
-        z1 = min(nz, z0 + zc)
+    for za in range(0, nz, zc):
+        zb = min(nz, za + zc)
         byz = (K[None, None, :, 1] * r[None, :, None] +
-               K[None, None, :, 2] * r[z0:z1, None, None])            # [z, y, m]
+               K[None, None, :, 2] * r[z0 + za:z0 + zb, None, None])  # [z, y, m]
         B = torch.cat([A * torch.cos(byz), A * torch.sin(byz)], -1)   # [z, y, 2m]
-        out[z0 * side:z1 * side] = B.reshape(-1, 2 * n_modes) @ C
+        out[za * side:zb * side] = B.reshape(-1, 2 * n_modes) @ C
         del byz, B
-    g = torch.Generator(device=dev)
-    g.manual_seed(seed)
     flat = out.reshape(-1)
     chunk = 1 << 26
-    for i in range(0, flat.numel(), chunk):
-        seg = flat[i:i + chunk]
-        seg += torch.randn(seg.numel(), dtype=torch.float64, device=dev, generator=g) * 1e-4
+    g0, g1 = z0 * side * side, (z0 + nz) * side * side                # global sample range
+    g = torch.Generator(device=dev)
+    for c in range(g0 // chunk, (g1 + chunk - 1) // chunk):
+        a, b = max(g0, c * chunk), min(g1, (c + 1) * chunk)
+        g.manual_seed(seed * 1000003 + c)
+        noise = torch.randn(min(chunk, side ** 3 - c * chunk), dtype=torch.float64, device=dev, generator=g)
+        flat[a - g0:b - g0] += noise[a - c * chunk:b - c * chunk] * 1e-4
+        del noise
     return flat
 
 

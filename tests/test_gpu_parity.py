@@ -342,7 +342,8 @@ def test_cast_random_vs_oracle(seed):
         else:
             dt = DT[str(rng.choice(["i8", "i16", "i32"]))]
             info = np.iinfo(dt.np_dtype)
-            x = (np.cumsum(rng.standard_normal(n)) * float(info.max) * rng.uniform(0.01, 0.3)).astype(np.int64)
+            x = np.clip(np.cumsum(rng.standard_normal(n)) * float(info.max) * rng.uniform(0.01, 0.3),
+                        -2.0 ** 32, 2.0 ** 32).astype(np.int64)
             mode = Mode(int(rng.integers(0, 3)))
         T = {Mode.LOSSLESS: 0.0, Mode.FIXED_RATE: float(rng.uniform(2, 12)),
              Mode.FIXED_QUALITY: float(rng.uniform(20, 90))}[mode]
