@@ -313,7 +313,13 @@ int apax_encode(const void* x, int64_t n, int dtype, int mode, double target, in
         if (cudaMemsetAsync(costs, 0, (size_t)p.n_blocks * 16 + 8, s) != cudaSuccess) return APAX_ERR_CUDA;
         if (mode != APAX_LOSSLESS) {
             P.meta = meta;
-            int r = launch_encode_v3_chain(dtype, P, p.smem, s);
+            // whole stream: the latency-optimised one-CTA chain (apax_encode_ws.cu);
+            // segments: the v3 kernel as a chain, one CTA per segment
+            // (fixed quality: the v3 chain measured faster, tools/time_encode.py)
+            const int wse = env_int("APAX_WS_CHAIN", -1);
+            const bool wsc = segment_blocks <= 0 && encode_ws_supported(dtype, block_size) &&
+                             (wse == 1 || (wse < 0 && mode == APAX_FIXED_RATE));
+            int r = wsc ? launch_encode_ws_chain(dtype, P, s) : launch_encode_v3_chain(dtype, P, p.smem, s);
             if (r) return r;
         }
         EncParams Q = P;

@@ -96,6 +96,9 @@ int launch_encode_v3_chain(int dt, const EncParams& P, size_t smem, cudaStream_t
 size_t encode_v4_smem_bytes(int dt);
 bool encode_v4_supported(int dt, int bs);
 int encode_v4_resident_ctas(int dt);
+bool encode_ws_supported(int dt, int bs);
+size_t encode_ws_smem_bytes(int dt, int mode);
+int launch_encode_ws_chain(int dt, const EncParams& P, cudaStream_t st);
 int launch_encode_v4(int dt, const EncParams& P, const BlockMeta* meta, unsigned long long* costs,
                      unsigned long long* lb, cudaStream_t st);
 int launch_decode(int dt, const DecParams& P, int grid, size_t smem, cudaStream_t st);
