@@ -1009,6 +1009,10 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
                     }
                 }
                 S->code = code; S->fbe = fbe; S->s = s; S->aq = aq;
+                if (emit && P.trace) {   // the attenuation in force for this block
+                    double* tr = P.trace + 10 * b;
+                    tr[0] = S->att; tr[1] = a; tr[2] = code; tr[3] = fbe;
+                }
                 S->rs = F ? __ddiv_rn(1.0, s) : 1.0;
                 S->ra = (!F && aq != 1.0) ? __ddiv_rn(1.0, aq) : 1.0;
                 S->sq = F ? (zero ? 0.0 : s) : aq;      // quantizer multiplier
@@ -1670,14 +1674,10 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
                 if (META) {
                     BlockMeta m;
                     m.sq = S->sq; m.code = S->code; m.fbe = (short)S->fbe; m.wide = (short)S->wide;
-                    P.meta[b] = m;
-                    if (P.trace) {   // the packer adds selector, costs, bytes, restart
-                        double* tr = P.trace + 10 * b;
-                        tr[0] = S->att; tr[1] = S->a; tr[2] = S->code; tr[3] = S->fbe;
-                    }
+                    P.meta[b] = m;   // (trace: S1 wrote the gain, the packer adds the rest)
                 } else if (P.trace) {
                     double* tr = P.trace + 10 * b;
-                    tr[0] = S->att; tr[1] = S->a; tr[2] = S->code; tr[3] = S->fbe; tr[4] = sel;
+                    tr[4] = sel;
                     tr[5] = (double)(4 * tt0 + 4LL * G); tr[6] = (double)(4 * tt1 + 4LL * G);
                     tr[7] = (double)(4 * tt2 + 4LL * G); tr[8] = (double)blen;
                     tr[9] = (S->emitted == 0);

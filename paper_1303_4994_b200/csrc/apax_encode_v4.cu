@@ -464,6 +464,7 @@ __global__ void __launch_bounds__(NT, 4) pack_kernel(EncParams P, const BlockMet
             if (S->bad) report_error(P.status, b, S->bad);
             if (P.trace) {
                 double* tr = P.trace + 10 * b;
+                if (!meta) { tr[0] = 0.0; tr[1] = 1.0; tr[2] = kScaleCodeOne; tr[3] = 0.0; }   // LOSSLESS: gain 1
                 tr[4] = sel;
                 tr[5] = (double)(4LL * tt0 + 4LL * G); tr[6] = (double)(4LL * tt1 + 4LL * G);
                 tr[7] = (double)(4LL * tt2 + 4LL * G);

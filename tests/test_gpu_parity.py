@@ -351,3 +351,43 @@ def test_cast_random_vs_oracle(seed):
         ref = O.encode(x, dt.wire_code, mode.value, T, bs)[0]
         assert encode_stream(x, cfg) == ref, (n, bs, dt, mode, T)
         assert np.array_equal(decode_stream(ref), O.decode(ref))
+
+
+# ---------------------------------------------------------------------------
+# per-block traces against the reference stepping encode_block: scale code,
+# block exponent, selector, costs, bytes and restart exact; the attenuation
+# within 1e-9 dB and its gain within 1e-12 relative (the device's exp10 /
+# log10 vs glibc's pow / log10)
+# ---------------------------------------------------------------------------
+def _trace_names():
+    from trace_cases import traces
+    return [t["name"] for t in traces()]
+
+
+@pytest.mark.parametrize("name", _trace_names())
+def test_trace_vs_reference(name):
+    from trace_cases import trace_input, traces
+    t = next(t for t in traces() if t["name"] == name)
+    x = torch.from_numpy(trace_input(t)).cuda()
+    cfg = StreamConfig(DT[t["dtype"]], 4096, Mode(t["mode"]), float.fromhex(t["target_hex"]),
+                       segment_blocks=t["segment_blocks"] or None)
+    res = encode_device(x, cfg, trace=True)
+    tr = res.trace.cpu().numpy()
+    ref = np.array(t["rows"], dtype=np.float64)
+    assert tr.shape == ref.shape
+    assert np.array_equal(tr[:, 2:], ref[:, 2:]), (name, np.argwhere(tr[:, 2:] != ref[:, 2:])[:5])
+    assert np.allclose(tr[:, 0], ref[:, 0], rtol=0, atol=1e-9), name
+    assert np.allclose(tr[:, 1], ref[:, 1], rtol=1e-12, atol=0), name
+
+
+def test_floor_log2_quirk_containers():
+    """glibc's floor(math.log2(s_des)) rounds up just below 2^32 and 2^-31:
+    the device reproduces the reference's (code, fbe) and container."""
+    for m in json.loads((GOLDEN / "quirk_manifest.json").read_text()):
+        c = load_container(GOLDEN / "containers" / f"{m['name']}.npz")
+        cfg = StreamConfig(DT[m["dtype"]], m["block_size"], Mode(m["mode"]), float.fromhex(m["target_hex"]))
+        res = encode_device(torch.from_numpy(c["x"]).cuda(), cfg, trace=True)
+        assert res.to_bytes() == c["blob"], m["name"]
+        tr = res.trace.cpu().numpy()
+        assert (int(tr[0][2]), int(tr[0][3])) == (m["first_block"]["code"], m["first_block"]["fbe"])
+        assert np.array_equal(decode_stream(c["blob"]), c["y"])

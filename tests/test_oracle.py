@@ -233,3 +233,38 @@ def test_reference_cast_routing():
     x = np.array([1.5, -2.7, 3e9])
     xw, kind = _reference_cast(x, Dtype.I32)
     assert kind == _IN_INT64 and xw.tolist() == [1, -2, 3000000000]
+
+
+# ---------------------------------------------------------------------------
+# per-block traces (attenuation, code, block exponent, selector, costs,
+# bytes, restart) against the reference stepping encode_block
+# (tests/golden/make_trace_golden.py); the oracle calls the same glibc
+# pow/log10 as the reference's CPython, so even att_db is exact
+# ---------------------------------------------------------------------------
+def _trace_names():
+    from trace_cases import traces
+    return [t["name"] for t in traces()]
+
+
+@pytest.mark.parametrize("name", _trace_names())
+def test_oracle_trace_vs_reference(name):
+    from trace_cases import trace_input, traces
+    t = next(t for t in traces() if t["name"] == name)
+    x = trace_input(t)
+    _, _, tr = O.encode(x, O.DTYPE_CODES[t["dtype"]], t["mode"], float.fromhex(t["target_hex"]), 4096,
+                        segment_blocks=t["segment_blocks"], trace=True)
+    ref = np.array(t["rows"], dtype=np.float64)
+    assert tr.shape == ref.shape
+    assert np.array_equal(tr, ref), (name, np.argwhere(tr != ref)[:5])
+
+
+def test_oracle_floor_log2_quirk_containers():
+    """glibc's floor(math.log2(s_des)) at the two boundaries where it changes
+    the container (codec.py:120-122)."""
+    for m in json.loads((GOLDEN / "quirk_manifest.json").read_text()):
+        c = load_container(GOLDEN / "containers" / f"{m['name']}.npz")
+        blob, _, tr = O.encode(c["x"], O.DTYPE_CODES[m["dtype"]], m["mode"], float.fromhex(m["target_hex"]),
+                               m["block_size"], trace=True)
+        assert blob == c["blob"], m["name"]
+        assert (int(tr[0][2]), int(tr[0][3])) == (m["first_block"]["code"], m["first_block"]["fbe"])
+        assert np.array_equal(O.decode(c["blob"]), c["y"])
