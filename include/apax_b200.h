@@ -41,6 +41,20 @@ enum { APAX_I8 = 0, APAX_I16 = 1, APAX_I32 = 2, APAX_F32 = 3, APAX_F64 = 4 };
 enum { APAX_LOSSLESS = 0, APAX_FIXED_RATE = 1, APAX_FIXED_QUALITY = 2 };
 enum { APAX_POLICY_COLD = 0, APAX_POLICY_WARM_SELF = 1 };
 
+/* The reference's per-stream encoder state (CodecState, codec.py:66-82):
+ * attenuation, derivative history, the previous block's stream costs
+ * (StreamCosts: 4*sum(e) + 4*groups per stream), blocks emitted, and
+ * whether the fixed-quality gain was initialised.  apax_encode_block reads
+ * it and writes the state after the block back. */
+typedef struct {
+    double att_db;
+    int64_t prev1, prev2;
+    int64_t costs[3];
+    int32_t has_costs;
+    int32_t initialized;
+    int64_t blocks_emitted;
+} apax_block_state;
+
 /* Library version string. */
 const char* apax_version(void);
 
@@ -151,6 +165,27 @@ int64_t apax_encode_cast_workspace_bytes(int64_t n, int in_kind, int dtype, int 
 int apax_encode_cast(const void* x, int in_kind, int64_t n, int dtype, int mode, double target, int block_size,
                      int64_t segment_blocks, int policy, uint8_t* out, int64_t out_cap, int64_t* block_offsets,
                      uint64_t* status, void* ws, int64_t ws_bytes, void* stream);
+
+/* ---- the reference's lower-level block API (codec.py:94-255) ----
+ * quantize_block: x (device) holds n samples widened as the reference does
+ * (float64 for float dtypes, int64 for integer ones); q (device, int64[n])
+ * receives the quantized block, hdr (device, int32[2]) the scale code and the
+ * float block exponent.  Errors (non-finite input, s_des overflow) land in
+ * status as block 0.  One CTA. */
+int apax_quantize_block(const void* x, int64_t n, int dtype, double a, int64_t* q, int32_t* hdr,
+                        uint64_t* status, void* stream);
+/* dequantize_block: y (device, n samples of dtype) = the decoder's dual of
+ * q under (scale code, float block exponent). */
+int apax_dequantize_block(const int64_t* q, int64_t n, int dtype, int code, int fbe, void* y, void* stream);
+/* encode_block: one block of n <= block_size samples (widened as above)
+ * under the state at *state (device), which receives the state after the
+ * block; out (device) receives the 28-byte file header, the block header and
+ * payload (status[2] = total bytes).  Workspace:
+ * apax_encode_cast_workspace_bytes(block_size, in_kind, dtype, mode,
+ * block_size, 0). */
+int apax_encode_block(const void* x, int64_t n, int dtype, int mode, double target, int block_size,
+                      apax_block_state* state, uint8_t* out, int64_t out_cap, uint64_t* status, void* ws,
+                      int64_t ws_bytes, void* stream);
 
 /* Device workspace needed by apax_decode (with offsets == NULL it includes
  * room for the block walk's offset table). */

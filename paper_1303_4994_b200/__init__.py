@@ -13,12 +13,16 @@ from .codec import (Decoder, EncodedStream, Encoder, decode_device, decode_range
                     wave_segment_blocks)
 from .dtypes import BlockHeader, Dtype, Mode, StreamConfig, decode_scale_code, encode_scale_code
 from . import errors
+from .block import (AttenuatorState, CodecState, DerivativeHistory, RateLoopState, StreamCosts, dequantize_block,
+                    encode_block, quality_loop_update, quantize_block, rate_loop_update)
 from .profiler import ProfileSession, profile
 
 __all__ = [
     "Dtype", "Mode", "StreamConfig", "BlockHeader", "encode_stream", "decode_stream",
     "parse_file_header", "encode_device", "decode_device", "decode_range", "encode_lossless_range", "Encoder", "Decoder",
     "EncodedStream", "max_encoded_bytes", "wave_segment_blocks", "profile", "ProfileSession", "encode_scale_code", "decode_scale_code", "errors",
+    "AttenuatorState", "CodecState", "DerivativeHistory", "RateLoopState", "StreamCosts", "quantize_block",
+    "dequantize_block", "encode_block", "rate_loop_update", "quality_loop_update",
 ]
 
-__version__ = "0.1.0"
+__version__ = "0.2.0"

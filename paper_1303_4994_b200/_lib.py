@@ -84,6 +84,12 @@ def lib():
     L.apax_encode_cast_workspace_bytes.restype = I64
     L.apax_encode_cast.argtypes = [P, I32, I64, I32, I32, D, I32, I64, I32, P, I64, P, P, P, I64, P]
     L.apax_encode_cast.restype = I32
+    L.apax_quantize_block.argtypes = [P, I64, I32, D, P, P, P, P]
+    L.apax_quantize_block.restype = I32
+    L.apax_dequantize_block.argtypes = [P, I64, I32, I32, I32, P, P]
+    L.apax_dequantize_block.restype = I32
+    L.apax_encode_block.argtypes = [P, I64, I32, I32, D, I32, P, P, I64, P, P, I64, P]
+    L.apax_encode_block.restype = I32
     L.apax_find_blocks.argtypes = [P, I64, I64, I32, I32, P, P, P]
     L.apax_find_blocks.restype = I32
     L.apax_parse_file_header.argtypes = [P, I64, P, P, P, P, P, P]
@@ -100,5 +106,6 @@ EXPORTED_SYMBOLS = (
     "apax_encode_wave_segment_blocks", "apax_profile_grid", "apax_profile_sums", "apax_profile_welch",
     "apax_profile_select", "apax_decode_range", "apax_status_to_host",
     "apax_encode_lossless_range", "apax_detect_segments",
-    "apax_max_encoded_bytes_cast", "apax_launch_count", "apax_encode_cast_workspace_bytes", "apax_encode_cast",
+    "apax_max_encoded_bytes_cast", "apax_launch_count", "apax_quantize_block", "apax_dequantize_block",
+    "apax_encode_block", "apax_encode_cast_workspace_bytes", "apax_encode_cast",
 )

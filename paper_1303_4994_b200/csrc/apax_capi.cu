@@ -411,6 +411,67 @@ int apax_encode_cast(const void* x, int in_kind, int64_t n, int dtype, int mode,
     return launch_encode(kdt, P, p.grid, p.smem, s);
 }
 
+int apax_encode_block(const void* x, int64_t n, int dtype, int mode, double target, int block_size,
+                      apax_block_state* state, uint8_t* out, int64_t out_cap, uint64_t* status, void* ws,
+                      int64_t ws_bytes, void* stream) {
+    // the reference's encode_block (codec.py:192-255): one block under the
+    // caller's CodecState, on the generic kernel (x widened: f64 / i64)
+    if (!state || n < 1 || n > block_size) return APAX_ERR_ARG;
+    const int in_kind = dtype >= APAX_F32 ? APAX_IN_FLOAT64 : APAX_IN_INT64;
+    const int kdt = dtype == APAX_F64 ? APAX_F64 : kdt_of_cast(in_kind, dtype);
+    if (kdt < 0) return APAX_ERR_ARG;
+    EncPlan p;
+    int st = plan_encode(n, kdt, mode, block_size, 0, &p);
+    if (st) return st;
+    if (mode == APAX_LOSSLESS && dtype >= APAX_F32) return APAX_ERR_CFG_LOSSLESS_FLOAT;
+    if (mode == APAX_FIXED_RATE && !(target > 0)) return APAX_ERR_CFG_FR_TARGET;
+    if (!x || !out || !status || (p.ws_total > 0 && !ws)) return APAX_ERR_ARG;
+    if (out_cap < kFileHeader + max_block_bytes(kdt, block_size)) return APAX_ERR_CAPACITY;
+    if (ws_bytes < p.ws_total) return APAX_ERR_WORKSPACE;
+    // the generic kernel: force it (v3 has no state input)
+    p.v3 = 0;
+    {
+        long long want = 48 * 1024;
+        long long mbb = max_block_bytes(kdt, block_size);
+        long long stb = want > mbb + 64 ? want : mbb + 64;
+        p.stage_bytes = (int)((stb + 15) & ~15LL);
+        p.x_in_smem = 1;
+        p.smem = encode_smem_bytes(kdt, block_size, p.stage_bytes, 1);
+        p.grid = 1;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    uint8_t* w = (uint8_t*)ws;
+    if (cudaMemsetAsync(status, 0xFF, 4 * sizeof(uint64_t), s) != cudaSuccess) return APAX_ERR_CUDA;
+    if (cudaMemsetAsync(w, 0, (size_t)p.ws_slots, s) != cudaSuccess) return APAX_ERR_CUDA;
+    EncParams P;
+    memset(&P, 0, sizeof(P));
+    P.x = x;
+    P.n = n;
+    P.mode = mode;
+    P.bs = block_size;
+    P.target = target;
+    P.n_blocks = 1;
+    P.unit_blocks = 1;
+    P.n_units = 1;
+    P.out = out;
+    P.out_cap = out_cap;
+    P.status = (unsigned long long*)status;
+    P.lookback = (unsigned long long*)(w + p.ws_lookback);
+    P.ticket = (unsigned int*)(w + p.ws_ticket);
+    P.slots = w + p.ws_slots;
+    P.slot_bytes = p.slot_bytes;
+    P.stage_bytes = p.stage_bytes;
+    P.x_in_smem = p.x_in_smem;
+    P.att_lo = 20.0 * log10(ldexp(1.0, -31));
+    P.pow10_t20 = pow(10.0, target / 20.0);
+    P.sqrt12 = sqrt(12.0);
+    P.wire = dtype;
+    P.clip_lo = dtype == APAX_I8 ? -128LL : (dtype == APAX_I16 ? -32768LL : -2147483648LL);
+    P.clip_hi = dtype == APAX_I8 ? 127LL : (dtype == APAX_I16 ? 32767LL : 2147483647LL);
+    P.state = state;
+    return launch_encode(kdt, P, 1, p.smem, s);
+}
+
 int apax_encode_lossless_range(const void* x, int64_t halo, int64_t n, int dtype, int block_size,
                                int64_t first_block, uint8_t* out, int64_t out_cap, int64_t* block_offsets,
                                uint64_t* status, void* ws, int64_t ws_bytes, void* stream) {

@@ -351,6 +351,14 @@ __global__ void __launch_bounds__(kNT) encode_kernel(EncParams P) {
             S->emitted = 0; S->staged = 0; S->win_base = 0; S->unit_len = 0;
             S->direct = (u == 0);
             S->prefix = 0;
+            if (P.state) {   // encode_block: the caller's CodecState (codec.py:66-82)
+                const apax_block_state* cs = P.state;
+                S->att = cs->att_db; S->p1 = cs->prev1; S->p2 = cs->prev2;
+                S->has_pc = cs->has_costs;
+                S->pc[0] = cs->costs[0]; S->pc[1] = cs->costs[1]; S->pc[2] = cs->costs[2];
+                S->initialized = cs->initialized;
+                S->emitted = cs->blocks_emitted;
+            }
         }
         __syncthreads();
 
@@ -903,6 +911,14 @@ __global__ void __launch_bounds__(kNT) encode_kernel(EncParams P) {
             __syncthreads();
         }
 
+        if (P.state && tid == 0) {   // the state after the block
+            apax_block_state* cs = P.state;
+            cs->att_db = S->att; cs->prev1 = S->p1; cs->prev2 = S->p2;
+            cs->has_costs = S->has_pc;
+            cs->costs[0] = S->pc[0]; cs->costs[1] = S->pc[1]; cs->costs[2] = S->pc[2];
+            cs->initialized = S->initialized;
+            cs->blocks_emitted = S->emitted;
+        }
         // ---------------- placement: decoupled look-back ----------------
         if (tid < 32) {
             const long long L = S->unit_len;

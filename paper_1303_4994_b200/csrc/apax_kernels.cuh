@@ -5,6 +5,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "../../include/apax_b200.h"
+
 namespace apax {
 
 // per-block quantizer record of the split encoder: the chain writes it, the
@@ -49,6 +51,7 @@ struct EncParams {
     int wire;
     long long clip_lo, clip_hi;
     BlockMeta* meta;              // split encoder: the chain's per-block records (v3 META)
+    apax_block_state* state;      // generic kernel, one unit: CodecState in / out (encode_block)
 };
 
 struct DecParams {
