@@ -187,6 +187,17 @@ int apax_encode_block(const void* x, int64_t n, int dtype, int mode, double targ
                       apax_block_state* state, uint8_t* out, int64_t out_cap, uint64_t* status, void* ws,
                       int64_t ws_bytes, void* stream);
 
+/* The profiler's output-free sweep point (rate_correlation_sweep,
+ * profiler.py:176-199): a whole-stream fixed-quality encode of x at
+ * `target` that writes no container -- status[2] receives the container's
+ * length and stats[3b .. 3b+2] block b's (sum x^2, sum x*y, sum y*y) with y
+ * the decode of x (the encoder's own dequantized block, bit-identical to
+ * the decoder's).  Block size 4096, dtype
+ * i16/i32/f32/f64, x 16-byte aligned; stats holds 3 * n_blocks doubles. */
+int64_t apax_sweep_point_workspace_bytes(int64_t n, int dtype);
+int apax_sweep_point(const void* x, int64_t n, int dtype, double target, double* stats, uint64_t* status, void* ws,
+                     int64_t ws_bytes, void* stream);
+
 /* Device workspace needed by apax_decode (with offsets == NULL it includes
  * room for the block walk's offset table). */
 int64_t apax_decode_workspace_bytes(int64_t n, int dtype, int block_size);
@@ -250,14 +261,16 @@ int apax_profile_sums(const void* x, const void* y, int64_t n, int dtype, int pa
 int apax_profile_welch(const void* x, const void* y, int64_t n, int dtype, int which, int seg,
                        const double* tables, double* partials, void* stream);
 
-/* One pass of the radix multi-select over the per-sample ratio keys
+/* One pass of the 4-pass radix multi-select over the per-sample ratio keys
  * (s2r_distribution :105-124): key = bits of |x| / |d| (d == 0: +inf,
- * x == 0 != d: 0), d = x - y when y_is_output, else y itself is d.
- * Pass p (0..15) counts the 4-bit digit p (most significant first) of
- * every key whose higher 4p bits equal one of the sorted, unique
- * `prefixes`: hist[j*16 + digit] (caller zeroes hist). */
+ * x == 0 != d: 0; the sign bit is 0), d = x - y when y_is_output, else y
+ * itself is d.  Digits, most significant first: pass 0 bits 62..48 (15
+ * bits, hist[digit], 2^15 uint32, prefixes unused), passes 1..3 bits
+ * 47..32, 31..16, 15..0 of the keys whose higher bits equal one of the
+ * sorted, unique `prefixes`: hist[j * 65536 + digit].  The caller zeroes
+ * hist; n < 2^32. */
 int apax_profile_select(const void* x, const void* y, int64_t n, int dtype, int pass, const uint64_t* prefixes,
-                        int n_prefixes, uint64_t* hist, int y_is_output, void* stream);
+                        int n_prefixes, uint32_t* hist, int y_is_output, void* stream);
 
 /* Host-side parse of the 28-byte file header (host pointer).  Returns an
  * apax_status code; *detail carries the offending value for messages. */

@@ -90,6 +90,10 @@ def lib():
     L.apax_dequantize_block.restype = I32
     L.apax_encode_block.argtypes = [P, I64, I32, I32, D, I32, P, P, I64, P, P, I64, P]
     L.apax_encode_block.restype = I32
+    L.apax_sweep_point_workspace_bytes.argtypes = [I64, I32]
+    L.apax_sweep_point_workspace_bytes.restype = I64
+    L.apax_sweep_point.argtypes = [P, I64, I32, D, P, P, P, I64, P]
+    L.apax_sweep_point.restype = I32
     L.apax_find_blocks.argtypes = [P, I64, I64, I32, I32, P, P, P]
     L.apax_find_blocks.restype = I32
     L.apax_parse_file_header.argtypes = [P, I64, P, P, P, P, P, P]
@@ -107,5 +111,5 @@ EXPORTED_SYMBOLS = (
     "apax_profile_select", "apax_decode_range", "apax_status_to_host",
     "apax_encode_lossless_range", "apax_detect_segments",
     "apax_max_encoded_bytes_cast", "apax_launch_count", "apax_quantize_block", "apax_dequantize_block",
-    "apax_encode_block", "apax_encode_cast_workspace_bytes", "apax_encode_cast",
+    "apax_encode_block", "apax_sweep_point", "apax_sweep_point_workspace_bytes", "apax_encode_cast_workspace_bytes", "apax_encode_cast",
 )

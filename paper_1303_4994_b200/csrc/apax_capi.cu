@@ -472,6 +472,59 @@ int apax_encode_block(const void* x, int64_t n, int dtype, int mode, double targ
     return launch_encode(kdt, P, 1, p.smem, s);
 }
 
+int64_t apax_sweep_point_workspace_bytes(int64_t n, int dtype) {
+    if (n < 1 || !encode_v4_supported(dtype, 4096)) return -1;
+    const int64_t nb = (n + 4095) / 4096;
+    return nb * (16 + 8 + 8 + 24) + 512;
+}
+
+int apax_sweep_point(const void* x, int64_t n, int dtype, double target, double* stats, uint64_t* status, void* ws,
+                     int64_t ws_bytes, void* stream) {
+    // rate_correlation_sweep's point (profiler.py:176-199) without the
+    // container: the chain with per-block (x, y) sums, then the packer
+    // counting bytes only (whole-stream fixed quality, bs 4096)
+    const int64_t need = apax_sweep_point_workspace_bytes(n, dtype);
+    if (need < 0 || !x || !stats || !status || !ws || ws_bytes < need || (((uintptr_t)x) & 15)) return APAX_ERR_ARG;
+    EncPlan p;
+    int st = plan_encode(n, dtype, APAX_FIXED_QUALITY, 4096, 0, &p);
+    if (st) return st;
+    if (!p.v3) return APAX_ERR_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t nb = p.n_blocks;
+    uint8_t* w = (uint8_t*)ws;
+    BlockMeta* meta = (BlockMeta*)w;
+    unsigned long long* costs = (unsigned long long*)(w + nb * 16);
+    unsigned long long* lb = costs + nb;
+    unsigned long long* ticket = lb + nb;
+    if (cudaMemsetAsync(status, 0xFF, 4 * sizeof(uint64_t), s) != cudaSuccess) return APAX_ERR_CUDA;
+    if (cudaMemsetAsync(costs, 0, (size_t)nb * 16 + 8, s) != cudaSuccess) return APAX_ERR_CUDA;
+    EncParams P;
+    memset(&P, 0, sizeof(P));
+    P.x = x;
+    P.n = n;
+    P.mode = APAX_FIXED_QUALITY;
+    P.bs = 4096;
+    P.target = target;
+    P.n_blocks = nb;
+    P.unit_blocks = nb;
+    P.n_units = 1;
+    P.status = (unsigned long long*)status;
+    P.stage_bytes = p.stage_bytes;
+    P.x_in_smem = 1;
+    P.att_lo = 20.0 * log10(ldexp(1.0, -31));
+    P.pow10_t20 = pow(10.0, target / 20.0);
+    P.sqrt12 = sqrt(12.0);
+    P.meta = meta;
+    P.stats = stats;
+    st = launch_encode_v3_chain(dtype, P, p.smem, s);
+    if (st) return st;
+    EncParams Q = P;
+    Q.stats = nullptr;
+    Q.count_only = 1;
+    Q.ticket = (unsigned int*)ticket;
+    return launch_encode_v4(dtype, Q, meta, costs, lb, s);
+}
+
 int apax_encode_lossless_range(const void* x, int64_t halo, int64_t n, int dtype, int block_size,
                                int64_t first_block, uint8_t* out, int64_t out_cap, int64_t* block_offsets,
                                uint64_t* status, void* ws, int64_t ws_bytes, void* stream) {
@@ -737,12 +790,12 @@ int apax_profile_welch(const void* x, const void* y, int64_t n, int dtype, int w
 }
 
 int apax_profile_select(const void* x, const void* y, int64_t n, int dtype, int pass, const uint64_t* prefixes,
-                        int n_prefixes, uint64_t* hist, int y_is_output, void* stream) {
-    if (!valid_dtype(dtype) || !x || !y || !prefixes || !hist || pass < 0 || pass > 15 || n_prefixes < 1 ||
-        n_prefixes > 1024)
+                        int n_prefixes, uint32_t* hist, int y_is_output, void* stream) {
+    if (!valid_dtype(dtype) || !x || !y || !hist || pass < 0 || pass > 3 || n < 0 || n >= (1LL << 32))
         return APAX_ERR_ARG;
-    return profile_select(x, y, n, dtype, pass, (const unsigned long long*)prefixes, n_prefixes,
-                          (unsigned long long*)hist, y_is_output ? 1 : 0, apax_profile_grid(), (cudaStream_t)stream);
+    if (pass > 0 && (!prefixes || n_prefixes < 1 || n_prefixes > 1024)) return APAX_ERR_ARG;
+    return profile_select(x, y, n, dtype, pass, (const unsigned long long*)prefixes, n_prefixes, (unsigned*)hist,
+                          y_is_output ? 1 : 0, apax_profile_grid(), (cudaStream_t)stream);
 }
 
 int apax_parse_file_header(const uint8_t* d, int64_t len, int* dt, int* mode, int* bs,

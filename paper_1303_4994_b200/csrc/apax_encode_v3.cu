@@ -95,6 +95,7 @@ struct __align__(16) St {
     double pxw[NCW];
     // phase B partials
     double pdw[NCW], pxbw[NCW];
+    double sxyw[NCW], syyw[NCW];    // META with stats: sum x*y, sum y*y of the warp
     // phase C per-warp results
     int sew[3][NCW];
     int flw[NCW];
@@ -1103,6 +1104,8 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
                         const double sd = F ? s : S->aq;
                         const bool idq = !F && S->aq == 1.0;
                         double rpd = 0.0, rpx = 0.0;
+                        double rxy = 0.0, ryy = 0.0;   // META with stats (the profiler's sweep)
+                        const bool wst = META && P.stats;
                         if (L < NL) {
 #pragma unroll
                             for (int i = 0; i < 16; i++) {
@@ -1115,7 +1118,13 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
                                 const double d2 = d * d;
                                 rpd = (i == 0) ? d2 : rpd + d2;
                                 rpx = (i == 0) ? xd * xd : (SQX ? __fma_rn(xd, xd, rpx) : rpx + xd * xd);
+                                if (META && wst) { rxy += xd * y; ryy += y * y; }
                             }
+                        }
+                        if (META && wst) {
+                            rxy = warp_allreduce(rxy, SumOp());
+                            ryy = warp_allreduce(ryy, SumOp());
+                            if (lane == 0) { S->sxyw[warp] = rxy; S->syyw[warp] = ryy; }
                         }
                         // leaf combine (all lanes: the shuffles use the full mask)
                         rpd += __shfl_xor_sync(0xffffffffu, rpd, 1);
@@ -1151,9 +1160,21 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
                 cbar();  // B3
                 PROF_MARK(2);
                 if (fq_emit && !regular) {
-                    if (tid == 0)
-                        fq_update(cold_px<DT>(xs, n),
-                                  cold_pd<DT>(xs, qbuf, n, F ? S->s : S->aq, F ? S->rs : S->ra, !F && S->aq == 1.0));
+                    if (tid == 0) {
+                        const double pxb = cold_px<DT>(xs, n);
+                        if (META && P.stats) {   // the sweep's (x, y) sums of a partial block
+                            const bool idq = !F && S->aq == 1.0;
+                            double sxy = 0.0, syy = 0.0;
+                            for (int i = 0; i < n; i++) {
+                                const double xd = xd_of<DT>(xs[i]);
+                                const double qd = (double)qbuf[qw(i)];
+                                const double y = idq ? qd : deq_of<DT>(qd, F ? S->s : S->aq, F ? S->rs : S->ra);
+                                sxy += xd * y; syy += y * y;
+                            }
+                            P.stats[3 * b] = pxb; P.stats[3 * b + 1] = sxy; P.stats[3 * b + 2] = syy;
+                        }
+                        fq_update(pxb, cold_pd<DT>(xs, qbuf, n, F ? S->s : S->aq, F ? S->rs : S->ra, !F && S->aq == 1.0));
+                    }
                     cbar();  // thread 0 read xs; the window zeroing follows
                 }
             }
@@ -1625,8 +1646,15 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
                     }
                 }
             }
-            if (fq_emit && regular && tid == 0)
-                fq_update(warp_tree(S->pxbw, (NL + 3) / 4), warp_tree(S->pdw, (NL + 3) / 4));
+            if (fq_emit && regular && tid == 0) {
+                const double pxb = warp_tree(S->pxbw, (NL + 3) / 4);
+                if (META && P.stats) {   // (x, y = the decode) sums of the block for the profiler's sweep
+                    double sxy = 0.0, syy = 0.0;
+                    for (int w = 0; w < NCW; w++) { sxy += S->sxyw[w]; syy += S->syyw[w]; }
+                    P.stats[3 * b] = pxb; P.stats[3 * b + 1] = sxy; P.stats[3 * b + 2] = syy;
+                }
+                fq_update(pxb, warp_tree(S->pdw, (NL + 3) / 4));
+            }
             if (emit && P.mode == 1 && tid == 0) {
                 // rate loop (codec.py:228-243) on this block's exact byte count;
                 // like the quality loop it only feeds the next S1

@@ -591,7 +591,8 @@ __global__ void __launch_bounds__(NT, 4) pack_kernel(EncParams P, const BlockMet
         const int bad = S->bad;
 
         // ---- phase D: header, JEE tokens, mantissas into the window ----
-        if (active && !bad) {
+        const bool pack = !bad && !P.count_only;
+        if (active && pack) {
             const unsigned below = nonA & ((1u << lane) - 1u);
             const int cin_t = below ? (int)((kbits >> (31 - __clz((int)below))) & 1u) : cin_w;
             const unsigned jx = jscan - jown;
@@ -684,7 +685,7 @@ __global__ void __launch_bounds__(NT, 4) pack_kernel(EncParams P, const BlockMet
                 }
             }
         }
-        if (tid == 0) {
+        if (tid == 0 && !P.count_only) {
             // block header (dtypes.py:156-165)
             const uint32_t hb[6] = {(uint32_t)((sel & 3) | (restart ? 4 : 0)), (uint32_t)(code & 0xFF),
                                     (uint32_t)((code >> 8) & 0xFF), 0u, (uint32_t)(uint8_t)(int8_t)fbe, 0u};
@@ -702,8 +703,8 @@ __global__ void __launch_bounds__(NT, 4) pack_kernel(EncParams P, const BlockMet
             }
         }
         bar();   // B4: window complete, prefix known
-        if (!bad) window_out(P.out + kFileHeader + S->prefix, win, blen, tid);
-        prev_len = blen;
+        if (pack) window_out(P.out + kFileHeader + S->prefix, win, blen, tid);
+        prev_len = P.count_only ? 0 : blen;
         // the next ticket only now: blocks start in ticket order, so a
         // block's predecessor is always already being coded
         if (tid == 0) S->blk = (long long)atomicAdd((unsigned long long*)P.ticket, 1ULL);

@@ -52,6 +52,8 @@ struct EncParams {
     long long clip_lo, clip_hi;
     BlockMeta* meta;              // split encoder: the chain's per-block records (v3 META)
     apax_block_state* state;      // generic kernel, one unit: CodecState in / out (encode_block)
+    double* stats;                // fixed-quality chain: per block sum x^2, sum x*y, sum y*y (y = the decode)
+    int count_only;               // packer: container length only, no output written
 };
 
 struct DecParams {
@@ -122,7 +124,7 @@ size_t profile_welch_smem(int seg);
 int profile_welch(const void* x, const void* y, long long n, int dt, int which, int seg, int lg,
                   long long nframes, const double* tw, double* partials, int grid, cudaStream_t st);
 int profile_select(const void* x, const void* y, long long n, int dt, int pass,
-                   const unsigned long long* prefixes, int npre, unsigned long long* hist, int ydiff, int grid,
+                   const unsigned long long* prefixes, int npre, unsigned* hist, int ydiff, int grid,
                    cudaStream_t st);
 int launch_walk(const uint8_t* blob, long long nbytes, long long n, int bs, int dt, long long n_blocks,
                 long long* offsets, unsigned long long* status, cudaStream_t st);

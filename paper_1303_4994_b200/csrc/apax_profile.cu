@@ -158,32 +158,49 @@ __device__ __forceinline__ unsigned long long ratio_key(const void* x, const voi
     return (unsigned long long)__double_as_longlong(r);
 }
 
+// digit plan of the 4-pass select: the key's sign bit is 0, so bits 62..0
+// split into 15 + 16 + 16 + 16 (most significant first)
+__host__ __device__ __forceinline__ int sel_shift(int pass) { return pass == 0 ? 48 : 48 - 16 * pass; }
+__host__ __device__ __forceinline__ int sel_width(int pass) { return pass == 0 ? 15 : 16; }
+
+// pass 0: one (empty) prefix, a 2^15-bin histogram per CTA in shared memory
+template <int DT>
+__global__ void __launch_bounds__(NT) select0_kernel(const void* x, const void* y, long long n,
+                                                     unsigned* hist, int ydiff) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned* h = (unsigned*)smem;   // 2^15 bins
+    for (int k = threadIdx.x; k < (1 << 15); k += NT) h[k] = 0u;
+    __syncthreads();
+    for (long long i = (long long)blockIdx.x * NT + threadIdx.x; i < n; i += (long long)gridDim.x * NT)
+        atomicAdd(&h[(int)((ratio_key<DT>(x, y, i, ydiff) >> 48) & 0x7fffULL)], 1u);
+    __syncthreads();
+    for (int k = threadIdx.x; k < (1 << 15); k += NT)
+        if (h[k]) atomicAdd(&hist[k], h[k]);
+}
+
+// passes 1..3: 16-bit digits of the keys whose higher bits equal one of the
+// sorted, unique prefixes, counted straight into hist[prefix][digit] (only
+// the keys in the target buckets get that far)
 template <int DT>
 __global__ void __launch_bounds__(NT) select_kernel(const void* x, const void* y, long long n, int pass,
                                                     const unsigned long long* prefixes, int npre,
-                                                    unsigned long long* hist, int ydiff) {
+                                                    unsigned* hist, int ydiff) {
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long* pre = (unsigned long long*)smem;   // npre
-    unsigned* h = (unsigned*)(pre + npre);                 // npre x 16
     for (int k = threadIdx.x; k < npre; k += NT) pre[k] = prefixes[k];
-    for (int k = threadIdx.x; k < npre * 16; k += NT) h[k] = 0u;
     __syncthreads();
-    const int sh = 60 - 4 * pass;
+    const int sh = sel_shift(pass);
     for (long long i = (long long)blockIdx.x * NT + threadIdx.x; i < n; i += (long long)gridDim.x * NT) {
         const unsigned long long key = ratio_key<DT>(x, y, i, ydiff);
-        const unsigned long long hi = pass == 0 ? 0ULL : (key >> (sh + 4));
-        // binary search in the sorted prefixes
+        const unsigned long long hi = key >> (sh + 16);
         int lo = 0, up = npre;
         while (lo < up) {
             const int mid = (lo + up) >> 1;
             if (pre[mid] < hi) lo = mid + 1;
             else up = mid;
         }
-        if (lo < npre && pre[lo] == hi) atomicAdd(&h[lo * 16 + (int)((key >> sh) & 15ULL)], 1u);
+        if (lo < npre && pre[lo] == hi) atomicAdd(&hist[(long long)lo * 65536 + (int)((key >> sh) & 0xffffULL)], 1u);
     }
-    __syncthreads();
-    for (int k = threadIdx.x; k < npre * 16; k += NT)
-        if (h[k]) atomicAdd(&hist[k], (unsigned long long)h[k]);
 }
 
 }  // namespace prof
@@ -224,16 +241,34 @@ int profile_welch(const void* x, const void* y, long long n, int dt, int which, 
 }
 
 int profile_select(const void* x, const void* y, long long n, int dt, int pass,
-                   const unsigned long long* prefixes, int npre, unsigned long long* hist, int ydiff, int grid,
+                   const unsigned long long* prefixes, int npre, unsigned* hist, int ydiff, int grid,
                    cudaStream_t st) {
-    const size_t smem = (size_t)npre * 8 + (size_t)npre * 16 * 4;
-    auto go = [&](auto kfn) -> int {
+    auto go0 = [&](auto kfn) -> int {
+        const size_t smem = (size_t)4 << 15;
         if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
             return APAX_ERR_CUDA;
+        int dev = 0, nsm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        note_launches(1);
+        kfn<<<nsm > 0 ? nsm : 148, prof::NT, smem, st>>>(x, y, n, hist, ydiff);
+        return cudaGetLastError() == cudaSuccess ? APAX_OK : APAX_ERR_CUDA;
+    };
+    auto go = [&](auto kfn) -> int {
+        const size_t smem = (size_t)npre * 8;
         note_launches(1);
         kfn<<<grid, prof::NT, smem, st>>>(x, y, n, pass, prefixes, npre, hist, ydiff);
         return cudaGetLastError() == cudaSuccess ? APAX_OK : APAX_ERR_CUDA;
     };
+    if (pass == 0) {
+        switch (dt) {
+            case 0: return go0(prof::select0_kernel<0>);
+            case 1: return go0(prof::select0_kernel<1>);
+            case 2: return go0(prof::select0_kernel<2>);
+            case 3: return go0(prof::select0_kernel<3>);
+            default: return go0(prof::select0_kernel<4>);
+        }
+    }
     switch (dt) {
         case 0: return go(prof::select_kernel<0>);
         case 1: return go(prof::select_kernel<1>);

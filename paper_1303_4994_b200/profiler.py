@@ -217,10 +217,14 @@ def fft_s2r_margin(x_spec: SpectrumStats, d_spec: SpectrumStats) -> float:
 # ---------------------------------------------------------------------------
 # S2R distribution: exact order statistics by radix multi-select
 # ---------------------------------------------------------------------------
+_SEL_DIGITS = ((48, 15), (32, 16), (16, 16), (0, 16))   # (shift, width); the key's sign bit is 0
+
+
 def _select_ratio_keys(xd, yd, dtype: Dtype, ranks: Sequence[int], y_is_output: bool,
                        reduce_hist=None) -> Dict[int, int]:
     """Ascending-rank order statistics (as uint64 bit patterns) of the
-    ratio keys |x| / |d| over all n samples (16 passes of 4-bit digits).
+    ratio keys |x| / |d| over all n samples: a radix multi-select in 4
+    passes over the keys (digits of 15, 16, 16, 16 bits; apax_profile_select).
     `reduce_hist` (multi-GPU) sums each pass's digit histograms over the
     ranks in place, so every rank picks the same digits and the ranks are
     global (distributed.sharded_window_stats)."""
@@ -229,29 +233,29 @@ def _select_ratio_keys(xd, yd, dtype: Dtype, ranks: Sequence[int], y_is_output: 
     targets = sorted(set(int(r) for r in ranks))
     prefix = {r: 0 for r in targets}
     resid = {r: r for r in targets}
-    for p in range(16):
+    sp = ctypes.c_void_p(_stream_ptr(None))
+    for p, (sh, width) in enumerate(_SEL_DIGITS):
         uniq = sorted(set(prefix.values()))
-        pre = torch.tensor(np.array(uniq, dtype=np.uint64).view(np.int64), device=xd.device)
-        hist = torch.zeros(len(uniq) * 16, dtype=torch.int64, device=xd.device)
+        nb = 1 << width
+        if p == 0:
+            pre = torch.zeros(1, dtype=torch.int64, device=xd.device)
+            hist = torch.zeros(nb, dtype=torch.int32, device=xd.device)
+        else:
+            pre = torch.tensor(np.array(uniq, dtype=np.uint64).view(np.int64), device=xd.device)
+            hist = torch.zeros(len(uniq) * nb, dtype=torch.int32, device=xd.device)
         raise_status(L.apax_profile_select(_ptr(xd), _ptr(yd), n, dtype.wire_code, p, _ptr(pre), len(uniq),
-                                           _ptr(hist), 1 if y_is_output else 0,
-                                           ctypes.c_void_p(_stream_ptr(None))))
+                                           _ptr(hist), 1 if y_is_output else 0, sp))
         if reduce_hist is not None:
             reduce_hist(hist)
-        h = hist.cpu().numpy().reshape(len(uniq), 16)
+        h = hist.cpu().numpy().view(np.uint32).astype(np.int64).reshape(-1, nb)
         slot = {v: i for i, v in enumerate(uniq)}
         for r in targets:
-            row = h[slot[prefix[r]]]
-            cum = 0
-            for dg in range(16):
-                c = int(row[dg])
-                if resid[r] < cum + c:
-                    prefix[r] = (prefix[r] << 4) | dg
-                    resid[r] -= cum
-                    break
-                cum += c
-            else:  # pragma: no cover - ranks are always < n
+            cum = np.cumsum(h[0 if p == 0 else slot[prefix[r]]])
+            dg = int(np.searchsorted(cum, resid[r], side="right"))
+            if dg >= nb:  # pragma: no cover - ranks are always < n
                 raise RuntimeError("radix select lost its rank")
+            resid[r] -= int(cum[dg - 1]) if dg else 0
+            prefix[r] = (prefix[r] << width) | dg
     return prefix
 
 
@@ -400,43 +404,100 @@ class RateCorrelationCurve:
 
 def _encode_decode(xd, dtype: Dtype, targets: Sequence[float], block_size: int):
     """Whole-stream fixed-quality encodes of xd at every target (concurrent
-    CUDA streams), each decoded on the GPU.  Returns [(nbytes, y tensor)]."""
+    CUDA streams), each decoded on the GPU.  Returns [(nbytes, y tensor)].
+    Encoder + decoder plans of a target hold ~2.3x the input; targets run in
+    groups that fit half of the free device memory."""
     torch, _ = _require_cuda()
     n = int(xd.numel())
+    w = dtype.width_bytes
+    per = 3 * n * max(w, 4) + (64 << 20)
+    free, _total = torch.cuda.mem_get_info(xd.device)
+    group = max(1, min(len(targets), int(0.5 * free // per)))
+    out = []
+    for g0 in range(0, len(targets), group):
+        jobs = []
+        for t in targets[g0:g0 + group]:
+            cfg = StreamConfig(dtype=dtype, block_size=block_size, mode=Mode.FIXED_QUALITY, target=float(t))
+            st = torch.cuda.Stream(device=xd.device)
+            st.wait_stream(torch.cuda.current_stream(xd.device))
+            enc = Encoder(n, cfg, device=xd.device)
+            dec = Decoder(n, dtype, block_size, device=xd.device)
+            with torch.cuda.stream(st):
+                enc.encode(xd, stream=st)
+                dec.decode(enc.out, enc.cap, enc.offsets, stream=st)
+            jobs.append((enc, dec, st))
+        for enc, dec, st in jobs:
+            nbytes = enc.finish(stream=st)
+            y = dec.finish(stream=st)
+            torch.cuda.current_stream(xd.device).wait_stream(st)
+            out.append((nbytes, y))
+        del jobs
+    return out
+
+
+def _sweep_supported(xd, dtype: Dtype, block_size: int) -> bool:
+    return (block_size == 4096 and dtype in (Dtype.I16, Dtype.I32, Dtype.F32, Dtype.F64)
+            and xd.data_ptr() % 16 == 0)
+
+
+def _sweep_points(xd, dtype: Dtype, targets: Sequence[float], block_size: int):
+    """(container bytes, sum x^2, sum x*y, sum y*y) of the whole-stream
+    fixed-quality encode at every target.  Output-free on the device
+    (apax_sweep_point: the chain's per-block (x, y = decode) sums and the
+    packer counting bytes; no container, no decoded array), all targets on
+    concurrent CUDA streams; other block sizes / dtypes encode and decode."""
+    torch, L = _require_cuda()
+    n = int(xd.numel())
+    if not _sweep_supported(xd, dtype, block_size):
+        res = []
+        for nbytes, y in _encode_decode(xd, dtype, targets, block_size):
+            s = _Sums(xd, y, dtype)
+            res.append((nbytes, s.sxx, s.sxy, s.syy))
+        return res
+    nb = (n + 4095) // 4096
+    wsb = int(L.apax_sweep_point_workspace_bytes(n, dtype.wire_code))
+    cur = torch.cuda.current_stream(xd.device)
     jobs = []
     for t in targets:
-        cfg = StreamConfig(dtype=dtype, block_size=block_size, mode=Mode.FIXED_QUALITY, target=float(t))
         st = torch.cuda.Stream(device=xd.device)
-        st.wait_stream(torch.cuda.current_stream(xd.device))
-        enc = Encoder(n, cfg, device=xd.device)
-        dec = Decoder(n, dtype, block_size, device=xd.device)
-        with torch.cuda.stream(st):
-            enc.encode(xd, stream=st)
-            dec.decode(enc.out, enc.cap, enc.offsets, stream=st)
-        jobs.append((enc, dec, st))
+        st.wait_stream(cur)
+        ws = torch.empty(wsb, dtype=torch.uint8, device=xd.device)
+        stats = torch.empty(3 * nb, dtype=torch.float64, device=xd.device)
+        status = torch.empty(4, dtype=torch.int64, device=xd.device)
+        raise_status(L.apax_sweep_point(_ptr(xd), n, dtype.wire_code, float(t), _ptr(stats), _ptr(status), _ptr(ws),
+                                        wsb, ctypes.c_void_p(int(st.cuda_stream))))
+        jobs.append((st, stats, status, ws))
     out = []
-    for enc, dec, st in jobs:
-        nbytes = enc.finish(stream=st)
-        y = dec.finish(stream=st)
-        torch.cuda.current_stream(xd.device).wait_stream(st)
-        out.append((nbytes, y))
+    from .codec import _check_status
+    for st, stats, status, _ws in jobs:
+        st.synchronize()
+        sv = status.cpu().numpy().view(np.uint64)
+        _check_status(sv)
+        tot = stats.cpu().numpy().reshape(nb, 3).sum(axis=0)
+        out.append((int(sv[2]), float(tot[0]), float(tot[1]), float(tot[2])))
+    cur.wait_stream(jobs[-1][0]) if jobs else None
     return out
+
+
+def _point(t: float, n: int, dtype: Dtype, nbytes: int, sxx: float, sxy: float, syy: float) -> OperatingPoint:
+    if sxx == 0.0 or syy == 0.0:
+        raise UndefinedCorrelation("a vector with zero energy has no correlation")
+    return OperatingPoint(t, n * dtype.width_bytes / nbytes, sxy / math.sqrt(sxx * syy))
 
 
 def rate_correlation_sweep(x, dtype: Dtype, grid: Sequence[float] = DEFAULT_GRID,
                            block_size: int = 4096) -> RateCorrelationCurve:
     """Encode at every SRR target on the grid; each point is independent."""
     xd = _dev(x, dtype)
-    input_bytes = int(xd.numel()) * dtype.width_bytes
+    n = int(xd.numel())
     targets = sorted(float(t) for t in grid)
     points: List[OperatingPoint] = []
-    for t, (nbytes, y) in zip(targets, _encode_decode(xd, dtype, targets, block_size)):
+    for t, (nbytes, sxx, sxy, syy) in zip(targets, _sweep_points(xd, dtype, targets, block_size)):
         try:
-            r = _Sums(xd, y, dtype).pearson()
+            points.append(_point(t, n, dtype, nbytes, sxx, sxy, syy))
         except UndefinedCorrelation:
             warnings.warn(f"correlation undefined at SRR target {t}; point dropped")
             continue
-        points.append(OperatingPoint(t, input_bytes / nbytes, r))
     return RateCorrelationCurve(points=tuple(points))
 
 
@@ -496,9 +557,8 @@ class ProfileSession:
         self.current_point = self.recommended
 
     def _reencode(self, target: float) -> OperatingPoint:
-        (nbytes, y), = _encode_decode(self._xd, self.dtype, [target], self.block_size)
-        ratio = int(self._xd.numel()) * self.dtype.width_bytes / nbytes
-        return OperatingPoint(target, ratio, _Sums(self._xd, y, self.dtype).pearson())
+        (nbytes, sxx, sxy, syy), = _sweep_points(self._xd, self.dtype, [target], self.block_size)
+        return _point(target, int(self._xd.numel()), self.dtype, nbytes, sxx, sxy, syy)
 
     def windows_at(self, srr_target: float) -> dict:
         """Windows 2-4 for one operating point (cached)."""

@@ -208,3 +208,28 @@ def test_session_cache_and_reencode_self_consistent():
     rec = s.recommended
     again = s._reencode(rec.srr_target)
     assert again.ratio == rec.ratio and again.r == pytest.approx(rec.r, abs=1e-15)
+
+
+@gpu
+@pytest.mark.parametrize("seed", range(3))
+def test_output_free_sweep_point_matches_full_encode_decode(seed):
+    """apax_sweep_point (the chain's per-block (x, y) sums, the packer
+    counting bytes) against a full encode + decode: container length exact,
+    sums to 1e-12."""
+    import torch
+    from paper_1303_4994_b200 import Dtype
+    from paper_1303_4994_b200.profiler import _Sums, _encode_decode, _sweep_points
+    rng = np.random.default_rng(500 + seed)
+    for dt in (Dtype.I16, Dtype.I32, Dtype.F32, Dtype.F64):
+        n = int(rng.integers(1, 60000))
+        x = np.cumsum(rng.standard_normal(n)) * 50.0
+        x = x.astype(dt.np_dtype) if dt.is_float else np.clip(x, -30000, 30000).astype(dt.np_dtype)
+        xd = torch.from_numpy(x).cuda()
+        targets = [float(t) for t in rng.uniform(20, 120, 3)]
+        fast = _sweep_points(xd, dt, targets, 4096)
+        full = _encode_decode(xd, dt, targets, 4096)
+        for (nb, sxx, sxy, syy), (nb2, y) in zip(fast, full):
+            s = _Sums(xd, y, dt)
+            assert nb == nb2, (dt, n)
+            for a, b in ((sxx, s.sxx), (sxy, s.sxy), (syy, s.syy)):
+                assert a == pytest.approx(b, rel=1e-12, abs=0.0), (dt, n)
