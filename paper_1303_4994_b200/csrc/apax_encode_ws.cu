@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(NT, 1) chain_kernel(EncParams P) {
         const bool full = n == BS;
         const int G = (n + 3) >> 2;
         const bool active = tid < G;
-        if (tid == 32) stage(b + NBUF - 1);
+        if (tid == 32 && FOLD) stage(b + NBUF - 1);
         WSP(0);
 
         // ---- S1 (warp 0: the peak and x^2 leaf trees; thread 0: gain,
@@ -309,6 +309,7 @@ __global__ void __launch_bounds__(NT, 1) chain_kernel(EncParams P) {
             double peak = 0.0;
             bool nonfin = false;
             if (NEED_PEAK) {
+                WSPX(13);
                 const unsigned hi = __reduce_max_sync(0xffffffffu, S->pk[lane]);
                 const unsigned lo = __reduce_max_sync(0xffffffffu, S->pk[lane] == hi ? S->pn[lane] : 0u);
                 const unsigned long long m = ((unsigned long long)hi << 32) | lo;
@@ -321,6 +322,7 @@ __global__ void __launch_bounds__(NT, 1) chain_kernel(EncParams P) {
                     px = S->lx[lane];
 #pragma unroll
                     for (int o = 1; o < 32; o <<= 1) px += __shfl_xor_sync(0xffffffffu, px, o);
+                    WSPX(14);
                 } else if (lane == 0) {
                     px = pairwise(scr, n);
                 }
@@ -412,6 +414,7 @@ __global__ void __launch_bounds__(NT, 1) chain_kernel(EncParams P) {
         }
         WSP(1);
         if (!FOLD) bar();   // B2
+        if (tid == 32 && !FOLD) stage(b + NBUF - 1);   // (after thread 0's S1: off its critical path)
         WSP(2);
         const double sq = S->sq;
         int q[4];
@@ -695,7 +698,7 @@ __global__ void __launch_bounds__(NT, 1) chain_kernel(EncParams P) {
 
 #ifdef APAX_WS_PROF
 extern "C" int apax_debug_ws_prof(unsigned long long* host) {
-    return (int)cudaMemcpyFromSymbol(host, ws::g_ws_prof, 13 * sizeof(unsigned long long));
+    return (int)cudaMemcpyFromSymbol(host, ws::g_ws_prof, 15 * sizeof(unsigned long long));
 }
 #endif
 

@@ -25,6 +25,7 @@ def main():
         build()
         return
     os.environ["APAX_LIB_PATH"] = SO
+    os.environ["APAX_WS_CHAIN"] = "1"
     sys.path.insert(0, ROOT)
     import torch
     from paper_1303_4994_b200 import Dtype, Encoder, Mode, StreamConfig, _lib
@@ -41,12 +42,13 @@ def main():
     enc.finish()
     L = _lib.lib()
     L.apax_debug_ws_prof.argtypes = [ctypes.c_void_p]
-    buf = (ctypes.c_ulonglong * 13)()
+    buf = (ctypes.c_ulonglong * 15)()
     L.apax_debug_ws_prof(buf)
     nb = (x.numel() + 4095) // 4096
     tot = sum(buf[:10])
     print("S1 sub-marks (cycles after the section start): lane-0 start %.0f, code done %.0f, before record %.0f" %
           tuple(buf[k] / nb for k in (10, 11, 12)))
+    print("S1 prelude: before peak reduce %.0f, after px butterfly %.0f" % (buf[13] / nb, buf[14] / nb))
     for k, nm in enumerate(NAMES):
         print(f"{nm:12s} {buf[k] / nb:9.1f} cycles/block ({100 * buf[k] / max(tot, 1):5.1f}%)")
     print(f"total {tot / nb:.1f} cycles/block")
