@@ -191,10 +191,7 @@ __device__ __noinline__ double pairwise(const double* v, int n0) {
 // per-phase cycles of thread 0 (tools/prof_ws.py): acc[k] += clock at mark k - clock at the previous mark
 __device__ unsigned long long g_ws_prof[16];
 #define WSP(k) do { if (threadIdx.x == 0) { const long long c_ = clock64(); wsp_acc[k] += (unsigned long long)(c_ - wsp_last); wsp_last = c_; } } while (0)
-// sub-marks inside a section (thread 0): g_ws_prof[k] += clock - clock at the section's mark
-#define WSPX(k) do { if (threadIdx.x == 0) g_ws_prof[k] += (unsigned long long)(clock64() - wsp_last); } while (0)
 #else
-#define WSPX(k) do { } while (0)
 #define WSP(k) do { } while (0)
 #endif
 
@@ -309,7 +306,6 @@ __global__ void __launch_bounds__(NT, 1) chain_kernel(EncParams P) {
             double peak = 0.0;
             bool nonfin = false;
             if (NEED_PEAK) {
-                WSPX(13);
                 const unsigned hi = __reduce_max_sync(0xffffffffu, S->pk[lane]);
                 const unsigned lo = __reduce_max_sync(0xffffffffu, S->pk[lane] == hi ? S->pn[lane] : 0u);
                 const unsigned long long m = ((unsigned long long)hi << 32) | lo;
@@ -322,13 +318,11 @@ __global__ void __launch_bounds__(NT, 1) chain_kernel(EncParams P) {
                     px = S->lx[lane];
 #pragma unroll
                     for (int o = 1; o < 32; o <<= 1) px += __shfl_xor_sync(0xffffffffu, px, o);
-                    WSPX(14);
                 } else if (lane == 0) {
                     px = pairwise(scr, n);
                 }
             }
           if (lane == 0) {
-            WSPX(10);
             if (nonfin) {
                 for (int i = 0; i < n; i++)
                     if (!isfinite((double)((const T*)P.x)[base + i])) {
@@ -390,7 +384,6 @@ __global__ void __launch_bounds__(NT, 1) chain_kernel(EncParams P) {
                     fbe = (int)fb;
                 }
             }
-            WSPX(11);
             S->code = code; S->fbe = fbe; S->aq = aq;
             S->sq = F ? (zero ? 0.0 : s) : aq;
             S->rs = FQ ? (F ? __ddiv_rn(1.0, s) : (aq != 1.0 ? __ddiv_rn(1.0, aq) : 1.0)) : 1.0;
@@ -402,7 +395,6 @@ __global__ void __launch_bounds__(NT, 1) chain_kernel(EncParams P) {
                 if (S->pc[2] < S->pc[sel]) sel = 2;
             }
             S->sel = sel;
-            WSPX(12);
             BlockMeta mt;
             mt.sq = S->sq; mt.code = code; mt.fbe = (short)fbe; mt.wide = (short)S->wide;
             P.meta[b] = mt;
