@@ -99,6 +99,27 @@ def test_cfg1_i16_fixed_rate_whole_stream():
     assert abs(x.size * 2 / len(ref) - 4.0) < 0.02     # reference full-size ratio 3.998
 
 
+def test_cfg2_f32_fixed_quality_full():
+    """cfg2 (the bench's workload): 2^26 f32 AR(2), fixed quality at the
+    reference profiler's target, one-wave cold segments."""
+    x = W.cfg2_ar2_f32()
+    ratio, r = _full_check(x, Dtype.F32, Mode.FIXED_QUALITY, W.CFG2_TARGET_DB)
+    assert 3.9 < ratio < 4.2 and r > 0.99999
+
+
+def test_cfg2_f32_fixed_quality_whole_stream():
+    """cfg2 with no segments: the reference's own container (a serial chain
+    of 16384 blocks: the v3 chain kernel + the block-parallel packer)."""
+    x = W.cfg2_ar2_f32()
+    cfg = StreamConfig(Dtype.F32, BS, Mode.FIXED_QUALITY, W.CFG2_TARGET_DB)
+    res = _encode(torch.from_numpy(x).cuda(), cfg)
+    ref, offs, _ = O.encode(x, 3, 2, W.CFG2_TARGET_DB, BS)
+    assert res.to_bytes() == ref
+    assert np.array_equal(res.block_offsets.cpu().numpy(), offs)
+    y = _decode(res, Dtype.F32, None).cpu().numpy()
+    assert np.array_equal(y, O.decode(ref, offs, nthreads=0))
+
+
 def test_cfg3_f32_image_fixed_rate_6to1_full():
     """cfg3: 8192x8192 f32 Gaussian random field, fixed rate 6:1 (32/6 bps);
     the adaptive selector realises the 1st difference along rows."""
