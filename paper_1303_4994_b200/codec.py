@@ -341,28 +341,10 @@ def decode_device(blob, nbytes: Optional[int] = None, offsets=None,
     n = _decodable_count(count, nbytes, cfg)
     dec = Decoder(n, cfg.dtype, cfg.block_size, device=blob.device)
     ok = n == count
-    if ok and offsets is None:
-        # index-less: discover the blocks on the device (K5); a clean segmented
-        # container (restart flags exactly every P blocks) then takes the
-        # segment-serial decoder, anything else (whole stream, corruption)
-        # the general one, which repeats the discovery and reports errors
-        _, L = _require_cuda()
-        nb = (count + cfg.block_size - 1) // cfg.block_size
-        offs = torch.empty(nb + 1, dtype=torch.int64, device=blob.device)
-        st = torch.empty(4, dtype=torch.int64, device=blob.device)
-        pseg = torch.zeros(1, dtype=torch.int64, device=blob.device)
-        sp = ctypes.c_void_p(_stream_ptr(None))
-        rc = L.apax_find_blocks(ctypes.c_void_p(blob.data_ptr()), nbytes, count, cfg.dtype.wire_code,
-                                cfg.block_size, ctypes.c_void_p(offs.data_ptr()), ctypes.c_void_p(st.data_ptr()), sp)
-        if rc == 0 and nb > 1:
-            rc = L.apax_detect_segments(ctypes.c_void_p(blob.data_ptr()), nbytes, ctypes.c_void_p(offs.data_ptr()),
-                                        nb, ctypes.c_void_p(pseg.data_ptr()), sp)
-        if rc == 0 and nb > 1:
-            torch.cuda.current_stream().synchronize()
-            clean = (st.cpu().numpy().view(np.uint64)[:2] == np.uint64(_U64_MAX)).all()
-            p = int(pseg.item())
-            if clean and p > 0:
-                offsets, segment_blocks = offs, p
+    # without offsets apax_decode discovers the blocks on the device (K5) and
+    # decodes a segmented container (restart flags every P blocks) segment-
+    # serially, anything else (whole stream, corruption) in two passes, with
+    # no host round trip
     dec.decode(blob, nbytes, offsets if ok else None, segment_blocks=segment_blocks if ok else None)
     return dec.finish()
 

@@ -194,6 +194,20 @@ __global__ void detect_segments_kernel(const uint8_t* blob, long long nbytes, co
     if (threadIdx.x == 0) out[0] = (P == ~0ULL || broken) ? 0ULL : P;
 }
 
+// index-less decode: the first restarting block > 0 on the speculative
+// offsets (the segment length of a segmented container) -> gate->first
+__global__ void seg_first_kernel(const uint8_t* blob, long long nbytes, const long long* offs, long long nb,
+                                 IlGate* gate) {
+    if (!gate->spec) return;
+    const long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long mine = ~0ULL;
+    for (long long b = 1 + i0; b < nb; b += (long long)gridDim.x * blockDim.x) {
+        const long long o = offs[b];
+        if (o >= 0 && o < nbytes && ((blob[o] >> 2) & 1) && (unsigned long long)b < mine) mine = (unsigned long long)b;
+    }
+    if (mine != ~0ULL) atomicMin(&gate->first, mine);
+}
+
 // status words to pinned host memory by plain stores from an SM: a copy-engine
 // D2H of 32 bytes would queue behind the bulk copies of a pipelined round trip
 __global__ void status_to_host_kernel(const unsigned long long* src, unsigned long long* dst, int n) {
@@ -629,14 +643,33 @@ int apax_decode(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, int b
     if (p.n_blocks == 0) return APAX_OK;
     if (cudaMemsetAsync(w, 0, (size_t)p.ws_offsets, s) != cudaSuccess) return APAX_ERR_CUDA;
     const long long* offs = (const long long*)block_offsets;
+    IlGate* gate = nullptr;
     if (!offs) {
         long long* wo = (long long*)(w + p.ws_offsets);
         if (cudaMemsetAsync(wo, 0xFF, (size_t)(p.n_blocks + 1) * 8, s) != cudaSuccess) return APAX_ERR_CUDA;
-        if (p.n_blocks >= 2 && env_int("APAX_K5", 1))
+        const bool k5 = p.n_blocks >= 2 && env_int("APAX_K5", 1);
+        if (k5 && decode_v3_supported(dtype, block_size) && env_int("APAX_DEC_VER", 0) != 2 &&
+            env_int("APAX_IL_SPEC", 1)) {
+            // index-less, speculative: the signature scan's candidates as the
+            // offsets (checked block by block by the segment decode below);
+            // the full discovery runs only when that path is not taken
+            gate = (IlGate*)(w + p.ws_ticket + 64);
+            st = launch_k5_speculate(blob, nbytes, dtype, p.n_blocks, wo, w + p.ws_k5, gate, s);
+            if (st) return st;
+            int dev = 0, nsm = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            long long sgrid = (p.n_blocks + 255) / 256;
+            if (sgrid > nsm) sgrid = nsm;
+            note_launches(1);
+            seg_first_kernel<<<(int)sgrid, 256, 0, s>>>(blob, nbytes, wo, p.n_blocks, gate);
+            if (cudaGetLastError() != cudaSuccess) return APAX_ERR_CUDA;
+        } else if (k5) {
             st = launch_find_blocks_k5(blob, nbytes, n, block_size, dtype, p.n_blocks, wo,
                                        (unsigned long long*)status, w + p.ws_k5, s);
-        else
+        } else {
             st = launch_walk(blob, nbytes, n, block_size, dtype, p.n_blocks, wo, (unsigned long long*)status, s);
+        }
         if (st) return st;
         offs = wo;
     }
@@ -654,11 +687,23 @@ int apax_decode(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, int b
     P.ticket = (unsigned int*)(w + p.ws_ticket);
     P.payload_cap = p.payload_cap;
     if (decode_v3_supported(dtype, block_size) && env_int("APAX_DEC_VER", 0) != 2) {
+        const size_t sm3 = decode_v3_smem_bytes(dtype, p.payload_cap);
+        const int g3 = decode_v3_resident_ctas(dtype, sm3);
+        if (gate) {
+            // the speculative segment decode; then (gated on the device) the
+            // full discovery and the two-pass decode for everything it did
+            // not take: whole-stream containers, other candidate sets, any
+            // inconsistency or error
+            P.il_gate = gate;
+            st = launch_decode_v3_seg_dev(dtype, P, g3, sm3, s);
+            if (st) return st;
+            st = launch_find_blocks_k5(blob, nbytes, n, block_size, dtype, p.n_blocks, (long long*)offs,
+                                       (unsigned long long*)status, w + p.ws_k5, s, gate);
+            if (st) return st;
+        }
         // any container through the segment-serial decoder: one-wave pseudo-
         // segments, pass 1 for their history maps, pass 2 with the composed
         // entries (the carry region holds maps + entries)
-        const size_t sm3 = decode_v3_smem_bytes(dtype, p.payload_cap);
-        const int g3 = decode_v3_resident_ctas(dtype, sm3);
         return launch_decode_v3_two_pass(dtype, P, g3, sm3, P.carry, s);
     }
     if (p.v2) return launch_decode_v2(dtype, P, p.grid, p.smem, s);

@@ -325,7 +325,8 @@ __global__ void __launch_bounds__(kNT) decode_kernel(DecParams P) {
 // are reset and the full walk runs, reporting the reference's exact error.
 __global__ void walk_kernel(const uint8_t* blob, long long nbytes, long long n, int bs, int dt,
                             long long n_blocks, long long* offsets, unsigned long long* status,
-                            const int* k5_fail) {
+                            const int* k5_fail, const IlGate* gate) {
+    if (gate && il_seg_ok(gate)) return;
     extern __shared__ __align__(16) unsigned char smem_w[];
     uint8_t* e = smem_w;
     const int lane = threadIdx.x & 31;
@@ -354,7 +355,19 @@ __global__ void walk_kernel(const uint8_t* blob, long long nbytes, long long n, 
         const long long maxj = (3LL * G + 2) / 2;
         const long long nbj = avail < maxj ? avail : maxj;
         long long used = 0, esum = 0;
-        int st = warp_jee_decode(p, 2 * nbj, G, e, used, esum);
+        int st = -1;
+        if (b0 > 0) {   // after K5: the last block, fast parser first
+            int u = 0;
+            st = warp_jee_fast(p, blob + nbytes, (int)(2 * nbj), G, e, u);
+            __syncwarp();
+            if (st == 0) {
+                unsigned sb = 0;
+                for (int g = lane; g < G; g += 32) sb += e[g];
+                esum = __reduce_add_sync(0xffffffffu, sb);
+                used = u;
+            }
+        }
+        if (st != 0) st = warp_jee_decode(p, 2 * nbj, G, e, used, esum);
         if (st) { if (lane == 0) report_error(status, b, st); return; }
         long long sz = (used + 1) / 2 + (4 * esum + 7) / 8;
         if (avail < sz) { if (lane == 0) report_error(status, b, APAX_ERR_MANTISSA_TRUNCATED); return; }
@@ -416,15 +429,16 @@ int launch_walk(const uint8_t* blob, long long nbytes, long long n, int bs, int 
                 long long* offsets, unsigned long long* status, cudaStream_t st) {
     size_t smem = (size_t)(bs / 4) + 64;
     note_launches(1);
-    walk_kernel<<<1, 32, smem, st>>>(blob, nbytes, n, bs, dt, n_blocks, offsets, status, nullptr);
+    walk_kernel<<<1, 32, smem, st>>>(blob, nbytes, n, bs, dt, n_blocks, offsets, status, nullptr, nullptr);
     return cudaGetLastError() == cudaSuccess ? APAX_OK : APAX_ERR_CUDA;
 }
 
 int launch_walk_after_k5(const uint8_t* blob, long long nbytes, long long n, int bs, int dt, long long n_blocks,
-                         long long* offsets, unsigned long long* status, const int* k5_fail, cudaStream_t st) {
+                         long long* offsets, unsigned long long* status, const int* k5_fail, cudaStream_t st,
+                         const IlGate* gate) {
     size_t smem = (size_t)(bs / 4) + 64;
     note_launches(1);
-    walk_kernel<<<1, 32, smem, st>>>(blob, nbytes, n, bs, dt, n_blocks, offsets, status, k5_fail);
+    walk_kernel<<<1, 32, smem, st>>>(blob, nbytes, n, bs, dt, n_blocks, offsets, status, k5_fail, gate);
     return cudaGetLastError() == cudaSuccess ? APAX_OK : APAX_ERR_CUDA;
 }
 

@@ -146,8 +146,24 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
     __syncthreads();
     uint32_t phs = 0u;
 
-    const long long P_seg = P.segment_blocks;
-    const long long s_begin = P.seg_begin, s_end = P.seg_end;
+    long long P_seg = P.segment_blocks;
+    long long s_begin = P.seg_begin, s_end = P.seg_end;
+    // index-less decode: the speculative segment path (TP 0) or the two-pass
+    // decode that replaces it (TP 1, 2) -- exactly one of them runs
+    const bool spec = TP == 0 && P.il_gate;
+    if (P.il_gate) {
+        const bool seg_ok = il_seg_ok(P.il_gate);
+        if (TP == 0) {
+            if (!seg_ok) return;
+            P_seg = (long long)P.il_gate->first;
+            const long long nseg = (P.n_blocks + P_seg - 1) / P_seg;
+            const long long sfull = (P.n % bs) ? nseg - 1 : nseg;
+            s_begin = P.seg_part == 2 ? sfull : 0;
+            s_end = P.seg_part == 1 ? sfull : nseg;
+        } else if (seg_ok) {
+            return;
+        }
+    }
 
     // issue the load of block bb into buffer slot (thread 0)
     auto issue = [&](long long bb, int slot) {
@@ -320,6 +336,9 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
             const int pay_off = S->ld_payoff[cur], avail = S->ld_avail[cur], staged = S->ld_staged[cur];
             const int4 ji = S->jinfo[kb];
             const int sel = ji.x & 3, restart = (ji.x >> 2) & 1;   // scale code, fbe: S->dq
+            // speculative segments: a segment head without a restart flag
+            // sends the container to the two-pass decode
+            if (spec && b == b0 && b0 > 0 && !restart && tid == 0) atomicExch(&P.il_gate->gp, 0u);
             if (!err) err = (sel == 3) ? APAX_ERR_SELECTOR : ji.y;
             const int used = ji.z;
             const bool bnarrow = ji.w <= 16;
@@ -340,9 +359,25 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                 const long long mant_bytes = ((long long)btot + 7) / 8;
                 if (avail < jee_bytes + mant_bytes) err = APAX_ERR_MANTISSA_TRUNCATED;
                 else if (jee_bytes + mant_bytes > staged) err = APAX_ERR_ARG;   // offsets inconsistent
+                else if (spec) {
+                    // the walk's recurrence (codec.py:317-323) on the speculative
+                    // offsets: block b ends where block b + 1 starts
+                    const long long bend_true = boff + HS + jee_bytes + mant_bytes;
+                    if (b + 1 < P.n_blocks) {
+                        if (bend_true != bend) err = -2;
+                    } else if (tid == 0) {
+                        ((long long*)P.offsets)[P.n_blocks] = bend_true;
+                    }
+                }
             }
             if (err) {
-                if (tid == 0 && err > 0) report_error(P.status, b, err);
+                // speculative offsets: any error or inconsistency hands the
+                // container to the full discovery, which reports the
+                // reference's error
+                if (tid == 0) {
+                    if (spec) atomicExch(&P.il_gate->gp, 0u);
+                    else if (err > 0) report_error(P.status, b, err);
+                }
                 cbar();
                 continue;
             }
@@ -669,7 +704,9 @@ static int launch_d3_range(int dt, bool fix, const DecParams& P, long long s0, l
 
 // entries of a two-pass decode: e_0 = (0, 0), e_{k+1} = F_k(e_k) (one thread;
 // a few hundred segments)
-__global__ void compose_entries_kernel(const unsigned long long* maps, long long nseg, unsigned long long* entries) {
+__global__ void compose_entries_kernel(const unsigned long long* maps, long long nseg, unsigned long long* entries,
+                                       const IlGate* gate) {
+    if (gate && il_seg_ok(gate)) return;
     unsigned long long h1 = 0, h2 = 0;
     for (long long k = 0; k < nseg; k++) {
         entries[2 * k] = h1;
@@ -699,12 +736,42 @@ int launch_decode_v3_two_pass(int dt, DecParams P, int grid, size_t smem, unsign
     int r = launch_decode_v3_tp(dt, P, grid, smem, st, 1);
     if (r) return r;
     note_launches(1);
-    compose_entries_kernel<<<1, 1, 0, st>>>(maps, nseg, entries);
+    compose_entries_kernel<<<1, 1, 0, st>>>(maps, nseg, entries, P.il_gate);
     if (cudaGetLastError() != cudaSuccess) return APAX_ERR_CUDA;
     P.seg_map = nullptr;
     P.seg_entry = entries;
     P.no_store = 0;
     return launch_decode_v3_tp(dt, P, grid, smem, st, 2);
+}
+
+// index-less segment path: P.il_gate set, the segment length
+// and count read on the device (full-block segments on the compile-time-
+// geometry kernel, the segment with a partial last block on the generic one)
+int launch_decode_v3_seg_dev(int dt, DecParams P, int grid, size_t smem, cudaStream_t st) {
+    const bool fixable = P.bs == d3::MAXBS && dt >= 1 && dt <= 4;
+    const bool partial = (P.n % P.bs) != 0;
+    P.segment_blocks = 1;
+    P.seg_begin = 0;
+    P.seg_end = 0;
+    if (fixable) {
+        P.seg_part = partial ? 1 : 0;
+        const void* fn = d3_kernel(dt, true, 0);
+        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return APAX_ERR_CUDA;
+        void* args[] = {&P};
+        note_launches(1);
+        if (cudaLaunchKernel(fn, dim3(grid), dim3(d3::NT), args, smem, st) != cudaSuccess) return APAX_ERR_CUDA;
+        if (!partial) return APAX_OK;
+    }
+    P.seg_part = fixable ? 2 : 0;
+    const void* fn = d3_kernel(dt, false, 0);
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return APAX_ERR_CUDA;
+    void* args[] = {&P};
+    note_launches(1);
+    if (cudaLaunchKernel(fn, dim3(fixable ? 1 : grid), dim3(d3::NT), args, smem, st) != cudaSuccess)
+        return APAX_ERR_CUDA;
+    return APAX_OK;
 }
 
 int launch_decode_v3(int dt, const DecParams& P, int grid, size_t smem, cudaStream_t st) {

@@ -164,6 +164,9 @@ static __device__ __noinline__ int warp_jee_decode(const uint8_t* p, long long t
 // runs the exact parser (apax_jee.cuh), which reports the reference's first
 // error.  e must hold G + 128 bytes (tokens are written before validation).
 // ---------------------------------------------------------------------------
+// LDG false: p / pend may point into shared memory (a staged copy whose
+// bytes keep their global alignment mod 4, with >= 4 bytes before p)
+template <bool LDG = true>
 static __device__ __forceinline__ int warp_jee_fast(const uint8_t* p, const uint8_t* pend, int total, int G,
                                              uint8_t* e, int& used) {
     const int lane = threadIdx.x & 31;
@@ -183,7 +186,8 @@ static __device__ __forceinline__ int warp_jee_fast(const uint8_t* p, const uint
             const unsigned sh = (unsigned)(a & 3) * 8u;
             uint32_t w0, w1, w2;
             if ((const uint8_t*)(wp + 3) <= pend) {
-                w0 = bswap32(__ldg(wp)); w1 = bswap32(__ldg(wp + 1)); w2 = bswap32(__ldg(wp + 2));
+                if (LDG) { w0 = bswap32(__ldg(wp)); w1 = bswap32(__ldg(wp + 1)); w2 = bswap32(__ldg(wp + 2)); }
+                else { w0 = bswap32(wp[0]); w1 = bswap32(wp[1]); w2 = bswap32(wp[2]); }
             } else {   // the last words of the container: bytewise, zero past the end
                 uint32_t w[3];
                 for (int k = 0; k < 3; k++) {

@@ -56,6 +56,22 @@ struct EncParams {
     int count_only;               // packer: container length only, no output written
 };
 
+// Index-less decode state (apax_decode without offsets, apax_capi.cu):
+// spec = 1 when the signature scan found exactly one candidate per block
+// starting at byte 28 and wrote them as speculative offsets; first = the
+// first restarting block > 0 (~0: none, a whole-stream container); gp =
+// 0xFFFFFFFF while nothing contradicts the speculation.  The segment path
+// runs while il_seg_ok; otherwise the full discovery (K5 parse, prune,
+// walk) and the two-pass decode run.
+struct IlGate {
+    unsigned long long first;
+    unsigned int gp;
+    unsigned int spec;
+};
+__device__ __forceinline__ bool il_seg_ok(const IlGate* g) {
+    return g->spec && g->first != ~0ULL && g->first > 0 && g->gp == 0xFFFFFFFFu;
+}
+
 struct DecParams {
     const uint8_t* blob;
     long long nbytes;
@@ -79,6 +95,13 @@ struct DecParams {
     unsigned long long* seg_map;
     const unsigned long long* seg_entry;
     int no_store;
+    // index-less decode (apax_decode without offsets), see IlGate: d3 with
+    // il_gate set and TP 0 decodes the speculative segments (seg_part 1: the
+    // full-block segments, 2: the last one, 0: all), checking every block's
+    // length against the speculative offsets; the two-pass kernels with
+    // il_gate set run only when that path was not taken or failed
+    IlGate* il_gate;
+    int seg_part;
 };
 
 // kernel launches enqueued by the library (apax_launch_count)
@@ -111,6 +134,10 @@ size_t decode_v3_smem_bytes(int dt, int payload_cap);
 bool decode_v3_supported(int dt, int bs);
 int decode_v3_resident_ctas(int dt, size_t smem);
 int launch_decode_v3(int dt, const DecParams& P, int grid, size_t smem, cudaStream_t st);
+int launch_decode_v3_seg_dev(int dt, DecParams P, int grid, size_t smem, cudaStream_t st);
+// index-less speculation (apax_k5.cu): signature scan + speculative offsets
+int launch_k5_speculate(const uint8_t* blob, long long nbytes, int dt, long long n_blocks, long long* offsets,
+                        void* ws, IlGate* gate, cudaStream_t st);
 int launch_decode_v3_two_pass(int dt, DecParams P, int grid, size_t smem, unsigned long long* scratch,
                               cudaStream_t st);
 size_t decode_v2_smem_bytes(int dt, int bs, int payload_cap);
@@ -129,10 +156,14 @@ int profile_select(const void* x, const void* y, long long n, int dt, int pass,
 int launch_walk(const uint8_t* blob, long long nbytes, long long n, int bs, int dt, long long n_blocks,
                 long long* offsets, unsigned long long* status, cudaStream_t st);
 int launch_walk_after_k5(const uint8_t* blob, long long nbytes, long long n, int bs, int dt, long long n_blocks,
-                         long long* offsets, unsigned long long* status, const int* k5_fail, cudaStream_t st);
+                         long long* offsets, unsigned long long* status, const int* k5_fail, cudaStream_t st,
+                         const IlGate* gate = nullptr);
 // K5 index-less block discovery (apax_k5.cu); ws of find_blocks_k5_ws_bytes
 size_t find_blocks_k5_ws_bytes(long long n_blocks);
+// gate non-null: the discovery after launch_k5_speculate (scan reused),
+// every kernel returns at once while il_seg_ok(gate)
 int launch_find_blocks_k5(const uint8_t* blob, long long nbytes, long long n, int bs, int dt, long long n_blocks,
-                          long long* offsets, unsigned long long* status, void* ws, cudaStream_t st);
+                          long long* offsets, unsigned long long* status, void* ws, cudaStream_t st,
+                          const IlGate* gate = nullptr);
 
 }  // namespace apax
