@@ -132,3 +132,93 @@ def test_k5_bench_size_cfg2_indexless_decode():
     y = decode_device(res.blob, res.nbytes).cpu().numpy()
     y2 = decode_device(res.blob, res.nbytes, res.block_offsets).cpu().numpy()
     assert np.array_equal(y, y2)
+
+
+def _gpu_indexless(blob: bytes, n, dt):
+    """apax_decode without offsets (signature scan + speculative segment
+    decode, full discovery + two-pass decode gated on the device)."""
+    from paper_1303_4994_b200 import Decoder
+    d = torch.zeros(len(blob) + 64, dtype=torch.uint8, device="cuda")
+    d[:len(blob)] = torch.from_numpy(np.frombuffer(blob, np.uint8).copy()).cuda()
+    dec = Decoder(n, dt, 4096)
+    dec.decode(d, len(blob), None)
+    torch.cuda.synchronize()
+    key = int(dec.status.cpu().numpy().view(np.uint64)[1])
+    if key != (1 << 64) - 1:
+        return ("err", key & 0xFF, key >> 8)
+    return ("ok", dec.y[:n].cpu().numpy())
+
+
+def _oracle_indexless(blob: bytes):
+    from oracle import oracle as O
+    try:
+        return ("ok", O.decode(blob, None, nthreads=0))
+    except O.OracleError as e:
+        return ("err", e.code, e.detail)
+
+
+def _same(a, b):
+    return a[0] == b[0] and (np.array_equal(a[1], b[1]) if a[0] == "ok" else a[1:] == b[1:])
+
+
+def test_indexless_speculation_matches_oracle():
+    """Containers that defeat the speculation (one candidate per block, the
+    first at byte 28) in every way it can be defeated: the decode must equal
+    the reference's walk-based decode (oracle), samples or first error."""
+    x = W.cfg2_ar2_f32(4096 * 24 + 1000)
+    n = x.size
+    res = encode_device(torch.from_numpy(x).cuda(),
+                        StreamConfig(Dtype.F32, 4096, Mode.FIXED_QUALITY, 60.0, segment_blocks=4))
+    blob = bytearray(res.to_bytes())
+    offs = res.block_offsets.cpu().numpy()
+    cases = {"clean": bytes(blob)}
+    # a reserved header byte set: still a block for the reference, no longer
+    # a candidate -> one candidate short
+    c = bytearray(blob)
+    c[int(offs[5]) + 3] = 1
+    cases["reserved_byte"] = bytes(c)
+    # ... plus a decoy signature in block 9's mantissas: one candidate per
+    # block again, at the wrong places -> the decode's length check
+    d = bytearray(c)
+    p = int(offs[10]) - 40
+    d[p:p + 7] = bytes([0, 0, 0, 0, 0, 0, 0xF0])
+    cases["reserved_byte_and_decoy"] = bytes(d)
+    # a segment head without its restart flag: the history runs on
+    c = bytearray(blob)
+    c[int(offs[8])] &= 0xFB
+    cases["head_without_restart"] = bytes(c)
+    # an extra restart inside a segment (the reference resets the history)
+    c = bytearray(blob)
+    c[int(offs[6])] |= 0x04
+    cases["extra_restart"] = bytes(c)
+    # errors: reserved selector, reserved JEE nibble, truncations
+    for b in (0, 9, 24):
+        c = bytearray(blob)
+        c[int(offs[b])] = (c[int(offs[b])] & 0xFC) | 3
+        cases[f"selector3_b{b}"] = bytes(c)
+        c = bytearray(blob)
+        c[int(offs[b]) + 6] = 0xE0
+        cases[f"nibble14_b{b}"] = bytes(c)
+    cases["truncated_mid"] = bytes(blob[: int(offs[13]) + 9])
+    cases["truncated_tail"] = bytes(blob[: len(blob) - 5])
+    for name, cb in cases.items():
+        a, b = _gpu_indexless(cb, n, Dtype.F32), _oracle_indexless(cb)
+        assert _same(a, b), (name, a[:1] + a[1:] if a[0] == "err" else "ok", b[:1] + b[1:] if b[0] == "err" else "ok")
+
+
+@pytest.mark.parametrize("dt,mode,target,seg", [(Dtype.I16, Mode.FIXED_RATE, 4.0, 7), (Dtype.F64, Mode.FIXED_RATE, 20.0, 3),
+                                                (Dtype.I32, Mode.FIXED_QUALITY, 40.0, 5), (Dtype.F32, Mode.LOSSLESS, 0.0, 0)])
+def test_indexless_speculation_dtypes(dt, mode, target, seg):
+    """Segmented (speculative path) and whole-stream (full discovery +
+    two-pass) containers of other dtypes, partial last block included."""
+    if dt is Dtype.F32 and mode is Mode.LOSSLESS:
+        dt = Dtype.I8
+    rng = np.random.default_rng(77)
+    n = 4096 * 19 + 123
+    xf = np.cumsum(rng.standard_normal(n)) * 30.0
+    x = xf.astype(dt.np_dtype) if dt.is_float else np.clip(xf, np.iinfo(dt.np_dtype).min,
+                                                             np.iinfo(dt.np_dtype).max).astype(dt.np_dtype)
+    res = encode_device(torch.from_numpy(x).cuda(), StreamConfig(dt, 4096, mode, target, segment_blocks=seg or None))
+    blob = res.to_bytes()
+    a, b = _gpu_indexless(blob, n, dt), _oracle_indexless(blob)
+    assert _same(a, b)
