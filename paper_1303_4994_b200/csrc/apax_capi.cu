@@ -194,18 +194,35 @@ __global__ void detect_segments_kernel(const uint8_t* blob, long long nbytes, co
     if (threadIdx.x == 0) out[0] = (P == ~0ULL || broken) ? 0ULL : P;
 }
 
-// index-less decode: the first restarting block > 0 on the speculative
-// offsets (the segment length of a segmented container) -> gate->first
+// index-less decode: the first restarting block > 0 (the segment length of
+// a segmented container) -> target->first.  The speculative pass (skip
+// null) runs on the candidate offsets when the scan found one per block;
+// the second (after the full discovery, skip = the first gate) only when
+// the speculation failed, and clears target->gp on a discovery error.
 __global__ void seg_first_kernel(const uint8_t* blob, long long nbytes, const long long* offs, long long nb,
-                                 IlGate* gate) {
-    if (!gate->spec) return;
+                                 IlGate* target, const IlGate* skip, const unsigned long long* status) {
+    if (skip && il_seg_ok(skip)) return;
+    if (!target->spec) return;
     const long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (status && i0 == 0 && status[1] != ~0ULL) atomicExch(&target->gp, 0u);
     unsigned long long mine = ~0ULL;
+    bool bad = false;
     for (long long b = 1 + i0; b < nb; b += (long long)gridDim.x * blockDim.x) {
         const long long o = offs[b];
-        if (o >= 0 && o < nbytes && ((blob[o] >> 2) & 1) && (unsigned long long)b < mine) mine = (unsigned long long)b;
+        if (o < 0 || o >= nbytes) { bad = true; continue; }
+        if (((blob[o] >> 2) & 1) && (unsigned long long)b < mine) mine = (unsigned long long)b;
     }
-    if (mine != ~0ULL) atomicMin(&gate->first, mine);
+    if (mine != ~0ULL) atomicMin(&target->first, mine);
+    if (bad && status) atomicExch(&target->gp, 0u);
+}
+
+static int seg_first_grid(long long nb) {
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    long long g = (nb + 255) / 256;
+    if (g > nsm) g = nsm;
+    return (int)(g < 1 ? 1 : g);
 }
 
 // status words to pinned host memory by plain stores from an SM: a copy-engine
@@ -654,15 +671,12 @@ int apax_decode(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, int b
             // offsets (checked block by block by the segment decode below);
             // the full discovery runs only when that path is not taken
             gate = (IlGate*)(w + p.ws_ticket + 64);
+            if (cudaMemsetAsync(w + p.ws_ticket + 96, 0xFF, 16, s) != cudaSuccess) return APAX_ERR_CUDA;   // gate 2
             st = launch_k5_speculate(blob, nbytes, dtype, p.n_blocks, wo, w + p.ws_k5, gate, s);
             if (st) return st;
-            int dev = 0, nsm = 148;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-            long long sgrid = (p.n_blocks + 255) / 256;
-            if (sgrid > nsm) sgrid = nsm;
             note_launches(1);
-            seg_first_kernel<<<(int)sgrid, 256, 0, s>>>(blob, nbytes, wo, p.n_blocks, gate);
+            seg_first_kernel<<<seg_first_grid(p.n_blocks), 256, 0, s>>>(blob, nbytes, wo, p.n_blocks, gate, nullptr,
+                                                                       nullptr);
             if (cudaGetLastError() != cudaSuccess) return APAX_ERR_CUDA;
         } else if (k5) {
             st = launch_find_blocks_k5(blob, nbytes, n, block_size, dtype, p.n_blocks, wo,
@@ -691,14 +705,23 @@ int apax_decode(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, int b
         const int g3 = decode_v3_resident_ctas(dtype, sm3);
         if (gate) {
             // the speculative segment decode; then (gated on the device) the
-            // full discovery and the two-pass decode for everything it did
-            // not take: whole-stream containers, other candidate sets, any
-            // inconsistency or error
+            // full discovery for everything it did not take (whole-stream
+            // containers, other candidate sets, any inconsistency or error),
+            // the segment decode on the verified offsets when they show
+            // segments, else the two-pass decode
+            IlGate* gate2 = (IlGate*)(w + p.ws_ticket + 96);
             P.il_gate = gate;
             st = launch_decode_v3_seg_dev(dtype, P, g3, sm3, s);
             if (st) return st;
             st = launch_find_blocks_k5(blob, nbytes, n, block_size, dtype, p.n_blocks, (long long*)offs,
                                        (unsigned long long*)status, w + p.ws_k5, s, gate);
+            if (st) return st;
+            note_launches(1);
+            seg_first_kernel<<<seg_first_grid(p.n_blocks), 256, 0, s>>>(blob, nbytes, offs, p.n_blocks, gate2, gate,
+                                                                       (const unsigned long long*)status);
+            if (cudaGetLastError() != cudaSuccess) return APAX_ERR_CUDA;
+            P.il_gate2 = gate2;
+            st = launch_decode_v3_seg_dev(dtype, P, g3, sm3, s);
             if (st) return st;
         }
         // any container through the segment-serial decoder: one-wave pseudo-

@@ -150,17 +150,20 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
     long long s_begin = P.seg_begin, s_end = P.seg_end;
     // index-less decode: the speculative segment path (TP 0) or the two-pass
     // decode that replaces it (TP 1, 2) -- exactly one of them runs
-    const bool spec = TP == 0 && P.il_gate;
+    const bool spec = TP == 0 && P.il_gate && !P.il_gate2;
+    IlGate* hg = nullptr;   // the gate a segment head without a restart flag clears
     if (P.il_gate) {
-        const bool seg_ok = il_seg_ok(P.il_gate);
+        const bool ok1 = il_seg_ok(P.il_gate);
+        const bool ok2 = P.il_gate2 && il_seg_ok(P.il_gate2);
         if (TP == 0) {
-            if (!seg_ok) return;
-            P_seg = (long long)P.il_gate->first;
+            if (P.il_gate2 ? (ok1 || !ok2) : !ok1) return;
+            hg = P.il_gate2 ? P.il_gate2 : P.il_gate;
+            P_seg = (long long)hg->first;
             const long long nseg = (P.n_blocks + P_seg - 1) / P_seg;
             const long long sfull = (P.n % bs) ? nseg - 1 : nseg;
             s_begin = P.seg_part == 2 ? sfull : 0;
             s_end = P.seg_part == 1 ? sfull : nseg;
-        } else if (seg_ok) {
+        } else if (ok1 || ok2) {
             return;
         }
     }
@@ -338,7 +341,7 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
             const int sel = ji.x & 3, restart = (ji.x >> 2) & 1;   // scale code, fbe: S->dq
             // speculative segments: a segment head without a restart flag
             // sends the container to the two-pass decode
-            if (spec && b == b0 && b0 > 0 && !restart && tid == 0) atomicExch(&P.il_gate->gp, 0u);
+            if (hg && b == b0 && b0 > 0 && !restart && tid == 0) atomicExch(&hg->gp, 0u);
             if (!err) err = (sel == 3) ? APAX_ERR_SELECTOR : ji.y;
             const int used = ji.z;
             const bool bnarrow = ji.w <= 16;
@@ -705,8 +708,8 @@ static int launch_d3_range(int dt, bool fix, const DecParams& P, long long s0, l
 // entries of a two-pass decode: e_0 = (0, 0), e_{k+1} = F_k(e_k) (one thread;
 // a few hundred segments)
 __global__ void compose_entries_kernel(const unsigned long long* maps, long long nseg, unsigned long long* entries,
-                                       const IlGate* gate) {
-    if (gate && il_seg_ok(gate)) return;
+                                       const IlGate* gate, const IlGate* gate2) {
+    if (gate && (il_seg_ok(gate) || (gate2 && il_seg_ok(gate2)))) return;
     unsigned long long h1 = 0, h2 = 0;
     for (long long k = 0; k < nseg; k++) {
         entries[2 * k] = h1;
@@ -736,7 +739,7 @@ int launch_decode_v3_two_pass(int dt, DecParams P, int grid, size_t smem, unsign
     int r = launch_decode_v3_tp(dt, P, grid, smem, st, 1);
     if (r) return r;
     note_launches(1);
-    compose_entries_kernel<<<1, 1, 0, st>>>(maps, nseg, entries, P.il_gate);
+    compose_entries_kernel<<<1, 1, 0, st>>>(maps, nseg, entries, P.il_gate, P.il_gate2);
     if (cudaGetLastError() != cudaSuccess) return APAX_ERR_CUDA;
     P.seg_map = nullptr;
     P.seg_entry = entries;

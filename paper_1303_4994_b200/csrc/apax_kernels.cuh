@@ -101,6 +101,11 @@ struct DecParams {
     // length against the speculative offsets; the two-pass kernels with
     // il_gate set run only when that path was not taken or failed
     IlGate* il_gate;
+    // the second chance of an index-less decode: after the full discovery
+    // (the speculation failed, e.g. a false candidate in integer data), the
+    // segment path on the verified offsets (il_gate2->first, normal error
+    // reports); the two-pass kernels then run only when neither path did
+    IlGate* il_gate2;
     int seg_part;
 };
 
