@@ -1914,7 +1914,10 @@ int launch_encode_v3(int dt, const EncParams& P, int grid, size_t smem, cudaStre
     if (fixable && (P.n % v3::MAXBS) != 0) ufull = P.n_units - 1;
     if (!fixable) ufull = 0;
     if (ufull > 0) {
-        const int r = launch_v3_range(dt, true, P, 0, ufull, grid, smem, st);
+        // segments of full blocks: the v5 kernel (pack warps + a service warp)
+        // when it takes the container, else the fused v3 kernel
+        const bool use5 = fixable && encode_v5_supported(dt, P.bs, P.mode, P);
+        const int r = use5 ? launch_encode_v5(dt, P, 0, ufull, st) : launch_v3_range(dt, true, P, 0, ufull, grid, smem, st);
         if (r) return r;
     }
     if (ufull < P.n_units) return launch_v3_range(dt, false, P, ufull, P.n_units, grid, smem, st);

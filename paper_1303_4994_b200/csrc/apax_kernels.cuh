@@ -50,7 +50,12 @@ struct EncParams {
     // for integer containers, the dequantizer's clip range (codec.py:143-145)
     int wire;
     long long clip_lo, clip_hi;
-    BlockMeta* meta;              // split encoder: the chain's per-block records (v3 META)
+    BlockMeta* meta;              // v5 (apax_encode_v5.cu): segments of full 4096-sample blocks, pack warps + a service warp
+size_t encode_v5_smem_bytes(int dt);
+bool encode_v5_supported(int dt, int bs, int mode, const EncParams& P);
+int encode_v5_resident_ctas(int dt);
+int launch_encode_v5(int dt, const EncParams& P, long long u0, long long u1, cudaStream_t st);
+// split encoder: the chain's per-block records (v3 META)
     apax_block_state* state;      // generic kernel, one unit: CodecState in / out (encode_block)
     double* stats;                // fixed-quality chain: per block sum x^2, sum x*y, sum y*y (y = the decode)
     int count_only;               // packer: container length only, no output written
@@ -123,6 +128,11 @@ bool encode_v3_supported(int dt, int bs);
 int encode_v3_resident_ctas(int dt, size_t smem);
 int encode_v3_resident_ctas_wave(int dt, size_t smem);
 int launch_encode_v3(int dt, const EncParams& P, int grid, size_t smem, cudaStream_t st);
+// v5 (apax_encode_v5.cu): segments of full 4096-sample blocks, pack warps + a service warp
+size_t encode_v5_smem_bytes(int dt);
+bool encode_v5_supported(int dt, int bs, int mode, const EncParams& P);
+int encode_v5_resident_ctas(int dt);
+int launch_encode_v5(int dt, const EncParams& P, long long u0, long long u1, cudaStream_t st);
 // split encoder: the chain (v3 with META: quantizer records, no output) and
 // the block-parallel packer (apax_encode_v4.cu)
 int launch_encode_v3_chain(int dt, const EncParams& P, size_t smem, cudaStream_t st);
