@@ -82,11 +82,23 @@ struct __align__(16) St {
     int mbw[NPW];
     int monc[NPW], monf[NPW];
     int hq[2][2];              // history entering the next block: q[n-1], q[n-2]
+    unsigned pkw[2][NPW], pnw[2][NPW];   // per-warp peak partials of the next pass's block
     long long slot_len, slot_b0, slot_b1, fin_prefix;
 };
 static_assert(sizeof(St) <= ST_BYTES, "St too large");
 
 using namespace apax::tma;
+
+#ifdef APAX_V5_TIMES
+// per-CTA timeline (tools/cta_times.py): globaltimer at start, at the end of
+// the last unit's coding, at exit; SM id
+__device__ unsigned long long g_times[8192 * 4];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
 
 // ---------------------------------------------------------------------------
 // helpers
@@ -95,7 +107,8 @@ template <int ID, int N> __device__ __forceinline__ void bar_sync() { asm volati
 template <int ID, int N> __device__ __forceinline__ void bar_arrive() { asm volatile("bar.arrive %0, %1;" :: "n"(ID), "n"(N) : "memory"); }
 // barrier ids: 1 quantizer ready (service -> pack), 2 window ready + widths done
 // (service -> pack, pack <-> pack), 3 results ready (pack -> service), 4 window
-// complete (pack -> service), 5 pack-only, 7 unit end (everyone)
+// complete (pack -> service), 5 pack-only, 6 next block's peak ready (pack ->
+// service), 7 unit end (everyone)
 __device__ __forceinline__ int bitlen32(unsigned v) {
     int r;
     asm("bfind.u32 %0, %1;" : "=r"(r) : "r"(v));
@@ -453,8 +466,20 @@ __device__ __noinline__ void final_place(long long u, long long n_units, long lo
 // ---------------------------------------------------------------------------
 // the service warp: one unit
 // ---------------------------------------------------------------------------
+// what the service warp needs of the launch parameters (by value: a reference
+// to the kernel's parameter block would force a local copy of it)
+struct SvcArgs {
+    const void* x;
+    unsigned long long* status;
+    unsigned long long* lookback;
+    long long* block_offsets;
+    double* trace;
+    double target, att_lo, pow10_t20, sqrt12;
+    int mode;
+};
+
 template <int DT>
-__device__ __noinline__ void service_unit(const EncParams& P, St* S, unsigned char* xb0, uint32_t* win, uint8_t* slot,
+__device__ __noinline__ void service_unit(const SvcArgs P, St* S, unsigned char* xb0, uint32_t* win, uint8_t* slot,
                                           long long u, long long b0, long long b1, bool warm, uint32_t& phs) {
     using Tr = DT_<DT>;
     using T = typename Tr::T;
@@ -484,6 +509,7 @@ __device__ __noinline__ void service_unit(const EncParams& P, St* S, unsigned ch
     long long wbase = 0;
     uint32_t tail[4] = {0u, 0u, 0u, 0u};
     bool store_pending = false;
+    unsigned pk0 = 0, pn0 = 0;          // the first block's peak (warm_self codes it twice)
 
     // store the finished block of pass pk (block pb) to the slot and clean the window
     auto flush = [&](int pk, long long pb) {
@@ -520,32 +546,36 @@ __device__ __noinline__ void service_unit(const EncParams& P, St* S, unsigned ch
         const int buf = (int)(bi & 1);
         const unsigned char* xb = xb0 + buf * XB;
         const bool emit = !pre;
-        mbar_wait(&S->full[buf], (phs >> buf) & 1u);
-        // ---- peak of the block (+ pairwise x^2 for the fixed-quality init) ----
+        // ---- peak of the block: the first pass reads it here, later passes take
+        // the pack warps' partials (computed during the previous pass) ----
         unsigned pk = 0, pn = 0;
-        if (NEED_PEAK) {
-            int ms = 0;
-            unsigned mu = 0;
-            int mx = 0, mn = 0;
+        if (kp == 0) {
+            mbar_wait(&S->full[buf], (phs >> buf) & 1u);
+            if (NEED_PEAK) {
+                int ms = 0;
+                unsigned mu = 0;
+                int mx = 0, mn = 0;
 #pragma unroll 4
-            for (int k = 0; k < 32; k++) {
-                const uint4 v = *(const uint4*)(xb + k * LB + 16 * lane);
-                if (DT == 3) {
-                    ms = __vimax3_s32(ms, (int)v.x, (int)v.y);
-                    ms = __vimax3_s32(ms, (int)v.z, (int)v.w);
-                    mu = __vimax3_u32(mu, v.x, v.y);
-                    mu = __vimax3_u32(mu, v.z, v.w);
-                } else {
-                    mx = __vimax3_s32(mx, (int)v.x, (int)v.y);
-                    mx = __vimax3_s32(mx, (int)v.z, (int)v.w);
-                    mn = __vimin3_s32(mn, (int)v.x, (int)v.y);
-                    mn = __vimin3_s32(mn, (int)v.z, (int)v.w);
+                for (int k = 0; k < 32; k++) {
+                    const uint4 v = *(const uint4*)(xb + k * LB + 16 * lane);
+                    if (DT == 3) {
+                        ms = __vimax3_s32(ms, (int)v.x, (int)v.y);
+                        ms = __vimax3_s32(ms, (int)v.z, (int)v.w);
+                        mu = __vimax3_u32(mu, v.x, v.y);
+                        mu = __vimax3_u32(mu, v.z, v.w);
+                    } else {
+                        mx = __vimax3_s32(mx, (int)v.x, (int)v.y);
+                        mx = __vimax3_s32(mx, (int)v.z, (int)v.w);
+                        mn = __vimin3_s32(mn, (int)v.x, (int)v.y);
+                        mn = __vimin3_s32(mn, (int)v.z, (int)v.w);
+                    }
                 }
+                if (DT == 3) { pk = (unsigned)ms; pn = mu; }
+                else { pk = (unsigned)mx; pn = (unsigned)(-(long long)mn); }
+                pk = (unsigned)__reduce_max_sync(0xffffffffu, (int)pk);
+                pn = __reduce_max_sync(0xffffffffu, pn);
             }
-            if (DT == 3) { pk = (unsigned)ms; pn = mu; }
-            else { pk = (unsigned)mx; pn = (unsigned)(-(long long)mn); }
-            pk = (unsigned)__reduce_max_sync(0xffffffffu, (int)pk);
-            pn = __reduce_max_sync(0xffffffffu, pn);
+            pk0 = pk; pn0 = pn;
         }
         double px0 = 0.0;
         if (FQ && emit && !initialized) {
@@ -568,8 +598,8 @@ __device__ __noinline__ void service_unit(const EncParams& P, St* S, unsigned ch
             px0 = t;
         }
         if (kp > 0) bar_sync<3, NT>();      // the previous pass's results
+        int bad = 0;
         if (lane == 0) {
-            int bad = 0;
             // ---- the loops on the previous pass's results ----
             if (kp > 0) {
                 const Res* R = &S->res[(kp - 1) & 1];
@@ -606,6 +636,17 @@ __device__ __noinline__ void service_unit(const EncParams& P, St* S, unsigned ch
                     emitted += 1;
                 }
             }
+        }
+        if (kp > 0) {
+            bar_sync<6, NT>();              // this pass's peak partials
+            if (warm && kp == 1) { pk = pk0; pn = pn0; }
+            else if (NEED_PEAK) {
+                const int w = lane & (NPW - 1);
+                pk = (unsigned)__reduce_max_sync(0xffffffffu, DT == 3 ? (int)S->pkw[kp & 1][w] : (int)S->pkw[kp & 1][w]);
+                pn = __reduce_max_sync(0xffffffffu, S->pnw[kp & 1][w]);
+            }
+        }
+        if (lane == 0) {
             // ---- S1: gain, scale code, quantizer (codec.py:94-132) ----
             double peak;
             bool nonfin = false;
@@ -618,7 +659,7 @@ __device__ __noinline__ void service_unit(const EncParams& P, St* S, unsigned ch
             } else {
                 peak = (double)((pk > pn) ? pk : pn);
             }
-            if (nonfin) cold_nonfinite<DT>(xb, b * (long long)BS, P.status);
+            if (nonfin) { mbar_wait(&S->full[buf], (phs >> buf) & 1u); cold_nonfinite<DT>(xb, b * (long long)BS, P.status); }
             if (emit && !initialized) {
                 if (FQ) {  // _init_attenuation (codec.py:155-168)
                     const double rms = sqrt(px0 / (double)BS);
@@ -696,7 +737,6 @@ __device__ __noinline__ void service_unit(const EncParams& P, St* S, unsigned ch
             if (!ppre) {
                 const long long pbi = warm ? kp - 2 : kp - 1;
                 flush((int)(kp - 1), b0 + pbi);
-                if (b0 + pbi + 2 < b1) stage(b0 + pbi + 2, (int)(pbi & 1));
             }
         }
         __threadfence_block();
@@ -742,7 +782,8 @@ __device__ __forceinline__ void pack_unit(const EncParams& P, St* S, unsigned ch
     constexpr int LB = leaf_bytes(DT);
     constexpr int LS = LB / (int)sizeof(T);     // leaf stride in samples
     constexpr int XB = x_bytes(DT);
-    constexpr bool SQX = (DT != 2);
+ constexpr bool SQX = (DT != 2);
+    constexpr bool NEED_PEAK = F || DT == 2;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool FQ = (P.mode == 2);
     const long long npass = (warm ? 1 : 0) + (b1 - b0);
@@ -765,6 +806,18 @@ __device__ __forceinline__ void pack_unit(const EncParams& P, St* S, unsigned ch
         mbar_wait(&S->full[buf], (phs >> buf) & 1u);
         if (emit) phs ^= 1u << buf;
         const T* xl = (const T*)(xb0 + buf * XB) + (tid >> 3) * LS;   // this thread's leaf
+        // the other buffer's block is finished (every pack thread is past its
+        // emission): stage the next block into it, four leaves per warp
+        const bool has_next = b + 1 < b1;
+        if (emit && bi >= 1 && has_next) {
+            const int nbuf = buf ^ 1;
+            if (tid == 0) mbar_expect(&S->full[nbuf], (uint32_t)(BS * sizeof(T)));
+            if (lane < 4) {
+                const int leaf = 4 * warp + lane;
+                bulk_load(xb0 + nbuf * XB + leaf * LB, (const T*)P.x + (b + 1) * (long long)BS + leaf * 128,
+                          (uint32_t)(128 * sizeof(T)), &S->full[nbuf]);
+            }
+        }
 
         // ---- fixed-quality sums, numpy's pairwise order (codec.py:248-249) ----
         if (FQ) {
@@ -892,6 +945,7 @@ __device__ __forceinline__ void pack_unit(const EncParams& P, St* S, unsigned ch
             }
             __threadfence_block();
             bar_arrive<3, NT>();
+            bar_arrive<6, NT>();
             bar_arrive<4, NT>();
             continue;
         }
@@ -1013,6 +1067,43 @@ __device__ __forceinline__ void pack_unit(const EncParams& P, St* S, unsigned ch
             __threadfence_block();
             bar_arrive<3, NT>();
         }
+        // ---- peak of the next block (staged at the start of this pass) for the
+        // service warp's next quantizer ----
+        if (NEED_PEAK && has_next) {
+            const int nbuf = buf ^ 1;
+            mbar_wait(&S->full[nbuf], (phs >> nbuf) & 1u);
+            const uint4* xn = (const uint4*)((const T*)(xb0 + nbuf * XB) + (tid >> 3) * LS + SPT * (tid & 7));
+            unsigned pk, pn;
+            if (DT == 3) {
+                int ms = 0;
+                unsigned mu = 0;
+#pragma unroll
+                for (int m = 0; m < 4; m++) {
+                    const uint4 v = xn[m];
+                    ms = __vimax3_s32(ms, (int)v.x, (int)v.y);
+                    ms = __vimax3_s32(ms, (int)v.z, (int)v.w);
+                    mu = __vimax3_u32(mu, v.x, v.y);
+                    mu = __vimax3_u32(mu, v.z, v.w);
+                }
+                pk = (unsigned)__reduce_max_sync(0xffffffffu, ms);
+                pn = __reduce_max_sync(0xffffffffu, mu);
+            } else {
+                int mx = 0, mi = 0;
+#pragma unroll
+                for (int m = 0; m < 4; m++) {
+                    const uint4 v = xn[m];
+                    mx = __vimax3_s32(mx, (int)v.x, (int)v.y);
+                    mx = __vimax3_s32(mx, (int)v.z, (int)v.w);
+                    mi = __vimin3_s32(mi, (int)v.x, (int)v.y);
+                    mi = __vimin3_s32(mi, (int)v.z, (int)v.w);
+                }
+                pk = (unsigned)__reduce_max_sync(0xffffffffu, mx);
+                pn = (unsigned)(-(long long)__reduce_min_sync(0xffffffffu, mi));
+            }
+            if (lane == 0) { S->pkw[(kp + 1) & 1][warp] = pk; S->pnw[(kp + 1) & 1][warp] = pn; }
+        }
+        __threadfence_block();
+        bar_arrive<6, NT>();
 
         // ---- JEE tokens + mantissas into the window ----
         if (!bad) {
@@ -1113,6 +1204,14 @@ __global__ void __launch_bounds__(NT, 4) encode_v5_kernel(EncParams P) {
     uint32_t* win = (uint32_t*)(smem + ST_BYTES + 2 * x_bytes(DT));
     const int tid = threadIdx.x, warp = tid >> 5;
     uint8_t* slot = P.slots + (long long)blockIdx.x * P.slot_bytes;
+#ifdef APAX_V5_TIMES
+    if (tid == 0 && blockIdx.x < 8192) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+        g_times[4 * blockIdx.x] = gtimer();
+        g_times[4 * blockIdx.x + 3] = smid;
+    }
+#endif
     if (tid == 0) {
         mbar_init(&S->full[0]);
         mbar_init(&S->full[1]);
@@ -1126,8 +1225,18 @@ __global__ void __launch_bounds__(NT, 4) encode_v5_kernel(EncParams P) {
     for (long long u = P.unit_begin + blockIdx.x; u < P.unit_end; u += gridDim.x) {
         const long long b0 = u * P.unit_blocks;
         const long long b1 = (b0 + P.unit_blocks < P.n_blocks) ? b0 + P.unit_blocks : P.n_blocks;
-        if (warp == NPW) service_unit<DT>(P, S, xb0, win, slot, u, b0, b1, warm, phs_v);
-        else pack_unit<DT>(P, S, xb0, win, b0, b1, warm, phs);
+        if (warp == NPW) {
+            SvcArgs A;
+            A.x = P.x; A.status = P.status; A.lookback = P.lookback; A.block_offsets = P.block_offsets;
+            A.trace = P.trace; A.target = P.target; A.att_lo = P.att_lo; A.pow10_t20 = P.pow10_t20;
+            A.sqrt12 = P.sqrt12; A.mode = P.mode;
+            service_unit<DT>(A, S, xb0, win, slot, u, b0, b1, warm, phs_v);
+        } else {
+            pack_unit<DT>(P, S, xb0, win, b0, b1, warm, phs);
+        }
+#ifdef APAX_V5_TIMES
+        if (tid == 0 && blockIdx.x < 8192) g_times[4 * blockIdx.x + 1] = gtimer();
+#endif
         if (u == 0 && tid < kFileHeader) {
             unsigned char h[kFileHeader];
             h[0] = 'A'; h[1] = 'P'; h[2] = 'A'; h[3] = 'X';
@@ -1140,9 +1249,18 @@ __global__ void __launch_bounds__(NT, 4) encode_v5_kernel(EncParams P) {
         }
         final_place(u, P.n_units, P.n_blocks, P.lookback, P.status, P.block_offsets, P.out, S, slot);
     }
+#ifdef APAX_V5_TIMES
+    if (tid == 0 && blockIdx.x < 8192) g_times[4 * blockIdx.x + 2] = gtimer();
+#endif
 }
 
 }  // namespace v5
+
+#ifdef APAX_V5_TIMES
+extern "C" int apax_debug_cta_times5(unsigned long long* host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, v5::g_times, (size_t)n * 4 * sizeof(unsigned long long));
+}
+#endif
 
 size_t encode_v5_smem_bytes(int dt) { return (size_t)v5::ST_BYTES + 2 * (size_t)v5::x_bytes(dt) + (size_t)v5::win_bytes(dt); }
 

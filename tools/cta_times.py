@@ -32,7 +32,7 @@ enc.finish()
 L = _lib.lib()
 ng = (16384 + seg - 1) // seg
 buf = np.zeros(ng * 4, np.uint64)
-L.apax_debug_cta_times(buf.ctypes.data_as(ctypes.c_void_p), ng)
+getattr(L, os.environ.get("TIMES_FN", "apax_debug_cta_times"))(buf.ctypes.data_as(ctypes.c_void_p), ng)
 t = buf.reshape(-1, 4).astype(np.int64)
 t0 = t[:, 0].min()
 st, ce, ex = (t[:, 0] - t0) / 1e3, (t[:, 1] - t0) / 1e3, (t[:, 2] - t0) / 1e3
