@@ -89,6 +89,9 @@ static_assert(sizeof(St) <= ST_BYTES, "St too large");
 
 using namespace apax::tma;
 
+#ifdef APAX_V5_PROF
+__device__ unsigned long long g_prof[16];
+#endif
 #ifdef APAX_V5_TIMES
 // per-CTA timeline (tools/cta_times.py): globaltimer at start, at the end of
 // the last unit's coding, at exit; SM id
@@ -159,6 +162,33 @@ __device__ __forceinline__ void mbar_expect(unsigned long long* bar, uint32_t by
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  :: "r"(sa(dst)), "l"(src), "r"(bytes), "r"(sa(bar)) : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst), "l"(src) : "memory");
+}
+// one net arrival per pack thread once its earlier cp.async copies have landed
+__device__ __forceinline__ void stage_arrive(unsigned long long* bar) {
+    asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" :: "r"(sa(bar)) : "memory");
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" :: "r"(sa(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_init_n(unsigned long long* b, int n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(sa(b)), "r"(n) : "memory");
+}
+// block b of the stream into a staging buffer, padded leaf layout: 16-byte
+// chunk c of the block (c = tid + 256 k) goes to leaf c >> 5, chunk c & 31
+// (i16: 16 chunks per leaf), all at immediate offsets from two per-thread bases
+template <int DT>
+__device__ __forceinline__ void stage_block(unsigned char* xbuf, const void* src, unsigned long long* bar) {
+    constexpr int LB = leaf_bytes(DT);
+    constexpr int CPL = 128 * dtw(DT) / 16;            // chunks per leaf (32 or 16)
+    constexpr int NCH = BS * dtw(DT) / 16;             // chunks per block
+    const int tid = threadIdx.x;
+    const uint32_t d0 = sa(xbuf) + (uint32_t)((tid / CPL) * LB + (tid % CPL) * 16);
+    const unsigned char* s0 = (const unsigned char*)src + tid * 16;
+#pragma unroll
+    for (int k = 0; k < NCH / NPT; k++)
+        cp_async16(d0 + (uint32_t)(k * (NPT / CPL) * LB), s0 + k * NPT * 16);
+    stage_arrive(bar);
 }
 __device__ __forceinline__ double warp_tree8(const double* v) {
     return ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
@@ -408,6 +438,12 @@ __device__ __forceinline__ long long unit_prefix(unsigned long long* lookback, l
     long long prefix = 0;
     long long kk = u - 1;
     unsigned nap = 256;
+    // most of the wait is for the neighbours to finish coding: one lane
+    // polls the predecessor's word (cheap) before the 32-wide look-back
+    if (lane == 0) {
+        while (ld_acquire(&lookback[u - 1]) == 0ULL) __nanosleep(1000);
+    }
+    __syncwarp();
     for (;;) {
         const long long idx = kk - lane;
         const unsigned long long v = (idx >= 0) ? ld_acquire(&lookback[idx]) : kFlagInc;
@@ -492,15 +528,6 @@ __device__ __noinline__ void service_unit(const SvcArgs P, St* S, unsigned char*
     const int lane = threadIdx.x & 31;
     const bool FQ = (P.mode == 2);
     const long long npass = (warm ? 1 : 0) + (b1 - b0);
-
-    auto stage = [&](long long b, int buf) {
-        const T* src = (const T*)P.x + b * (long long)BS;
-        if (lane == 0) mbar_expect(&S->full[buf], (uint32_t)(BS * sizeof(T)));
-        __syncwarp();
-        bulk_load(xb0 + buf * XB + lane * LB, src + lane * 128, (uint32_t)(128 * sizeof(T)), &S->full[buf]);
-    };
-    stage(b0, 0);
-    if (b0 + 1 < b1) stage(b0 + 1, 1);
 
     // CodecState (codec.py:66-82), lane 0
     double att = 0.0, a_cur = 1.0;
@@ -787,11 +814,22 @@ __device__ __forceinline__ void pack_unit(const EncParams& P, St* S, unsigned ch
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool FQ = (P.mode == 2);
     const long long npass = (warm ? 1 : 0) + (b1 - b0);
+#ifdef APAX_V5_PROF
+    // phase cycles of thread 0 (tools/prof_v5.py): acc[k] += clock at mark k - clock at the previous mark
+    unsigned long long prof_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long prof_last = clock64();
+#define PMARK(k) do { if (tid == 0) { const long long c_ = clock64(); prof_acc[k] += (unsigned long long)(c_ - prof_last); prof_last = c_; } } while (0)
+#else
+#define PMARK(k) do { } while (0)
+#endif
     int wb = 0;                 // window bytes carried in from the previous block (< 16)
     int sel_next = 0;           // argmin of the previous block's costs
     bool has_pc = false;
     auto bsum = [](uint32_t e) -> int { return (int)__dp4a(e, 0x01010101u, 0u); };
 
+    // the unit's first two blocks (every buffer is free: the previous unit is placed)
+    stage_block<DT>(xb0, (const T*)P.x + b0 * (long long)BS, &S->full[0]);
+    if (b0 + 1 < b1) stage_block<DT>(xb0 + XB, (const T*)P.x + (b0 + 1) * (long long)BS, &S->full[1]);
     for (long long kp = 0; kp < npass; kp++) {
         const bool pre = warm && kp == 0;
         const bool emit = !pre;
@@ -799,7 +837,9 @@ __device__ __forceinline__ void pack_unit(const EncParams& P, St* S, unsigned ch
         const long long b = b0 + bi;
         const int buf = (int)(bi & 1);
         const bool restart = (bi == 0);
+        PMARK(0);
         bar_sync<1, NT>();
+        PMARK(1);
         const Blk* B = &S->blk[kp & 1];
         const double sq = B->sq;
         const bool bwide = B->wide != 0;
@@ -809,15 +849,8 @@ __device__ __forceinline__ void pack_unit(const EncParams& P, St* S, unsigned ch
         // the other buffer's block is finished (every pack thread is past its
         // emission): stage the next block into it, four leaves per warp
         const bool has_next = b + 1 < b1;
-        if (emit && bi >= 1 && has_next) {
-            const int nbuf = buf ^ 1;
-            if (tid == 0) mbar_expect(&S->full[nbuf], (uint32_t)(BS * sizeof(T)));
-            if (lane < 4) {
-                const int leaf = 4 * warp + lane;
-                bulk_load(xb0 + nbuf * XB + leaf * LB, (const T*)P.x + (b + 1) * (long long)BS + leaf * 128,
-                          (uint32_t)(128 * sizeof(T)), &S->full[nbuf]);
-            }
-        }
+        if (emit && bi >= 1 && has_next)
+            stage_block<DT>(xb0 + (buf ^ 1) * XB, (const T*)P.x + (b + 1) * (long long)BS, &S->full[buf ^ 1]);
 
         // ---- fixed-quality sums, numpy's pairwise order (codec.py:248-249) ----
         if (FQ) {
@@ -845,6 +878,7 @@ __device__ __forceinline__ void pack_unit(const EncParams& P, St* S, unsigned ch
             bar_arrive<3, NT>();
         }
 
+        PMARK(2);
         // ---- samples -> q (registers), history ----
         const T* xc = xl + SPT * (tid & 7);
         int q[SPT];
@@ -918,7 +952,47 @@ __device__ __forceinline__ void pack_unit(const EncParams& P, St* S, unsigned ch
                 S->edge[warp][0] = f0; S->edge[warp][1] = l0;
             }
         }
+        // ---- peak of the next block (staged at the start of this pass, landed by now) for the
+        // service warp's next quantizer ----
+        if (NEED_PEAK && has_next) {
+            const int nbuf = buf ^ 1;
+            mbar_wait(&S->full[nbuf], (phs >> nbuf) & 1u);
+            const uint4* xn = (const uint4*)((const T*)(xb0 + nbuf * XB) + (tid >> 3) * LS + SPT * (tid & 7));
+            unsigned pk, pn;
+            if (DT == 3) {
+                int ms = 0;
+                unsigned mu = 0;
+#pragma unroll
+                for (int m = 0; m < 4; m++) {
+                    const uint4 v = xn[m];
+                    ms = __vimax3_s32(ms, (int)v.x, (int)v.y);
+                    ms = __vimax3_s32(ms, (int)v.z, (int)v.w);
+                    mu = __vimax3_u32(mu, v.x, v.y);
+                    mu = __vimax3_u32(mu, v.z, v.w);
+                }
+                pk = (unsigned)__reduce_max_sync(0xffffffffu, ms);
+                pn = __reduce_max_sync(0xffffffffu, mu);
+            } else {
+                int mx = 0, mi = 0;
+#pragma unroll
+                for (int m = 0; m < 4; m++) {
+                    const uint4 v = xn[m];
+                    mx = __vimax3_s32(mx, (int)v.x, (int)v.y);
+                    mx = __vimax3_s32(mx, (int)v.z, (int)v.w);
+                    mi = __vimin3_s32(mi, (int)v.x, (int)v.y);
+                    mi = __vimin3_s32(mi, (int)v.z, (int)v.w);
+                }
+                pk = (unsigned)__reduce_max_sync(0xffffffffu, mx);
+                pn = (unsigned)(-(long long)__reduce_min_sync(0xffffffffu, mi));
+            }
+            if (lane == 0) { S->pkw[(kp + 1) & 1][warp] = pk; S->pnw[(kp + 1) & 1][warp] = pn; }
+        }
+        __threadfence_block();
+        bar_arrive<6, NT>();
+
+        PMARK(3);
         bar_sync<2, NT>();   // every warp's widths; the window is clean
+        PMARK(4);
 
         // ---- totals, the exact gate, the selector ----
         int tt0, tt1, tt2, flt;
@@ -945,7 +1019,6 @@ __device__ __forceinline__ void pack_unit(const EncParams& P, St* S, unsigned ch
             }
             __threadfence_block();
             bar_arrive<3, NT>();
-            bar_arrive<6, NT>();
             bar_arrive<4, NT>();
             continue;
         }
@@ -1013,7 +1086,9 @@ __device__ __forceinline__ void pack_unit(const EncParams& P, St* S, unsigned ch
                 S->jc[warp] = (nonA ? 1 : 0) | (nonA ? (int)(((kbits >> top) & 1u) << 1) : 0);
             }
         }
+        PMARK(5);
         bar_sync<5, NPT>();
+        PMARK(6);
 
         // ---- warp carry chain and prefixes (lanes 0..NPW-1 = warps) ----
         int cin_w, nib_pre, mb_pre, nib_total, mb_total;
@@ -1067,44 +1142,7 @@ __device__ __forceinline__ void pack_unit(const EncParams& P, St* S, unsigned ch
             __threadfence_block();
             bar_arrive<3, NT>();
         }
-        // ---- peak of the next block (staged at the start of this pass) for the
-        // service warp's next quantizer ----
-        if (NEED_PEAK && has_next) {
-            const int nbuf = buf ^ 1;
-            mbar_wait(&S->full[nbuf], (phs >> nbuf) & 1u);
-            const uint4* xn = (const uint4*)((const T*)(xb0 + nbuf * XB) + (tid >> 3) * LS + SPT * (tid & 7));
-            unsigned pk, pn;
-            if (DT == 3) {
-                int ms = 0;
-                unsigned mu = 0;
-#pragma unroll
-                for (int m = 0; m < 4; m++) {
-                    const uint4 v = xn[m];
-                    ms = __vimax3_s32(ms, (int)v.x, (int)v.y);
-                    ms = __vimax3_s32(ms, (int)v.z, (int)v.w);
-                    mu = __vimax3_u32(mu, v.x, v.y);
-                    mu = __vimax3_u32(mu, v.z, v.w);
-                }
-                pk = (unsigned)__reduce_max_sync(0xffffffffu, ms);
-                pn = __reduce_max_sync(0xffffffffu, mu);
-            } else {
-                int mx = 0, mi = 0;
-#pragma unroll
-                for (int m = 0; m < 4; m++) {
-                    const uint4 v = xn[m];
-                    mx = __vimax3_s32(mx, (int)v.x, (int)v.y);
-                    mx = __vimax3_s32(mx, (int)v.z, (int)v.w);
-                    mi = __vimin3_s32(mi, (int)v.x, (int)v.y);
-                    mi = __vimin3_s32(mi, (int)v.z, (int)v.w);
-                }
-                pk = (unsigned)__reduce_max_sync(0xffffffffu, mx);
-                pn = (unsigned)(-(long long)__reduce_min_sync(0xffffffffu, mi));
-            }
-            if (lane == 0) { S->pkw[(kp + 1) & 1][warp] = pk; S->pnw[(kp + 1) & 1][warp] = pn; }
-        }
-        __threadfence_block();
-        bar_arrive<6, NT>();
-
+        PMARK(7);
         // ---- JEE tokens + mantissas into the window ----
         if (!bad) {
             const unsigned below = nonA & ((1u << lane) - 1u);
@@ -1194,6 +1232,9 @@ __device__ __forceinline__ void pack_unit(const EncParams& P, St* S, unsigned ch
         __threadfence_block();
         bar_arrive<4, NT>();
     }
+#ifdef APAX_V5_PROF
+    if (tid == 0) for (int k2 = 0; k2 < 8; k2++) atomicAdd(&g_prof[k2], prof_acc[k2]);
+#endif
 }
 
 template <int DT>
@@ -1213,8 +1254,8 @@ __global__ void __launch_bounds__(NT, 4) encode_v5_kernel(EncParams P) {
     }
 #endif
     if (tid == 0) {
-        mbar_init(&S->full[0]);
-        mbar_init(&S->full[1]);
+        mbar_init_n(&S->full[0], NPT);
+        mbar_init_n(&S->full[1], NPT);
         fence_mbar_init();
     }
     for (int i = tid; i < win_bytes(DT) / 16; i += NT) ((uint4*)win)[i] = make_uint4(0u, 0u, 0u, 0u);
@@ -1256,6 +1297,12 @@ __global__ void __launch_bounds__(NT, 4) encode_v5_kernel(EncParams P) {
 
 }  // namespace v5
 
+#ifdef APAX_V5_PROF
+extern "C" int apax_debug_prof5(unsigned long long* host, int reset) {
+    if (reset) { unsigned long long z[16] = {0}; return (int)cudaMemcpyToSymbol(v5::g_prof, z, sizeof(z)); }
+    return (int)cudaMemcpyFromSymbol(host, v5::g_prof, 16 * sizeof(unsigned long long));
+}
+#endif
 #ifdef APAX_V5_TIMES
 extern "C" int apax_debug_cta_times5(unsigned long long* host, int n) {
     return (int)cudaMemcpyFromSymbol(host, v5::g_times, (size_t)n * 4 * sizeof(unsigned long long));
