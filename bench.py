@@ -425,7 +425,8 @@ def main():
     ach_dec = alg_dec / (mean_dec * 1e-3) / 1e9
     # the kernels bench's configs dispatch to (apax_capi.cu): v3 encoder and
     # segment-serial d3 decoder for every dtype at bs 4096
-    enc_k = f"encode_v3_kernel<{wdt.wire_code}"
+    enc_k = (_lib.lib().apax_encode_kernel_name(wdt.wire_code, cfg.mode.value, cfg.block_size,
+                                                 int(cfg.segment_blocks or 0)).decode() + f"<{wdt.wire_code}")
     dec_k = f"decode_v3_kernel<{wdt.wire_code}"
     dominant = enc_k if mean_enc >= mean_dec else dec_k
     ach = ach_enc if mean_enc >= mean_dec else ach_dec  # noqa: E501

@@ -74,6 +74,11 @@ int64_t apax_max_encoded_bytes(int64_t n, int dtype, int block_size);
  * the value passed to apax_encode. */
 int64_t apax_encode_wave_segment_blocks(int64_t n, int dtype, int mode, int block_size);
 
+/* Name of the kernel that codes the full blocks of a container with these
+ * parameters on this device (for profiler look-ups and benchmark labels;
+ * the library's dispatch, not a knob). */
+const char* apax_encode_kernel_name(int dtype, int mode, int block_size, int64_t segment_blocks);
+
 /* Decode blocks [b0, b1) of a container of n samples (whole-stream or
  * segmented) given the GLOBAL side-band index `block_offsets` and the
  * derivative history (q[-1], q[-2] as two's-complement u64) entering block b0

@@ -52,6 +52,8 @@ def lib():
     L.apax_decode.restype = I32
     L.apax_encode_wave_segment_blocks.argtypes = [I64, I32, I32, I32]
     L.apax_encode_wave_segment_blocks.restype = I64
+    L.apax_encode_kernel_name.argtypes = [I32, I32, I32, I64]
+    L.apax_encode_kernel_name.restype = ctypes.c_char_p
     # (bound only when present: APAX_LIB_PATH may point at an older tuning build)
     if hasattr(L, "apax_decode_range"):
         L.apax_decode_range.argtypes = [P, I64, I64, I32, I32, P, I64, I64, ctypes.c_uint64, ctypes.c_uint64,
@@ -112,4 +114,5 @@ EXPORTED_SYMBOLS = (
     "apax_encode_lossless_range", "apax_detect_segments",
     "apax_max_encoded_bytes_cast", "apax_launch_count", "apax_quantize_block", "apax_dequantize_block",
     "apax_encode_block", "apax_sweep_point", "apax_sweep_point_workspace_bytes", "apax_encode_cast_workspace_bytes", "apax_encode_cast",
+    "apax_encode_kernel_name",
 )

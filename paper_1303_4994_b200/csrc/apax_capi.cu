@@ -785,9 +785,28 @@ int64_t apax_encode_wave_segment_blocks(int64_t n, int dtype, int mode, int bloc
     if (p.v3) {
         resident = encode_v3_resident_ctas_wave(dtype, p.smem);
         if (resident < 1) resident = encode_v3_resident_ctas(dtype, p.smem);
+        EncParams P;
+        memset(&P, 0, sizeof(P));
+        if (encode_v5_supported(dtype, block_size, mode, P)) resident = encode_v5_resident_ctas(dtype);
     }
     if (resident < 1) resident = 1;
     return (p.n_blocks + resident - 1) / resident;
+}
+
+const char* apax_encode_kernel_name(int dtype, int mode, int block_size, int64_t segment_blocks) {
+    // the kernel that codes the full blocks of such a container (mirrors the
+    // dispatch of apax_encode / launch_encode_v3)
+    EncPlan p;
+    if (plan_encode(1 << 20, dtype, mode, block_size, segment_blocks, &p)) return "";
+    if (p.split) return mode == APAX_LOSSLESS ? "pack_kernel" : "chain + pack_kernel";
+    if (p.v3) {
+        EncParams P;
+        memset(&P, 0, sizeof(P));
+        P.halo = p.halo;
+        // (one-wave launches; longer ones take the persistent v3 kernel)
+        return encode_v5_supported(dtype, block_size, mode, P) ? "encode_v5_kernel" : "encode_v3_kernel";
+    }
+    return "encode_kernel";
 }
 
 int64_t apax_decode_segments_workspace_bytes(int64_t n, int dtype, int block_size) {

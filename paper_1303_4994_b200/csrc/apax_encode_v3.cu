@@ -1916,7 +1916,12 @@ int launch_encode_v3(int dt, const EncParams& P, int grid, size_t smem, cudaStre
     if (ufull > 0) {
         // segments of full blocks: the v5 kernel (pack warps + a service warp)
         // when it takes the container, else the fused v3 kernel
-        const bool use5 = fixable && encode_v5_supported(dt, P.bs, P.mode, P);
+        // (v5 places a unit only after coding it: it takes the one-wave launches,
+        // the persistent v3 kernel with its placement warp the longer ones;
+        // APAX_ENC_V5=2 forces v5)
+        const char* e5 = getenv("APAX_ENC_V5");
+        const bool use5 = fixable && encode_v5_supported(dt, P.bs, P.mode, P) &&
+                          (ufull <= encode_v5_resident_ctas(dt) || (e5 && atoi(e5) == 2));
         const int r = use5 ? launch_encode_v5(dt, P, 0, ufull, st) : launch_v3_range(dt, true, P, 0, ufull, grid, smem, st);
         if (r) return r;
     }

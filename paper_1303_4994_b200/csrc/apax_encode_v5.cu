@@ -770,7 +770,9 @@ __device__ __noinline__ void service_unit(const SvcArgs P, St* S, unsigned char*
         bar_arrive<2, NT>();                 // the window is clean
         if (emit) phs ^= 1u << buf;
     }
-    // ---- unit end ----
+    // ---- unit end: the last pass's hand-offs (results, peak, window) ----
+    bar_sync<3, NT>();
+    bar_sync<6, NT>();
     bar_sync<4, NT>();
     {
         const long long pbi = (b1 - b0) - 1;

@@ -38,13 +38,19 @@ def main():
         ("i32 FR P=4 warm", (W.cfg2_ar2_f32(1 << 21) * 1000).astype(np.int32), Dtype.I32, Mode.FIXED_RATE, 10.0, 4, "warm_self"),
         ("i32 FQ big P=6", (W.cfg2_ar2_f32(1 << 21) * 4e5).astype(np.int32), Dtype.I32, Mode.FIXED_QUALITY, 150.0, 6, "cold"),
     ]
+    cases += [
+        ("f32 FQ P=1 many units", W.cfg2_ar2_f32(1 << 22), Dtype.F32, Mode.FIXED_QUALITY, W.CFG2_TARGET_DB, 1, "cold"),
+        ("i16 FR P=1 warm many", W.cfg1_sines_i16((1 << 22) + 100), Dtype.I16, Mode.FIXED_RATE, 4.0, 1, "warm_self"),
+        ("f32 FR P=2 warm many", W.cfg2_ar2_f32((1 << 23) + 4096), Dtype.F32, Mode.FIXED_RATE, 6.0, 2, "warm_self"),
+        ("i32 FQ P=3 many", (W.cfg2_ar2_f32(1 << 23) * 1000).astype(np.int32), Dtype.I32, Mode.FIXED_QUALITY, 60.0, 3, "cold"),
+    ]
     ok = True
     for name, xh, dt, mode, T, P, pol in cases:
         x = torch.from_numpy(xh).cuda()
         cfg = StreamConfig(dt, 4096, mode, T, segment_blocks=P, segment_policy=pol)
         res = {}
         for v5 in ("0", "1"):
-            os.environ["APAX_ENC_V5"] = v5
+            os.environ["APAX_ENC_V5"] = "2" if v5 == "1" else "0"
             enc = Encoder(x.numel(), cfg)
             res[v5] = run(enc, x)
         same = res["0"][1] == res["1"][1]
