@@ -84,6 +84,7 @@ struct __align__(16) St {
     int hq[2][2];              // history entering the next block: q[n-1], q[n-2]
     unsigned pkw[2][NPW], pnw[2][NPW];   // per-warp peak partials of the next pass's block
     long long slot_len, slot_b0, slot_b1, fin_prefix;
+    long long unit;
 };
 static_assert(sizeof(St) <= ST_BYTES, "St too large");
 
@@ -96,6 +97,7 @@ __device__ unsigned long long g_prof[16];
 // per-CTA timeline (tools/cta_times.py): globaltimer at start, at the end of
 // the last unit's coding, at exit; SM id
 __device__ unsigned long long g_times[8192 * 4];
+__device__ unsigned long long g_times2[8192 * 2];   // prefix known, copy done
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -482,6 +484,9 @@ __device__ __noinline__ void final_place(long long u, long long n_units, long lo
             prefix = unit_prefix(lookback, u);
             if (tid == 0) st_release(&lookback[u], kFlagInc | (unsigned long long)(prefix + len));
         }
+#ifdef APAX_V5_TIMES
+        if (tid == 0 && blockIdx.x < 8192) g_times2[2 * blockIdx.x] = gtimer();
+#endif
         if (tid == 0) {
             S->fin_prefix = prefix;
             if (u == n_units - 1) {
@@ -494,6 +499,9 @@ __device__ __noinline__ void final_place(long long u, long long n_units, long lo
     const long long prefix = S->fin_prefix;
     group_copy_out(out + kFileHeader + prefix, (const uint32_t*)slot, len, tid, NT);
     bar_sync<7, NT>();   // every thread has read its slot words: the lines are dead
+#ifdef APAX_V5_TIMES
+    if (tid == 0 && blockIdx.x < 8192) g_times2[2 * blockIdx.x + 1] = gtimer();
+#endif
     for (long long l = (long long)tid * 128; l < len; l += (long long)NT * 128) discard_l2(slot + l);
     if (block_offsets)
         for (long long bb = b0 + tid; bb < b1; bb += NT) block_offsets[bb] += kFileHeader + prefix;
@@ -503,7 +511,8 @@ __device__ __noinline__ void final_place(long long u, long long n_units, long lo
 // the service warp: one unit
 // ---------------------------------------------------------------------------
 // what the service warp needs of the launch parameters (by value: a reference
-// to the kernel's parameter block would force a local copy of it)
+// to the kernel's parameter block would force a local copy of it; keep it at
+// 80 bytes -- a 96-byte version faulted in the noinline call)
 struct SvcArgs {
     const void* x;
     unsigned long long* status;
@@ -1265,7 +1274,15 @@ __global__ void __launch_bounds__(NT, 4) encode_v5_kernel(EncParams P) {
     uint32_t phs = 0u;          // bit k: mbarrier phase parity of buffer k (each role keeps its own copy)
     uint32_t phs_v = 0u;
     const bool warm = P.policy == 1 && P.mode == 1;
-    for (long long u = P.unit_begin + blockIdx.x; u < P.unit_end; u += gridDim.x) {
+    // units by ticket: a CTA that finishes a unit takes the next one (several
+    // units per CTA balance dynamically; a unit's placement waits only for
+    // lower units, all of which are running or done)
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) S->unit = P.unit_begin + (long long)atomicAdd(P.ticket, 1u);
+        __syncthreads();
+        const long long u = S->unit;
+        if (u >= P.unit_end) break;
         const long long b0 = u * P.unit_blocks;
         const long long b1 = (b0 + P.unit_blocks < P.n_blocks) ? b0 + P.unit_blocks : P.n_blocks;
         if (warp == NPW) {
@@ -1308,6 +1325,9 @@ extern "C" int apax_debug_prof5(unsigned long long* host, int reset) {
 #ifdef APAX_V5_TIMES
 extern "C" int apax_debug_cta_times5(unsigned long long* host, int n) {
     return (int)cudaMemcpyFromSymbol(host, v5::g_times, (size_t)n * 4 * sizeof(unsigned long long));
+}
+extern "C" int apax_debug_cta_times5b(unsigned long long* host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, v5::g_times2, (size_t)n * 2 * sizeof(unsigned long long));
 }
 #endif
 

@@ -51,3 +51,15 @@ sm_mean = np.array([ct[sm == k].mean() if (sm == k).any() else np.nan for k in r
 print("per-SM mean coding time, SMs 0..147 (us):")
 print(" ".join(f"{v:.0f}" for v in sm_mean))
 print("coding time by CTA id, in blocks of 32 CTAs:", " ".join(f"{ct[i:i + 32].mean():.0f}" for i in range(0, len(ct), 32)))
+
+if os.environ.get("TIMES_FN", "").endswith("5"):
+    b2 = np.zeros(ng * 2, np.uint64)
+    L.apax_debug_cta_times5b(b2.ctypes.data_as(ctypes.c_void_p), ng)
+    t2 = b2.reshape(-1, 2).astype(np.int64)
+    pk, cd = (t2[:, 0] - t0) / 1e3, (t2[:, 1] - t0) / 1e3
+    for name, v in (("prefix known", pk), ("copy done", cd), ("prefix wait", pk - ce), ("copy time", cd - pk)):
+        q = np.percentile(v, [0, 10, 50, 90, 99, 100])
+        print(f"{name:12s} us: " + " ".join(f"{a:8.1f}" for a in q))
+    print("id: coding end, prefix known, copy done, exit")
+    for i in list(range(0, 12)) + list(range(140, 156)) + list(range(290, 300)) + list(range(576, ng)):
+        print(f"  {i:4d} {ce[i]:8.1f} {pk[i]:8.1f} {cd[i]:8.1f} {ex[i]:8.1f}")
