@@ -206,20 +206,29 @@ __device__ __forceinline__ uint32_t consumed_word(uint32_t P, uint32_t cin, uint
     const uint32_t inv = (uint32_t)s << 1;
     return (even ^ inv) & follows;
 }
+// OR a word into the window when it is non-zero: a predicated reduction (no
+// branch around the atomic; a zero word is what a piece contributes to a word
+// it does not reach)
+__device__ __forceinline__ void or_word(uint32_t* w, uint32_t v) {
+    asm volatile("{ .reg .pred p; setp.ne.u32 p, %1, 0; @p red.shared.or.b32 [%0], %1; }"
+                 :: "r"(sa(w)), "r"(v) : "memory");
+}
+// MSB-first piece writers: `c` (nb bits) at bit position pos of the window
 __device__ __forceinline__ void put_bits(uint32_t* win, int pos, uint32_t c, int nb) {
     const uint32_t a = c << (32 - nb);
     const int sh = pos & 31;
     uint32_t* w = win + (pos >> 5);
-    atomicOr(w, bswap32(a >> sh));
-    if (sh + nb > 32) atomicOr(w + 1, bswap32(a << (32 - sh)));
+    or_word(w, bswap32(a >> sh));
+    or_word(w + 1, bswap32(__funnelshift_r(0u, a, sh)));   // a << (32 - sh), 0 when sh == 0
 }
 __device__ __forceinline__ void put_bits64(uint32_t* win, int pos, unsigned long long c, int nb) {
     const unsigned long long a = c << (64 - nb);
     const int sh = pos & 31;
+    const uint32_t hi = (uint32_t)(a >> 32), lo = (uint32_t)a;
     uint32_t* w = win + (pos >> 5);
-    atomicOr(w, bswap32((uint32_t)(a >> (32 + sh))));
-    if (sh + nb > 32) atomicOr(w + 1, bswap32((uint32_t)(a >> sh)));
-    if (sh + nb > 64) atomicOr(w + 2, bswap32((uint32_t)(a << (32 - sh))));
+    or_word(w, bswap32(hi >> sh));
+    or_word(w + 1, bswap32(__funnelshift_r(lo, hi, sh)));
+    or_word(w + 2, bswap32(__funnelshift_r(0u, lo, sh)));      // lo << (32 - sh), 0 when sh == 0
 }
 
 template <int DT>
@@ -824,7 +833,8 @@ __device__ __forceinline__ void pack_unit(const EncParams& P, St* S, unsigned ch
     constexpr bool NEED_PEAK = F || DT == 2;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool FQ = (P.mode == 2);
-    const long long npass = (warm ? 1 : 0) + (b1 - b0);
+    const int nblk = (int)(b1 - b0);
+    const int npass = (warm ? 1 : 0) + nblk;
 #ifdef APAX_V5_PROF
     // phase cycles of thread 0 (tools/prof_v5.py): acc[k] += clock at mark k - clock at the previous mark
     unsigned long long prof_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -841,12 +851,12 @@ __device__ __forceinline__ void pack_unit(const EncParams& P, St* S, unsigned ch
     // the unit's first two blocks (every buffer is free: the previous unit is placed)
     stage_block<DT>(xb0, (const T*)P.x + b0 * (long long)BS, &S->full[0]);
     if (b0 + 1 < b1) stage_block<DT>(xb0 + XB, (const T*)P.x + (b0 + 1) * (long long)BS, &S->full[1]);
-    for (long long kp = 0; kp < npass; kp++) {
+    for (int kp = 0; kp < npass; kp++) {
         const bool pre = warm && kp == 0;
         const bool emit = !pre;
-        const long long bi = warm ? (kp == 0 ? 0 : kp - 1) : kp;
+        const int bi = warm ? (kp == 0 ? 0 : kp - 1) : kp;
         const long long b = b0 + bi;
-        const int buf = (int)(bi & 1);
+        const int buf = bi & 1;
         const bool restart = (bi == 0);
         PMARK(0);
         bar_sync<1, NT>();
@@ -859,7 +869,7 @@ __device__ __forceinline__ void pack_unit(const EncParams& P, St* S, unsigned ch
         const T* xl = (const T*)(xb0 + buf * XB) + (tid >> 3) * LS;   // this thread's leaf
         // the other buffer's block is finished (every pack thread is past its
         // emission): stage the next block into it, four leaves per warp
-        const bool has_next = b + 1 < b1;
+        const bool has_next = bi + 1 < nblk;
         if (emit && bi >= 1 && has_next)
             stage_block<DT>(xb0 + (buf ^ 1) * XB, (const T*)P.x + (b + 1) * (long long)BS, &S->full[buf ^ 1]);
 
