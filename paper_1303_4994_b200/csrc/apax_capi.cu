@@ -113,7 +113,9 @@ int plan_encode(long long n, int kdt, int mode, int bs, long long seg, EncPlan* 
     p->slot_bytes = (p->n_units > 1 || p->v3) ? ((p->unit_blocks * mbb + 64 + 255) & ~255LL) : 0;
     p->ws_lookback = 0;
     p->ws_ticket = (p->n_units * 8 + 255) & ~255LL;
-    p->ws_slots = p->ws_ticket + 256;
+    // ticket words, then v5's unit numbering tables (per-SM arrival counts,
+    // per-rank counts, one claim word per unit)
+    p->ws_slots = p->ws_ticket + 256 + ((8448 + 4 * p->n_units + 255) & ~255LL);
     p->ws_total = p->ws_slots + p->slot_bytes * (p->v3 ? v3_slots : (long long)p->grid);
     // split encoder (bs 4096, i16/i32/f32/f64): per-block quantizer records,
     // published costs, look-back words, one ticket counter

@@ -1274,6 +1274,16 @@ __global__ void __launch_bounds__(NT, 4) encode_v5_kernel(EncParams P) {
         g_times[4 * blockIdx.x + 3] = smid;
     }
 #endif
+    // one-wave launches: register on this SM (see the unit numbering below)
+    const bool by_rank = P.nsm > 0 && (P.unit_end - P.unit_begin) == (long long)gridDim.x;
+    unsigned* const tab = (unsigned*)P.ticket + 64;   // [8 * smid ..): count + ids; [2048, 2056): rank counts; [2112, ..): claims
+    unsigned my_sm = 0;
+    if (by_rank && tid == 0) {
+        asm volatile("mov.u32 %0, %smid;" : "=r"(my_sm));
+        my_sm &= 255u;
+        const unsigned slot = atomicAdd(&tab[8 * my_sm], 1u);
+        if (slot < 7u) atomicExch(&tab[8 * my_sm + 1 + slot], blockIdx.x + 1u);
+    }
     if (tid == 0) {
         mbar_init_n(&S->full[0], NPT);
         mbar_init_n(&S->full[1], NPT);
@@ -1287,9 +1297,43 @@ __global__ void __launch_bounds__(NT, 4) encode_v5_kernel(EncParams P) {
     // units by ticket: a CTA that finishes a unit takes the next one (several
     // units per CTA balance dynamically; a unit's placement waits only for
     // lower units, all of which are running or done)
-    for (;;) {
+    // One-wave launches (one unit per CTA) number the units by the CTAs'
+    // rank on their SM: the warp scheduler favours older warps, the CTAs of
+    // an SM finish in blockIdx order (tools/cta_times.py: 147 of 148 SMs),
+    // the first ~25% before the last, and a unit's placement waits for every
+    // lower unit -- with rank-major numbers the early finishers place while
+    // the late ones still code, instead of one burst of copies at the end.
+    // Claim words keep the numbering a bijection whatever the hardware's
+    // distribution (or a late registration) was.
+    for (int iter = 0;; iter++) {
         __syncthreads();
-        if (tid == 0) S->unit = P.unit_begin + (long long)atomicAdd(P.ticket, 1u);
+        if (tid == 0) {
+            if (by_rank) {
+                long long unit = P.unit_end;
+                if (iter == 0) {
+                    __nanosleep(1000);      // the other CTAs of this SM register within ~0.5 us of the launch
+                    const unsigned cnt = *(volatile unsigned*)&tab[8 * my_sm];
+                    unsigned rank = 0;
+                    for (unsigned k = 0; k < cnt && k < 7u; k++) {
+                        const unsigned id = *(volatile unsigned*)&tab[8 * my_sm + 1 + k];
+                        if (id != 0u && id - 1u < blockIdx.x) rank++;
+                    }
+                    const unsigned idx = atomicAdd(&tab[2048 + (rank < 7u ? rank : 7u)], 1u);
+                    const long long nu = P.unit_end - P.unit_begin;
+                    const long long pref = (long long)rank * P.nsm + idx;
+                    unsigned* claim = tab + 2112;
+                    if (pref < nu && idx < (unsigned)P.nsm && atomicCAS(&claim[pref], 0u, 1u) == 0u) {
+                        unit = P.unit_begin + pref;
+                    } else {
+                        for (long long c = nu - 1; c >= 0; c--)
+                            if (atomicCAS(&claim[c], 0u, 1u) == 0u) { unit = P.unit_begin + c; break; }
+                    }
+                }
+                S->unit = unit;
+            } else {
+                S->unit = P.unit_begin + (long long)atomicAdd(P.ticket, 1u);
+            }
+        }
         __syncthreads();
         const long long u = S->unit;
         if (u >= P.unit_end) break;
@@ -1378,6 +1422,13 @@ int launch_encode_v5(int dt, const EncParams& P, long long u0, long long u1, cud
     EncParams p = P;
     p.unit_begin = u0;
     p.unit_end = u1;
+    {
+        int dev = 0, nsm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        const char* e = getenv("APAX_V5_RANK");
+        p.nsm = (e && atoi(e) == 0) ? 0 : (nsm > 0 && nsm <= 256 ? nsm : 0);
+    }
     const int g = (int)(nu < res ? nu : res);
     void* args[] = {&p};
     note_launches(1);

@@ -59,6 +59,7 @@ int launch_encode_v5(int dt, const EncParams& P, long long u0, long long u1, cud
     apax_block_state* state;      // generic kernel, one unit: CodecState in / out (encode_block)
     double* stats;                // fixed-quality chain: per block sum x^2, sum x*y, sum y*y (y = the decode)
     int count_only;               // packer: container length only, no output written
+    int nsm;                      // v5 one-wave launches: SM count (units numbered by arrival rank), 0: by ticket
 };
 
 // Index-less decode state (apax_decode without offsets, apax_capi.cu):

@@ -63,3 +63,20 @@ if os.environ.get("TIMES_FN", "").endswith("5"):
     print("id: coding end, prefix known, copy done, exit")
     for i in list(range(0, 12)) + list(range(140, 156)) + list(range(290, 300)) + list(range(576, ng)):
         print(f"  {i:4d} {ce[i]:8.1f} {pk[i]:8.1f} {cd[i]:8.1f} {ex[i]:8.1f}")
+
+# within an SM: does blockIdx order predict the finishing order?
+agree = tot = 0
+inv = []
+for k in range(148):
+    ids = np.nonzero(sm == k)[0]
+    if len(ids) < 2:
+        continue
+    order_id = ids[np.argsort(ids)]
+    order_t = ids[np.argsort(ce[ids])]
+    tot += 1
+    agree += int(np.array_equal(order_id, order_t))
+    if not np.array_equal(order_id, order_t) and len(inv) < 12:
+        inv.append((k, [(int(i), round(float(ce[i]), 1)) for i in order_id]))
+print(f"SMs whose CTAs finish in blockIdx order: {agree} of {tot}")
+for k, v in inv:
+    print("  SM", k, v)

@@ -1,3 +1,4 @@
 #!/bin/bash
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests/test_encode_v5.py -m gpu -x -q --timeout 180 > gpurun_out/t5_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/t5_pytest.log
+timeout 1500 python -m pytest tests -m gpu -x -q --timeout 300 > gpurun_out/t5_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/t5_pytest.log
+timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/t5_bench.json 2> gpurun_out/t5_bench.err
