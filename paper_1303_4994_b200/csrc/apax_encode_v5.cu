@@ -532,7 +532,7 @@ struct SvcArgs {
     int mode;
 };
 
-template <int DT>
+template <int DT, bool FQ>
 __device__ __noinline__ void service_unit(const SvcArgs P, St* S, unsigned char* xb0, uint32_t* win, uint8_t* slot,
                                           long long u, long long b0, long long b1, bool warm, uint32_t& phs) {
     using Tr = DT_<DT>;
@@ -544,7 +544,6 @@ __device__ __noinline__ void service_unit(const SvcArgs P, St* S, unsigned char*
     constexpr bool NEED_PEAK = F || DT == 2;
     constexpr bool SQX = (DT != 2);
     const int lane = threadIdx.x & 31;
-    const bool FQ = (P.mode == 2);
     const long long npass = (warm ? 1 : 0) + (b1 - b0);
 
     // CodecState (codec.py:66-82), lane 0
@@ -794,7 +793,7 @@ __device__ __noinline__ void service_unit(const SvcArgs P, St* S, unsigned char*
     bar_sync<4, NT>();
     {
         const long long pbi = (b1 - b0) - 1;
-        if (lane == 0 && P.mode == 2) {
+        if (FQ && lane == 0) {
             // the last block's quality-loop error status (codec.py:251)
             const Res* R = &S->res[(npass - 1) & 1];
             const double px = warp_tree8(R->px), pd = warp_tree8(R->pd);
@@ -819,7 +818,7 @@ __device__ __noinline__ void service_unit(const SvcArgs P, St* S, unsigned char*
 // ---------------------------------------------------------------------------
 // the pack warps: one unit
 // ---------------------------------------------------------------------------
-template <int DT>
+template <int DT, bool FQ>
 __device__ __forceinline__ void pack_unit(const EncParams& P, St* S, unsigned char* xb0, uint32_t* win,
                                           long long b0, long long b1, bool warm, uint32_t& phs) {
     using Tr = DT_<DT>;
@@ -832,7 +831,6 @@ __device__ __forceinline__ void pack_unit(const EncParams& P, St* S, unsigned ch
  constexpr bool SQX = (DT != 2);
     constexpr bool NEED_PEAK = F || DT == 2;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const bool FQ = (P.mode == 2);
     const int nblk = (int)(b1 - b0);
     const int npass = (warm ? 1 : 0) + nblk;
 #ifdef APAX_V5_PROF
@@ -1258,7 +1256,8 @@ __device__ __forceinline__ void pack_unit(const EncParams& P, St* S, unsigned ch
 #endif
 }
 
-template <int DT>
+// FQ: fixed quality (else fixed rate): each instantiation carries only its own loop
+template <int DT, bool FQ>
 __global__ void __launch_bounds__(NT, 4) encode_v5_kernel(EncParams P) {
     extern __shared__ __align__(128) unsigned char smem[];
     St* S = (St*)smem;
@@ -1293,7 +1292,7 @@ __global__ void __launch_bounds__(NT, 4) encode_v5_kernel(EncParams P) {
     __syncthreads();
     uint32_t phs = 0u;          // bit k: mbarrier phase parity of buffer k (each role keeps its own copy)
     uint32_t phs_v = 0u;
-    const bool warm = P.policy == 1 && P.mode == 1;
+    const bool warm = !FQ && P.policy == 1;
     // units by ticket: a CTA that finishes a unit takes the next one (several
     // units per CTA balance dynamically; a unit's placement waits only for
     // lower units, all of which are running or done)
@@ -1344,9 +1343,9 @@ __global__ void __launch_bounds__(NT, 4) encode_v5_kernel(EncParams P) {
             A.x = P.x; A.status = P.status; A.lookback = P.lookback; A.block_offsets = P.block_offsets;
             A.trace = P.trace; A.target = P.target; A.att_lo = P.att_lo; A.pow10_t20 = P.pow10_t20;
             A.sqrt12 = P.sqrt12; A.mode = P.mode;
-            service_unit<DT>(A, S, xb0, win, slot, u, b0, b1, warm, phs_v);
+            service_unit<DT, FQ>(A, S, xb0, win, slot, u, b0, b1, warm, phs_v);
         } else {
-            pack_unit<DT>(P, S, xb0, win, b0, b1, warm, phs);
+            pack_unit<DT, FQ>(P, S, xb0, win, b0, b1, warm, phs);
         }
 #ifdef APAX_V5_TIMES
         if (tid == 0 && blockIdx.x < 8192) g_times[4 * blockIdx.x + 1] = gtimer();
@@ -1393,11 +1392,11 @@ bool encode_v5_supported(int dt, int bs, int mode, const EncParams& P) {
            (((uintptr_t)P.x) & 15) == 0;
 }
 
-static const void* v5_fn(int dt) {
+static const void* v5_fn(int dt, bool fq) {
     switch (dt) {
-        case 1: return (const void*)v5::encode_v5_kernel<1>;
-        case 2: return (const void*)v5::encode_v5_kernel<2>;
-        default: return (const void*)v5::encode_v5_kernel<3>;
+        case 1: return fq ? (const void*)v5::encode_v5_kernel<1, true> : (const void*)v5::encode_v5_kernel<1, false>;
+        case 2: return fq ? (const void*)v5::encode_v5_kernel<2, true> : (const void*)v5::encode_v5_kernel<2, false>;
+        default: return fq ? (const void*)v5::encode_v5_kernel<3, true> : (const void*)v5::encode_v5_kernel<3, false>;
     }
 }
 
@@ -1406,14 +1405,19 @@ int encode_v5_resident_ctas(int dt) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const size_t smem = encode_v5_smem_bytes(dt);
-    cudaFuncSetAttribute(v5_fn(dt), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, v5_fn(dt), v5::NT, smem) != cudaSuccess || per < 1) per = 1;
+    for (int fq = 0; fq < 2; fq++) {   // both instantiations must fit
+        int p = 0;
+        cudaFuncSetAttribute(v5_fn(dt, fq != 0), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p, v5_fn(dt, fq != 0), v5::NT, smem) != cudaSuccess || p < 1)
+            p = 1;
+        per = fq == 0 ? p : (p < per ? p : per);
+    }
     return per * (nsm > 0 ? nsm : 148);
 }
 
 // units [u0, u1) of full blocks; one slot per CTA (P.slots holds >= grid slots)
 int launch_encode_v5(int dt, const EncParams& P, long long u0, long long u1, cudaStream_t st) {
-    const void* fn = v5_fn(dt);
+    const void* fn = v5_fn(dt, P.mode == 2);
     const size_t smem = encode_v5_smem_bytes(dt);
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return APAX_ERR_CUDA;
