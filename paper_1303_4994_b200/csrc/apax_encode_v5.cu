@@ -1310,7 +1310,9 @@ __global__ void __launch_bounds__(NT, 4) encode_v5_kernel(EncParams P) {
             if (by_rank) {
                 long long unit = P.unit_end;
                 if (iter == 0) {
-                    __nanosleep(1000);      // the other CTAs of this SM register within ~0.5 us of the launch
+                    // the other CTAs of this SM register within ~0.5 us of the launch
+                    // (a grid of at most one CTA per SM has nothing to rank)
+                    if (gridDim.x > (unsigned)P.nsm) __nanosleep(1000);
                     const unsigned cnt = *(volatile unsigned*)&tab[8 * my_sm];
                     unsigned rank = 0;
                     for (unsigned k = 0; k < cnt && k < 7u; k++) {
