@@ -12,10 +12,10 @@
 //     costs (transform.py:52-64), the JEE structure of the selected stream
 //     (entropy.py:63-88) and the MSB-first emission (entropy.py:222-240).
 //     q never leaves the registers between quantization and emission.
-//   * 1 service warp runs everything scalar or asynchronous: TMA bulk copies
-//     of the next blocks into a two-buffer ring (one 128-sample leaf per
-//     lane, padded so both read patterns are cheap), the block peak, the
-//     gain recurrence (fixed-quality / fixed-rate update, attenuation ->
+//     They also stage the next block (cp.async into a two-buffer ring, padded
+//     leaf layout) and take its peak.
+//   * 1 service warp runs everything scalar or asynchronous: the gain
+//     recurrence (fixed-quality / fixed-rate update, attenuation ->
 //     scale code -> quantizer multiplier, codec.py:94-132,155-189,228-252),
 //     the window's bulk store to the segment's slot and its re-zeroing.
 //
@@ -157,13 +157,6 @@ __device__ __forceinline__ void bulk_wait_all() {
 }
 __device__ __forceinline__ void discard_l2(const void* p) {
     asm volatile("discard.global.L2 [%0], 128;" :: "l"(p) : "memory");
-}
-__device__ __forceinline__ void mbar_expect(unsigned long long* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(sa(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 :: "r"(sa(dst)), "l"(src), "r"(bytes), "r"(sa(bar)) : "memory");
 }
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst), "l"(src) : "memory");
