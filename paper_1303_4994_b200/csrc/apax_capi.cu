@@ -672,14 +672,12 @@ int apax_decode(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, int b
             // index-less, speculative: the signature scan's candidates as the
             // offsets (checked block by block by the segment decode below);
             // the full discovery runs only when that path is not taken
+            // (the scan also finds the first restarting block > 0, the segment
+            // length, and initialises the second gate)
             gate = (IlGate*)(w + p.ws_ticket + 64);
-            if (cudaMemsetAsync(w + p.ws_ticket + 96, 0xFF, 16, s) != cudaSuccess) return APAX_ERR_CUDA;   // gate 2
-            st = launch_k5_speculate(blob, nbytes, dtype, p.n_blocks, wo, w + p.ws_k5, gate, s);
+            st = launch_k5_speculate(blob, nbytes, dtype, p.n_blocks, wo, w + p.ws_k5, gate,
+                                     (IlGate*)(w + p.ws_ticket + 96), s);
             if (st) return st;
-            note_launches(1);
-            seg_first_kernel<<<seg_first_grid(p.n_blocks), 256, 0, s>>>(blob, nbytes, wo, p.n_blocks, gate, nullptr,
-                                                                       nullptr);
-            if (cudaGetLastError() != cudaSuccess) return APAX_ERR_CUDA;
         } else if (k5) {
             st = launch_find_blocks_k5(blob, nbytes, n, block_size, dtype, p.n_blocks, wo,
                                        (unsigned long long*)status, w + p.ws_k5, s);

@@ -114,52 +114,41 @@ __device__ __forceinline__ unsigned low2_ok(unsigned z, unsigned hi) {   // (b &
     return zero_bytes((z & hi) | (z & (z >> 1) & 0x01010101u));
 }
 
-// the candidates among positions p0 .. p0+15 (bytes p0 .. p0+23 in w) ->
-// sc (any order; *scount counts all, sc keeps KCAP).  Position 4k+j is a
-// candidate when header byte 0 is valid, bytes +3 (and +5 for floats) are 0
-// and the payload byte +hs is F0..F2: per-byte flag words aligned to the
-// position by funnel shifts; the (rare) hits are listed bit by bit
-__device__ __forceinline__ void test16(const unsigned* w, long long p0, int hs, long long phi, long long* sc,
-                                       int* scount) {
+// the candidates among positions p0 .. p0+15 (bytes p0 .. p0+23 in w, also
+// readable at base[0..23]) -> sc (any order; *scount counts all, sc keeps
+// KCAP).  A position is a candidate when header byte 0 is valid, bytes +3 (and
+// +5 for floats) are 0 and the payload byte +hs is F0..F2 (is_cand).  The
+// dense part tests only the most selective and cheapest condition, a zero
+// byte at +3 (one byte in 256 of codec output): approximate per-byte flags
+// (x - 0x01..) & ~x & 0x80.. cost two operations a word and can only
+// over-report (a byte 0x01 above a zero byte); the flagged positions, about
+// one per 256 bytes, are then checked exactly byte by byte.
+__device__ __forceinline__ void test16(const unsigned* w, const uint8_t* base, long long p0, int hs, long long phi,
+                                       long long* sc, int* scount) {
     if (p0 >= phi) return;
-    // pre-filter: a payload byte F0..F3 somewhere at +hs (3 ops per word;
-    // about one window in six of codec output passes)
-    unsigned fpre = 0;
+    unsigned m = 0;   // bit j: byte j + 3 may be zero
 #pragma unroll
-    for (int k = 1; k < 6; k++)
-        if (k < 5 || hs == 6) fpre |= zero_bytes((w[k] ^ 0xF0F0F0F0u) & 0xFCFCFCFCu);
-    if (!fpre) return;
-    unsigned Zw[6], Fw[6];
-#pragma unroll
-    for (int k = 0; k < 6; k++) {
-        Zw[k] = zero_bytes(w[k]);
-        Fw[k] = k ? low2_ok(w[k] ^ 0xF0F0F0F0u, 0xFCFCFCFCu) : 0u;
+    for (int k = 0; k < 5; k++) {
+        const unsigned f = (w[k] - 0x01010101u) & ~w[k] & 0x80808080u;
+        // the four flags of the word as a nibble (bits 7, 15, 23, 31 -> 28..31)
+        const unsigned nib = (((f >> 7) & 0x01010101u) * 0x10204080u) >> 28;
+        // byte 4k + t is position 4k + t - 3
+        if (k == 0) m |= nib >> 3;
+        else m |= nib << (4 * k - 3);
     }
-    unsigned cw[4], any = 0;
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-        unsigned c = low2_ok(w[k], 0xF8F8F8F8u) & __funnelshift_r(Zw[k], Zw[k + 1], 24);
-        if (hs == 6) c &= __funnelshift_r(Zw[k + 1], Zw[k + 2], 8) & __funnelshift_r(Fw[k + 1], Fw[k + 2], 16);
-        else c &= Fw[k + 1];
-        cw[k] = c;
-        any |= c;
-    }
-    if (!any) return;
-    unsigned cm = 0;
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-        const unsigned c = cw[k];
-        cm |= (((c >> 7) & 1u) | ((c >> 14) & 2u) | ((c >> 21) & 4u) | ((c >> 28) & 8u)) << (4 * k);
-    }
-    if (p0 < kFileHeader) cm &= (kFileHeader - p0 >= 16) ? 0u : ~((1u << (kFileHeader - p0)) - 1u);
-    if (p0 + 16 > phi) cm &= (1u << (phi - p0)) - 1u;
-    if (!cm) return;
-    int at = atomicAdd(scount, __popc(cm));
-    while (cm) {
-        const int i = __ffs(cm) - 1;
-        cm &= cm - 1;
-        if (at < KCAP) sc[at] = p0 + i;
-        at++;
+    m &= 0xffffu;
+    if (p0 < kFileHeader) m &= (kFileHeader - p0 >= 16) ? 0u : ~((1u << (kFileHeader - p0)) - 1u);
+    if (p0 + 16 > phi) m &= (1u << (phi - p0)) - 1u;
+    while (m) {
+        const int i = __ffs(m) - 1;
+        m &= m - 1;
+        const uint8_t b0 = base[i], b3 = base[i + 3], f = base[i + hs];
+        bool ok = !(b0 & 0xF8) && (b0 & 3) != 3 && b3 == 0 && f >= 0xF0 && f <= 0xF2;
+        if (hs == 6) ok = ok && base[i + 5] == 0;
+        if (ok) {
+            const int at = atomicAdd(scount, 1);
+            if (at < KCAP) sc[at] = p0 + i;
+        }
     }
 }
 
@@ -192,7 +181,7 @@ __device__ void scan_chunk_global(const uint8_t* blob, long long nbytes, int hs,
         unsigned w[6];
         if (pc + o >= phi) break;
         load24(blob, nbytes, pc + o, w);
-        test16(w, pc + o, hs, phi, sc, scount);
+        test16(w, blob + (pc + o), pc + o, hs, phi, sc, scount);
     }
 }
 
@@ -239,7 +228,7 @@ __device__ __forceinline__ void grid_barrier(unsigned int* count, unsigned int G
 // says whether there is exactly one per block, the first at byte 28.
 __global__ void __launch_bounds__(NT) scan_place_kernel(const uint8_t* blob, long long nbytes, int hs, uintptr_t a0,
                                                         long long nchunks, Ws W, long long n_blocks,
-                                                        long long* offsets, IlGate* gate) {
+                                                        long long* offsets, IlGate* gate, IlGate* gate2) {
     extern __shared__ __align__(128) unsigned char smem_sp[];
     ScanSm* S = (ScanSm*)smem_sp;
     uint8_t* buf0 = smem_sp + ((sizeof(ScanSm) + 127) & ~(size_t)127);
@@ -262,6 +251,7 @@ __global__ void __launch_bounds__(NT) scan_place_kernel(const uint8_t* blob, lon
             gate->gp = 0xFFFFFFFFu;
             gate->spec = 1u;   // cleared below (after the grid barrier) when not
             offsets[n_blocks] = nbytes;   // the last block's end: checked by the decode
+            if (gate2) { gate2->first = ~0ULL; gate2->gp = 0xFFFFFFFFu; gate2->spec = 0xFFFFFFFFu; }
         }
     }
     __syncthreads();
@@ -299,11 +289,12 @@ __global__ void __launch_bounds__(NT) scan_place_kernel(const uint8_t* blob, lon
                 const uint4 v = *(const uint4*)(b + o);
                 const uint2 u = *(const uint2*)(b + o + 16);
                 w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w; w[4] = u.x; w[5] = u.y;
+                test16(w, b + o, pc + o, hs, phi, S->sc, &S->n);
             } else {
                 if (pc + o >= phi) continue;
                 load24(blob, nbytes, pc + o, w);
+                test16(w, blob + (pc + o), pc + o, hs, phi, S->sc, &S->n);
             }
-            test16(w, pc + o, hs, phi, S->sc, &S->n);
         }
         __syncthreads();   // the buffer is free for the chunk after next
     }
@@ -350,6 +341,8 @@ __global__ void __launch_bounds__(NT) scan_place_kernel(const uint8_t* blob, lon
             W.cpos[base + r] = p;
             if (spec) offsets[base + r] = p;
             if (spec && base + r == 0 && p != kFileHeader) gate->spec = 0u;
+            // the first restarting block > 0 is the segment length (header byte 0, bit 2)
+            if (spec && base + r > 0 && ((blob[p] >> 2) & 1)) atomicMin(&gate->first, (unsigned long long)(base + r));
         }
         return;
     }
@@ -376,6 +369,7 @@ __global__ void __launch_bounds__(NT) scan_place_kernel(const uint8_t* blob, lon
             W.cpos[run + r] = p;
             if (spec) offsets[run + r] = p;
             if (spec && run + r == 0 && p != kFileHeader) gate->spec = 0u;
+            if (spec && run + r > 0 && ((blob[p] >> 2) & 1)) atomicMin(&gate->first, (unsigned long long)(run + r));
         }
         run += m;
     }
@@ -584,7 +578,7 @@ static int scan_grid(long long nchunks) {
 // speculative offsets): one cooperative launch over SCB-byte chunks from a
 // 16-aligned start
 static int launch_scan(const uint8_t* blob, long long nbytes, int hs, const Ws& W, long long n_blocks,
-                       long long* offsets, IlGate* gate, cudaStream_t st) {
+                       long long* offsets, IlGate* gate, IlGate* gate2, cudaStream_t st) {
     const uintptr_t a0 = ((uintptr_t)blob + kFileHeader) & ~(uintptr_t)15;
     const long long span = (long long)((uintptr_t)blob + (uintptr_t)nbytes) - (long long)a0;
     const long long nchunks = span > 0 ? (span + SCB - 1) / SCB : 1;
@@ -594,7 +588,7 @@ static int launch_scan(const uint8_t* blob, long long nbytes, int hs, const Ws& 
     if (cudaFuncSetAttribute(scan_place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
         return APAX_ERR_CUDA;
     void* args[] = {(void*)&blob, (void*)&nbytes, (void*)&hs, (void*)&a0, (void*)&nchunks, (void*)&W,
-                    (void*)&n_blocks, (void*)&offsets, (void*)&gate};
+                    (void*)&n_blocks, (void*)&offsets, (void*)&gate, (void*)&gate2};
     note_launches(1);
     if (cudaLaunchCooperativeKernel((const void*)scan_place_kernel, dim3(grid), dim3(NT), args, sm, st) != cudaSuccess)
         return APAX_ERR_CUDA;
@@ -613,11 +607,11 @@ static int sm_count() {
 size_t find_blocks_k5_ws_bytes(long long n_blocks) { return k5::layout(n_blocks, nullptr, nullptr); }
 
 int launch_k5_speculate(const uint8_t* blob, long long nbytes, int dt, long long n_blocks, long long* offsets,
-                        void* ws, IlGate* gate, cudaStream_t st) {
+                        void* ws, IlGate* gate, IlGate* gate2, cudaStream_t st) {
     using namespace k5;
     Ws W;
     layout(n_blocks, (uint8_t*)ws, &W);
-    return launch_scan(blob, nbytes, hdr_size(dt), W, n_blocks, offsets, gate, st);
+    return launch_scan(blob, nbytes, hdr_size(dt), W, n_blocks, offsets, gate, gate2, st);
 }
 
 int launch_find_blocks_k5(const uint8_t* blob, long long nbytes, long long n, int bs, int dt, long long n_blocks,
@@ -629,7 +623,7 @@ int launch_find_blocks_k5(const uint8_t* blob, long long nbytes, long long n, in
     const int hs = hdr_size(dt);
     const int nsm = sm_count();
     if (!gate) {
-        const int r = launch_scan(blob, nbytes, hs, W, n_blocks, offsets, nullptr, st);
+        const int r = launch_scan(blob, nbytes, hs, W, n_blocks, offsets, nullptr, nullptr, st);
         if (r) return r;
     }
     const size_t psmem = (size_t)NW * ((((bs >> 2) + 16 + 15) & ~15) + KSTAGE);

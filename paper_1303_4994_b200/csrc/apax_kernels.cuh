@@ -151,9 +151,11 @@ bool decode_v3_supported(int dt, int bs);
 int decode_v3_resident_ctas(int dt, size_t smem);
 int launch_decode_v3(int dt, const DecParams& P, int grid, size_t smem, cudaStream_t st);
 int launch_decode_v3_seg_dev(int dt, DecParams P, int grid, size_t smem, cudaStream_t st);
-// index-less speculation (apax_k5.cu): signature scan + speculative offsets
+// index-less speculation (apax_k5.cu): signature scan + speculative offsets;
+// the scan also sets gate->first (the first restarting block > 0) from the
+// candidates it places and initialises gate2 (all ones) for the second chance
 int launch_k5_speculate(const uint8_t* blob, long long nbytes, int dt, long long n_blocks, long long* offsets,
-                        void* ws, IlGate* gate, cudaStream_t st);
+                        void* ws, IlGate* gate, IlGate* gate2, cudaStream_t st);
 int launch_decode_v3_two_pass(int dt, DecParams P, int grid, size_t smem, unsigned long long* scratch,
                               cudaStream_t st);
 size_t decode_v2_smem_bytes(int dt, int bs, int payload_cap);
