@@ -236,6 +236,120 @@ __global__ void status_to_host_kernel(const unsigned long long* src, unsigned lo
 }
 }  // namespace
 
+namespace {
+// ---------------------------------------------------------------------------
+// Index-less decode: the fall-back behind the speculative segment decode
+// (full discovery, second-chance segment decode, two-pass decode: nine
+// kernels) is needed only when the speculation failed, which only the device
+// knows.  Launched unconditionally, the nine kernels return at once but still
+// cost a launch each (~27 us for cfg2's 0.19 ms decode).  Instead they are
+// captured once into the body of a CUDA-graph IF node whose condition a
+// one-thread kernel sets from the gate word; the instantiated graph is kept
+// for repeated decodes with the same buffers (built at the second decode of a
+// set of buffers: a build costs ~0.4 ms of host time).  Any failure of the
+// graph path falls back to the plain launches.
+// ---------------------------------------------------------------------------
+__global__ void il_gate_setter_kernel(const IlGate* gate, cudaGraphConditionalHandle h) {
+    cudaGraphSetConditional(h, il_seg_ok(gate) ? 0u : 1u);
+}
+
+struct IlGraphKey {
+    const void* blob; long long nbytes, n; int dt, bs, dev; const void* y; const void* status; const void* ws;
+    bool operator==(const IlGraphKey& o) const {
+        return blob == o.blob && nbytes == o.nbytes && n == o.n && dt == o.dt && bs == o.bs && dev == o.dev &&
+               y == o.y && status == o.status && ws == o.ws;
+    }
+};
+struct IlGraphEntry { IlGraphKey key; cudaGraphExec_t exec; unsigned long long stamp; };
+constexpr int kIlGraphSlots = 16;
+std::mutex g_il_mu;
+IlGraphEntry g_il_cache[kIlGraphSlots];
+int g_il_count = 0;
+unsigned long long g_il_stamp = 0;
+cudaStream_t g_il_capture_stream[64] = {};
+IlGraphKey g_il_seen[kIlGraphSlots];
+bool g_il_seen_valid[kIlGraphSlots] = {};
+int g_il_seen_next = 0;
+
+// enqueue(stream) must enqueue the fall-back on the given stream
+template <typename F>
+int launch_gated_fallback(const IlGraphKey& key, const IlGate* gate, F&& enqueue, cudaStream_t s) {
+    std::lock_guard<std::mutex> lock(g_il_mu);
+    for (int i = 0; i < g_il_count; i++) {
+        if (g_il_cache[i].key == key) {
+            g_il_cache[i].stamp = ++g_il_stamp;
+            return cudaGraphLaunch(g_il_cache[i].exec, s) == cudaSuccess ? APAX_OK : APAX_ERR_CUDA;
+        }
+    }
+    if (key.dev < 0 || key.dev >= 64) return APAX_ERR_ARG;
+    // building a graph costs ~0.4 ms of host time: only for buffers seen before
+    // (a one-off decode takes the plain launches)
+    {
+        bool seen = false;
+        for (int i = 0; i < kIlGraphSlots; i++) seen = seen || (g_il_seen_valid[i] && g_il_seen[i] == key);
+        if (!seen) {
+            g_il_seen[g_il_seen_next] = key;
+            g_il_seen_valid[g_il_seen_next] = true;
+            g_il_seen_next = (g_il_seen_next + 1) % kIlGraphSlots;
+            return APAX_ERR_ARG;
+        }
+    }
+    cudaStream_t& cap = g_il_capture_stream[key.dev];
+    if (!cap && cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) != cudaSuccess) { cap = nullptr; return APAX_ERR_CUDA; }
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ex = nullptr;
+    bool ok = cudaGraphCreate(&g, 0) == cudaSuccess;
+    cudaGraphConditionalHandle h;
+    ok = ok && cudaGraphConditionalHandleCreate(&h, g, 0, cudaGraphCondAssignDefault) == cudaSuccess;
+    cudaGraphNode_t n_set = nullptr, n_if = nullptr;
+    if (ok) {
+        void* kargs[] = {(void*)&gate, (void*)&h};
+        cudaKernelNodeParams kp;
+        memset(&kp, 0, sizeof(kp));
+        kp.func = (void*)il_gate_setter_kernel;
+        kp.gridDim = dim3(1);
+        kp.blockDim = dim3(1);
+        kp.kernelParams = kargs;
+        ok = cudaGraphAddKernelNode(&n_set, g, nullptr, 0, &kp) == cudaSuccess;
+    }
+    cudaGraph_t body = nullptr;
+    if (ok) {
+        cudaGraphNodeParams cp = {cudaGraphNodeTypeConditional};
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeIf;
+        cp.conditional.size = 1;
+        ok = cudaGraphAddNode(&n_if, g, &n_set, 1, &cp) == cudaSuccess;
+        if (ok) body = cp.conditional.phGraph_out[0];
+    }
+    if (ok) {
+        ok = cudaStreamBeginCaptureToGraph(cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+        if (ok) {
+            const int st = enqueue(cap);
+            cudaGraph_t got = nullptr;
+            ok = cudaStreamEndCapture(cap, &got) == cudaSuccess && st == APAX_OK;
+        }
+    }
+    ok = ok && cudaGraphInstantiate(&ex, g, 0) == cudaSuccess;
+    if (g) cudaGraphDestroy(g);
+    if (!ok) {
+        if (ex) cudaGraphExecDestroy(ex);
+        cudaGetLastError();
+        return APAX_ERR_CUDA;
+    }
+    int slot = g_il_count;
+    if (g_il_count < kIlGraphSlots) g_il_count++;
+    else {
+        slot = 0;
+        for (int i = 1; i < kIlGraphSlots; i++) if (g_il_cache[i].stamp < g_il_cache[slot].stamp) slot = i;
+        cudaGraphExecDestroy(g_il_cache[slot].exec);
+    }
+    g_il_cache[slot].key = key;
+    g_il_cache[slot].exec = ex;
+    g_il_cache[slot].stamp = ++g_il_stamp;
+    return cudaGraphLaunch(ex, s) == cudaSuccess ? APAX_OK : APAX_ERR_CUDA;
+}
+}  // namespace
+
 extern "C" {
 
 const char* apax_version(void) { return "apax-b200 0.2.0 (sm_100a)"; }
@@ -713,16 +827,27 @@ int apax_decode(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, int b
             P.il_gate = gate;
             st = launch_decode_v3_seg_dev(dtype, P, g3, sm3, s);
             if (st) return st;
-            st = launch_find_blocks_k5(blob, nbytes, n, block_size, dtype, p.n_blocks, (long long*)offs,
-                                       (unsigned long long*)status, w + p.ws_k5, s, gate);
-            if (st) return st;
-            note_launches(1);
-            seg_first_kernel<<<seg_first_grid(p.n_blocks), 256, 0, s>>>(blob, nbytes, offs, p.n_blocks, gate2, gate,
-                                                                       (const unsigned long long*)status);
-            if (cudaGetLastError() != cudaSuccess) return APAX_ERR_CUDA;
-            P.il_gate2 = gate2;
-            st = launch_decode_v3_seg_dev(dtype, P, g3, sm3, s);
-            if (st) return st;
+            auto fallback = [&](cudaStream_t fs) -> int {
+                int r = launch_find_blocks_k5(blob, nbytes, n, block_size, dtype, p.n_blocks, (long long*)offs,
+                                              (unsigned long long*)status, w + p.ws_k5, fs, gate);
+                if (r) return r;
+                note_launches(1);
+                seg_first_kernel<<<seg_first_grid(p.n_blocks), 256, 0, fs>>>(blob, nbytes, offs, p.n_blocks, gate2,
+                                                                            gate, (const unsigned long long*)status);
+                if (cudaGetLastError() != cudaSuccess) return APAX_ERR_CUDA;
+                DecParams Q = P;
+                Q.il_gate2 = gate2;
+                r = launch_decode_v3_seg_dev(dtype, Q, g3, sm3, fs);
+                if (r) return r;
+                return launch_decode_v3_two_pass(dtype, Q, g3, sm3, Q.carry, fs);
+            };
+            if (env_int("APAX_IL_GRAPH", 1)) {
+                int dev = 0;
+                cudaGetDevice(&dev);
+                const IlGraphKey key{blob, nbytes, n, dtype, block_size, dev, y, status, ws};
+                if (launch_gated_fallback(key, gate, fallback, s) == APAX_OK) return APAX_OK;
+            }
+            return fallback(s);
         }
         // any container through the segment-serial decoder: one-wave pseudo-
         // segments, pass 1 for their history maps, pass 2 with the composed
