@@ -705,20 +705,65 @@ static int launch_d3_range(int dt, bool fix, const DecParams& P, long long s0, l
     return APAX_OK;
 }
 
-// entries of a two-pass decode: e_0 = (0, 0), e_{k+1} = F_k(e_k) (one thread;
-// a few hundred segments)
-__global__ void compose_entries_kernel(const unsigned long long* maps, long long nseg, unsigned long long* entries,
-                                       const IlGate* gate, const IlGate* gate2) {
+// entries of a two-pass decode: e_0 = (0, 0), e_{k+1} = F_k(e_k).  The maps
+// are affine on (p1, p2) over Z / 2^64 and composition is associative, so the
+// entries are the translation parts of the prefix compositions: a scan in
+// shared memory, 512 segments at a time (one thread walking the maps in
+// global memory took 172 us for 592 segments: longer than a decode pass).
+constexpr int CE_T = 512;
+struct Aff { unsigned long long a11, a12, a21, a22, c1, c2; };
+// (second after first): x -> s(f(x))
+__device__ __forceinline__ Aff aff_after(const Aff& s2, const Aff& f) {
+    Aff r;
+    r.a11 = s2.a11 * f.a11 + s2.a12 * f.a21;
+    r.a12 = s2.a11 * f.a12 + s2.a12 * f.a22;
+    r.a21 = s2.a21 * f.a11 + s2.a22 * f.a21;
+    r.a22 = s2.a21 * f.a12 + s2.a22 * f.a22;
+    r.c1 = s2.a11 * f.c1 + s2.a12 * f.c2 + s2.c1;
+    r.c2 = s2.a21 * f.c1 + s2.a22 * f.c2 + s2.c2;
+    return r;
+}
+__global__ void __launch_bounds__(CE_T) compose_entries_kernel(const unsigned long long* maps, long long nseg,
+                                                               unsigned long long* entries, const IlGate* gate,
+                                                               const IlGate* gate2) {
     if (gate && (il_seg_ok(gate) || (gate2 && il_seg_ok(gate2)))) return;
-    unsigned long long h1 = 0, h2 = 0;
-    for (long long k = 0; k < nseg; k++) {
-        entries[2 * k] = h1;
-        entries[2 * k + 1] = h2;
-        const unsigned long long* m = maps + 6 * k;
-        const unsigned long long o1 = m[0] * h1 + m[1] * h2 + m[4];
-        const unsigned long long o2 = m[2] * h1 + m[3] * h2 + m[5];
-        h1 = o1;
-        h2 = o2;
+    __shared__ Aff sm[CE_T];
+    __shared__ Aff carry;     // composition of every segment before this chunk
+    const int tid = threadIdx.x;
+    if (tid == 0) { carry.a11 = 1; carry.a12 = 0; carry.a21 = 0; carry.a22 = 1; carry.c1 = 0; carry.c2 = 0; }
+    for (long long base = 0; base < nseg; base += CE_T) {
+        const long long k = base + tid;
+        Aff me;
+        if (k < nseg) {
+            const unsigned long long* m = maps + 6 * k;
+            me.a11 = m[0]; me.a12 = m[1]; me.a21 = m[2]; me.a22 = m[3]; me.c1 = m[4]; me.c2 = m[5];
+        } else {
+            me.a11 = 1; me.a12 = 0; me.a21 = 0; me.a22 = 1; me.c1 = 0; me.c2 = 0;
+        }
+        sm[tid] = me;
+        __syncthreads();
+        for (int d = 1; d < CE_T; d <<= 1) {      // inclusive scan: me = F_k after ... after F_base
+            Aff prev;
+            const bool has = tid >= d;
+            if (has) prev = sm[tid - d];
+            __syncthreads();
+            if (has) { me = aff_after(me, prev); sm[tid] = me; }
+            __syncthreads();
+        }
+        const Aff c = carry;
+        // the entry of segment k: every earlier segment applied to (0, 0)
+        if (k < nseg) {
+            unsigned long long e1 = c.c1, e2 = c.c2;
+            if (tid > 0) {
+                const Aff g = aff_after(sm[tid - 1], c);
+                e1 = g.c1; e2 = g.c2;
+            }
+            entries[2 * k] = e1;
+            entries[2 * k + 1] = e2;
+        }
+        __syncthreads();
+        if (tid == CE_T - 1) carry = aff_after(me, c);
+        __syncthreads();
     }
 }
 
@@ -739,7 +784,7 @@ int launch_decode_v3_two_pass(int dt, DecParams P, int grid, size_t smem, unsign
     int r = launch_decode_v3_tp(dt, P, grid, smem, st, 1);
     if (r) return r;
     note_launches(1);
-    compose_entries_kernel<<<1, 1, 0, st>>>(maps, nseg, entries, P.il_gate, P.il_gate2);
+    compose_entries_kernel<<<1, CE_T, 0, st>>>(maps, nseg, entries, P.il_gate, P.il_gate2);
     if (cudaGetLastError() != cudaSuccess) return APAX_ERR_CUDA;
     P.seg_map = nullptr;
     P.seg_entry = entries;
