@@ -929,7 +929,8 @@ const char* apax_encode_kernel_name(int dtype, int mode, int block_size, int64_t
         memset(&P, 0, sizeof(P));
         P.halo = p.halo;
         // (one-wave launches; longer ones take the persistent v3 kernel)
-        return encode_v5_supported(dtype, block_size, mode, P) ? "encode_v5_kernel" : "encode_v3_kernel";
+        return (encode_v5_supported(dtype, block_size, mode, P) && p.unit_blocks >= 3) ? "encode_v5_kernel"
+                                                                                      : "encode_v3_kernel";
     }
     return "encode_kernel";
 }

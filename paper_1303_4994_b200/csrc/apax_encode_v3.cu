@@ -1920,8 +1920,11 @@ int launch_encode_v3(int dt, const EncParams& P, int grid, size_t smem, cudaStre
         // the persistent v3 kernel with its placement warp the longer ones;
         // APAX_ENC_V5=2 forces v5)
         const char* e5 = getenv("APAX_ENC_V5");
+        // (and units of one or two blocks stay on v3: v5's unit start -- the
+        // service warp's first peak and quantizer before any pack warp moves --
+        // costs ~2 us more than v3's, 5-8% of such launches: profiles/r2d_cfg5_sweep.jsonl)
         const bool use5 = fixable && encode_v5_supported(dt, P.bs, P.mode, P) &&
-                          (ufull <= encode_v5_resident_ctas(dt) || (e5 && atoi(e5) == 2));
+                          ((ufull <= encode_v5_resident_ctas(dt) && P.unit_blocks >= 3) || (e5 && atoi(e5) == 2));
         const int r = use5 ? launch_encode_v5(dt, P, 0, ufull, st) : launch_v3_range(dt, true, P, 0, ufull, grid, smem, st);
         if (r) return r;
     }

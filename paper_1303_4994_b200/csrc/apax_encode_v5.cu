@@ -1396,8 +1396,11 @@ static const void* v5_fn(int dt, bool fq) {
 }
 
 int encode_v5_resident_ctas(int dt) {
+    // (per device and dtype: the occupancy queries cost host time on every launch otherwise)
+    static int cached[64][5] = {};
     int dev = 0, nsm = 0, per = 0;
     cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64 && dt >= 0 && dt < 5 && cached[dev][dt] > 0) return cached[dev][dt];
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const size_t smem = encode_v5_smem_bytes(dt);
     for (int fq = 0; fq < 2; fq++) {   // both instantiations must fit
@@ -1407,7 +1410,9 @@ int encode_v5_resident_ctas(int dt) {
             p = 1;
         per = fq == 0 ? p : (p < per ? p : per);
     }
-    return per * (nsm > 0 ? nsm : 148);
+    const int res = per * (nsm > 0 ? nsm : 148);
+    if (dev >= 0 && dev < 64 && dt >= 0 && dt < 5) cached[dev][dt] = res;
+    return res;
 }
 
 // units [u0, u1) of full blocks; one slot per CTA (P.slots holds >= grid slots)
