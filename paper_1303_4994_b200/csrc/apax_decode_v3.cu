@@ -44,6 +44,15 @@
 
 namespace apax {
 namespace d3 {
+#ifdef APAX_D3_TIMES
+// per-CTA timeline (tools/cta_times_dec.py): globaltimer at start and exit, SM id
+__device__ unsigned long long g_times[8192 * 4];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
 
 constexpr int NT = 256;
 constexpr int NW = NT / 32;
@@ -137,6 +146,14 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
     uint8_t* pbuf1 = smem + off + bufsz;
     const long long limit = P.nbytes & ~15LL;             // TMA never reads past the blob
 
+#ifdef APAX_D3_TIMES
+    if (tid == 0 && blockIdx.x < 8192) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+        g_times[4 * blockIdx.x] = gtimer();
+        g_times[4 * blockIdx.x + 3] = smid;
+    }
+#endif
     if (tid == 0) {
         mbar_init(&S->mbar[0]);
         mbar_init(&S->mbar[1]);
@@ -649,9 +666,18 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
         }
     }
     if (tid == 0 && S->store_pending) bulk_wait_all();
+#ifdef APAX_D3_TIMES
+    if (tid == 0 && blockIdx.x < 8192) g_times[4 * blockIdx.x + 2] = gtimer();
+#endif
 }
 
 }  // namespace d3
+
+#ifdef APAX_D3_TIMES
+extern "C" int apax_debug_cta_times_d3(unsigned long long* host, int n) {
+    return (int)cudaMemcpyFromSymbol(host, d3::g_times, (size_t)n * 4 * sizeof(unsigned long long));
+}
+#endif
 
 size_t decode_v3_smem_bytes(int dt, int payload_cap) {
     auto al = [](size_t v) { return (v + 127) & ~(size_t)127; };
