@@ -204,7 +204,9 @@ int apax_sweep_point(const void* x, int64_t n, int dtype, double target, double*
                      int64_t ws_bytes, void* stream);
 
 /* Device workspace needed by apax_decode (with offsets == NULL it includes
- * room for the block walk's offset table). */
+ * room for the block walk's offset table; for block sizes up to 4096 also
+ * 1600 bytes per block: the parse pass 1 of a two-pass decode saves for
+ * pass 2). */
 int64_t apax_decode_workspace_bytes(int64_t n, int dtype, int block_size);
 
 /* Decode a container body.  blob (device) holds the full container of

@@ -135,7 +135,7 @@ struct DecPlan {
     int v2;
     size_t smem;
     int grid;
-    long long ws_carry, ws_ticket, ws_offsets, ws_k5, ws_total;
+    long long ws_carry, ws_ticket, ws_offsets, ws_k5, ws_jee, ws_total;
 };
 
 int plan_decode(long long n, int dt, int bs, DecPlan* p) {
@@ -161,7 +161,9 @@ int plan_decode(long long n, int dt, int bs, DecPlan* p) {
     p->ws_ticket = (p->n_blocks * 128 + 255) & ~255LL;
     p->ws_offsets = p->ws_ticket + 256;
     p->ws_k5 = p->ws_offsets + (((p->n_blocks + 1) * 8 + 255) & ~255LL);
-    p->ws_total = p->ws_k5 + (long long)find_blocks_k5_ws_bytes(p->n_blocks);
+    p->ws_jee = (p->ws_k5 + (long long)find_blocks_k5_ws_bytes(p->n_blocks) + 255) & ~255LL;
+    // the two-pass decode's saved JEE parse (apax_decode_v3.cu, DecParams::jee_cache)
+    p->ws_total = p->ws_jee + (decode_v3_supported(dt, bs) ? p->n_blocks * kJeeRecBytes : 0);
     return APAX_OK;
 }
 
@@ -815,6 +817,7 @@ int apax_decode(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, int b
     P.ticket = (unsigned int*)(w + p.ws_ticket);
     P.payload_cap = p.payload_cap;
     if (decode_v3_supported(dtype, block_size) && env_int("APAX_DEC_VER", 0) != 2) {
+        if (env_int("APAX_JEE_CACHE", 1)) P.jee_cache = w + p.ws_jee;
         const size_t sm3 = decode_v3_smem_bytes(dtype, p.payload_cap);
         const int g3 = decode_v3_resident_ctas(dtype, sm3);
         if (gate) {

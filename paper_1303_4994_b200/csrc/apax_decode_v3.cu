@@ -244,7 +244,23 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
         const int nbat = (int)((b1 - bb) < JB ? (b1 - bb) : JB);
         // ---- JEE of the batch (entropy.py:118-164): warp w parses block bb + w
         // from global memory, no CTA barrier inside; the CTA phases below use it
-        if (warp < nbat) {
+        if (TP == 2 && P.jee_cache) {
+            // pass 2: the parse pass 1 saved
+            if (warp < nbat) {
+                const uint8_t* rec = P.jee_cache + (size_t)(bb + warp) * (size_t)kJeeRecBytes;
+                uint8_t* ej = ebufs + (size_t)warp * (((size_t)EBS + 127) & ~(size_t)127);
+                if (lane == 0) {
+                    S->jinfo[warp] = *(const int4*)rec;
+                    S->dq[warp] = *(const double2*)(rec + 16);
+                }
+                if (lane < 8) S->wbits[warp][lane] = ((const unsigned*)(rec + 32))[lane];
+                uint32_t* tp = (uint32_t*)&S->tpre[warp][0];
+#pragma unroll
+                for (int i = 0; i < 4; i++) tp[lane + 32 * i] = ((const uint32_t*)(rec + 64))[lane + 32 * i];
+                ((uint4*)ej)[lane] = ((const uint4*)(rec + 576))[lane];
+                ((uint4*)ej)[lane + 32] = ((const uint4*)(rec + 576))[lane + 32];
+            }
+        } else if (warp < nbat) {
             const long long bj = bb + warp;
             const long long sj = bj * (long long)bs;
             const int nj = FIX ? MAXBS : (int)((P.n - sj) < bs ? (P.n - sj) : bs);
@@ -314,6 +330,23 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                 const int code = (hdr >> 8) & 0xFFFF;
                 const double ds = Tr::F ? decode_scale_code(code) * ldexp(1.0, hdr >> 24) : decode_scale_code(code);
                 S->dq[warp] = make_double2(ds, __ddiv_rn(1.0, ds));
+            }
+            if (TP == 1 && P.jee_cache) {
+                // pass 1: save the parse for pass 2 (a block with an error keeps
+                // its status in jinfo; the rest of its record is not used)
+                __syncwarp();
+                uint8_t* rec = P.jee_cache + (size_t)bj * (size_t)kJeeRecBytes;
+                const uint8_t* ej = ebufs + (size_t)warp * (((size_t)EBS + 127) & ~(size_t)127);
+                if (lane == 0) {
+                    *(int4*)rec = S->jinfo[warp];
+                    *(double2*)(rec + 16) = S->dq[warp];
+                }
+                if (lane < 8) ((unsigned*)(rec + 32))[lane] = S->wbits[warp][lane];
+                const uint32_t* tp = (const uint32_t*)&S->tpre[warp][0];
+#pragma unroll
+                for (int i = 0; i < 4; i++) ((uint32_t*)(rec + 64))[lane + 32 * i] = tp[lane + 32 * i];
+                ((uint4*)(rec + 576))[lane] = ((const uint4*)ej)[lane];
+                ((uint4*)(rec + 576))[lane + 32] = ((const uint4*)ej)[lane + 32];
             }
         }
         cbar();

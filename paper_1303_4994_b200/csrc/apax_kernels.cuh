@@ -113,7 +113,12 @@ struct DecParams {
     // reports); the two-pass kernels then run only when neither path did
     IlGate* il_gate2;
     int seg_part;
+    // two-pass decode: pass 1 saves every block's parsed JEE (group widths,
+    // mantissa bit offsets, header, scale: kJeeRecBytes per block) and pass 2
+    // loads it instead of parsing the tokens again (nullptr: parse again)
+    uint8_t* jee_cache;
 };
+constexpr long long kJeeRecBytes = 1600;   // 16 jinfo + 16 scale + 32 warp bits + 512 thread bits + 1024 widths
 
 // kernel launches enqueued by the library (apax_launch_count)
 void note_launches(int k);
