@@ -141,6 +141,8 @@ int64_t apax_encode_workspace_bytes(int64_t n, int dtype, int mode, int block_si
  *   policy              : APAX_POLICY_COLD (= reference encode_stream per
  *                         segment) or APAX_POLICY_WARM_SELF (FIXED_RATE:
  *                         attenuator preset from the segment's first block).
+ *                         Ignored when segment_blocks <= 0: a whole stream
+ *                         is always the reference's encode_stream.
  *   out_cap must be >= apax_max_encoded_bytes(n, dtype, block_size).
  *   block_offsets (nullable, n_blocks + 1 int64): byte offset of every block
  *   header, then the container length (side-band index for apax_decode).

@@ -415,6 +415,8 @@ int apax_encode(const void* x, int64_t n, int dtype, int mode, double target, in
     EncPlan p;
     int st = plan_encode(n, dtype, mode, block_size, segment_blocks, &p);
     if (st) return st;
+    // the policy belongs to segments: a whole stream is the reference's encode_stream
+    if (segment_blocks <= 0) policy = APAX_POLICY_COLD;
     if (mode == APAX_LOSSLESS && dtype >= APAX_F32) return APAX_ERR_CFG_LOSSLESS_FLOAT;
     if (mode == APAX_FIXED_RATE && !(target > 0)) return APAX_ERR_CFG_FR_TARGET;
     if (!x || !out || !status || (p.ws_total > 0 && !ws)) return APAX_ERR_ARG;
@@ -520,6 +522,7 @@ int apax_encode_cast(const void* x, int in_kind, int64_t n, int dtype, int mode,
     EncPlan p;
     int st = plan_encode(n, kdt, mode, block_size, segment_blocks, &p);
     if (st) return st;
+    if (segment_blocks <= 0) policy = APAX_POLICY_COLD;
     if (mode == APAX_LOSSLESS && dtype >= APAX_F32) return APAX_ERR_CFG_LOSSLESS_FLOAT;
     if (mode == APAX_FIXED_RATE && !(target > 0)) return APAX_ERR_CFG_FR_TARGET;
     if (!x || !out || !status || (p.ws_total > 0 && !ws)) return APAX_ERR_ARG;

@@ -391,3 +391,20 @@ def test_floor_log2_quirk_containers():
         tr = res.trace.cpu().numpy()
         assert (int(tr[0][2]), int(tr[0][3])) == (m["first_block"]["code"], m["first_block"]["fbe"])
         assert np.array_equal(decode_stream(c["blob"]), c["y"])
+
+
+@pytest.mark.parametrize("bs", [4096, 1000])
+def test_whole_stream_ignores_segment_policy(bs):
+    """segment_policy belongs to segments: a whole stream (segment_blocks=None)
+    is the reference's encode_stream under either policy, on the split encoder
+    (block size 4096) and the general one alike."""
+    n = bs * 9 + 321
+    for dt, x, target in ((Dtype.I16, W.cfg1_sines_i16(n), 4.0), (Dtype.F32, W.cfg2_ar2_f32(n), 6.0),
+                          (Dtype.F64, W.cfg2_ar2_f32(n).astype(np.float64), 3.0)):
+        ref, _, _ = O.encode(x, dt.wire_code, Mode.FIXED_RATE.value, target, bs, segment_blocks=0, policy=0)
+        ref_w, _, _ = O.encode(x, dt.wire_code, Mode.FIXED_RATE.value, target, bs, segment_blocks=0, policy=1)
+        assert ref == ref_w
+        for pol in ("cold", "warm_self"):
+            res = encode_device(torch.from_numpy(x).cuda(), StreamConfig(dt, bs, Mode.FIXED_RATE, target,
+                                                                         segment_policy=pol))
+            assert res.to_bytes() == ref, (dt, pol)

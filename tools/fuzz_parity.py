@@ -42,6 +42,8 @@ for i in range(cases):
     if ok and not isinstance(ref, Exception):
         yo = O.decode(ref)
         ok = np.array_equal(decode_device(res.blob, res.nbytes).cpu().numpy(), yo)
+        if ok:   # with the side-band index, segment structure not given (two-pass decode)
+            ok = np.array_equal(decode_device(res.blob, res.nbytes, res.block_offsets).cpu().numpy(), yo)
         if ok and seg:
             ok = np.array_equal(decode_device(res.blob, res.nbytes, res.block_offsets,
                                               segment_blocks=seg).cpu().numpy(), yo)
