@@ -709,6 +709,9 @@ __global__ void __launch_bounds__(kNT) encode_kernel(EncParams P) {
             __syncthreads();
             analyze(b0, n0, 1.0, false);
             if (tid == 0) {
+                // the cost pass at gain 1 can fail on its own (widened samples
+                // beyond 34 bits): the preset pass below starts a new status
+                if (S->bad) report_error(P.status, b0, S->bad);
                 long long c0 = 4 * S->sum_e[0] + 4 * (long long)G0;
                 long long c1 = 4 * S->sum_e[1] + 4 * (long long)G0;
                 long long c2 = 4 * S->sum_e[2] + 4 * (long long)G0;

@@ -353,6 +353,33 @@ def test_cast_random_vs_oracle(seed):
         assert np.array_equal(decode_stream(ref), O.decode(ref))
 
 
+def test_cast_segmented_warm_self_vs_oracle():
+    """Widened samples in segmented fixed-rate containers under warm_self: the
+    preset's cost pass at gain 1 fails on samples beyond 34 bits exactly where
+    the oracle's does (the first block of the first such segment), and codes
+    the same bytes otherwise."""
+    rng = np.random.default_rng(3100)
+    t = np.arange(128 * 8 + 50)
+    v = np.sin(t * 0.07) + rng.normal(0, 0.1, t.size)
+    for scale, fails in ((0.3, False), (3.0, False), (50.0, True), (900.0, True)):
+        x = np.rint(v * scale * (2 ** 31 - 1)).astype(np.int64)
+        if fails:
+            x[:128 * 3] //= 1000       # the first segment fits: the error is segment 1's
+        cfg = StreamConfig(Dtype.I32, 128, Mode.FIXED_RATE, 6.0, segment_blocks=3, segment_policy="warm_self")
+        try:
+            ref = O.encode(x, 2, Mode.FIXED_RATE.value, 6.0, 128, segment_blocks=3, policy=1)[0]
+        except O.OracleError as e:
+            ref = e
+        assert isinstance(ref, O.OracleError) == fails
+        if fails:
+            assert (ref.code, ref.detail) == (10, 3)
+            with pytest.raises(Exception) as ei:
+                encode_stream(x, cfg)
+            assert "34-bit" in str(ei.value)
+        else:
+            assert encode_stream(x, cfg) == ref
+
+
 # ---------------------------------------------------------------------------
 # per-block traces against the reference stepping encode_block: scale code,
 # block exponent, selector, costs, bytes and restart exact; the attenuation
