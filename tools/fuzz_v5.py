@@ -1,7 +1,9 @@
 """Randomised parity search for the v5 encoder (not a test: a bug hunt):
 block size 4096, i16 / i32 / f32, fixed rate / fixed quality, cold and
 warm_self, one-wave and several units per CTA (APAX_ENC_V5=2), against the
-oracle.  Usage: python tools/fuzz_v5.py [cases] [seed]"""
+oracle.  FUZZ_NBLK_MIN / FUZZ_NBLK_MAX set the range of block counts (more
+segments than resident CTAs: several units per CTA, the persistent v3 kernel).
+Usage: python tools/fuzz_v5.py [cases] [seed]"""
 import os
 import sys
 
@@ -21,7 +23,7 @@ bad = 0
 for i in range(cases):
     dt = [Dtype.I16, Dtype.I32, Dtype.F32][rng.integers(0, 3)]
     mode = [Mode.FIXED_RATE, Mode.FIXED_QUALITY][rng.integers(0, 2)]
-    nblk = int(rng.integers(1, 60))
+    nblk = int(rng.integers(int(os.environ.get("FUZZ_NBLK_MIN", "1")), int(os.environ.get("FUZZ_NBLK_MAX", "60"))))
     n = 4096 * nblk + int(rng.integers(0, 2)) * int(rng.integers(1, 4096))
     seg = int(rng.choice([1, 2, 3, 5, 8, 13]))
     pol = "warm_self" if (mode is Mode.FIXED_RATE and rng.integers(0, 2)) else "cold"
