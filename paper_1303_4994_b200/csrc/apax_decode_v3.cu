@@ -541,6 +541,48 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                     bp += 4 * wd;
                 }
                 unsigned long long q0 = 0, d0 = 0;   // q and d1 entering this thread (exact, 64-bit)
+                if (TP == 1 && bnarrow && sel >= 1) {
+                    // pass 1 needs only the history leaving the block: the last
+                    // sample of D1 is h1 + sum v, of D2 h1 + np (h1 - h2) +
+                    // sum (np - i) v_i, the one before it follows from the last
+                    // difference -- CTA sums instead of the scan (widths <= 16:
+                    // the warp sums fit 32 bits; the totals are exact mod 2^64)
+                    int s32 = 0, t32 = 0;
+#pragma unroll
+                    for (int i = 0; i < SPT; i++) { s32 += v[i]; t32 += s32; }
+                    const long long bq = (long long)(np - i0 - SPT) * (long long)s32 + (long long)t32;
+                    const int aw = __reduce_add_sync(0xffffffffu, s32);
+                    const unsigned blo = __reduce_add_sync(0xffffffffu, (unsigned)(bq & 0xffff));
+                    const int bhi = __reduce_add_sync(0xffffffffu, (int)(bq >> 16));
+                    if (lane == 0) {
+                        S->rs_w[warp] = (long long)aw;
+                        S->rt_w[warp] = (long long)bhi * 65536LL + (long long)blo;
+                    }
+                    cbar();
+                    if (hist_thread) {
+                        unsigned long long A = 0, B = 0;
+#pragma unroll
+                        for (int w8 = 0; w8 < NW; w8++) {
+                            A += (unsigned long long)S->rs_w[w8];
+                            B += (unsigned long long)S->rt_w[w8];
+                        }
+                        int vlast = 0;
+#pragma unroll
+                        for (int i = 0; i < SPT; i++)
+                            if (i == j1) vlast = v[i];
+                        unsigned long long P1, P2;
+                        if (sel == 1) {
+                            P1 = h1 + A;
+                            P2 = P1 - (unsigned long long)(long long)vlast;
+                        } else {
+                            const unsigned long long dl = (h1 - h2) + A;
+                            P1 = h1 + (unsigned long long)np * (h1 - h2) + B;
+                            P2 = P1 - dl;
+                        }
+                        S->p1 = (long long)P1;
+                        S->p2 = (long long)P2;
+                    }
+                } else {
                 if (sel >= 1) {
                     int s32 = 0, t32 = 0;
 #pragma unroll
@@ -601,6 +643,7 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
                         if (want_y) out[i] = deq((double)qv);
                     }
                 }
+                }   // scan path
             } else {
                 long long q[SPT];
 #pragma unroll
