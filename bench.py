@@ -547,6 +547,41 @@ def main():
                 "welch_x_peak_db": float(10 * np.log10(wx.max() + 1e-30)),
                 "welch_d_peak_db": float(10 * np.log10(wd.max() + 1e-30))}
 
+    # ---- the reference's own container format: one whole stream, no segments ----
+    # (encode_stream's output; what a user of the reference hands to
+    # decode_stream).  Device times of its decode with and without the
+    # side-band index: two passes over pseudo-segments (history maps, then the
+    # samples from the composed entries).  N = 1, untimed encode.
+    ref_container = None
+    if world == 1 and not args.profile and not args.no_e2e and not args.shard_global and n <= (1 << 27):
+        wenc = Encoder(n, StreamConfig(wdt, 4096, wmode, target), device=dev)
+        wenc.encode(x)
+        wnb = wenc.finish()
+        wdec = Decoder(n, wdt, 4096, device=dev)
+
+        def _timed_decode(offs):
+            wdec.decode(wenc.out, wnb, offs, stream=stream)
+            wdec.finish(stream)
+            ts = []
+            for _ in range(5):
+                flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                wdec.decode(wenc.out, wnb, offs, stream=stream)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            return float(np.median(ts)), wdec.finish(stream)[:n].clone()
+        t_idx, y_idx = _timed_decode(wenc.offsets)
+        t_il, y_il = _timed_decode(None)
+        ref_container = {"what": "whole-stream container of the same array (byte-identical to the reference's "
+                                 "encode_stream), decoded on the device; median of 5, L2 flushed",
+                         "container_bytes": int(wnb),
+                         "decode_with_index_ms": t_idx, "decode_indexless_ms": t_il,
+                         "indexless_equals_indexed": bool(torch.equal(y_idx, y_il)),
+                         "finite": bool(torch.isfinite(y_idx.double()).all()) if wdt.is_float else True}
+        del wenc, wdec, y_idx, y_il
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
         threads = os.cpu_count() or 1
@@ -597,6 +632,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "profile_stats": prof,
+            "reference_container": ref_container,
             "gpu_launches": gpu_launches,
             "clocks": sampler.summary(),
             "self_check": {"decoded_finite": ok_roundtrip},
