@@ -768,7 +768,10 @@ __global__ void __launch_bounds__(kNT) encode_kernel(EncParams P) {
             if (tid == 0) {
                 long long jee_bytes = (S->nib_total + 1) >> 1;
                 long long mant_bytes = (S->bits_total + 7) >> 3;
-                S->block_bytes = hs + jee_bytes + mant_bytes;
+                // a block in error emits its header only: its widths (up to 64
+                // bits for samples outside the 34-bit range) say nothing about
+                // the window, which is sized for legal blocks
+                S->block_bytes = S->bad ? hs : hs + jee_bytes + mant_bytes;
                 if (S->staged + S->block_bytes + 4 > (long long)P.stage_bytes) S->red_u[0] = 1;
                 else S->red_u[0] = 0;
             }

@@ -1022,6 +1022,13 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
                 // the headroom guarantees it) and every |d1| < 2^30 (checked
                 // per warp in phase C)
                 S->wide = (qpk > (1LL << 30)) ? 1 : 0;
+                // the block exponent stops at -127 (an int8 field): f64 samples
+                // beyond 2^189 then quantize past the q buffers' 32 bits.  From
+                // 2^33 on the reference raises "sample outside 34-bit range"
+                // (entropy.py:53-54) for the block; so does this kernel from 2^31
+                // on (between the two the reference raises unless both
+                // differences of the block stay inside 34 bits)
+                if (F && qpk >= (1LL << 31) && !bad) bad = APAX_ERR_INTERNAL;
                 S->bad = bad;
                 int sel = 0;
                 if (S->has_pc) {
@@ -1701,7 +1708,9 @@ __global__ void __launch_bounds__(PW ? NT : NCT, PW ? APAX_V3_MINB : APAX_V3_MIN
                 const int sel = S->gate ? 0 : S->sel_spec;
                 if (META) {
                     BlockMeta m;
-                    m.sq = S->sq; m.code = S->code; m.fbe = (short)S->fbe; m.wide = (short)S->wide;
+                    // (a block in error: a zero quantizer, the packer codes a silent block)
+                    m.sq = S->bad ? 0.0 : S->sq; m.code = S->code; m.fbe = (short)S->fbe;
+                    m.wide = S->bad ? (short)0 : (short)S->wide;
                     P.meta[b] = m;   // (trace: S1 wrote the gain, the packer adds the rest)
                 } else if (P.trace) {
                     double* tr = P.trace + 10 * b;

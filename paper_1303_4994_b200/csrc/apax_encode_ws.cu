@@ -388,6 +388,9 @@ __global__ void __launch_bounds__(NT, 1) chain_kernel(EncParams P) {
             S->sq = F ? (zero ? 0.0 : s) : aq;
             S->rs = FQ ? (F ? __ddiv_rn(1.0, s) : (aq != 1.0 ? __ddiv_rn(1.0, aq) : 1.0)) : 1.0;
             S->wide = qpk > (1LL << 30) ? 1 : 0;
+            // f64 samples quantized past 32 bits (the block exponent stops at
+            // -127): "sample outside 34-bit range", see apax_encode_v3.cu
+            if (F && qpk >= (1LL << 31) && !bad) bad = APAX_ERR_INTERNAL;
             S->bad = bad;
             int sel = 0;
             if (S->has_pc) {
@@ -396,7 +399,8 @@ __global__ void __launch_bounds__(NT, 1) chain_kernel(EncParams P) {
             }
             S->sel = sel;
             BlockMeta mt;
-            mt.sq = S->sq; mt.code = code; mt.fbe = (short)fbe; mt.wide = (short)S->wide;
+            // (a block in error: a zero quantizer, the packer codes a silent block)
+            mt.sq = bad ? 0.0 : S->sq; mt.code = code; mt.fbe = (short)fbe; mt.wide = bad ? (short)0 : (short)S->wide;
             P.meta[b] = mt;
             if (P.trace) {
                 double* tr = P.trace + 10 * b;

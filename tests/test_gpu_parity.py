@@ -435,3 +435,36 @@ def test_whole_stream_ignores_segment_policy(bs):
             res = encode_device(torch.from_numpy(x).cuda(), StreamConfig(dt, bs, Mode.FIXED_RATE, target,
                                                                          segment_policy=pol))
             assert res.to_bytes() == ref, (dt, pol)
+
+
+@pytest.mark.parametrize("bs,mode,target,seg,pol", [
+    (8192, Mode.FIXED_QUALITY, 40.0, None, "cold"),        # the general encoder
+    (4096, Mode.FIXED_RATE, 8.0, 2, "warm_self"),          # the fused segment encoder
+    (4096, Mode.FIXED_RATE, 8.0, None, "cold"),            # the whole-stream chain + packer
+    (4096, Mode.FIXED_QUALITY, 300.0, 4, "cold"),
+    (128, Mode.FIXED_RATE, 16.0, None, "cold"),
+])
+def test_f64_beyond_block_exponent_range_vs_oracle(bs, mode, target, seg, pol):
+    """f64 samples so large that the int8 block exponent stops at -127
+    (|x| > 2^191): the quantized samples leave the 34-bit range and the
+    reference raises InternalError for the first such block (entropy.py:53-54).
+    The encoders report the same block, touch nothing outside their buffers,
+    and the next encode on the same device is unaffected."""
+    rng = np.random.default_rng(77)
+    n = bs * 5 + 33
+    x = np.cumsum(rng.standard_normal(n)) * 1e3
+    x[bs * 2 + 7] = np.finfo(np.float64).max        # block 2
+    x[bs * 3:bs * 3 + 50] = -1e200                  # block 3
+    with pytest.raises(O.OracleError) as e_ref:
+        O.encode(x, 4, mode.value, target, bs, segment_blocks=seg or 0, policy=1 if pol == "warm_self" else 0)
+    assert e_ref.value.code == 10
+    cfg = StreamConfig(Dtype.F64, bs, mode, target, segment_blocks=seg, segment_policy=pol)
+    enc = Encoder(n, cfg)
+    enc.encode(torch.from_numpy(x).cuda())
+    torch.cuda.synchronize()
+    key = int(enc.status.cpu().numpy().view(np.uint64)[1])
+    assert (key & 0xFF, key >> 8) == (10, e_ref.value.detail)
+    x[bs * 2 + 7] = 1.0
+    x[bs * 3:bs * 3 + 50] = 2.0
+    ref = O.encode(x, 4, mode.value, target, bs, segment_blocks=seg or 0, policy=1 if pol == "warm_self" else 0)[0]
+    assert encode_device(torch.from_numpy(x).cuda(), cfg).to_bytes() == ref
