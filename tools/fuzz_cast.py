@@ -30,6 +30,9 @@ for i in range(cases):
     v = np.sin(t * rng.uniform(1e-3, 0.5)) * rng.uniform(0.1, 1.0) + rng.normal(0, rng.uniform(0, 0.3), n)
     if dt.is_float:
         x = v * 10.0 ** rng.uniform(-8, 8)          # float64: not exactly representable in f32
+        if os.environ.get("FUZZ_CAST_EXTREME") and rng.integers(0, 2):
+            # beyond f32's range, up to f64's maximum, and below f32's denormals
+            x = v * 10.0 ** float(rng.choice([-320, -300, -60, -40, 37, 39, 60, 190, 300, 307.5]))
         if rng.integers(0, 4) == 0:
             x = x.astype(np.float32).astype(np.float64)
         if rng.integers(0, 5) == 0:
