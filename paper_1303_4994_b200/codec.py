@@ -369,7 +369,8 @@ def _reference_cast(x: np.ndarray, dt: Dtype):
         xf = np.ascontiguousarray(x.astype(np.float64))
         if dt is Dtype.F64:
             return xf, _IN_NATIVE
-        x32 = xf.astype(np.float32)
+        with np.errstate(over="ignore", invalid="ignore"):   # values beyond f32: not representable, no warning
+            x32 = xf.astype(np.float32)
         if np.array_equal(x32.astype(np.float64), xf, equal_nan=True):
             return x32, _IN_NATIVE
         return xf, _IN_FLOAT64
