@@ -782,6 +782,12 @@ int apax_decode(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, int b
     if (cudaMemsetAsync(w, 0, (size_t)p.ws_offsets, s) != cudaSuccess) return APAX_ERR_CUDA;
     const long long* offs = (const long long*)block_offsets;
     IlGate* gate = nullptr;
+    // index-less: the discovery's candidate parse fills the two-pass decode's
+    // per-block records (DecParams::jee_cache, jee_k5)
+    uint8_t* k5_cache = (decode_v3_supported(dtype, block_size) && env_int("APAX_DEC_VER", 0) != 2 &&
+                         env_int("APAX_JEE_CACHE", 1) && env_int("APAX_JEE_K5", 1))
+                            ? w + p.ws_jee : nullptr;
+    const int* k5_flag = nullptr;
     if (!offs) {
         long long* wo = (long long*)(w + p.ws_offsets);
         if (cudaMemsetAsync(wo, 0xFF, (size_t)(p.n_blocks + 1) * 8, s) != cudaSuccess) return APAX_ERR_CUDA;
@@ -799,7 +805,8 @@ int apax_decode(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, int b
             if (st) return st;
         } else if (k5) {
             st = launch_find_blocks_k5(blob, nbytes, n, block_size, dtype, p.n_blocks, wo,
-                                       (unsigned long long*)status, w + p.ws_k5, s);
+                                       (unsigned long long*)status, w + p.ws_k5, s, nullptr, k5_cache);
+            k5_flag = k5_cache ? k5_flags(w + p.ws_k5, p.n_blocks) : nullptr;
         } else {
             st = launch_walk(blob, nbytes, n, block_size, dtype, p.n_blocks, wo, (unsigned long long*)status, s);
         }
@@ -835,7 +842,7 @@ int apax_decode(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, int b
             if (st) return st;
             auto fallback = [&](cudaStream_t fs) -> int {
                 int r = launch_find_blocks_k5(blob, nbytes, n, block_size, dtype, p.n_blocks, (long long*)offs,
-                                              (unsigned long long*)status, w + p.ws_k5, fs, gate);
+                                              (unsigned long long*)status, w + p.ws_k5, fs, gate, k5_cache);
                 if (r) return r;
                 note_launches(1);
                 seg_first_kernel<<<seg_first_grid(p.n_blocks), 256, 0, fs>>>(blob, nbytes, offs, p.n_blocks, gate2,
@@ -843,6 +850,7 @@ int apax_decode(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, int b
                 if (cudaGetLastError() != cudaSuccess) return APAX_ERR_CUDA;
                 DecParams Q = P;
                 Q.il_gate2 = gate2;
+                if (k5_cache && Q.jee_cache) Q.jee_k5 = k5_flags(w + p.ws_k5, p.n_blocks);
                 r = launch_decode_v3_seg_dev(dtype, Q, g3, sm3, fs);
                 if (r) return r;
                 return launch_decode_v3_two_pass(dtype, Q, g3, sm3, Q.carry, fs);
@@ -858,6 +866,7 @@ int apax_decode(const uint8_t* blob, int64_t nbytes, int64_t n, int dtype, int b
         // any container through the segment-serial decoder: one-wave pseudo-
         // segments, pass 1 for their history maps, pass 2 with the composed
         // entries (the carry region holds maps + entries)
+        if (k5_flag && P.jee_cache) P.jee_k5 = k5_flag;
         return launch_decode_v3_two_pass(dtype, P, g3, sm3, P.carry, s);
     }
     if (p.v2) return launch_decode_v2(dtype, P, p.grid, p.smem, s);

@@ -185,6 +185,7 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
         }
     }
 
+    const bool k5_rec = TP == 1 && P.jee_k5 && P.jee_k5[0] == 0 && P.jee_k5[1] == 0;
     // issue the load of block bb into buffer slot (thread 0)
     auto issue = [&](long long bb, int slot) {
         const long long o0 = P.offsets[bb], o1 = P.offsets[bb + 1];
@@ -244,9 +245,13 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
         const int nbat = (int)((b1 - bb) < JB ? (b1 - bb) : JB);
         // ---- JEE of the batch (entropy.py:118-164): warp w parses block bb + w
         // from global memory, no CTA barrier inside; the CTA phases below use it
-        if (TP == 2 && P.jee_cache) {
-            // pass 2: the parse pass 1 saved
-            if (warp < nbat) {
+        // pass 2: the parse pass 1 saved; pass 1 of an index-less decode: the
+        // parse the block discovery saved (every block but the last, whose
+        // group count the discovery did not know)
+        const bool rec_load = warp < nbat && P.jee_cache &&
+                              (TP == 2 || (TP == 1 && k5_rec && bb + warp + 1 < P.n_blocks));
+        if (rec_load) {
+            {
                 const uint8_t* rec = P.jee_cache + (size_t)(bb + warp) * (size_t)kJeeRecBytes;
                 uint8_t* ej = ebufs + (size_t)warp * (((size_t)EBS + 127) & ~(size_t)127);
                 if (lane == 0) {

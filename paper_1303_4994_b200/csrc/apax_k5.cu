@@ -59,6 +59,7 @@ constexpr int LBMAX = 4096;    // scan CTAs at most
 constexpr int SCB = 16384;     // bytes per scan chunk (one TMA bulk copy)
 constexpr int KCAP = 1024;     // candidates of one chunk held in shared memory
 constexpr int KSTAGE = 2048;   // staged bytes per parse warp (>= 16 + 1537 + 8 for 4096-sample blocks)
+constexpr int KREC = 32 + 512;  // per parse warp: the record's warp bits and thread bit offsets
 
 struct Ws {
     Hdr* hdr;
@@ -379,7 +380,7 @@ __global__ void __launch_bounds__(NT) scan_place_kernel(const uint8_t* blob, lon
 // with a full block's group count -> next block position or -1; then the
 // index of the candidate at that position (usually the next one)
 __global__ void __launch_bounds__(NT) parse_kernel(const uint8_t* blob, long long nbytes, int bs, int dt, Ws W,
-                                                   const IlGate* gate) {
+                                                   const IlGate* gate, uint8_t* jee_cache, long long n_blocks) {
     if (gate && il_seg_ok(gate)) return;
     extern __shared__ __align__(16) unsigned char smem_k5[];
     if (W.hdr->fail) return;
@@ -387,8 +388,10 @@ __global__ void __launch_bounds__(NT) parse_kernel(const uint8_t* blob, long lon
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int G = bs >> 2;
     const int ebytes = (G + 16 + 15) & ~15;   // the fast parser may write e[G]
-    uint8_t* e = smem_k5 + warp * (ebytes + KSTAGE);
+    uint8_t* e = smem_k5 + warp * (ebytes + KSTAGE + KREC);
     uint8_t* stg = e + ebytes;                  // the candidate's JEE bytes, staged
+    unsigned* rwb = (unsigned*)(stg + KSTAGE);  // record: bits up to the end of each decode warp
+    unsigned short* rtp = (unsigned short*)(rwb + 8);   // record: each decode thread's bit offset
     const int hs = hdr_size(dt);
     const long long maxj = (3LL * G + 2) / 2;
     const long long nwarps = (long long)gridDim.x * NW;
@@ -454,6 +457,56 @@ __global__ void __launch_bounds__(NT) parse_kernel(const uint8_t* blob, long lon
             }
             const long long sz = (used + 1) / 2 + (4 * esum + 7) / 8;
             if (!st && avail >= sz) nxt = pos + hs + sz;
+            if (!st && jee_cache && i + 1 < n_blocks) {
+                // candidate i's parse as block i's record of the two-pass decode
+                // (the JEE phase of decode_v3_kernel, same layout and values):
+                // used by pass 1 when every candidate turns out to be a block
+                __syncwarp();
+                unsigned sb = 0, em = 0, wb[8];
+#pragma unroll
+                for (int k = 0; k < 32; k += 4) {
+                    const int g = 32 * lane + k;
+                    uint32_t ew;
+                    if (g + 4 <= G) ew = *(const uint32_t*)(e + g);
+                    else {
+                        ew = 0;
+                        for (int c = 0; c < 4; c++) ew |= (g + c < G ? (uint32_t)e[g + c] : 0u) << (8 * c);
+                    }
+                    wb[k >> 2] = 4u * (unsigned)__dp4a(ew, 0x01010101u, 0u);
+                    sb += wb[k >> 2];
+                    em = __vmaxu4(em, ew);
+                }
+                const unsigned own = sb;
+                em = max(max(em & 0xffu, (em >> 8) & 0xffu), max((em >> 16) & 0xffu, em >> 24));
+                const unsigned wmax = __reduce_max_sync(0xffffffffu, em);
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const unsigned o = __shfl_up_sync(0xffffffffu, sb, d);
+                    if (lane >= d) sb += o;
+                }
+                if ((lane & 3) == 3) rwb[lane >> 2] = sb;
+                const unsigned sx = sb - own;
+                unsigned run = sx - __shfl_sync(0xffffffffu, sx, lane & ~3);
+#pragma unroll
+                for (int q = 0; q < 8; q++) { rtp[8 * lane + q] = (unsigned short)run; run += wb[q]; }
+                __syncwarp();
+                uint8_t* rec = jee_cache + (size_t)i * (size_t)kJeeRecBytes;
+                if (lane == 0) {
+                    const uint8_t* h = blob + pos;
+                    const bool isf = dt >= 3;
+                    const int hdr = (int)(h[0] & 7) | ((int)h[1] << 8) | ((int)h[2] << 16) | (isf ? ((int)h[4] << 24) : 0);
+                    const int code = (hdr >> 8) & 0xFFFF;
+                    const double ds = isf ? decode_scale_code(code) * ldexp(1.0, hdr >> 24) : decode_scale_code(code);
+                    *(int4*)rec = make_int4(hdr, 0, (int)used, (int)wmax);
+                    *(double2*)(rec + 16) = make_double2(ds, __ddiv_rn(1.0, ds));
+                }
+                if (lane < 8) ((unsigned*)(rec + 32))[lane] = rwb[lane];
+                const uint32_t* tp = (const uint32_t*)rtp;
+#pragma unroll
+                for (int q = 0; q < 4; q++) ((uint32_t*)(rec + 64))[lane + 32 * q] = tp[lane + 32 * q];
+                ((uint4*)(rec + 576))[lane] = ((const uint4*)e)[lane];
+                ((uint4*)(rec + 576))[lane + 32] = ((const uint4*)e)[lane + 32];
+            }
         }
         // successor index: the candidate at position nxt (32-ary search)
         int s = -1;
@@ -614,9 +667,16 @@ int launch_k5_speculate(const uint8_t* blob, long long nbytes, int dt, long long
     return launch_scan(blob, nbytes, hdr_size(dt), W, n_blocks, offsets, gate, gate2, st);
 }
 
+const int* k5_flags(void* ws, long long n_blocks) {
+    k5::Ws W;
+    k5::layout(n_blocks, (uint8_t*)ws, &W);
+    static_assert(offsetof(k5::Hdr, chain_bad) == offsetof(k5::Hdr, fail) + sizeof(int), "fail, chain_bad adjacent");
+    return &W.hdr->fail;
+}
+
 int launch_find_blocks_k5(const uint8_t* blob, long long nbytes, long long n, int bs, int dt, long long n_blocks,
                           long long* offsets, unsigned long long* status, void* ws, cudaStream_t st,
-                          const IlGate* gate) {
+                          const IlGate* gate, uint8_t* jee_cache) {
     using namespace k5;
     Ws W;
     layout(n_blocks, (uint8_t*)ws, &W);
@@ -626,13 +686,14 @@ int launch_find_blocks_k5(const uint8_t* blob, long long nbytes, long long n, in
         const int r = launch_scan(blob, nbytes, hs, W, n_blocks, offsets, nullptr, nullptr, st);
         if (r) return r;
     }
-    const size_t psmem = (size_t)NW * ((((bs >> 2) + 16 + 15) & ~15) + KSTAGE);
+    const size_t psmem = (size_t)NW * ((((bs >> 2) + 16 + 15) & ~15) + KSTAGE + KREC);
+    if (bs > 4096) jee_cache = nullptr;   // the records hold up to 1024 groups
     if (cudaFuncSetAttribute(parse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem) != cudaSuccess)
         return APAX_ERR_CUDA;
     long long pgrid = (W.cap + NW - 1) / NW;
     if (pgrid > (long long)nsm * 8) pgrid = (long long)nsm * 8;
     note_launches(1);
-    parse_kernel<<<(int)pgrid, NT, psmem, st>>>(blob, nbytes, bs, dt, W, gate);
+    parse_kernel<<<(int)pgrid, NT, psmem, st>>>(blob, nbytes, bs, dt, W, gate, jee_cache, n_blocks);
     long long cgrid = (W.cap + NT - 1) / NT;
     if (cgrid > (long long)nsm * 4) cgrid = (long long)nsm * 4;
     note_launches(1);

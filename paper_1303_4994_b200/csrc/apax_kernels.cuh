@@ -117,6 +117,10 @@ struct DecParams {
     // mantissa bit offsets, header, scale: kJeeRecBytes per block) and pass 2
     // loads it instead of parsing the tokens again (nullptr: parse again)
     uint8_t* jee_cache;
+    // index-less decode: the block discovery's candidate parse filled the
+    // records of blocks 0 .. n_blocks-2 when its two flags (fail, chain_bad)
+    // are both zero -- every candidate was a block; pass 1 then loads them too
+    const int* jee_k5;
 };
 constexpr long long kJeeRecBytes = 1600;   // 16 jinfo + 16 scale + 32 warp bits + 512 thread bits + 1024 widths
 
@@ -185,8 +189,12 @@ int launch_walk_after_k5(const uint8_t* blob, long long nbytes, long long n, int
 size_t find_blocks_k5_ws_bytes(long long n_blocks);
 // gate non-null: the discovery after launch_k5_speculate (scan reused),
 // every kernel returns at once while il_seg_ok(gate)
+// jee_cache non-null (block sizes up to 4096): the candidate parse also writes
+// candidate i's parse as record i (DecParams::jee_cache); k5_flags(ws) are the
+// two ints that say whether candidate i is block i (DecParams::jee_k5)
 int launch_find_blocks_k5(const uint8_t* blob, long long nbytes, long long n, int bs, int dt, long long n_blocks,
                           long long* offsets, unsigned long long* status, void* ws, cudaStream_t st,
-                          const IlGate* gate = nullptr);
+                          const IlGate* gate = nullptr, uint8_t* jee_cache = nullptr);
+const int* k5_flags(void* ws, long long n_blocks);
 
 }  // namespace apax

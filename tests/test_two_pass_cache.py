@@ -1,6 +1,8 @@
 """Two-pass decode of whole-stream containers (apax_decode): pass 2 loads the
 JEE parse pass 1 saved in the workspace (DecParams::jee_cache) instead of
-parsing the tokens again.  The result must be the oracle's, and the same as
+parsing the tokens again, and without a side-band index pass 1 loads the
+parse the block discovery saved (DecParams::jee_k5, APAX_JEE_K5=0 to switch
+it off).  The result must be the oracle's, and the same as
 with the cache switched off (APAX_JEE_CACHE=0), for clean containers of every
 sample type, ragged last blocks, other block sizes, and corrupted containers
 (the reference's error code and position)."""
@@ -21,9 +23,11 @@ from paper_1303_4994_b200 import workloads as W  # noqa: E402
 U64 = (1 << 64) - 1
 
 
-def _decode(blob, offs, n, dt, bs, cache):
+def _decode(blob, offs, n, dt, bs, cache, k5=True):
     old = os.environ.get("APAX_JEE_CACHE")
+    old5 = os.environ.get("APAX_JEE_K5")
     os.environ["APAX_JEE_CACHE"] = "1" if cache else "0"
+    os.environ["APAX_JEE_K5"] = "1" if k5 else "0"
     try:
         d = torch.zeros(len(blob) + 64, dtype=torch.uint8, device="cuda")
         d[:len(blob)] = torch.from_numpy(np.frombuffer(blob, np.uint8).copy()).cuda()
@@ -33,10 +37,11 @@ def _decode(blob, offs, n, dt, bs, cache):
         key = int(dec.status.cpu().numpy().view(np.uint64)[1])
         return ("err", key & 0xFF, key >> 8) if key != U64 else ("ok", dec.y[:n].cpu().numpy().copy())
     finally:
-        if old is None:
-            os.environ.pop("APAX_JEE_CACHE", None)
-        else:
-            os.environ["APAX_JEE_CACHE"] = old
+        for k, v in (("APAX_JEE_CACHE", old), ("APAX_JEE_K5", old5)):
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
 
 
 def _oracle(blob):
@@ -81,6 +86,8 @@ def test_whole_stream_cached_parse_vs_oracle(case):
         on = _decode(blob, offs, n, dt, bs, True)
         off = _decode(blob, offs, n, dt, bs, False)
         assert _same(on, ref) and _same(off, ref), (case, "index" if offs is not None else "index-less")
+        if offs is None:   # without the block discovery's records (pass 1 parses every block itself)
+            assert _same(_decode(blob, None, n, dt, bs, True, k5=False), ref), (case, "index-less, no K5 records")
 
 
 def test_whole_stream_cached_parse_errors():
@@ -102,3 +109,5 @@ def test_whole_stream_cached_parse_errors():
             on = _decode(blob, o, n, Dtype.F32, 4096, True)
             off = _decode(blob, o, n, Dtype.F32, 4096, False)
             assert _same(on, ref) and _same(off, ref), (ref, on[0], on[1:] if on[0] == "err" else "")
+            if o is None:
+                assert _same(_decode(blob, None, n, Dtype.F32, 4096, True, k5=False), ref)
