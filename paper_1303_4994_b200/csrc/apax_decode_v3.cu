@@ -85,6 +85,20 @@ struct __align__(16) St {
 
 using namespace apax::tma;
 
+// a segment's history map x -> A x + c on (p1, p2) over Z / 2^64
+struct Aff { unsigned long long a11, a12, a21, a22, c1, c2; };
+// (second after first): x -> s(f(x))
+__device__ __forceinline__ Aff aff_after(const Aff& s2, const Aff& f) {
+    Aff r;
+    r.a11 = s2.a11 * f.a11 + s2.a12 * f.a21;
+    r.a12 = s2.a11 * f.a12 + s2.a12 * f.a22;
+    r.a21 = s2.a21 * f.a11 + s2.a22 * f.a21;
+    r.a22 = s2.a21 * f.a12 + s2.a22 * f.a22;
+    r.c1 = s2.a11 * f.c1 + s2.a12 * f.c2 + s2.c1;
+    r.c2 = s2.a21 * f.c1 + s2.a22 * f.c2 + s2.c2;
+    return r;
+}
+
 __device__ __forceinline__ void cbar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 __device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
@@ -234,7 +248,40 @@ __global__ void __launch_bounds__(NT, APAX_D3_MINB) decode_v3_kernel(DecParams P
         const long long b1 = (b0 + P_seg < P.n_blocks) ? b0 + P_seg : P.n_blocks;
         // history entering the segment: (0, 0) at a restart (a segmented
         // container), or the composed entry of pass 2 of a two-pass decode
-        if (tid == 0) {
+        if (TP == 2 && !P.seg_entry) {
+            // the entry of segment sg: the maps of segments 0 .. sg-1 (pass 1)
+            // applied in order to (0, 0).  Composition is associative: every
+            // thread composes a run of maps, the warps and the CTA combine the
+            // runs in order (no launch of its own for a few hundred maps)
+            Aff acc = {1ULL, 0ULL, 0ULL, 1ULL, 0ULL, 0ULL};
+            const long long per = (sg + NT - 1) / NT;
+            const long long k1 = ((long long)tid + 1) * per < sg ? ((long long)tid + 1) * per : sg;
+            for (long long k = (long long)tid * per; k < k1; k++) {
+                const ulonglong2* m = (const ulonglong2*)(P.seg_map + 6 * k);
+                const ulonglong2 m0 = m[0], m1 = m[1], m2 = m[2];
+                const Aff f = {m0.x, m0.y, m1.x, m1.y, m2.x, m2.y};
+                acc = aff_after(f, acc);
+            }
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                Aff o;
+                o.a11 = __shfl_down_sync(0xffffffffu, acc.a11, d); o.a12 = __shfl_down_sync(0xffffffffu, acc.a12, d);
+                o.a21 = __shfl_down_sync(0xffffffffu, acc.a21, d); o.a22 = __shfl_down_sync(0xffffffffu, acc.a22, d);
+                o.c1 = __shfl_down_sync(0xffffffffu, acc.c1, d); o.c2 = __shfl_down_sync(0xffffffffu, acc.c2, d);
+                if ((lane & (2 * d - 1)) == 0) acc = aff_after(o, acc);   // the later run after the earlier
+            }
+            Aff* wa = (Aff*)ebufs;
+            if (lane == 0) wa[warp] = acc;
+            cbar();
+            if (tid == 0) {
+                Aff tot = wa[0];
+#pragma unroll
+                for (int w8 = 1; w8 < NW; w8++) tot = aff_after(wa[w8], tot);
+                S->p1 = (long long)tot.c1;
+                S->p2 = (long long)tot.c2;
+            }
+            cbar();   // ebufs are the JEE phase's from here on
+        } else if (tid == 0) {
             S->p1 = TP == 2 ? (long long)P.seg_entry[2 * sg] : 0;
             S->p2 = TP == 2 ? (long long)P.seg_entry[2 * sg + 1] : 0;
         }
@@ -818,18 +865,8 @@ static int launch_d3_range(int dt, bool fix, const DecParams& P, long long s0, l
 // shared memory, 512 segments at a time (one thread walking the maps in
 // global memory took 172 us for 592 segments: longer than a decode pass).
 constexpr int CE_T = 512;
-struct Aff { unsigned long long a11, a12, a21, a22, c1, c2; };
-// (second after first): x -> s(f(x))
-__device__ __forceinline__ Aff aff_after(const Aff& s2, const Aff& f) {
-    Aff r;
-    r.a11 = s2.a11 * f.a11 + s2.a12 * f.a21;
-    r.a12 = s2.a11 * f.a12 + s2.a12 * f.a22;
-    r.a21 = s2.a21 * f.a11 + s2.a22 * f.a21;
-    r.a22 = s2.a21 * f.a12 + s2.a22 * f.a22;
-    r.c1 = s2.a11 * f.c1 + s2.a12 * f.c2 + s2.c1;
-    r.c2 = s2.a21 * f.c1 + s2.a22 * f.c2 + s2.c2;
-    return r;
-}
+using d3::Aff;
+using d3::aff_after;
 __global__ void __launch_bounds__(CE_T) compose_entries_kernel(const unsigned long long* maps, long long nseg,
                                                                unsigned long long* entries, const IlGate* gate,
                                                                const IlGate* gate2) {
@@ -890,11 +927,18 @@ int launch_decode_v3_two_pass(int dt, DecParams P, int grid, size_t smem, unsign
     P.no_store = 1;
     int r = launch_decode_v3_tp(dt, P, grid, smem, st, 1);
     if (r) return r;
-    note_launches(1);
-    compose_entries_kernel<<<1, CE_T, 0, st>>>(maps, nseg, entries, P.il_gate, P.il_gate2);
-    if (cudaGetLastError() != cudaSuccess) return APAX_ERR_CUDA;
-    P.seg_map = nullptr;
-    P.seg_entry = entries;
+    // the entries: composed by pass 2's CTAs themselves, or (APAX_D3_COMPOSE=1)
+    // by a scan kernel of its own
+    const char* ce = getenv("APAX_D3_COMPOSE");
+    if (ce && atoi(ce) == 1) {
+        note_launches(1);
+        compose_entries_kernel<<<1, CE_T, 0, st>>>(maps, nseg, entries, P.il_gate, P.il_gate2);
+        if (cudaGetLastError() != cudaSuccess) return APAX_ERR_CUDA;
+        P.seg_map = nullptr;
+        P.seg_entry = entries;
+    } else {
+        P.seg_entry = nullptr;   // maps stay in P.seg_map
+    }
     P.no_store = 0;
     return launch_decode_v3_tp(dt, P, grid, smem, st, 2);
 }
