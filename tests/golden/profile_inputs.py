@@ -35,7 +35,15 @@ def make(name: str) -> tuple:
         rng = np.random.default_rng(35)
         x = (np.sin(0.05 * np.arange(3000)) * 50 + rng.normal(0, 0.5, 3000)).astype(np.float32)
         return x, "f32", (30.0, 50.0, 70.0), 512, 4096
+    if name == "const_i16":
+        # a constant: every difference stream is silent, the correlation of x
+        # and y is undefined at most targets (points dropped with a warning)
+        return np.full(16384, 7, np.int16), "i16", (2.0, 4.0, 20.0), 4096, 4096
+    if name == "ramp_i32_unreachable":
+        # no grid point reaches the correlation threshold: target_unreachable
+        return np.arange(16384, dtype=np.int32), "i32", (2.0, 4.0), 4096, 4096
     raise KeyError(name)
 
 
-NAMES = ("ar2_f32", "sines_i16", "walk_f64", "noise_i32_default_grid", "short_f32")
+NAMES = ("ar2_f32", "sines_i16", "walk_f64", "noise_i32_default_grid", "short_f32", "const_i16",
+         "ramp_i32_unreachable")

@@ -184,7 +184,14 @@ def test_profile_report_vs_reference(name):
     for k in P.METRIC_KEYS:
         va, vb = wa["metrics"][k], wb["metrics"][k]
         if "spectral" in k or k == "fft_s2r_margin_db":
-            assert _close(va, vb, rel=0, abs_=1e-6), k
+            # a floor more than 150 dB under its peak is the transform's own
+            # rounding noise (see the bins below): 1 dB there
+            def is_noise(kk):
+                f = wb["metrics"][kk]
+                return isinstance(f, float) and np.isfinite(f) and f < wb["metrics"][kk.replace("floor", "peak")] - 150.0
+            noise = is_noise(k) if "floor" in k else (
+                k == "fft_s2r_margin_db" and any(is_noise(f"spectral_floor_{c}_db") for c in "xyd"))
+            assert _close(va, vb, rel=0, abs_=1.0 if noise else 1e-6), k
         elif k == "two_sigma_s2r_margin_db":
             assert va == pytest.approx(vb, abs=1e-9), k
         else:
@@ -192,8 +199,16 @@ def test_profile_report_vs_reference(name):
             assert _close(va, vb, rel=1e-9, abs_=1e-12 * scale), k
     for sig in ("x", "d"):
         ba, bb = np.array(wa["spectra"][sig]["bins_db"]), np.array(wb["spectra"][sig]["bins_db"])
-        assert ba.shape == bb.shape and np.allclose(ba, bb, rtol=0, atol=1e-6)
-        assert wa["spectra"][sig]["floor_db"] == pytest.approx(wb["spectra"][sig]["floor_db"], abs=1e-6)
+        assert ba.shape == bb.shape
+        # bins within 150 dB of the spectrum's peak to 1e-6 dB; below that a bin
+        # is the rounding noise of the transform itself (2^-50 of the peak in
+        # power: a constant or a ramp has nothing else there) and cuFFT's noise
+        # is not pocketfft's: those only have to be noise on both sides
+        live = bb >= bb.max() - 150.0
+        assert np.allclose(ba[live], bb[live], rtol=0, atol=1e-6)
+        assert np.all(ba[~live] < bb.max() - 140.0)
+        assert wa["spectra"][sig]["floor_db"] == pytest.approx(wb["spectra"][sig]["floor_db"],
+                                                                abs=1e-6 if live.all() else 1.0)
     ca, cb = wa["s2r"]["cdf"], wb["s2r"]["cdf"]
     assert len(ca) == len(cb)
     assert np.allclose(np.array(ca), np.array(cb), rtol=1e-12, atol=1e-9)
