@@ -248,3 +248,14 @@ def test_output_free_sweep_point_matches_full_encode_decode(seed):
             assert nb == nb2, (dt, n)
             for a, b in ((sxx, s.sxx), (sxy, s.sxy), (syy, s.syy)):
                 assert a == pytest.approx(b, rel=1e-12, abs=0.0), (dt, n)
+
+
+@gpu
+def test_profile_of_silence_raises_like_the_reference():
+    """An all-zero array: the correlation is undefined at every grid point, the
+    reference drops each with a warning and raises NoData("empty
+    rate-correlation curve") (profiler.py:196, :228)."""
+    x = np.zeros(8192 * 2, np.float32)
+    with pytest.warns(UserWarning, match="correlation undefined at SRR target"):
+        with pytest.raises(NoData, match="empty rate-correlation curve"):
+            P.profile(x, Dtype.F32, grid=(2.0, 4.0), block_size=4096, name="zeros")
